@@ -1,0 +1,405 @@
+"""Benchmark: SpMV GB/s & GFLOP/s per format vs the HBM roofline (C2), and
+Krylov ms/iteration (C1/C4/C5 workloads).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c2|c3|c1|c4b|c4g|c5]
+
+Default workload (N=1) is BASELINE.json config C2: the 3-D 27-point stencil
+128^3 (2,097,152 rows, 55,742,968 entries), fp64. One *step* = one Csr
+(automatic strategy) SpMV x = A b through the C ABI; inputs are larger than
+L2 and L2 is additionally flushed (256 MiB write) between timed steps, each
+step timed with CUDA events on the launching stream. Every other format
+(Csr classical / load-balanced, Coo, Ell, Sellp, Hybrid) in fp64 and fp32 is
+timed the same way and reported under "formats". N>1: replicas (weak
+scaling; C2 does not shard -- see DESIGN.md).
+
+``--impl reference`` times the reference's CPU algorithm (oracle port of
+ParallelExecutor + csr_row_sums) on all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "SpMV GB/s & GFLOP/s per format vs HBM peak; CG ms/iter at 1/2/4/8 GPUs"
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------
+def bytes_csr(n, nnz, vt, it=4):
+    return nnz * (vt + it) + (n + 1) * it + 2 * n * vt
+
+
+def bytes_format(m, vt, it=4):
+    from paper_2006_16852_b200 import Coo, Csr, Ell, Hybrid, Sellp
+
+    n = m.size.rows
+    if isinstance(m, Csr):
+        return bytes_csr(n, m.nnz, vt, it)
+    if isinstance(m, Coo):
+        return m.nnz * (vt + 2 * it) + 2 * n * vt
+    if isinstance(m, Ell):
+        return n * m.width * (vt + it) + 2 * n * vt
+    if isinstance(m, Sellp):
+        return m.num_stored_elements * (vt + it) + 2 * m._sl.numel() * it + 2 * n * vt
+    if isinstance(m, Hybrid):
+        return n * m.ell.width * (vt + it) + m.coo.nnz * (vt + 2 * it) + 2 * n * vt
+    raise TypeError(type(m))
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML, 5 ms sampling)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torchrun: one process per GPU)
+# ---------------------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allmax(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# timing helpers
+# ---------------------------------------------------------------------------
+class Timer:
+    """Per-step CUDA-event timing on the launching stream, L2 flushed between
+    steps (outside the events)."""
+
+    def __init__(self, exc):
+        import torch
+
+        self.torch = torch
+        self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=exc.device)
+
+    def run(self, fn, steps, warmup):
+        torch = self.torch
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        stream = torch.cuda.current_stream()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        for s, e in ev:
+            self.flush_buf.fill_(1)
+            s.record(stream)
+            fn()
+            e.record(stream)
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in ev]  # ms
+
+
+def traffic_from_profiles(kernel_key):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_key)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# C2: SpMV format sweep
+# ---------------------------------------------------------------------------
+def bench_c2(args, world, rank, local):
+    import torch
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib, problems
+
+    peak, peak_src = peaks()
+    exc = b2.CudaExecutor(local)
+    torch.cuda.set_device(local)
+    g = 128
+    timer = Timer(exc)
+    rng = np.random.default_rng(0)
+    a64 = problems.stencil(exc, "27pt", g, value_dtype="float64")
+    n, nnz = a64.size.rows, a64.nnz
+    bvec = rng.standard_normal((n, 1))
+    results = {}
+    head = None
+    for dt, vt in (("float64", 8), ("float32", 4)):
+        base = a64 if dt == "float64" else problems.stencil(exc, "27pt", g, value_dtype=dt)
+        b = b2.Dense(exc, bvec, value_dtype=dt)
+        x = b2.Dense.zeros(exc, n, 1, value_dtype=dt)
+        variants = [("csr", b2.convert(base, "csr")), ("csr_classical", b2.convert(base, "csr_classical")),
+                    ("csr_lb", b2.convert(base, "csr_lb")), ("coo", b2.convert(base, "coo")),
+                    ("ell", b2.convert(base, "ell")), ("sellp", b2.convert(base, "sellp")),
+                    ("hybrid", b2.convert(base, "hybrid"))]
+        for name, m in variants:
+            key = f"{name}_{'f64' if vt == 8 else 'f32'}"
+            m.apply(b, x)  # build plans/workspaces outside timing
+            if name == "csr" and dt == "float64":
+                head = (m, b, x)
+                continue
+            ms = timer.run(lambda: m.apply(b, x), max(5, min(args.steps, 50)), 3)
+            t = statistics.mean(ms) * 1e-3
+            by = bytes_format(m, vt)
+            results[key] = {"us": round(t * 1e6, 2), "gbs": round(by / t / 1e9, 1),
+                            "gbs_useful": round(bytes_csr(n, nnz, vt) / t / 1e9, 1),
+                            "gflops": round(2 * nnz / t / 1e9, 1), "frac": round(by / t / 1e9 / peak, 4),
+                            "bytes": by}
+            if name == "csr":
+                results[key]["strategy"] = m.strategy
+            del m
+        torch.cuda.empty_cache()
+
+    # ---- headline: Csr (automatic) fp64, exactly K timed steps ------------
+    m, b, x = head
+    by = bytes_format(m, 8)
+    launches0 = _lib.launch_count()
+    for _ in range(args.warmup):
+        m.apply(b, x)
+    barrier(world)
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        ms = timer.run(lambda: m.apply(b, x), args.steps, 0)
+    launches = _lib.launch_count() - launches0
+    barrier(world)
+    t_step = allmax(world, statistics.mean(ms) * 1e-3)
+    total_bytes = allsum(world, by)
+    value = total_bytes / t_step / 1e9
+    results["csr_f64"] = {"us": round(t_step * 1e6, 2), "gbs": round(by / t_step / 1e9, 1),
+                          "gbs_useful": round(by / t_step / 1e9, 1),
+                          "gflops": round(2 * nnz / t_step / 1e9, 1),
+                          "frac": round(by / t_step / 1e9 / peak, 4), "bytes": by,
+                          "strategy": m.strategy}
+    kern = "csr_classical_kernel" if m.strategy == "classical" else "csr_lb_kernel"
+    roofline = {"bound": "hbm", "achieved": round(by / t_step / 1e9, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(by / t_step / 1e9 / peak, 4), "traffic": traffic_from_profiles(kern),
+                "peak_source": peak_src, "kernel": kern, "bytes_per_launch": by}
+
+    # ---- e2e: public API with host (pinned) operands ------------------------
+    host = exc.master
+    bh = b2.Dense(host, bvec)
+    xh = b2.Dense(host, np.zeros((n, 1)))
+    for _ in range(max(1, args.warmup)):
+        m.apply(bh, xh)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 20))):
+        t0 = time.perf_counter()
+        m.apply(bh, xh)  # H2D b, SpMV, D2H x (synchronous on return)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_step = allmax(world, statistics.mean(e2e_t))
+    e2e = {"value": round(total_bytes / e2e_step / 1e9, 1), "unit": "GB/s",
+           "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8,
+           "ms_per_step": round(e2e_step * 1e3, 3)}
+
+    # ---- CPU baseline: reference algorithm on host cores (rank 0, N=1) ------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle.cpu_baseline import time_csr_spmv
+
+        rp = m._rp.cpu().numpy()
+        ci = m._ci.cpu().numpy()
+        vals = m._v.cpu().numpy()
+        reps = 3
+        tc, cores, _ = time_csr_spmv(rp, ci, vals, bvec, reps=reps, warmup=1)
+        cpu = {"value": round(by / tc / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": f"full C2 matrix, Csr SpMV (ParallelExecutor restatement, {cores} threads), "
+                         f"median of {reps} after 1 warm-up; {tc * 1e3:.1f} ms/SpMV"}
+
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated 27-point stencil, b ~ N(0,1) seed 0)",
+        "config": {"workload": "C2: Csr SpMV x = A b, 3-D 27-point stencil 128^3 "
+                               "(2,097,152 rows, 55,742,968 nnz), fp64 values / int32 indices",
+                   "format": f"csr ({m.strategy})", "rows": n, "nnz": nnz,
+                   "l2": "inputs larger than L2 and L2 flushed (256 MiB write) between steps",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "gflops": round(2 * nnz / t_step / 1e9, 1),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk.summary(), "formats": results,
+    }
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU algorithm on host cores
+# ---------------------------------------------------------------------------
+def bench_reference(args):
+    from oracle import problems as P
+    from oracle.cpu_baseline import ParallelCsr
+
+    n, r, c, v = P.stencil3d(128, "27pt")
+    rp, ci, vals = P.to_csr(n, r, c, v)
+    del r, c, v
+    ci = ci.astype(np.int32)
+    b = np.random.default_rng(0).standard_normal((n, 1))
+    op = ParallelCsr(rp, ci, vals)
+    out = np.empty((n, 1))
+    for _ in range(args.warmup):
+        op.apply(b, out)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        op.apply(b, out)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    by = bytes_csr(n, int(rp[-1]), 8)
+    val = by / t / 1e9
+    cores = len(op.blocks)
+    op.close()
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (oracle-generated 27-point stencil, b ~ N(0,1) seed 0)",
+        "config": {"workload": "C2: Csr SpMV x = A b, 3-D 27-point stencil 128^3 "
+                               "(2,097,152 rows, 55,742,968 nnz), fp64 values / int32 indices",
+                   "format": "csr", "rows": n, "nnz": int(rp[-1])},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": "full C2 matrix per step: reference ParallelExecutor + csr_row_sums "
+                                   "restated (oracle/cpu_baseline.py)"},
+        "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        print(json.dumps(bench_reference(args)))
+        return
+
+    world, rank, local = dist_setup()
+    if args.workload == "c2":
+        out = bench_c2(args, world, rank, local)
+    else:
+        from bench_solvers import bench_workload  # solver workloads
+
+        out = bench_workload(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

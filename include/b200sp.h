@@ -1,0 +1,201 @@
+/* libb200sp -- C ABI of the B200-native SpMV + Krylov hot path.
+ *
+ * This is the drop-in boundary for the reference's executor/operation plugin
+ * point: the reference dispatches every numeric operation through
+ *     Executor.run(op) -> _dispatch -> op.<kind>(exc)     (src/executor.py:123-154)
+ * and a new backend is "a new Executor subclass plus a per-kernel Operation
+ * variant". Each function below is the body of one such
+ * `Operation.cuda` variant; the reference kernel it replaces is cited beside
+ * it (paths relative to /root/reference/pkg/src/opalg/).
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer owned by the caller (borrowed for the
+ *     call only, = `lend`, src/ownership.py:75-78); nothing is freed here;
+ *   - sizes are int64_t, matrix indices int32_t (DEFAULT_INDEX_DTYPE,
+ *     src/config.py:22), values double (_f64) or float (_f32);
+ *   - `stream` is a cudaStream_t passed as void*; launches are asynchronous
+ *     and stream-ordered, callers synchronise before any host read
+ *     (Executor.run is observably synchronous);
+ *   - return 0 (B200SP_OK) or a B200SP_E* code; b200sp_last_error() returns
+ *     the thread-local message. Codes map to src/errors.py classes.
+ *   - SpMV semantics, one right-hand-side column per call:
+ *         x[i] = alpha * (A b)[i] + beta * x_in[i]     (x_in == NULL -> 0)
+ *     alpha/beta are the host values unless the *_dev pointer is non-NULL.
+ *     Strides are row strides (elements) of the (n, m) row-major Dense.
+ */
+#ifndef B200SP_H
+#define B200SP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200SP_ABI_VERSION 1
+
+#define B200SP_OK 0
+#define B200SP_EINVAL 1      /* ParameterError / DimensionMismatch */
+#define B200SP_ECUDA 2       /* OpalgError (CUDA runtime failure)   */
+#define B200SP_ESINGULAR 3   /* Singular (src/errors.py:36-37)      */
+#define B200SP_EUNSUPPORTED 4 /* Unsupported (src/errors.py:18-19)  */
+
+/* ---- runtime ---------------------------------------------------------- */
+const char* b200sp_last_error(void);
+long long b200sp_launch_count(void);
+int b200sp_version(void);
+int b200sp_device_sync(void);
+int64_t b200sp_reduce_workspace_elems(void);
+int64_t b200sp_scan_workspace_elems(int64_t count);
+int b200sp_exclusive_scan_i32(int64_t count, const int32_t* in, int32_t* out, long long* ws, void* stream);
+int b200sp_exclusive_scan_i64(int64_t count, const int32_t* in, int64_t* out, long long* ws, void* stream);
+int b200sp_reduce_max_i32(int64_t count, const int32_t* in, int32_t* out, void* stream);
+
+/* ---- BLAS-1 on Dense (n, m) blocks -------------------------------------
+ * replaces CopyKernel/FillKernel/ScaleKernel/AddScaledKernel (kernels.py:30-99)
+ * and DotKernel/Norm2Kernel (kernels.py:102-137). alpha_dev: (1, m) scalars. */
+int b200sp_fill_f64(int64_t n, int32_t m, double* x, int64_t xs, double value, void* stream);
+int b200sp_fill_f32(int64_t n, int32_t m, float* x, int64_t xs, float value, void* stream);
+int b200sp_copy_f64(int64_t n, int32_t m, const double* s, int64_t ss, double* d, int64_t ds, void* stream);
+int b200sp_copy_f32(int64_t n, int32_t m, const float* s, int64_t ss, float* d, int64_t ds, void* stream);
+int b200sp_scale_f64(int64_t n, int32_t m, double alpha, const double* alpha_dev, double* x, int64_t xs, void* stream);
+int b200sp_scale_f32(int64_t n, int32_t m, float alpha, const float* alpha_dev, float* x, int64_t xs, void* stream);
+int b200sp_add_scaled_f64(int64_t n, int32_t m, double alpha, const double* alpha_dev, const double* x, int64_t xs,
+                          double* y, int64_t ys, void* stream);
+int b200sp_add_scaled_f32(int64_t n, int32_t m, float alpha, const float* alpha_dev, const float* x, int64_t xs,
+                          float* y, int64_t ys, void* stream);
+/* partials: b200sp_reduce_workspace_elems() values; counter: one zeroed uint32 */
+int b200sp_dot_f64(int64_t n, int32_t m, const double* x, int64_t xs, const double* y, int64_t ys, double* out,
+                   double* partials, uint32_t* counter, void* stream);
+int b200sp_dot_f32(int64_t n, int32_t m, const float* x, int64_t xs, const float* y, int64_t ys, float* out,
+                   float* partials, uint32_t* counter, void* stream);
+int b200sp_norm2_f64(int64_t n, int32_t m, const double* x, int64_t xs, double* out, double* partials,
+                     uint32_t* counter, void* stream);
+int b200sp_norm2_f32(int64_t n, int32_t m, const float* x, int64_t xs, float* out, float* partials,
+                     uint32_t* counter, void* stream);
+
+/* ---- SpMV ---------------------------------------------------------------- */
+/* Csr, classical strategy (sub-warp of `subwarp` lanes per row);
+ * replaces CsrSpmvKernel + csr_row_sums (kernels.py:278-316) */
+int b200sp_csr_spmv_classical_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
+                                  const double* b, int64_t b_stride, double* x, int64_t x_stride, double alpha,
+                                  const double* alpha_dev, double beta, const double* beta_dev, const double* x_in,
+                                  int64_t x_in_stride, int32_t subwarp, void* stream);
+int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
+                                  const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
+                                  const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
+                                  int64_t x_in_stride, int32_t subwarp, void* stream);
+/* Csr, load-balanced (merge-path) strategy: plan once per matrix
+ * (coords: 2*(num_tiles+1) int32), workspace carry_row/carry_val: num_tiles each */
+int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes);
+int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* row_ptrs, int32_t value_bytes, int32_t* coords,
+                       void* stream);
+int b200sp_csr_spmv_lb_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
+                           const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
+                           double alpha, const double* alpha_dev, double beta, const double* beta_dev,
+                           const double* x_in, int64_t x_in_stride, const int32_t* coords, int32_t* carry_row,
+                           double* carry_val, void* stream);
+int b200sp_csr_spmv_lb_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
+                           const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride,
+                           float alpha, const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
+                           int64_t x_in_stride, const int32_t* coords, int32_t* carry_row, float* carry_val,
+                           void* stream);
+/* Coo (entries sorted by row); replaces CooSpmvKernel / CooAdvSpmvKernel /
+ * CooResidualKernel (kernels.py:163-275). Rows with no entry are NOT written:
+ * the caller prefills them with b200sp_rows_scale_*. carry_head/carry_tail:
+ * ceil(nnz/chunk) values each. */
+int b200sp_coo_spmv_f64(int64_t nnz, int32_t chunk, const int32_t* row_idxs, const int32_t* col_idxs,
+                        const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
+                        double alpha, const double* alpha_dev, double beta, const double* beta_dev,
+                        const double* x_in, int64_t x_in_stride, double* carry_head, double* carry_tail,
+                        void* stream);
+int b200sp_coo_spmv_f32(int64_t nnz, int32_t chunk, const int32_t* row_idxs, const int32_t* col_idxs,
+                        const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
+                        const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
+                        int64_t x_in_stride, float* carry_head, float* carry_tail, void* stream);
+int b200sp_rows_scale_f64(int64_t count, const int32_t* rows, double* x, int64_t x_stride, double beta,
+                          const double* beta_dev, const double* x_in, int64_t x_in_stride, void* stream);
+int b200sp_rows_scale_f32(int64_t count, const int32_t* rows, float* x, int64_t x_stride, float beta,
+                          const float* beta_dev, const float* x_in, int64_t x_in_stride, void* stream);
+/* Ell (column-major, padding col = -1); no reference kernel */
+int b200sp_ell_spmv_f64(int64_t n, int64_t width, int64_t stride, const int32_t* col_idxs, const double* vals,
+                        const double* b, int64_t b_stride, double* x, int64_t x_stride, double alpha,
+                        const double* alpha_dev, double beta, const double* beta_dev, const double* x_in,
+                        int64_t x_in_stride, void* stream);
+int b200sp_ell_spmv_f32(int64_t n, int64_t width, int64_t stride, const int32_t* col_idxs, const float* vals,
+                        const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
+                        const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
+                        int64_t x_in_stride, void* stream);
+/* Sellp (slice_size rows per slice); no reference kernel */
+int b200sp_sellp_spmv_f64(int64_t n, int32_t slice_size, const int32_t* slice_lengths, const int32_t* slice_sets,
+                          const int32_t* col_idxs, const double* vals, const double* b, int64_t b_stride, double* x,
+                          int64_t x_stride, double alpha, const double* alpha_dev, double beta,
+                          const double* beta_dev, const double* x_in, int64_t x_in_stride, void* stream);
+int b200sp_sellp_spmv_f32(int64_t n, int32_t slice_size, const int32_t* slice_lengths, const int32_t* slice_sets,
+                          const int32_t* col_idxs, const float* vals, const float* b, int64_t b_stride, float* x,
+                          int64_t x_stride, float alpha, const float* alpha_dev, float beta, const float* beta_dev,
+                          const float* x_in, int64_t x_in_stride, void* stream);
+
+/* Dense operator times one column (DenseSpmvKernel, kernels.py:319-332) */
+int b200sp_dense_spmv_f64(int64_t n, int64_t k, const double* a, int64_t a_stride, const double* b, int64_t b_stride,
+                         double* x, int64_t x_stride, void* stream);
+int b200sp_dense_spmv_f32(int64_t n, int64_t k, const float* a, int64_t a_stride, const float* b, int64_t b_stride,
+                         float* x, int64_t x_stride, void* stream);
+
+/* ---- conversions (Csr hub); replaces convert/from_data/to_data
+ * (formats.py:40-53, :196-221, :301-329) for the device formats ------------ */
+int b200sp_csr_row_lengths(int64_t n, const int32_t* row_ptrs, int32_t* len, void* stream);
+int b200sp_csr_to_coo_rows(int64_t n, const int32_t* row_ptrs, int32_t* row_idxs, void* stream);
+int b200sp_coo_to_csr_ptrs(int64_t nnz, int64_t n, const int32_t* row_idxs, int32_t* row_ptrs, void* stream);
+int b200sp_sellp_slice_lengths(int64_t n, const int32_t* row_ptrs, int32_t slice_size, int32_t stride_factor,
+                               int32_t* slice_lengths, void* stream);
+int b200sp_hybrid_overflow_counts(int64_t n, const int32_t* row_ptrs, int32_t width, int32_t* counts, void* stream);
+int b200sp_ell_row_lengths(int64_t n, int64_t width, int64_t stride, const int32_t* col_idxs, int32_t* len,
+                           void* stream);
+int b200sp_sellp_row_lengths(int64_t n, int32_t slice_size, const int32_t* slice_lengths, const int32_t* slice_sets,
+                             const int32_t* col_idxs, int32_t* len, void* stream);
+int b200sp_add_csr_lengths(int64_t n, const int32_t* row_ptrs2, int32_t* len, void* stream);
+int b200sp_length_histogram(int64_t n, const int32_t* row_ptrs, int32_t nbins, unsigned long long* hist,
+                            void* stream);
+int b200sp_empty_row_flags(int64_t n, const int32_t* row_ptrs, int32_t* flag, void* stream);
+int b200sp_compact_flags(int64_t n, const int32_t* flag, const int32_t* pos, int32_t* out, void* stream);
+#define B200SP_CONVERT_DECL(T, SUF)                                                                              \
+    int b200sp_csr_to_ell_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, int64_t width,      \
+                                int64_t stride, int32_t* ell_ci, T* ell_v, void* stream);                        \
+    int b200sp_csr_to_sellp_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, int32_t slice_size, \
+                                  const int32_t* slice_lengths, const int32_t* slice_sets, int32_t* sellp_ci,    \
+                                  T* sellp_v, void* stream);                                                     \
+    int b200sp_csr_to_hybrid_coo_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, int32_t width, \
+                                       const int32_t* offsets, int32_t* coo_rows, int32_t* coo_ci, T* coo_v,      \
+                                       void* stream);                                                             \
+    int b200sp_ell_to_csr_fill_##SUF(int64_t n, int64_t width, int64_t stride, const int32_t* ell_ci,            \
+                                     const T* ell_v, const int32_t* rp, int32_t* ci, T* v, void* stream);         \
+    int b200sp_sellp_to_csr_fill_##SUF(int64_t n, int32_t slice_size, const int32_t* slice_lengths,              \
+                                       const int32_t* slice_sets, const int32_t* sellp_ci, const T* sellp_v,      \
+                                       const int32_t* rp, int32_t* ci, T* v, void* stream);                       \
+    int b200sp_hybrid_coo_append_##SUF(int64_t n, const int32_t* rp, const int32_t* ell_len, const int32_t* coo_rp, \
+                                       const int32_t* coo_ci, const T* coo_v, int32_t* ci, T* v, void* stream);   \
+    int b200sp_dense_row_nnz_##SUF(int64_t n, int64_t k, const T* a, int64_t as, int32_t* len, void* stream);    \
+    int b200sp_dense_to_csr_fill_##SUF(int64_t n, int64_t k, const T* a, int64_t as, const int32_t* rp,          \
+                                       int32_t* ci, T* v, void* stream);                                          \
+    int b200sp_csr_to_dense_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* a, int64_t as, \
+                                  void* stream);
+B200SP_CONVERT_DECL(double, f64)
+B200SP_CONVERT_DECL(float, f32)
+
+/* ---- generators (replace src/problems.py:11-45 at device scale) --------- */
+int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t n, int32_t* len, void* stream);
+int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t n, const int32_t* rp, int32_t* ci,
+                            double* v, void* stream);
+int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t n, const int32_t* rp, int32_t* ci,
+                            float* v, void* stream);
+int b200sp_powerlaw_lengths(int64_t n, uint64_t seed, const double* thresholds, int32_t max_len, int32_t* len,
+                            void* stream);
+int b200sp_powerlaw_fill_f64(int64_t n, uint64_t seed, const int32_t* rp, int32_t* ci, double* v, void* stream);
+int b200sp_powerlaw_fill_f32(int64_t n, uint64_t seed, const int32_t* rp, int32_t* ci, float* v, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B200SP_H */

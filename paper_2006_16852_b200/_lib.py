@@ -1,0 +1,173 @@
+"""ctypes binding of libb200sp.so (the C ABI declared in include/b200sp.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` /
+``make -C paper_2006_16852_b200/csrc``. There is no CPU fallback: if the
+shared object is missing every kernel call raises KernelNotImplemented.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import KernelNotImplemented, OpalgError, ParameterError, Singular, Unsupported
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libb200sp.so")
+
+# type codes: l=int64 i=int32 u=uint64 p=pointer d=double V=value type of the suffix
+_P = ctypes.c_void_p
+_CT = {"l": ctypes.c_int64, "i": ctypes.c_int32, "u": ctypes.c_uint64, "p": _P,
+       "d": ctypes.c_double}
+
+_SPMV_TAIL = "VpVppl"          # alpha, alpha_dev, beta, beta_dev, x_in, x_in_stride
+_TYPED = {
+    # BLAS-1
+    "fill": "liplVp",
+    "copy": "liplplp",
+    "scale": "liVpplp",
+    "add_scaled": "liVpplplp",
+    "dot": "liplplpppp",
+    "norm2": "liplpppp",
+    # SpMV
+    "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
+    "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
+    "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
+    "rows_scale": "lpplVpplp",
+    "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
+    "sellp_spmv": "lippppplpl" + _SPMV_TAIL + "p",
+    "dense_spmv": "llplplplp",
+    # conversions
+    "csr_to_ell": "lpppllppp",
+    "csr_to_sellp": "lpppippppp",
+    "csr_to_hybrid_coo": "lpppippppp",
+    "ell_to_csr_fill": "lllpppppp",
+    "sellp_to_csr_fill": "lipppppppp",
+    "hybrid_coo_append": "lpppppppp",
+    "dense_row_nnz": "llplpp",
+    "dense_to_csr_fill": "llplpppp",
+    "csr_to_dense": "lpppplp",
+    # generators
+    "stencil_fill": "ildlpppp",
+    "powerlaw_fill": "lupppp",
+}
+_UNTYPED = {
+    "last_error": ("", ctypes.c_char_p),
+    "launch_count": ("", ctypes.c_longlong),
+    "version": ("", ctypes.c_int),
+    "device_sync": ("", ctypes.c_int),
+    "reduce_workspace_elems": ("", ctypes.c_int64),
+    "scan_workspace_elems": ("l", ctypes.c_int64),
+    "exclusive_scan_i32": ("lpppp", ctypes.c_int),
+    "exclusive_scan_i64": ("lpppp", ctypes.c_int),
+    "reduce_max_i32": ("lppp", ctypes.c_int),
+    "csr_lb_num_tiles": ("lli", ctypes.c_int64),
+    "csr_lb_plan": ("llpipp", ctypes.c_int),
+    "csr_row_lengths": ("lppp", ctypes.c_int),
+    "csr_to_coo_rows": ("lppp", ctypes.c_int),
+    "coo_to_csr_ptrs": ("llppp", ctypes.c_int),
+    "sellp_slice_lengths": ("lpiipp", ctypes.c_int),
+    "hybrid_overflow_counts": ("lpipp", ctypes.c_int),
+    "ell_row_lengths": ("lllppp", ctypes.c_int),
+    "sellp_row_lengths": ("lippppp", ctypes.c_int),
+    "add_csr_lengths": ("lppp", ctypes.c_int),
+    "length_histogram": ("lpipp", ctypes.c_int),
+    "empty_row_flags": ("lppp", ctypes.c_int),
+    "compact_flags": ("lpppp", ctypes.c_int),
+    "stencil_lengths": ("illpp", ctypes.c_int),
+    "powerlaw_lengths": ("lupipp", ctypes.c_int),
+}
+
+_lock = threading.Lock()
+_lib = None
+_funcs = {}
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise KernelNotImplemented(
+                f"CUDA extension {LIB_PATH} is missing: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (sig, res) in _UNTYPED.items():
+            fn = getattr(lib, "b200sp_" + name)
+            fn.argtypes = [_CT[c] for c in sig]
+            fn.restype = res
+            _funcs[name] = fn
+        for name, sig in _TYPED.items():
+            for suf, vt in (("f64", ctypes.c_double), ("f32", ctypes.c_float)):
+                fn = getattr(lib, f"b200sp_{name}_{suf}", None)
+                if fn is None:
+                    continue
+                fn.argtypes = [vt if c == "V" else _CT[c] for c in sig]
+                fn.restype = ctypes.c_int
+                _funcs[f"{name}_{suf}"] = fn
+        _lib = lib
+        return lib
+
+
+def available():
+    try:
+        _load()
+        return True
+    except KernelNotImplemented:
+        return False
+
+
+def _raise(code, name):
+    msg = _funcs["last_error"]().decode(errors="replace")
+    text = f"b200sp_{name}: {msg}"
+    if code == 1:
+        raise ParameterError(text)
+    if code == 3:
+        raise Singular(text)
+    if code == 4:
+        raise Unsupported(text)
+    raise OpalgError(text)
+
+
+def call(name, *args):
+    """Invoke b200sp_<name>; raise the mapped error on a non-zero return."""
+    _load()
+    fn = _funcs[name]
+    rc = fn(*args)
+    if fn.restype is ctypes.c_int and rc != 0:
+        _raise(rc, name)
+    return rc
+
+
+def query(name, *args):
+    """Invoke a function returning a value (not an error code)."""
+    _load()
+    return _funcs[name](*args)
+
+
+def launch_count():
+    _load()
+    return int(_funcs["launch_count"]())
+
+
+def suffix(dtype):
+    """'f64' / 'f32' for a torch or numpy float dtype."""
+    s = str(dtype)
+    if s.endswith("float64"):
+        return "f64"
+    if s.endswith("float32"):
+        return "f32"
+    raise Unsupported(f"value type {dtype} (supported: float64, float32)")
+
+
+def exported_symbols():
+    """Every b200sp_* symbol named in include/b200sp.h (for the CPU ABI test)."""
+    names = ["b200sp_" + n for n in _UNTYPED]
+    for n in _TYPED:
+        names += [f"b200sp_{n}_f64", f"b200sp_{n}_f32"]
+    return names

@@ -1,0 +1,20 @@
+"""Configuration knobs (mirror of the reference's src/config.py:1-22).
+
+``DEFAULT_VALUE_DTYPE`` / ``DEFAULT_INDEX_DTYPE`` define the parity contract
+(8-byte values, 4-byte indices). ``OPALG_DEBUG_CONTRACTS`` keeps the
+give-then-use guard of src/ownership.py:37-41 switchable.
+"""
+
+import os
+
+DEFAULT_VALUE_DTYPE = "float64"
+DEFAULT_INDEX_DTYPE = "int32"
+
+#: raise ContractViolation on use after give() (reference src/config.py:13-15)
+debug_contracts = os.environ.get("OPALG_DEBUG_CONTRACTS", "1") != "0"
+
+#: default CUDA device ordinal for CudaExecutor()
+DEFAULT_DEVICE = int(os.environ.get("B200SP_DEVICE", "0"))
+
+#: iterations launched per CUDA-graph batch by the device solvers
+SOLVER_BATCH = int(os.environ.get("B200SP_SOLVER_BATCH", "16"))

@@ -1,0 +1,128 @@
+// Shared device helpers for libb200sp (sm_100a).
+//
+// Everything on this path is HBM-bound integer/FP streaming work: no tensor
+// cores. The helpers here are the B200 building blocks every kernel uses:
+// streaming (L1::no_allocate, read-only) loads for matrix arrays that are
+// touched exactly once per apply, cached read-only loads for the gathered
+// input vector (reused across neighbouring rows through L1/L2), warp-shuffle
+// reductions and the thread-local error string of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/b200sp.h"
+
+namespace b200sp {
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// error plumbing (C ABI returns codes; the message is thread-local)
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+void count_launch(int n = 1);
+
+#define B200SP_CHECK_CUDA(expr)                                              \
+    do {                                                                     \
+        cudaError_t _e = (expr);                                             \
+        if (_e != cudaSuccess) {                                             \
+            ::b200sp::set_error("%s: %s", #expr, cudaGetErrorString(_e));    \
+            return B200SP_ECUDA;                                             \
+        }                                                                    \
+    } while (0)
+
+#define B200SP_REQUIRE(cond, code, ...)                                      \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            ::b200sp::set_error(__VA_ARGS__);                                \
+            return (code);                                                   \
+        }                                                                    \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Grid sized as a multiple of the SM count (grid-stride kernels).
+inline int grid_for(int64_t work_items, int block, int per_sm = 8) {
+    int64_t g = ceil_div(work_items, block);
+    int64_t cap = (int64_t)kNumSMs * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// loads
+// ---------------------------------------------------------------------------
+// Matrix arrays (values, column indices, row pointers) are read exactly once
+// per apply: stream them past L1 so L1 stays free for the x gather.
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// Gathered vector entries: read-only path, allocate in L1 (neighbouring rows
+// of a stencil share most of their columns).
+template <typename T>
+__device__ __forceinline__ T ld_gather(const T* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------------------
+// scalar coefficients: host value or device pointer (device scalars keep the
+// solver loops free of host synchronisation)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Coef {
+    T v;
+    const T* p;
+    __device__ __forceinline__ T get() const { return p ? *p : v; }
+};
+
+// ---------------------------------------------------------------------------
+// warp reductions
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int SW, typename T>
+__device__ __forceinline__ T subwarp_sum(T v) {
+#pragma unroll
+    for (int o = SW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum; result valid in thread 0. `sh` needs blockDim/32 slots.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    T r = 0;
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        r = lane < nw ? sh[lane] : T(0);
+        r = warp_sum(r);
+    }
+    return r;
+}
+
+}  // namespace b200sp

@@ -1,0 +1,651 @@
+// SpMV kernels for every storage format on the path (sm_100a, HBM-bound).
+//
+// Semantics shared by all kernels (one right-hand-side column per launch):
+//     x[i] = alpha * (A b)[i] + beta * x_in[i]        (x_in may be NULL -> 0)
+// which covers LinOp.apply (alpha=1, x_in=NULL; reference src/base.py:60-70),
+// apply_advanced (x_in == x; src/base.py:72-82) and the fused residual
+// r = b - A x (alpha=-1, beta=1, x_in=b; src/kernels.py:243-275).
+//
+// Reference kernels these replace (all host NumPy in the reference):
+//   Csr  -> CsrSpmvKernel + csr_row_sums     src/kernels.py:278-316
+//   Coo  -> CooSpmvKernel / CooAdvSpmvKernel src/kernels.py:163-240
+//   Ell / Sellp / Hybrid have no reference kernel; their results
+//   are pinned through the format-independent SpMV result.
+#include <climits>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace b200sp {
+
+// ===========================================================================
+// Csr, classical strategy: one sub-warp of SW lanes per row (SW = 1..32).
+// ===========================================================================
+template <typename T, int SW, bool XIN>
+__global__ void __launch_bounds__(256)
+csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
+                     const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
+                     T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+                     const T* __restrict__ xin, int64_t xins) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & (SW - 1);
+    const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    for (int64_t row = tid / SW; row < n; row += nsw) {
+        const int s = ld_stream(rp + row);
+        const int e = ld_stream(rp + row + 1);
+        T s0 = 0, s1 = 0;
+        int k = s + lane;
+        // two independent accumulators: two gathers in flight per lane
+        for (; k + SW < e; k += 2 * SW) {
+            const int c0 = ld_stream(ci + k), c1 = ld_stream(ci + k + SW);
+            const T v0 = ld_stream(v + k), v1 = ld_stream(v + k + SW);
+            s0 += v0 * ld_gather(b + (int64_t)c0 * bs);
+            s1 += v1 * ld_gather(b + (int64_t)c1 * bs);
+        }
+        if (k < e) s0 += ld_stream(v + k) * ld_gather(b + (int64_t)ld_stream(ci + k) * bs);
+        T sum = subwarp_sum<SW>(s0 + s1);
+        if (lane == 0) {
+            T r = a * sum;
+            if (XIN) r += bt * xin[row * xins];
+            x[row * xs] = r;
+        }
+    }
+}
+
+template <typename T, int SW>
+static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v, const T* b,
+                             int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be,
+                             const T* xin, int64_t xins, cudaStream_t st) {
+    const int block = 256;
+    int grid = grid_for(n * SW, block, 8);
+    if (xin)
+        csr_classical_kernel<T, SW, true><<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
+    else
+        csr_classical_kernel<T, SW, false><<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
+}
+
+template <typename T>
+static int csr_classical(int64_t n, const int* rp, const int* ci, const T* v, const T* b, int64_t bs,
+                         T* x, int64_t xs, T alpha, const T* alpha_dev, T beta, const T* beta_dev,
+                         const T* xin, int64_t xins, int subwarp, void* stream) {
+    if (n == 0) return B200SP_OK;
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    switch (subwarp) {
+        case 1: launch_classical<T, 1>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        case 2: launch_classical<T, 2>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        case 4: launch_classical<T, 4>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        case 8: launch_classical<T, 8>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        case 16: launch_classical<T, 16>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        case 32: launch_classical<T, 32>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        default: set_error("csr classical: subwarp must be a power of two <= 32 (got %d)", subwarp);
+                 return B200SP_EINVAL;
+    }
+    count_launch();
+    return check_launch("csr_classical");
+}
+
+// ===========================================================================
+// Csr, load-balanced strategy: merge-path decomposition (Merrill & Garland).
+// The merge of the row-end offsets rp[1..n] with the nonzero indices 0..nnz-1
+// is cut into equal tiles of LB_TILE items; each CTA stages its tile's row
+// ends and products in shared memory, every thread consumes LB_IPT items,
+// partial rows are combined with a block-wide segmented scan, and the partial
+// row straddling each tile end is carried out and added by a deterministic
+// fix-up pass. Work per CTA is bounded regardless of row-length skew.
+// ===========================================================================
+constexpr int LB_BLOCK = 256;
+template <typename T> struct LbIpt { static constexpr int v = 7; };
+template <> struct LbIpt<float> { static constexpr int v = 9; };
+
+template <typename T>
+constexpr int lb_tile() { return LB_BLOCK * LbIpt<T>::v; }
+
+// merge-path search: returns number of row-end items (rows) consumed at `diag`
+__device__ __forceinline__ int64_t merge_search_global(int64_t diag, const int* rp, int64_t n,
+                                                       int64_t nnz) {
+    int64_t lo = diag > nnz ? diag - nnz : 0;
+    int64_t hi = diag < n ? diag : n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        // row-end of row `mid` is rp[mid+1]; compare with nonzero index diag-mid-1
+        if ((int64_t)rp[mid + 1] <= diag - mid - 1) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void csr_lb_plan_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp,
+                                   int64_t ntiles, int tile, int* __restrict__ coords) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    int64_t diag = t * (int64_t)tile;
+    if (diag > n + nnz) diag = n + nnz;
+    int64_t r = merge_search_global(diag, rp, n, nnz);
+    coords[2 * t] = (int)r;
+    coords[2 * t + 1] = (int)(diag - r);
+}
+
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(LB_BLOCK)
+csr_lb_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
+              const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+              int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+              const int* __restrict__ coords, int* __restrict__ carry_row,
+              T* __restrict__ carry_val) {
+    constexpr int IPT = LbIpt<T>::v;
+    constexpr int TILE = LB_BLOCK * IPT;
+    __shared__ int s_rowend[TILE];
+    __shared__ T s_prod[TILE];
+    __shared__ T s_wval[LB_BLOCK / 32];
+    __shared__ int s_wflag[LB_BLOCK / 32];
+
+    const int tile = blockIdx.x;
+    const int r0 = coords[2 * tile], k0 = coords[2 * tile + 1];
+    const int r1 = coords[2 * tile + 2], k1 = coords[2 * tile + 3];
+    const int nrows = r1 - r0, nnzt = k1 - k0;
+    const int tid = threadIdx.x;
+
+    // stage row ends and products (coalesced streams, gathered x)
+    for (int i = tid; i < nrows; i += LB_BLOCK) s_rowend[i] = ld_stream(rp + r0 + 1 + i);
+#pragma unroll 4
+    for (int i = tid; i < nnzt; i += LB_BLOCK) {
+        const int k = k0 + i;
+        s_prod[i] = ld_stream(v + k) * ld_gather(b + (int64_t)ld_stream(ci + k) * bs);
+    }
+    __syncthreads();
+
+    // per-thread merge-path search inside the tile
+    const int items = nrows + nnzt;
+    int diag = tid * IPT;
+    if (diag > items) diag = items;
+    int lo = diag > nnzt ? diag - nnzt : 0, hi = diag < nrows ? diag : nrows;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (s_rowend[mid] <= k0 + diag - mid - 1) lo = mid + 1;
+        else hi = mid;
+    }
+    int tr = lo, tk = diag - lo;
+    const int dend = min(diag + IPT, items);
+
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    T acc = 0, first_val = 0;
+    int first_row = -1;
+    for (int d = diag; d < dend; ++d) {
+        if (tk < nnzt && (tr >= nrows || k0 + tk < s_rowend[tr])) {
+            acc += s_prod[tk];
+            ++tk;
+        } else {
+            if (first_row < 0) {
+                first_row = r0 + tr;
+                first_val = acc;
+            } else {
+                const int64_t row = r0 + tr;
+                T out = a * acc;
+                if (XIN) out += bt * xin[row * xins];
+                x[row * xs] = out;
+            }
+            acc = 0;
+            ++tr;
+        }
+    }
+
+    // block-wide segmented inclusive scan of carry-outs; heads = threads with a close
+    const int lane = tid & 31, wid = tid >> 5;
+    T sv = acc;
+    int sf = first_row >= 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T vn = __shfl_up_sync(0xffffffffu, sv, o);
+        int fn = __shfl_up_sync(0xffffffffu, sf, o);
+        if (lane >= o) {
+            if (!sf) sv += vn;
+            sf |= fn;
+        }
+    }
+    if (lane == 31) {
+        s_wval[wid] = sv;
+        s_wflag[wid] = sf;
+    }
+    __syncthreads();
+    // exclusive prefix over previous warps
+    T wpre = 0;
+    for (int w = 0; w < wid; ++w) {
+        if (s_wflag[w]) wpre = s_wval[w];
+        else wpre += s_wval[w];
+    }
+    T incl = sf ? sv : sv + wpre;  // inclusive value for this thread
+    T excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = wpre;
+    if (tid == 0) excl = 0;
+    if (first_row >= 0) {
+        const int64_t row = first_row;
+        T out = a * (first_val + excl);
+        if (XIN) out += bt * xin[row * xins];
+        x[row * xs] = out;
+    }
+    if (tid == LB_BLOCK - 1) {
+        carry_row[tile] = r1;
+        carry_val[tile] = incl;
+    }
+}
+
+// deterministic fix-up: the first tile of each run of equal carry rows adds the
+// whole run (tiles are in row order, so equal rows are adjacent)
+template <typename T>
+__global__ void csr_lb_fixup_kernel(int64_t n, int64_t ntiles, const int* __restrict__ carry_row,
+                                    const T* __restrict__ carry_val, T* __restrict__ x, int64_t xs,
+                                    Coef<T> alpha) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const int row = carry_row[t];
+    if (row >= n) return;
+    if (t > 0 && carry_row[t - 1] == row) return;
+    T sum = carry_val[t];
+    for (int64_t u = t + 1; u < ntiles && carry_row[u] == row; ++u) sum += carry_val[u];
+    x[(int64_t)row * xs] += alpha.get() * sum;
+}
+
+template <typename T>
+static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
+                  int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
+                  const T* beta_dev, const T* xin, int64_t xins, const int* coords,
+                  int* carry_row, T* carry_val, void* stream) {
+    if (n == 0) return B200SP_OK;
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    const int64_t ntiles = ceil_div(n + nnz, lb_tile<T>());
+    if (xin)
+        csr_lb_kernel<T, true><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
+    else
+        csr_lb_kernel<T, false><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
+    csr_lb_fixup_kernel<T><<<(unsigned)ceil_div(ntiles, 256), 256, 0, st>>>(n, ntiles, carry_row, carry_val, x, xs, al);
+    count_launch(2);
+    return check_launch("csr_lb");
+}
+
+// ===========================================================================
+// Coo: warp-chunked segmented reduction over the (row, col)-sorted entries.
+// Each warp owns a contiguous chunk of entries, streams it 32 entries per
+// round (coalesced), reduces equal-row runs with a shuffle scan-by-key and
+// writes every row it owns completely. Rows that straddle a chunk boundary
+// leave per-chunk partials that a fix-up pass sums in chunk order, so the
+// result is deterministic (no floating-point atomics) and needs no pre-zero
+// pass over x.
+// ===========================================================================
+constexpr int COO_BLOCK = 256;
+
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(COO_BLOCK)
+coo_kernel(int64_t nnz, int chunk, const int* __restrict__ rows, const int* __restrict__ cols,
+           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = c * chunk;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(e0 + (int64_t)chunk, nnz);
+    const int head_row = rows[e0], tail_row = rows[e1 - 1];
+    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
+    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+
+    int run_row = INT_MIN;
+    T run = 0;
+    for (int64_t base = e0; base < e1; base += 32) {
+        const int64_t k = base + lane;
+        const bool valid = k < e1;
+        const int r = valid ? ld_stream(rows + k) : INT_MAX;
+        T p = valid ? ld_stream(vals + k) * ld_gather(b + (int64_t)ld_stream(cols + k) * bs) : T(0);
+        // inclusive scan by (sorted) key
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T pn = __shfl_up_sync(0xffffffffu, p, o);
+            int rn = __shfl_up_sync(0xffffffffu, r, o);
+            if (lane >= o && rn == r) p += pn;
+        }
+        if (r == run_row) p += run;
+        int rnext = __shfl_down_sync(0xffffffffu, r, 1);
+        if (lane == 31) rnext = (k + 1 < e1) ? rows[k + 1] : INT_MIN;
+        if (valid && k == e1 - 1) rnext = INT_MIN;
+        const bool is_end = valid && rnext != r;
+        if (is_end) {
+            const bool at_end = (k == e1 - 1);
+            const bool shared = (r == head_row && head_shared) || (at_end && tail_shared);
+            if (!shared) {
+                T out = a * p;
+                if (XIN) out += bt * xin[(int64_t)r * xins];
+                x[(int64_t)r * xs] = out;
+            } else if (r == head_row) {
+                carry_head[c] = p;
+            } else {
+                carry_tail[c] = p;
+            }
+        }
+        run_row = __shfl_sync(0xffffffffu, is_end ? INT_MIN : r, 31);
+        run = __shfl_sync(0xffffffffu, p, 31);
+    }
+}
+
+template <typename T, bool XIN>
+__global__ void coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
+                                 const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
+                                 T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+                                 const T* __restrict__ xin, int64_t xins) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const int64_t e0 = c * chunk, e1 = min(e0 + (int64_t)chunk, nnz);
+    const int head_row = rows[e0], tail_row = rows[e1 - 1];
+    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
+    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+    const bool single = head_row == tail_row;
+    if (!tail_shared || (single && head_shared)) return;  // not the owner of a shared row
+    T sum = single ? carry_head[c] : carry_tail[c];
+    for (int64_t u = c + 1; u < nchunks; ++u) {
+        sum += carry_head[u];
+        const int64_t f0 = u * chunk, f1 = min(f0 + (int64_t)chunk, nnz);
+        const bool u_single = rows[f0] == rows[f1 - 1];
+        const bool u_tail_shared = f1 < nnz && rows[f1] == rows[f1 - 1];
+        if (!(u_single && u_tail_shared)) break;
+    }
+    T out = alpha.get() * sum;
+    if (XIN) out += beta.get() * xin[(int64_t)tail_row * xins];
+    x[(int64_t)tail_row * xs] = out;
+}
+
+template <typename T>
+static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, const T* vals,
+                    const T* b, int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
+                    const T* beta_dev, const T* xin, int64_t xins, T* carry_head, T* carry_tail,
+                    void* stream) {
+    if (nnz == 0) return B200SP_OK;
+    B200SP_REQUIRE(chunk > 0 && chunk % 32 == 0, B200SP_EINVAL, "coo: chunk must be a positive multiple of 32");
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    const int64_t nchunks = ceil_div(nnz, chunk);
+    const int64_t threads = nchunks * 32;
+    const unsigned grid = (unsigned)ceil_div(threads, COO_BLOCK);
+    const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
+    if (xin) {
+        coo_kernel<T, true><<<grid, COO_BLOCK, 0, st>>>(nnz, chunk, rows, cols, vals, b, bs, x, xs, al, be, xin, xins, carry_head, carry_tail);
+        coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nnz, chunk, nchunks, rows, carry_head, carry_tail, x, xs, al, be, xin, xins);
+    } else {
+        coo_kernel<T, false><<<grid, COO_BLOCK, 0, st>>>(nnz, chunk, rows, cols, vals, b, bs, x, xs, al, be, xin, xins, carry_head, carry_tail);
+        coo_fixup_kernel<T, false><<<fgrid, 256, 0, st>>>(nnz, chunk, nchunks, rows, carry_head, carry_tail, x, xs, al, be, xin, xins);
+    }
+    count_launch(2);
+    return check_launch("coo_spmv");
+}
+
+// x[rows[i]] = beta * x_in[rows[i]] (or 0): rows that hold no entry
+template <typename T>
+__global__ void rows_scale_kernel(int64_t count, const int* __restrict__ rows, T* __restrict__ x,
+                                  int64_t xs, Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t r = rows[i];
+    x[r * xs] = xin ? beta.get() * xin[r * xins] : T(0);
+}
+
+template <typename T>
+static int rows_scale(int64_t count, const int* rows, T* x, int64_t xs, T beta, const T* beta_dev,
+                      const T* xin, int64_t xins, void* stream) {
+    if (count == 0) return B200SP_OK;
+    rows_scale_kernel<T><<<(unsigned)ceil_div(count, 256), 256, 0, as_stream(stream)>>>(
+        count, rows, x, xs, Coef<T>{beta, beta_dev}, xin, xins);
+    count_launch();
+    return check_launch("rows_scale");
+}
+
+// ===========================================================================
+// Ell: column-major (stride >= n), one thread per row, padding col = -1.
+// Consecutive threads read consecutive addresses of every stored column.
+// ===========================================================================
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(256)
+ell_kernel(int64_t n, int64_t width, int64_t stride, const int* __restrict__ ci,
+           const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        T s0 = 0, s1 = 0;
+        int64_t k = 0;
+        for (; k + 1 < width; k += 2) {
+            const int c0 = ld_stream(ci + k * stride + row), c1 = ld_stream(ci + (k + 1) * stride + row);
+            const T v0 = ld_stream(v + k * stride + row), v1 = ld_stream(v + (k + 1) * stride + row);
+            if (c0 >= 0) s0 += v0 * ld_gather(b + (int64_t)c0 * bs);
+            if (c1 >= 0) s1 += v1 * ld_gather(b + (int64_t)c1 * bs);
+        }
+        if (k < width) {
+            const int c0 = ld_stream(ci + k * stride + row);
+            if (c0 >= 0) s0 += ld_stream(v + k * stride + row) * ld_gather(b + (int64_t)c0 * bs);
+        }
+        T out = a * (s0 + s1);
+        if (XIN) out += bt * xin[row * xins];
+        x[row * xs] = out;
+    }
+}
+
+template <typename T>
+static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, const T* v, const T* b,
+                    int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
+                    const T* beta_dev, const T* xin, int64_t xins, void* stream) {
+    if (n == 0) return B200SP_OK;
+    B200SP_REQUIRE(stride >= n, B200SP_EINVAL, "ell: stride %lld < rows %lld", (long long)stride, (long long)n);
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    const int grid = grid_for(n, 256, 16);
+    if (xin)
+        ell_kernel<T, true><<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
+    else
+        ell_kernel<T, false><<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
+    count_launch();
+    return check_launch("ell_spmv");
+}
+
+// ===========================================================================
+// Sellp: slices of `slice_size` rows, each stored column-major with its own
+// length (slice_sets = exclusive prefix of slice lengths). Thread per row.
+// ===========================================================================
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(256)
+sellp_kernel(int64_t n, int slice_size, const int* __restrict__ slice_lengths,
+             const int* __restrict__ slice_sets, const int* __restrict__ ci, const T* __restrict__ v,
+             const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha,
+             Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slice = row / slice_size;
+        const int64_t local = row - slice * slice_size;
+        const int len = slice_lengths[slice];
+        const int64_t base = (int64_t)slice_sets[slice] * slice_size + local;
+        T s0 = 0, s1 = 0;
+        int k = 0;
+        for (; k + 1 < len; k += 2) {
+            const int64_t i0 = base + (int64_t)k * slice_size, i1 = i0 + slice_size;
+            const int c0 = ld_stream(ci + i0), c1 = ld_stream(ci + i1);
+            const T v0 = ld_stream(v + i0), v1 = ld_stream(v + i1);
+            if (c0 >= 0) s0 += v0 * ld_gather(b + (int64_t)c0 * bs);
+            if (c1 >= 0) s1 += v1 * ld_gather(b + (int64_t)c1 * bs);
+        }
+        if (k < len) {
+            const int64_t i0 = base + (int64_t)k * slice_size;
+            const int c0 = ld_stream(ci + i0);
+            if (c0 >= 0) s0 += ld_stream(v + i0) * ld_gather(b + (int64_t)c0 * bs);
+        }
+        T out = a * (s0 + s1);
+        if (XIN) out += bt * xin[row * xins];
+        x[row * xs] = out;
+    }
+}
+
+template <typename T>
+static int sellp_spmv(int64_t n, int slice_size, const int* sl, const int* ss, const int* ci,
+                      const T* v, const T* b, int64_t bs, T* x, int64_t xs, T alpha,
+                      const T* alpha_dev, T beta, const T* beta_dev, const T* xin, int64_t xins,
+                      void* stream) {
+    if (n == 0) return B200SP_OK;
+    B200SP_REQUIRE(slice_size > 0, B200SP_EINVAL, "sellp: slice_size must be positive");
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    const int grid = grid_for(n, 256, 16);
+    if (xin)
+        sellp_kernel<T, true><<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
+    else
+        sellp_kernel<T, false><<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
+    count_launch();
+    return check_launch("sellp_spmv");
+}
+
+// ===========================================================================
+// Dense (n, k) row-major times b: warp per row (DenseSpmvKernel,
+// src/kernels.py:319-332; small operators only, not a performance target)
+// ===========================================================================
+template <typename T>
+__global__ void dense_spmv_kernel(int64_t n, int64_t k, const T* __restrict__ a, int64_t as,
+                                  const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+        T s = 0;
+        for (int64_t j = lane; j < k; j += 32) s += a[r * as + j] * b[j * bs];
+        s = warp_sum(s);
+        if (lane == 0) x[r * xs] = s;
+    }
+}
+
+template <typename T>
+static int dense_spmv(int64_t n, int64_t k, const T* a, int64_t as, const T* b, int64_t bs, T* x,
+                      int64_t xs, void* stream) {
+    if (n == 0) return B200SP_OK;
+    dense_spmv_kernel<T><<<grid_for(n * 32, 256, 8), 256, 0, as_stream(stream)>>>(n, k, a, as, b, bs, x, xs);
+    count_launch();
+    return check_launch("dense_spmv");
+}
+
+}  // namespace b200sp
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace b200sp;
+
+#define SPMV_TAIL_ARGS(T) T alpha, const T *alpha_dev, T beta, const T *beta_dev, const T *x_in, int64_t x_in_stride, void *stream
+
+extern "C" {
+
+int b200sp_csr_spmv_classical_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+                                  const double* b, int64_t bs, double* x, int64_t xs, double alpha,
+                                  const double* alpha_dev, double beta, const double* beta_dev,
+                                  const double* xin, int64_t xins, int32_t subwarp, void* stream) {
+    return csr_classical<double>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, subwarp, stream);
+}
+int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v,
+                                  const float* b, int64_t bs, float* x, int64_t xs, float alpha,
+                                  const float* alpha_dev, float beta, const float* beta_dev,
+                                  const float* xin, int64_t xins, int32_t subwarp, void* stream) {
+    return csr_classical<float>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, subwarp, stream);
+}
+
+int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes) {
+    const int tile = value_bytes == 4 ? lb_tile<float>() : lb_tile<double>();
+    return ceil_div(n + nnz, tile);
+}
+
+int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* rp, int32_t value_bytes,
+                       int32_t* coords, void* stream) {
+    const int tile = value_bytes == 4 ? lb_tile<float>() : lb_tile<double>();
+    const int64_t ntiles = ceil_div(n + nnz, tile);
+    csr_lb_plan_kernel<<<(unsigned)ceil_div(ntiles + 1, 256), 256, 0, as_stream(stream)>>>(
+        n, nnz, rp, ntiles, tile, coords);
+    count_launch();
+    return check_launch("csr_lb_plan");
+}
+
+int b200sp_csr_spmv_lb_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci,
+                           const double* v, const double* b, int64_t bs, double* x, int64_t xs,
+                           double alpha, const double* alpha_dev, double beta,
+                           const double* beta_dev, const double* xin, int64_t xins,
+                           const int32_t* coords, int32_t* carry_row, double* carry_val,
+                           void* stream) {
+    return csr_lb<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords, carry_row, carry_val, stream);
+}
+int b200sp_csr_spmv_lb_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci,
+                           const float* v, const float* b, int64_t bs, float* x, int64_t xs,
+                           float alpha, const float* alpha_dev, float beta, const float* beta_dev,
+                           const float* xin, int64_t xins, const int32_t* coords,
+                           int32_t* carry_row, float* carry_val, void* stream) {
+    return csr_lb<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords, carry_row, carry_val, stream);
+}
+
+int b200sp_coo_spmv_f64(int64_t nnz, int32_t chunk, const int32_t* rows, const int32_t* cols,
+                        const double* vals, const double* b, int64_t bs, double* x, int64_t xs,
+                        double alpha, const double* alpha_dev, double beta, const double* beta_dev,
+                        const double* xin, int64_t xins, double* carry_head, double* carry_tail,
+                        void* stream) {
+    return coo_spmv<double>(nnz, chunk, rows, cols, vals, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, carry_head, carry_tail, stream);
+}
+int b200sp_coo_spmv_f32(int64_t nnz, int32_t chunk, const int32_t* rows, const int32_t* cols,
+                        const float* vals, const float* b, int64_t bs, float* x, int64_t xs,
+                        float alpha, const float* alpha_dev, float beta, const float* beta_dev,
+                        const float* xin, int64_t xins, float* carry_head, float* carry_tail,
+                        void* stream) {
+    return coo_spmv<float>(nnz, chunk, rows, cols, vals, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, carry_head, carry_tail, stream);
+}
+
+int b200sp_rows_scale_f64(int64_t count, const int32_t* rows, double* x, int64_t xs, double beta,
+                          const double* beta_dev, const double* xin, int64_t xins, void* stream) {
+    return rows_scale<double>(count, rows, x, xs, beta, beta_dev, xin, xins, stream);
+}
+int b200sp_rows_scale_f32(int64_t count, const int32_t* rows, float* x, int64_t xs, float beta,
+                          const float* beta_dev, const float* xin, int64_t xins, void* stream) {
+    return rows_scale<float>(count, rows, x, xs, beta, beta_dev, xin, xins, stream);
+}
+
+int b200sp_ell_spmv_f64(int64_t n, int64_t width, int64_t stride, const int32_t* ci, const double* v,
+                        const double* b, int64_t bs, double* x, int64_t xs, double alpha,
+                        const double* alpha_dev, double beta, const double* beta_dev,
+                        const double* xin, int64_t xins, void* stream) {
+    return ell_spmv<double>(n, width, stride, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, stream);
+}
+int b200sp_ell_spmv_f32(int64_t n, int64_t width, int64_t stride, const int32_t* ci, const float* v,
+                        const float* b, int64_t bs, float* x, int64_t xs, float alpha,
+                        const float* alpha_dev, float beta, const float* beta_dev, const float* xin,
+                        int64_t xins, void* stream) {
+    return ell_spmv<float>(n, width, stride, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, stream);
+}
+
+int b200sp_sellp_spmv_f64(int64_t n, int32_t slice_size, const int32_t* slice_lengths,
+                          const int32_t* slice_sets, const int32_t* ci, const double* v,
+                          const double* b, int64_t bs, double* x, int64_t xs, double alpha,
+                          const double* alpha_dev, double beta, const double* beta_dev,
+                          const double* xin, int64_t xins, void* stream) {
+    return sellp_spmv<double>(n, slice_size, slice_lengths, slice_sets, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, stream);
+}
+int b200sp_sellp_spmv_f32(int64_t n, int32_t slice_size, const int32_t* slice_lengths,
+                          const int32_t* slice_sets, const int32_t* ci, const float* v,
+                          const float* b, int64_t bs, float* x, int64_t xs, float alpha,
+                          const float* alpha_dev, float beta, const float* beta_dev,
+                          const float* xin, int64_t xins, void* stream) {
+    return sellp_spmv<float>(n, slice_size, slice_lengths, slice_sets, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, stream);
+}
+
+int b200sp_dense_spmv_f64(int64_t n, int64_t k, const double* a, int64_t as, const double* b, int64_t bs,
+                         double* x, int64_t xs, void* stream) {
+    return dense_spmv<double>(n, k, a, as, b, bs, x, xs, stream);
+}
+int b200sp_dense_spmv_f32(int64_t n, int64_t k, const float* a, int64_t as, const float* b, int64_t bs,
+                         float* x, int64_t xs, void* stream) {
+    return dense_spmv<float>(n, k, a, as, b, bs, x, xs, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,984 @@
+"""Matrix formats on the device: Dense, Csr, Coo, Ell, Sellp, Hybrid.
+
+API mirror of the reference's src/formats.py:21-329 (MatrixData interchange,
+Dense doubling as the vector type, Csr/Coo with from_data / to_data /
+convert_to / clone_to, ``convert`` and ``matrix_from_data``) extended with the
+formats the paper names but the reference omits: Ell, Sellp,
+Hybrid, and the Csr strategies ``classical`` / ``load_balance``.
+
+Storage lives in HBM as torch tensors; every numeric operation is an
+sm_100a kernel of libb200sp. Conversions use Csr as the hub and run on the
+device (two-phase: size query, fill). ``MatrixData`` is the host interchange
+form (file I/O, assembly) exactly as in the reference.
+"""
+
+from __future__ import annotations
+
+import copy
+import math
+
+import numpy as np
+
+from . import _lib, config
+from .base import Dim2, LinOp
+from .errors import DimensionMismatch, Unsupported
+from .executor import CudaExecutor, DeviceView, HostExecutor, ptr
+from .kernels import AddScaledOp, CopyOp, DotOp, FillOp, ScaleOp, SpmvOp
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+def _np_vt(value_dtype):
+    dt = np.dtype(value_dtype or config.DEFAULT_VALUE_DTYPE)
+    if dt not in (np.dtype("float64"), np.dtype("float32")):
+        raise Unsupported(f"value type {dt} (supported: float64, float32)")
+    return dt
+
+
+def _torch_vt(np_dt):
+    return torch.float64 if np.dtype(np_dt) == np.float64 else torch.float32
+
+
+def _check_index_dtype(index_dtype):
+    if index_dtype is not None and np.dtype(index_dtype) != np.dtype("int32"):
+        raise Unsupported("this backend stores 32-bit indices (DEFAULT_INDEX_DTYPE)")
+
+
+def _to_device(exc, arr, torch_dtype):
+    if torch is not None and isinstance(arr, torch.Tensor):
+        return arr.to(device=exc.device, dtype=torch_dtype).contiguous()
+    if isinstance(arr, DeviceView):
+        return arr.tensor.to(dtype=torch_dtype).contiguous()
+    a = np.ascontiguousarray(np.asarray(arr))
+    t = torch.from_numpy(a).to(torch_dtype) if a.size else torch.empty(a.shape, dtype=torch_dtype)
+    return t.to(exc.device)
+
+
+def _scan(exc, counts):
+    """Exclusive scan of int32 counts -> int32 tensor of len+1 (total last)."""
+    n = counts.numel()
+    out = torch.empty(n + 1, dtype=torch.int32, device=exc.device)
+    ws = torch.empty(max(1, int(_lib.query("scan_workspace_elems", n))), dtype=torch.int64,
+                     device=exc.device)
+    _lib.call("exclusive_scan_i32", n, ptr(counts), ptr(out), ptr(ws), exc.stream)
+    return out
+
+
+def _max_i32(exc, t):
+    out = torch.empty(1, dtype=torch.int32, device=exc.device)
+    _lib.call("reduce_max_i32", t.numel(), ptr(t), ptr(out), exc.stream)
+    return int(out.item())
+
+
+def _require_cuda(exc):
+    if not isinstance(exc, CudaExecutor):
+        raise Unsupported("sparse matrices live on a CudaExecutor "
+                          "(the host arena runs no numeric kernels)")
+
+
+# ---------------------------------------------------------------------------
+# MatrixData (host interchange; src/formats.py:21-64)
+# ---------------------------------------------------------------------------
+class MatrixData:
+    """Size plus coordinate triples; canonical order is (row, col) with
+    duplicates summed in their original order (src/formats.py:40-53)."""
+
+    def __init__(self, size, rows=(), cols=(), vals=()):
+        self.size = size if isinstance(size, Dim2) else Dim2(*size)
+        self.rows = np.asarray(rows, dtype=np.int64).reshape(-1)
+        self.cols = np.asarray(cols, dtype=np.int64).reshape(-1)
+        self.vals = np.asarray(vals, dtype=np.float64).reshape(-1)
+        if not (self.rows.size == self.cols.size == self.vals.size):
+            raise DimensionMismatch("triple arrays must have equal length")
+
+    @property
+    def nnz(self):
+        return int(self.vals.size)
+
+    def is_canonical(self):
+        if self.nnz < 2:
+            return True
+        key_ok = (self.rows[1:] > self.rows[:-1]) | (
+            (self.rows[1:] == self.rows[:-1]) & (self.cols[1:] > self.cols[:-1]))
+        return bool(key_ok.all())
+
+    def canonicalize(self):
+        if self.nnz == 0:
+            return MatrixData(self.size)
+        if self.is_canonical():
+            return MatrixData(self.size, self.rows, self.cols, self.vals)
+        order = np.lexsort((self.cols, self.rows))
+        r, c, v = self.rows[order], self.cols[order], self.vals[order]
+        first = np.ones(r.size, dtype=bool)
+        first[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+        if not first.all():
+            grp = np.cumsum(first) - 1
+            acc = np.zeros(int(grp[-1]) + 1, dtype=np.float64)
+            np.add.at(acc, grp, v)
+            r, c, v = r[first], c[first], acc
+        return MatrixData(self.size, r, c, v)
+
+    def to_dense_array(self):
+        out = np.zeros(tuple(self.size), dtype=np.float64)
+        np.add.at(out, (self.rows, self.cols), self.vals)
+        return out
+
+    @classmethod
+    def from_dense_array(cls, arr, drop_zeros=True):
+        arr = np.asarray(arr, dtype=np.float64)
+        if drop_zeros:
+            r, c = np.nonzero(arr)
+        else:
+            r, c = np.indices(arr.shape).reshape(2, -1)
+        return cls(Dim2(*arr.shape), r, c, arr[r, c])
+
+
+# ---------------------------------------------------------------------------
+# Dense (src/formats.py:67-158)
+# ---------------------------------------------------------------------------
+class Dense(LinOp):
+    """Row-major (rows, cols) block; doubles as the multi-column vector type.
+
+    ``values`` is the storage (torch tensor on a CudaExecutor, numpy array on
+    the host arena); ``data`` is numpy-compatible in both cases (a
+    synchronising DeviceView for device storage)."""
+
+    is_dense = True
+
+    def __init__(self, exc, data=None, size=None, value_dtype=None):
+        if data is not None:
+            if torch is not None and isinstance(data, torch.Tensor):
+                vt = _np_vt(value_dtype or str(data.dtype).replace("torch.", ""))
+                t = data if data.dim() == 2 else data.reshape(1, -1)
+                vals = self._adopt(exc, t, vt)
+            else:
+                vt = _np_vt(value_dtype)
+                arr = np.array(data, dtype=vt, ndmin=2)
+                vals = self._adopt(exc, arr, vt)
+        else:
+            vt = _np_vt(value_dtype)
+            vals = exc.alloc(tuple(int(s) for s in size), vt.name)
+        super().__init__(exc, Dim2(*vals.shape))
+        self.values = vals
+
+    @staticmethod
+    def _adopt(exc, arr, vt):
+        if isinstance(exc, CudaExecutor):
+            return _to_device(exc, arr, _torch_vt(vt))
+        if torch is not None and isinstance(arr, torch.Tensor):
+            arr = arr.detach().cpu().numpy()
+        out = exc.alloc(arr.shape, vt.name)
+        out[...] = arr
+        return out
+
+    # -- storage views -----------------------------------------------------
+    @property
+    def on_device(self):
+        return isinstance(self.exec, CudaExecutor)
+
+    @property
+    def data(self):
+        return DeviceView(self.values) if self.on_device else self.values
+
+    @property
+    def dtype(self):
+        return np.dtype(str(self.values.dtype).replace("torch.", ""))
+
+    @property
+    def stride(self):
+        if self.on_device:
+            return self.values.stride(0)
+        return self.values.strides[0] // self.values.itemsize
+
+    # -- constructors --------------------------------------------------------
+    @classmethod
+    def zeros(cls, exc, rows, cols=1, value_dtype=None):
+        out = cls(exc, size=(rows, cols), value_dtype=value_dtype)
+        out.fill(0.0)
+        return out
+
+    @classmethod
+    def vector(cls, exc, values, value_dtype=None):
+        if torch is not None and isinstance(values, torch.Tensor):
+            return cls(exc, values.reshape(-1, 1), value_dtype=value_dtype)
+        arr = np.asarray(values, dtype=_np_vt(value_dtype))
+        return cls(exc, arr.reshape(-1, 1), value_dtype=value_dtype)
+
+    @classmethod
+    def wrap(cls, exc, arr):
+        """Dense view over existing storage (no copy); arr is a 2-D tensor
+        (device) or ndarray (host)."""
+        obj = cls.__new__(cls)
+        LinOp.__init__(obj, exc, Dim2(*arr.shape))
+        obj.values = arr
+        return obj
+
+    def like(self, rows, cols):
+        return Dense(self.exec, size=(rows, cols), value_dtype=self.dtype)
+
+    def empty_like_on(self, target):
+        return Dense(target, size=tuple(self.size), value_dtype=self.dtype)
+
+    def column(self, j):
+        """(n, 1) view of column j (no copy)."""
+        return Dense.wrap(self.exec, self.values[:, j:j + 1])
+
+    def clone_to(self, target):
+        out = Dense(target, size=tuple(self.size), value_dtype=self.dtype)
+        out.copy_from(self)
+        return out
+
+    def to_numpy(self):
+        return np.asarray(self.data).copy()
+
+    # -- BLAS-1 (kernels; src/formats.py:121-147) ----------------------------
+    def fill(self, value=0.0):
+        self.exec.run(FillOp(self, value))
+
+    def copy_from(self, other):
+        """self <- other (same shape); handles host<->device migration."""
+        if other.exec is self.exec:
+            self.exec.run(CopyOp(other, self))
+            return
+        src, dst = other.values, self.values
+        if self.on_device and other.on_device:
+            dst.copy_(src)
+        elif self.on_device:  # H2D (pinned source -> async on the current stream)
+            dst.copy_(torch.from_numpy(np.asarray(src)), non_blocking=True)
+        elif other.on_device:  # D2H into the host arena; synchronous on return
+            host = torch.from_numpy(dst) if dst.flags.c_contiguous else None
+            if host is not None:
+                host.copy_(src, non_blocking=True)
+                torch.cuda.current_stream(src.device).synchronize()
+            else:
+                dst[...] = src.detach().cpu().numpy()
+        else:
+            dst[...] = src
+
+    def scale(self, alpha):
+        self.exec.run(ScaleOp(alpha, self))
+
+    def add_scaled(self, alpha, x):
+        self.exec.run(AddScaledOp(alpha, x, self))
+
+    def compute_dot(self, other, out):
+        self.exec.run(DotOp(self, other, out))
+
+    def compute_norm2(self, out):
+        self.exec.run(DotOp(self, self, out, norm=True))
+
+    def dot(self, other):
+        out = self.like(1, self.size.cols)
+        self.compute_dot(other, out)
+        return np.asarray(out.data)[0].copy()
+
+    def norm2(self):
+        out = self.like(1, self.size.cols)
+        self.compute_norm2(out)
+        return np.asarray(out.data)[0].copy()
+
+    # -- operator interface ------------------------------------------------------
+    def _apply_impl(self, b, x):
+        self.exec.run(SpmvOp(self, b, x))
+
+    def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):
+        a = self.values
+        if a_p or xin or a_h != 1.0:
+            raise Unsupported("Dense advanced apply goes through the generic path")
+        _lib.call("dense_spmv_" + suf, a.shape[0], a.shape[1], ptr(a), a.stride(0), bp, bs, xp, xs,
+                  exc.stream)
+
+    def convert_to(self, kind):
+        return convert(self, kind)
+
+    def to_data(self):
+        return MatrixData.from_dense_array(np.asarray(self.data))
+
+    def _to_csr(self, **kw):
+        _require_cuda(self.exec)
+        exc, a = self.exec, self.values
+        n, k = a.shape
+        suf = _lib.suffix(a.dtype)
+        lens = torch.empty(n, dtype=torch.int32, device=exc.device)
+        _lib.call("dense_row_nnz_" + suf, n, k, ptr(a), a.stride(0), ptr(lens), exc.stream)
+        rp = _scan(exc, lens)
+        nnz = int(rp[-1].item())
+        ci = torch.empty(nnz, dtype=torch.int32, device=exc.device)
+        v = torch.empty(nnz, dtype=a.dtype, device=exc.device)
+        _lib.call("dense_to_csr_fill_" + suf, n, k, ptr(a), a.stride(0), ptr(rp), ptr(ci), ptr(v),
+                  exc.stream)
+        return Csr._from_device(exc, Dim2(n, k), rp, ci, v, **kw)
+
+    @classmethod
+    def _from_csr(cls, csr, **_):
+        exc = csr.exec
+        out = cls.zeros(exc, csr.size.rows, csr.size.cols, value_dtype=csr.value_dtype)
+        a = out.values
+        _lib.call("csr_to_dense_" + _lib.suffix(a.dtype), csr.size.rows, ptr(csr._rp), ptr(csr._ci),
+                  ptr(csr._v), ptr(a), a.stride(0), exc.stream)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# sparse base
+# ---------------------------------------------------------------------------
+class _Sparse(LinOp):
+    def __init__(self, exc, size):
+        _require_cuda(exc)
+        super().__init__(exc, size)
+
+    @property
+    def value_dtype(self):
+        return np.dtype(str(self._v.dtype).replace("torch.", ""))
+
+    def _apply_impl(self, b, x):
+        self.exec.run(SpmvOp(self, b, x))
+
+    def _apply_advanced_impl(self, alpha, b, beta, x):
+        self.exec.run(SpmvOp(self, b, x, alpha=alpha, beta=beta, x_in=x))
+
+    def residual(self, x, b, r):
+        """r <- b - A x in one fused launch per column (CooResidualKernel,
+        src/kernels.py:243-275, generalised to every format)."""
+        self.exec.run(SpmvOp(self, x, r, alpha=-1.0, beta=1.0, x_in=b))
+
+    def convert_to(self, kind, **kw):
+        return convert(self, kind, **kw)
+
+    @classmethod
+    def from_data(cls, exc, data, **kw):
+        csr = Csr._from_host_data(exc, data, kw.pop("value_dtype", None),
+                                  kw.pop("index_dtype", None))
+        return csr if cls is Csr and not kw else cls._from_csr(csr, **kw)
+
+    def to_data(self):
+        return self._to_csr().to_data()
+
+    def clone_to(self, target):
+        """Deep copy with identical apply behaviour on ``target``."""
+        _require_cuda(target)
+        obj = copy.copy(self)
+        LinOp.__init__(obj, target, self.size)
+        for name, val in vars(self).items():
+            if torch is not None and isinstance(val, torch.Tensor):
+                setattr(obj, name, val.clone().to(target.device))
+            elif isinstance(val, _Sparse):
+                setattr(obj, name, val.clone_to(target))
+        for cache in ("_plan", "_ws"):
+            if hasattr(obj, cache):
+                setattr(obj, cache, None)
+        return obj
+
+
+# ---------------------------------------------------------------------------
+# Csr (src/formats.py:168-221) + strategies
+# ---------------------------------------------------------------------------
+CSR_STRATEGIES = ("classical", "load_balance", "automatic")
+
+
+class Csr(_Sparse):
+    """Compressed sparse row with an SpMV strategy:
+
+    * ``classical``    -- sub-warp per row (sub-warp = next power of two of
+                          the longest row, capped at 32; Ginkgo's classical);
+    * ``load_balance`` -- merge-path tiles of equal (rows + nonzeros) work
+                          with a deterministic carry fix-up;
+    * ``automatic``    -- classical unless the row lengths are skewed
+                          (max > 4 x mean + 64), then load_balance.
+    """
+
+    def __init__(self, exc, size, row_ptrs, col_idxs, vals, index_dtype=None, value_dtype=None,
+                 strategy="automatic"):
+        super().__init__(exc, size)
+        _check_index_dtype(index_dtype)
+        vt = _np_vt(value_dtype or (getattr(vals, "dtype", None) if not isinstance(vals, (list, tuple))
+                                    else None) or config.DEFAULT_VALUE_DTYPE)
+        host_check = not (torch is not None and isinstance(row_ptrs, torch.Tensor))
+        if host_check:
+            rp_h = np.asarray(row_ptrs, dtype=np.int64).reshape(-1)
+            ci_h = np.asarray(col_idxs, dtype=np.int64).reshape(-1)
+            nv = np.asarray(vals).size
+            self._check_structure(rp_h, ci_h, nv)
+        self._rp = _to_device(exc, row_ptrs, torch.int32)
+        self._ci = _to_device(exc, col_idxs, torch.int32)
+        self._v = _to_device(exc, vals, _torch_vt(vt))
+        self._set_strategy(strategy)
+
+    def _check_structure(self, rp, ci, nvals):
+        rows, cols = self.size
+        if rp.size != rows + 1 or rp[0] != 0 or rp[-1] != nvals:
+            raise DimensionMismatch("bad row_ptrs")
+        if np.any(np.diff(rp) < 0):
+            raise DimensionMismatch("row_ptrs must be non-decreasing")
+        if ci.size and (ci.min() < 0 or ci.max() >= cols):
+            raise DimensionMismatch("column index out of range")
+        if rp[-1] >= 2 ** 31:
+            raise Unsupported("more than 2^31-1 stored entries need 64-bit indices")
+
+    @classmethod
+    def _from_device(cls, exc, size, rp, ci, v, strategy="automatic"):
+        obj = cls.__new__(cls)
+        _Sparse.__init__(obj, exc, size)
+        obj._rp, obj._ci, obj._v = rp, ci, v
+        obj._set_strategy(strategy)
+        return obj
+
+    @classmethod
+    def _from_host_data(cls, exc, data, value_dtype=None, index_dtype=None):
+        _require_cuda(exc)
+        _check_index_dtype(index_dtype)
+        data = data.canonicalize()
+        n = data.size.rows
+        counts = np.bincount(data.rows, minlength=n) if data.nnz else np.zeros(n, np.int64)
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(counts, out=rp[1:])
+        return cls(exc, data.size, rp, data.cols, data.vals, value_dtype=value_dtype)
+
+    # -- strategy ----------------------------------------------------------------
+    def _set_strategy(self, strategy):
+        if strategy not in CSR_STRATEGIES:
+            raise Unsupported(f"csr strategy {strategy!r} (known: {CSR_STRATEGIES})")
+        self._requested = strategy
+        self._plan = None      # (coords, carry_row, carry_val) for load_balance
+        self._subwarp = None
+        self._max_row = None
+
+    @property
+    def strategy(self):
+        return self._resolved_strategy()
+
+    def set_strategy(self, strategy):
+        self._set_strategy(strategy)
+
+    def _row_stats(self):
+        if self._max_row is None:
+            n = self.size.rows
+            if n == 0:
+                self._max_row = 0
+            else:
+                lens = torch.empty(n, dtype=torch.int32, device=self.exec.device)
+                _lib.call("csr_row_lengths", n, ptr(self._rp), ptr(lens), self.exec.stream)
+                self._max_row = _max_i32(self.exec, lens)
+        return self._max_row
+
+    def _resolved_strategy(self):
+        if self._requested != "automatic":
+            return self._requested
+        n = self.size.rows
+        if n == 0:
+            return "classical"
+        mean = self.nnz / n
+        return "load_balance" if self._row_stats() > 4 * mean + 64 else "classical"
+
+    def subwarp(self):
+        if self._subwarp is None:
+            longest = max(1, self._row_stats())
+            self._subwarp = min(32, 1 << (longest - 1).bit_length())
+        return self._subwarp
+
+    def lb_plan(self):
+        if self._plan is None:
+            exc = self.exec
+            n, nnz = self.size.rows, self.nnz
+            vb = self._v.element_size()
+            nt = int(_lib.query("csr_lb_num_tiles", n, nnz, vb))
+            coords = torch.empty(2 * (nt + 1), dtype=torch.int32, device=exc.device)
+            _lib.call("csr_lb_plan", n, nnz, ptr(self._rp), vb, ptr(coords), exc.stream)
+            carry_row = torch.empty(max(nt, 1), dtype=torch.int32, device=exc.device)
+            carry_val = torch.empty(max(nt, 1), dtype=self._v.dtype, device=exc.device)
+            self._plan = (coords, carry_row, carry_val)
+        return self._plan
+
+    # -- attributes (reference names) --------------------------------------------
+    @property
+    def nnz(self):
+        return int(self._v.numel())
+
+    @property
+    def row_ptrs(self):
+        return DeviceView(self._rp)
+
+    @property
+    def col_idxs(self):
+        return DeviceView(self._ci)
+
+    @property
+    def vals(self):
+        return DeviceView(self._v)
+
+    # -- kernels -------------------------------------------------------------------
+    def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):
+        n = self.size.rows
+        if self._resolved_strategy() == "load_balance":
+            coords, crow, cval = self.lb_plan()
+            _lib.call("csr_spmv_lb_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
+                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(coords), ptr(crow),
+                      ptr(cval), exc.stream)
+        else:
+            _lib.call("csr_spmv_classical_" + suf, n, ptr(self._rp), ptr(self._ci), ptr(self._v),
+                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.subwarp(), exc.stream)
+
+    # -- conversions -------------------------------------------------------------------
+    def _to_csr(self, **kw):
+        return self
+
+    @classmethod
+    def _from_csr(cls, csr, strategy=None, exec=None, **_):
+        target = exec or csr.exec
+        return cls._from_device(target, csr.size, csr._rp.clone().to(target.device),
+                                csr._ci.clone().to(target.device), csr._v.clone().to(target.device),
+                                strategy=strategy or csr._requested)
+
+    def to_data(self):
+        rp = self._rp.cpu().numpy().astype(np.int64)
+        rows = np.repeat(np.arange(self.size.rows, dtype=np.int64), np.diff(rp))
+        return MatrixData(self.size, rows, self._ci.cpu().numpy().astype(np.int64),
+                          self._v.cpu().numpy().astype(np.float64))
+
+
+# ---------------------------------------------------------------------------
+# Coo (src/formats.py:224-265)
+# ---------------------------------------------------------------------------
+COO_CHUNK = 256
+
+
+class Coo(_Sparse):
+    """Coordinate format, entries sorted by (row, col)."""
+
+    def __init__(self, exc, size, row_idxs, col_idxs, vals, index_dtype=None, value_dtype=None):
+        super().__init__(exc, size)
+        _check_index_dtype(index_dtype)
+        vt = _np_vt(value_dtype or (getattr(vals, "dtype", None) if not isinstance(vals, (list, tuple))
+                                    else None) or config.DEFAULT_VALUE_DTYPE)
+        if not (torch is not None and isinstance(row_idxs, torch.Tensor)):
+            r = np.asarray(row_idxs, dtype=np.int64).reshape(-1)
+            if r.size > 1 and np.any(np.diff(r) < 0):
+                raise Unsupported("Coo entries must be sorted by row (use from_data)")
+        self._ri = _to_device(exc, row_idxs, torch.int32)
+        self._ci = _to_device(exc, col_idxs, torch.int32)
+        self._v = _to_device(exc, vals, _torch_vt(vt))
+        self._ws = None
+
+    @classmethod
+    def _from_device(cls, exc, size, ri, ci, v):
+        obj = cls.__new__(cls)
+        _Sparse.__init__(obj, exc, size)
+        obj._ri, obj._ci, obj._v = ri, ci, v
+        obj._ws = None
+        return obj
+
+    @property
+    def nnz(self):
+        return int(self._v.numel())
+
+    @property
+    def row_idxs(self):
+        return DeviceView(self._ri)
+
+    @property
+    def col_idxs(self):
+        return DeviceView(self._ci)
+
+    @property
+    def vals(self):
+        return DeviceView(self._v)
+
+    def _workspace(self):
+        """carry buffers + the list of rows that hold no entry (prefilled)."""
+        if self._ws is None:
+            exc = self.exec
+            nch = max(1, math.ceil(self.nnz / COO_CHUNK))
+            head = torch.empty(nch, dtype=self._v.dtype, device=exc.device)
+            tail = torch.empty(nch, dtype=self._v.dtype, device=exc.device)
+            n = self.size.rows
+            rp = torch.empty(n + 1, dtype=torch.int32, device=exc.device)
+            _lib.call("coo_to_csr_ptrs", self.nnz, n, ptr(self._ri), ptr(rp), exc.stream)
+            flags = torch.empty(max(n, 1), dtype=torch.int32, device=exc.device)
+            _lib.call("empty_row_flags", n, ptr(rp), ptr(flags), exc.stream)
+            pos = _scan(exc, flags[:n])
+            ne = int(pos[-1].item())
+            empty = torch.empty(max(ne, 1), dtype=torch.int32, device=exc.device)
+            _lib.call("compact_flags", n, ptr(flags), ptr(pos), ptr(empty), exc.stream)
+            self._ws = (head, tail, empty, ne)
+        return self._ws
+
+    def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins,
+                       prefill=True):
+        head, tail, empty, ne = self._workspace()
+        if prefill and ne:
+            _lib.call("rows_scale_" + suf, ne, ptr(empty), xp, xs, b_h, b_p, xin, xins, exc.stream)
+        _lib.call("coo_spmv_" + suf, self.nnz, COO_CHUNK, ptr(self._ri), ptr(self._ci), ptr(self._v),
+                  bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(head), ptr(tail), exc.stream)
+
+    def _to_csr(self, **kw):
+        exc = self.exec
+        n = self.size.rows
+        rp = torch.empty(n + 1, dtype=torch.int32, device=exc.device)
+        _lib.call("coo_to_csr_ptrs", self.nnz, n, ptr(self._ri), ptr(rp), exc.stream)
+        return Csr._from_device(exc, self.size, rp, self._ci.clone(), self._v.clone(), **kw)
+
+    @classmethod
+    def _from_csr(cls, csr, exec=None, **_):
+        exc = csr.exec
+        ri = torch.empty(csr.nnz, dtype=torch.int32, device=exc.device)
+        _lib.call("csr_to_coo_rows", csr.size.rows, ptr(csr._rp), ptr(ri), exc.stream)
+        target = exec or exc
+        return cls._from_device(target, csr.size, ri.to(target.device), csr._ci.clone().to(target.device),
+                                csr._v.clone().to(target.device))
+
+
+# ---------------------------------------------------------------------------
+# Ell (no reference implementation)
+# ---------------------------------------------------------------------------
+def _ell_stride(n):
+    return max(1, (n + 31) // 32 * 32)
+
+
+class Ell(_Sparse):
+    """ELLPACK: ``num_stored_elements_per_row`` slots per row, column-major
+    with ``stride`` >= rows (rounded to 32 for aligned, coalesced columns);
+    padding slots hold column -1 and value 0."""
+
+    def __init__(self, exc, size, col_idxs, vals, num_stored_elements_per_row, stride=None,
+                 value_dtype=None):
+        super().__init__(exc, size)
+        n = self.size.rows
+        self.width = int(num_stored_elements_per_row)
+        self.stride = int(stride if stride is not None else _ell_stride(n))
+        if self.stride < n:
+            raise DimensionMismatch("ell stride must be >= number of rows")
+        vt = _np_vt(value_dtype or getattr(vals, "dtype", None) or config.DEFAULT_VALUE_DTYPE)
+        self._ci = _to_device(exc, col_idxs, torch.int32).reshape(-1)
+        self._v = _to_device(exc, vals, _torch_vt(vt)).reshape(-1)
+        if self._ci.numel() != self.width * self.stride or self._v.numel() != self.width * self.stride:
+            raise DimensionMismatch("ell arrays must hold width * stride entries")
+
+    @classmethod
+    def _from_device(cls, exc, size, ci, v, width, stride):
+        obj = cls.__new__(cls)
+        _Sparse.__init__(obj, exc, size)
+        obj._ci, obj._v, obj.width, obj.stride = ci, v, int(width), int(stride)
+        return obj
+
+    @property
+    def num_stored_elements_per_row(self):
+        return self.width
+
+    @property
+    def col_idxs(self):
+        return DeviceView(self._ci)
+
+    @property
+    def vals(self):
+        return DeviceView(self._v)
+
+    @property
+    def num_stored_elements(self):
+        return self.width * self.stride
+
+    def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):
+        _lib.call("ell_spmv_" + suf, self.size.rows, self.width, self.stride, ptr(self._ci), ptr(self._v),
+                  bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, exc.stream)
+
+    def _row_lengths(self):
+        n = self.size.rows
+        lens = torch.empty(max(n, 1), dtype=torch.int32, device=self.exec.device)
+        _lib.call("ell_row_lengths", n, self.width, self.stride, ptr(self._ci), ptr(lens), self.exec.stream)
+        return lens[:n]
+
+    def _to_csr(self, **kw):
+        exc = self.exec
+        n = self.size.rows
+        rp = _scan(exc, self._row_lengths())
+        nnz = int(rp[-1].item())
+        ci = torch.empty(nnz, dtype=torch.int32, device=exc.device)
+        v = torch.empty(nnz, dtype=self._v.dtype, device=exc.device)
+        _lib.call("ell_to_csr_fill_" + _lib.suffix(self._v.dtype), n, self.width, self.stride,
+                  ptr(self._ci), ptr(self._v), ptr(rp), ptr(ci), ptr(v), exc.stream)
+        return Csr._from_device(exc, self.size, rp, ci, v, **kw)
+
+    @classmethod
+    def _from_csr(cls, csr, width=None, stride=None, exec=None, **_):
+        exc = csr.exec
+        n = csr.size.rows
+        w = csr._row_stats() if width is None else int(width)
+        st = _ell_stride(n) if stride is None else int(stride)
+        ci = torch.empty(w * st, dtype=torch.int32, device=exc.device)
+        v = torch.empty(w * st, dtype=csr._v.dtype, device=exc.device)
+        _lib.call("csr_to_ell_" + _lib.suffix(csr._v.dtype), n, ptr(csr._rp), ptr(csr._ci), ptr(csr._v),
+                  w, st, ptr(ci), ptr(v), exc.stream)
+        target = exec or exc
+        return cls._from_device(target, csr.size, ci.to(target.device), v.to(target.device), w, st)
+
+
+# ---------------------------------------------------------------------------
+# Sellp (no reference implementation)
+# ---------------------------------------------------------------------------
+SELLP_SLICE = 64
+
+
+class Sellp(_Sparse):
+    """Sliced ELLPACK: slices of ``slice_size`` rows, each column-major with
+    its own length (max row length in the slice rounded up to
+    ``stride_factor``); ``slice_sets`` is the exclusive prefix of lengths."""
+
+    def __init__(self, exc, size, slice_lengths, slice_sets, col_idxs, vals, slice_size=SELLP_SLICE,
+                 stride_factor=1, value_dtype=None):
+        super().__init__(exc, size)
+        self.slice_size = int(slice_size)
+        self.stride_factor = int(stride_factor)
+        vt = _np_vt(value_dtype or getattr(vals, "dtype", None) or config.DEFAULT_VALUE_DTYPE)
+        self._sl = _to_device(exc, slice_lengths, torch.int32)
+        self._ss = _to_device(exc, slice_sets, torch.int32)
+        self._ci = _to_device(exc, col_idxs, torch.int32)
+        self._v = _to_device(exc, vals, _torch_vt(vt))
+        ns = math.ceil(self.size.rows / self.slice_size)
+        if self._sl.numel() != ns or self._ss.numel() != ns + 1:
+            raise DimensionMismatch("sellp: slice_lengths needs one entry per slice and "
+                                    "slice_sets one more")
+
+    @classmethod
+    def _from_device(cls, exc, size, sl, ss, ci, v, slice_size, stride_factor):
+        obj = cls.__new__(cls)
+        _Sparse.__init__(obj, exc, size)
+        obj._sl, obj._ss, obj._ci, obj._v = sl, ss, ci, v
+        obj.slice_size, obj.stride_factor = int(slice_size), int(stride_factor)
+        return obj
+
+    @property
+    def slice_lengths(self):
+        return DeviceView(self._sl)
+
+    @property
+    def slice_sets(self):
+        return DeviceView(self._ss)
+
+    @property
+    def col_idxs(self):
+        return DeviceView(self._ci)
+
+    @property
+    def vals(self):
+        return DeviceView(self._v)
+
+    @property
+    def num_stored_elements(self):
+        return int(self._v.numel())
+
+    def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):
+        _lib.call("sellp_spmv_" + suf, self.size.rows, self.slice_size, ptr(self._sl), ptr(self._ss),
+                  ptr(self._ci), ptr(self._v), bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, exc.stream)
+
+    def _to_csr(self, **kw):
+        exc = self.exec
+        n = self.size.rows
+        lens = torch.empty(max(n, 1), dtype=torch.int32, device=exc.device)
+        _lib.call("sellp_row_lengths", n, self.slice_size, ptr(self._sl), ptr(self._ss), ptr(self._ci),
+                  ptr(lens), exc.stream)
+        rp = _scan(exc, lens[:n])
+        nnz = int(rp[-1].item())
+        ci = torch.empty(nnz, dtype=torch.int32, device=exc.device)
+        v = torch.empty(nnz, dtype=self._v.dtype, device=exc.device)
+        _lib.call("sellp_to_csr_fill_" + _lib.suffix(self._v.dtype), n, self.slice_size, ptr(self._sl),
+                  ptr(self._ss), ptr(self._ci), ptr(self._v), ptr(rp), ptr(ci), ptr(v), exc.stream)
+        return Csr._from_device(exc, self.size, rp, ci, v, **kw)
+
+    @classmethod
+    def _from_csr(cls, csr, slice_size=SELLP_SLICE, stride_factor=1, exec=None, **_):
+        exc = csr.exec
+        n = csr.size.rows
+        ns = math.ceil(n / slice_size)
+        sl = torch.empty(max(ns, 1), dtype=torch.int32, device=exc.device)
+        _lib.call("sellp_slice_lengths", n, ptr(csr._rp), slice_size, stride_factor, ptr(sl), exc.stream)
+        sl = sl[:ns]
+        ss = _scan(exc, sl)
+        total = int(ss[-1].item())
+        ci = torch.empty(total * slice_size, dtype=torch.int32, device=exc.device)
+        v = torch.empty(total * slice_size, dtype=csr._v.dtype, device=exc.device)
+        _lib.call("csr_to_sellp_" + _lib.suffix(csr._v.dtype), n, ptr(csr._rp), ptr(csr._ci), ptr(csr._v),
+                  slice_size, ptr(sl), ptr(ss), ptr(ci), ptr(v), exc.stream)
+        target = exec or exc
+        return cls._from_device(target, csr.size, sl.to(target.device), ss.to(target.device),
+                                ci.to(target.device), v.to(target.device), slice_size, stride_factor)
+
+
+# ---------------------------------------------------------------------------
+# Hybrid = Ell + Coo (no reference implementation)
+# ---------------------------------------------------------------------------
+class HybridStrategy:
+    """Chooses the Ell width from the row-length histogram (host decision on
+    a device-computed histogram)."""
+
+    def width(self, hist, n, vt_bytes):
+        raise NotImplementedError
+
+
+class column_limit(HybridStrategy):
+    def __init__(self, num_columns=0):
+        self.num_columns = int(num_columns)
+
+    def width(self, hist, n, vt_bytes):
+        return self.num_columns
+
+
+class imbalance_limit(HybridStrategy):
+    """Width = row length at quantile ``percent`` of the sorted row lengths."""
+
+    def __init__(self, percent=0.8):
+        if not 0.0 <= percent <= 1.0:
+            raise ValueError("percent must lie in [0, 1]")
+        self.percent = float(percent)
+
+    def width(self, hist, n, vt_bytes):
+        if n == 0:
+            return 0
+        rank = min(n - 1, int(math.floor(self.percent * n)))
+        cum = np.cumsum(hist)
+        return int(np.searchsorted(cum, rank + 1))
+
+
+class minimal_storage_limit(HybridStrategy):
+    """Width minimising Ell bytes n*w*(VT+4) + Coo bytes overflow(w)*(VT+8)."""
+
+    def width(self, hist, n, vt_bytes):
+        if n == 0:
+            return 0
+        hist = np.asarray(hist, dtype=np.float64)
+        lens = np.arange(hist.size, dtype=np.float64)
+        cum = np.cumsum(hist)
+        total = float((hist * lens).sum())
+        # entries beyond width w: over[w+1] = over[w] - #(rows longer than w)
+        over = np.empty(hist.size)
+        over[0] = total
+        over[1:] = total - np.cumsum(n - cum[:-1])
+        cost = n * lens * (vt_bytes + 4) + over * (vt_bytes + 8)
+        return int(np.argmin(cost))
+
+
+class automatic(minimal_storage_limit):
+    pass
+
+
+class Hybrid(_Sparse):
+    """Ell part (first ``width`` entries of each row) + Coo part (the rest)."""
+
+    def __init__(self, exc, size, ell, coo, strategy=None):
+        super().__init__(exc, size)
+        self.ell, self.coo = ell, coo
+        self.hybrid_strategy = strategy or automatic()
+
+    @property
+    def _v(self):
+        return self.ell._v
+
+    @property
+    def nnz(self):
+        return self.coo.nnz + int((self.ell._ci >= 0).sum().item())
+
+    def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):
+        self.ell._launch_column(exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins)
+        if self.coo.nnz:
+            # accumulate: x += alpha * A_coo b (rows absent from the Coo part untouched)
+            self.coo._launch_column(exc, suf, bp, bs, xp, xs, a_h, a_p, 1.0, 0, xp, xs, prefill=False)
+
+    def _to_csr(self, **kw):
+        exc = self.exec
+        n = self.size.rows
+        ell_len = self.ell._row_lengths()
+        crp = torch.empty(n + 1, dtype=torch.int32, device=exc.device)
+        _lib.call("coo_to_csr_ptrs", self.coo.nnz, n, ptr(self.coo._ri), ptr(crp), exc.stream)
+        lens = ell_len.clone()
+        _lib.call("add_csr_lengths", n, ptr(crp), ptr(lens), exc.stream)
+        rp = _scan(exc, lens)
+        nnz = int(rp[-1].item())
+        ci = torch.empty(nnz, dtype=torch.int32, device=exc.device)
+        v = torch.empty(nnz, dtype=self._v.dtype, device=exc.device)
+        suf = _lib.suffix(self._v.dtype)
+        _lib.call("ell_to_csr_fill_" + suf, n, self.ell.width, self.ell.stride, ptr(self.ell._ci),
+                  ptr(self.ell._v), ptr(rp), ptr(ci), ptr(v), exc.stream)
+        _lib.call("hybrid_coo_append_" + suf, n, ptr(rp), ptr(ell_len), ptr(crp), ptr(self.coo._ci),
+                  ptr(self.coo._v), ptr(ci), ptr(v), exc.stream)
+        return Csr._from_device(exc, self.size, rp, ci, v, **kw)
+
+    @classmethod
+    def _from_csr(cls, csr, strategy=None, exec=None, **_):
+        exc = csr.exec
+        strategy = strategy or automatic()
+        n = csr.size.rows
+        if isinstance(strategy, column_limit):
+            w = strategy.num_columns
+        else:
+            nbins = max(2, min(csr._row_stats() + 1, 1 << 16))
+            hist = torch.empty(nbins, dtype=torch.int64, device=exc.device)
+            _lib.call("length_histogram", n, ptr(csr._rp), nbins, ptr(hist), exc.stream)
+            w = strategy.width(hist.cpu().numpy().astype(np.float64), n, csr._v.element_size())
+        ell = Ell._from_csr(csr, width=w)
+        cnt = torch.empty(max(n, 1), dtype=torch.int32, device=exc.device)
+        _lib.call("hybrid_overflow_counts", n, ptr(csr._rp), w, ptr(cnt), exc.stream)
+        offs = _scan(exc, cnt[:n])
+        nc = int(offs[-1].item())
+        crow = torch.empty(nc, dtype=torch.int32, device=exc.device)
+        cci = torch.empty(nc, dtype=torch.int32, device=exc.device)
+        cv = torch.empty(nc, dtype=csr._v.dtype, device=exc.device)
+        _lib.call("csr_to_hybrid_coo_" + _lib.suffix(csr._v.dtype), n, ptr(csr._rp), ptr(csr._ci),
+                  ptr(csr._v), w, ptr(offs), ptr(crow), ptr(cci), ptr(cv), exc.stream)
+        coo = Coo._from_device(exc, csr.size, crow, cci, cv)
+        out = cls(exc, csr.size, ell, coo, strategy)
+        if exec is not None and exec is not exc:
+            return convert(out, Hybrid, exec=exec)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# conversions (src/formats.py:301-329)
+# ---------------------------------------------------------------------------
+_FORMAT_NAMES = {"dense": Dense, "csr": Csr, "coo": Coo, "ell": Ell, "sellp": Sellp, "hybrid": Hybrid}
+
+
+def _resolve(target):
+    if isinstance(target, str):
+        key = target.lower()
+        if key in ("csr_classical", "csr_lb", "csr_load_balance"):
+            return Csr, {"strategy": "classical" if key == "csr_classical" else "load_balance"}
+        try:
+            return _FORMAT_NAMES[key], {}
+        except KeyError:
+            raise Unsupported(f"unknown format {target!r}") from None
+    if target in _FORMAT_NAMES.values():
+        return target, {}
+    raise Unsupported(f"no conversion to {target}")
+
+
+def convert(a, target, **params):
+    """Value-equivalent copy of ``a`` in another format (device-side, Csr hub).
+
+    Dense -> sparse drops explicit zeros (as in the reference). Extra keyword
+    parameters reach the target constructor (``strategy``, ``width``,
+    ``slice_size``, ``stride_factor``)."""
+    cls, extra = _resolve(target)
+    params = {**extra, **params}
+    csr_kw = {"strategy": params.pop("strategy")} if cls is Csr and "strategy" in params else {}
+    if isinstance(a, Csr) and cls is Csr:
+        return Csr._from_csr(a, **csr_kw, **params)
+    csr = a._to_csr(**csr_kw)
+    if cls is Csr:
+        return csr if "exec" not in params else Csr._from_csr(csr, **params)
+    return cls._from_csr(csr, **params)
+
+
+def matrix_from_data(exc, data, fmt="csr", **params):
+    cls, extra = _resolve(fmt)
+    if cls is Dense:
+        return Dense(exc, data.to_dense_array(), value_dtype=params.get("value_dtype"))
+    csr = Csr._from_host_data(exc, data, params.pop("value_dtype", None))
+    if cls is Csr:
+        if extra or params:
+            csr.set_strategy((extra or params).get("strategy", "automatic"))
+        return csr
+    return cls._from_csr(csr, **params)
