@@ -102,7 +102,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.ok:
@@ -256,15 +256,14 @@ def bench_c2(args, world, rank, local):
     # ---- headline: Csr (automatic) fp64, exactly K timed steps ------------
     m, b, x = head
     by = bytes_format(m, 8)
-    launches0 = _lib.launch_count()
-    for _ in range(args.warmup):
-        m.apply(b, x)
-    barrier(world)
-    torch.cuda.synchronize()
-    launches0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:  # sampling spans the warm-up and the timed steps
+        for _ in range(args.warmup):
+            m.apply(b, x)
+        barrier(world)
+        torch.cuda.synchronize()
+        launches0 = _lib.launch_count()
         ms = timer.run(lambda: m.apply(b, x), args.steps, 0)
-    launches = _lib.launch_count() - launches0
+        launches = _lib.launch_count() - launches0
     barrier(world)
     t_step = allmax(world, statistics.mean(ms) * 1e-3)
     total_bytes = allsum(world, by)

@@ -45,6 +45,10 @@ const char* b200sp_last_error(void);
 long long b200sp_launch_count(void);
 int b200sp_version(void);
 int b200sp_device_sync(void);
+/* Thread-local launch guard: SpMV / fix-up kernels launched by this host
+ * thread while a guard is set return immediately when *guard != 0 (device
+ * flag). Solvers set it to their "done" flag around CUDA-graph batches. */
+void b200sp_set_guard(const int32_t* guard);
 int64_t b200sp_reduce_workspace_elems(void);
 int64_t b200sp_scan_workspace_elems(int64_t count);
 int b200sp_exclusive_scan_i32(int64_t count, const int32_t* in, int32_t* out, long long* ws, void* stream);
@@ -85,6 +89,22 @@ int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* row_ptrs, const int3
                                   const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
                                   const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
                                   int64_t x_in_stride, int32_t subwarp, void* stream);
+/* Csr, stream strategy: b200sp_csr_stream_rows() consecutive rows per CTA,
+ * their nonzeros staged through shared memory with 128-bit loads (col_idxs /
+ * vals 16-byte aligned) in chunks of chunk_cap entries (multiple of 4, at
+ * most b200sp_csr_stream_capacity(); rows_per_CTA * longest_row + 4 keeps a
+ * block in one chunk). Same result contract as csr_row_sums
+ * (kernels.py:304-316). */
+int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
+                               const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
+                               double alpha, const double* alpha_dev, double beta, const double* beta_dev,
+                               const double* x_in, int64_t x_in_stride, int32_t chunk_cap, void* stream);
+int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
+                               const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride,
+                               float alpha, const float* alpha_dev, float beta, const float* beta_dev,
+                               const float* x_in, int64_t x_in_stride, int32_t chunk_cap, void* stream);
+int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
+int32_t b200sp_csr_stream_rows(int32_t value_bytes);
 /* Csr, load-balanced (merge-path) strategy: plan once per matrix
  * (coords: 2*(num_tiles+1) int32), workspace carry_row/carry_val: num_tiles each */
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes);
@@ -193,6 +213,83 @@ int b200sp_powerlaw_lengths(int64_t n, uint64_t seed, const double* thresholds, 
                             void* stream);
 int b200sp_powerlaw_fill_f64(int64_t n, uint64_t seed, const int32_t* rp, int32_t* ci, double* v, void* stream);
 int b200sp_powerlaw_fill_f32(int64_t n, uint64_t seed, const int32_t* rp, int32_t* ci, float* v, void* stream);
+
+/* ---- block-Jacobi (replaces _JacobiGenerateKernel / gauss_jordan_inverse /
+ * _extract_block / _JacobiApplyKernel, precond.py:28-125, :200-208) --------
+ * Generation: block sizes^2 -> exclusive scan (off64) -> invert into fp64
+ * column-major blocks (bit-identical Gauss-Jordan), kappa_inf, precision
+ * flag and stored byte size per block; singular: smallest singular block
+ * index (init to INT64_MAX). Pack: fp64 -> mixed storage at byte offsets. */
+int b200sp_jacobi_block_sizes_sq(int64_t nblocks, const int32_t* starts, int32_t* out, void* stream);
+int b200sp_jacobi_invert_f64(int64_t nblocks, const int32_t* starts, const int32_t* rp, const int32_t* ci,
+                             const double* vals, const int64_t* off64, double* inv64, double* cond, uint8_t* prec,
+                             int32_t* nbytes, int32_t adaptive, double threshold, int64_t* singular, void* stream);
+int b200sp_jacobi_invert_f32(int64_t nblocks, const int32_t* starts, const int32_t* rp, const int32_t* ci,
+                             const float* vals, const int64_t* off64, double* inv64, double* cond, uint8_t* prec,
+                             int32_t* nbytes, int32_t adaptive, double threshold, int64_t* singular, void* stream);
+int b200sp_jacobi_pack(int64_t nblocks, const int32_t* starts, const int64_t* off64, const double* inv64,
+                       const uint8_t* prec, const int64_t* offs, void* storage, void* stream);
+int b200sp_jacobi_apply_f64(int64_t nblocks, const int32_t* starts, const int64_t* offs, const uint8_t* prec,
+                            const void* storage, int32_t m, const double* r, int64_t rs, double* z, int64_t zs,
+                            void* stream);
+int b200sp_jacobi_apply_f32(int64_t nblocks, const int32_t* starts, const int64_t* offs, const uint8_t* prec,
+                            const void* storage, int32_t m, const float* r, int64_t rs, float* z, int64_t zs,
+                            void* stream);
+
+/* ---- device-resident Krylov iterations (m = 1) ---------------------------
+ * Control block (b200sp_krylov_ctl_bytes) holds iteration count, status
+ * (stopped / stopping_id / finalized), breakdown, criteria (type 1 =
+ * Iteration(max), 2 = ResidualNormReduction(factor); src/stop.py:118-246)
+ * and the solver scalars; part: b200sp_krylov_part_elems() doubles; hist:
+ * optional per-check residual norms (hist_cap entries). Every kernel is a
+ * no-op once the solve is done, so a batch of iterations can be captured in
+ * one CUDA graph. JAC = (nblocks, starts, offs, prec, storage); nblocks = 0
+ * means no preconditioner (z aliases r).
+ *   CG       src/solvers/krylov.py:36-77:   per iteration step1, SpMV, sigma, step2
+ *   BiCGSTAB src/solvers/krylov.py:190-271: step1, SpMV, gamma, step2, SpMV, tst, step3
+ *   GMRES    src/solvers/gmres.py:183-340:  per Arnoldi step j: [Jacobi], SpMV,
+ *            dot0, mgs(i = 0..j-1), normalize; per cycle: backsolve, combine,
+ *            after_commit, residual SpMV, reset, scale_v0 */
+int64_t b200sp_krylov_ctl_bytes(void);
+int64_t b200sp_krylov_part_elems(void);
+int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,
+                           int32_t needs_residual, int32_t hist_cap, int32_t kdim, void* stream);
+int b200sp_krylov_status(const void* ctl, int32_t* out_i8, double* out_d8, void* stream);
+int b200sp_krylov_force_stop(void* ctl, int32_t stopping_id, int32_t gmres, void* stream);
+const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which);
+int64_t b200sp_gmres_workspace_elems(int32_t k);
+int b200sp_gmres_backsolve(void* ctl, double* gm, void* stream);
+int b200sp_gmres_after_commit(void* ctl, void* stream);
+#define B200SP_JAC_DECL int64_t jnb, const int32_t *jstarts, const int64_t *joffs, const uint8_t *jprec, const void *jstore
+#define B200SP_KRYLOV_DECL(T, SUF)                                                                                 \
+    int b200sp_cg_init_##SUF(int64_t n, const T* r, T* z, T* p, B200SP_JAC_DECL, void* ctl, double* part,           \
+                             double* hist, void* stream);                                                          \
+    int b200sp_cg_step1_##SUF(int64_t n, T* p, const T* z, const void* ctl, void* stream);                         \
+    int b200sp_cg_sigma_##SUF(int64_t n, const T* p, const T* q, void* ctl, double* part, void* stream);            \
+    int b200sp_cg_step2_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* p, const T* q, T* z, B200SP_JAC_DECL,     \
+                              void* ctl, double* part, double* hist, void* stream);                                \
+    int b200sp_bicgstab_init_##SUF(int64_t n, const T* b, int64_t bs, const T* r, T* rt, T* p, T* v, T* s, T* t,    \
+                                   T* y, T* z, void* ctl, double* part, double* hist, void* stream);               \
+    int b200sp_bicgstab_step1_##SUF(int64_t n, const T* r, T* p, const T* v, T* y, B200SP_JAC_DECL,                \
+                                    const void* ctl, void* stream);                                                \
+    int b200sp_bicgstab_gamma_##SUF(int64_t n, const T* rt, const T* v, void* ctl, double* part, void* stream);     \
+    int b200sp_bicgstab_step2_##SUF(int64_t n, const T* r, const T* v, T* s, T* z, B200SP_JAC_DECL, void* ctl,     \
+                                    double* part, double* hist, void* stream);                                     \
+    int b200sp_bicgstab_tst_##SUF(int64_t n, const T* t, const T* s, void* ctl, double* part, void* stream);        \
+    int b200sp_bicgstab_step3_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* s, const T* t, const T* y,         \
+                                    const T* z, const T* rt, void* ctl, double* part, double* hist, void* stream); \
+    int b200sp_gmres_reset_##SUF(int64_t n, const T* r, void* ctl, double* part, double* gm, double* hist,          \
+                                 int32_t first, void* stream);                                                     \
+    int b200sp_gmres_scale_v0_##SUF(int64_t n, const T* r, T* V, const void* ctl, void* stream);                   \
+    int b200sp_gmres_dot0_##SUF(int64_t n, int32_t j, const T* V, const T* w, void* ctl, double* part, double* gm,  \
+                                void* stream);                                                                     \
+    int b200sp_gmres_mgs_##SUF(int64_t n, int32_t j, int32_t i, const T* V, T* w, void* ctl, double* part,          \
+                               double* gm, double* hist, void* stream);                                            \
+    int b200sp_gmres_normalize_##SUF(int64_t n, int32_t j, T* V, const T* w, const void* ctl, void* stream);        \
+    int b200sp_gmres_combine_##SUF(int64_t n, const T* V, T* x, int64_t xs, B200SP_JAC_DECL, void* ctl,            \
+                                   const double* gm, void* stream);
+B200SP_KRYLOV_DECL(double, f64)
+B200SP_KRYLOV_DECL(float, f32)
 
 #ifdef __cplusplus
 }

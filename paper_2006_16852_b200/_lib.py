@@ -33,6 +33,7 @@ _TYPED = {
     # SpMV
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
+    "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "ip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
@@ -51,6 +52,26 @@ _TYPED = {
     # generators
     "stencil_fill": "ildlpppp",
     "powerlaw_fill": "lupppp",
+    # block-Jacobi
+    "jacobi_invert": "lpppppppppidpp",
+    "jacobi_apply": "lppppiplplp",
+    # Krylov (JAC = l p p p p)
+    "cg_init": "lppp" + "lpppp" + "pppp",
+    "cg_step1": "lpppp",
+    "cg_sigma": "lppppp",
+    "cg_step2": "lplpppp" + "lpppp" + "pppp",
+    "bicgstab_init": "lplpppppppppppp",
+    "bicgstab_step1": "lpppp" + "lpppp" + "pp",
+    "bicgstab_gamma": "lppppp",
+    "bicgstab_step2": "lpppp" + "lpppp" + "pppp",
+    "bicgstab_tst": "lppppp",
+    "bicgstab_step3": "lplpppppppppp",
+    "gmres_reset": "lppppp" + "ip",
+    "gmres_scale_v0": "lpppp",
+    "gmres_dot0": "lipppppp",
+    "gmres_mgs": "lii" + "ppppppp",
+    "gmres_normalize": "lipppp",
+    "gmres_combine": "lppl" + "lpppp" + "ppp",
 }
 _UNTYPED = {
     "last_error": ("", ctypes.c_char_p),
@@ -63,6 +84,8 @@ _UNTYPED = {
     "exclusive_scan_i64": ("lpppp", ctypes.c_int),
     "reduce_max_i32": ("lppp", ctypes.c_int),
     "csr_lb_num_tiles": ("lli", ctypes.c_int64),
+    "csr_stream_capacity": ("i", ctypes.c_int32),
+    "csr_stream_rows": ("i", ctypes.c_int32),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),
@@ -77,6 +100,18 @@ _UNTYPED = {
     "compact_flags": ("lpppp", ctypes.c_int),
     "stencil_lengths": ("illpp", ctypes.c_int),
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
+    "set_guard": ("p", None),
+    "jacobi_block_sizes_sq": ("lppp", ctypes.c_int),
+    "jacobi_pack": ("lppppppp", ctypes.c_int),
+    "krylov_ctl_bytes": ("", ctypes.c_int64),
+    "krylov_part_elems": ("", ctypes.c_int64),
+    "krylov_ctl_init": ("pippiiip", ctypes.c_int),
+    "krylov_status": ("pppp", ctypes.c_int),
+    "krylov_force_stop": ("piip", ctypes.c_int),
+    "krylov_guard": ("pi", ctypes.c_void_p),
+    "gmres_workspace_elems": ("i", ctypes.c_int64),
+    "gmres_backsolve": ("ppp", ctypes.c_int),
+    "gmres_after_commit": ("pp", ctypes.c_int),
 }
 
 _lock = threading.Lock()

@@ -75,6 +75,51 @@ __device__ __forceinline__ int ld_stream(const int* p) {
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
+// 128-bit streaming loads (caller guarantees 16-byte alignment)
+__device__ __forceinline__ int4 ld_stream_v4(const int* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ld_stream_v2(const double* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float4 ld_stream_v4(const float* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+// load E consecutive values (E % 4 == 0, 16-byte aligned) with 128-bit loads
+template <int E>
+__device__ __forceinline__ void ld_stream_vec(const int* p, int (&out)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; i += 4) {
+        int4 q = ld_stream_v4(p + i);
+        out[i] = q.x; out[i + 1] = q.y; out[i + 2] = q.z; out[i + 3] = q.w;
+    }
+}
+template <int E>
+__device__ __forceinline__ void ld_stream_vec(const double* p, double (&out)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; i += 2) {
+        double2 q = ld_stream_v2(p + i);
+        out[i] = q.x; out[i + 1] = q.y;
+    }
+}
+template <int E>
+__device__ __forceinline__ void ld_stream_vec(const float* p, float (&out)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; i += 4) {
+        float4 q = ld_stream_v4(p + i);
+        out[i] = q.x; out[i + 1] = q.y; out[i + 2] = q.z; out[i + 3] = q.w;
+    }
+}
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 // Gathered vector entries: read-only path, allocate in L1 (neighbouring rows
 // of a stencil share most of their columns).
 template <typename T>
@@ -84,12 +129,20 @@ __device__ __forceinline__ T ld_gather(const T* p) { return __ldg(p); }
 // scalar coefficients: host value or device pointer (device scalars keep the
 // solver loops free of host synchronisation)
 // ---------------------------------------------------------------------------
+// `guard` (nullable device flag): when it reads non-zero the launch is a
+// no-op. Krylov solvers point it at their "done" flag so SpMVs captured in a
+// CUDA-graph batch cost nothing once the solve has stopped.
 template <typename T>
 struct Coef {
     T v;
     const T* p;
+    const int* guard;
     __device__ __forceinline__ T get() const { return p ? *p : v; }
+    __device__ __forceinline__ bool skip() const { return guard && *(volatile const int*)guard; }
 };
+const int* current_guard();
+template <typename T>
+inline Coef<T> coef(T v, const T* p) { return Coef<T>{v, p, current_guard()}; }
 
 // ---------------------------------------------------------------------------
 // warp reductions

@@ -1,0 +1,692 @@
+// Device-resident Krylov iterations: CG, BiCGSTAB, restarted GMRES (m = 1).
+//
+// Each solver is a fixed sequence of kernels per iteration whose scalar
+// control (criteria, breakdown tests, alpha/beta/omega, Givens rotations)
+// runs in the last-block epilogue of the reduction that produces its inputs
+// (see krylov.cuh). Vectors are contiguous except x / b (user columns, row
+// stride xs / bs). Element-wise kernels walk "row blocks" warp-per-block:
+// Jacobi blocks when a block-Jacobi preconditioner is present (so z = M r is
+// fused into the update that produces r), else 32-row chunks.
+//
+// Reference loops restated:
+//   CG        src/solvers/krylov.py:36-77   + steps.py:87-158
+//   BiCGSTAB  src/solvers/krylov.py:190-271 + steps.py:238-243, :348-480
+//   GMRES     src/solvers/gmres.py:75-340
+#include <cstring>
+
+#include "krylov.cuh"
+
+namespace b200sp {
+
+__device__ __forceinline__ void hist_put(const KrylovCtl* c, double* hist, int it, double v) {
+    if (hist && it < c->hist_cap) hist[it] = v;
+}
+
+// ===========================================================================
+// CG
+// ===========================================================================
+// after r = b - A x: z = M r, p = 0, rho = r.z, baseline = ||r||, check(0)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cg_init_kernel(RowBlocks rb, const T* __restrict__ r, T* __restrict__ z, T* __restrict__ p, KrylovCtl* c,
+               double* part, double* hist) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double rz = 0, rr = 0;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        const T rv = lane < bs ? r[r0 + lane] : T(0);
+        T zv = rv;
+        if (rb.J.nblocks) zv = jacobi_row<T>(rb.J, b, bs, lane, rv);
+        if (lane < bs) {
+            if (rb.J.nblocks) z[r0 + lane] = zv;
+            p[r0 + lane] = T(0);
+            rz += (double)rv * (double)zv;
+            rr += (double)rv * (double)rv;
+        }
+    }
+    double v[2] = {rz, rr}, tot[2];
+    if (!grid_reduce<2>(v, part, &c->ticket[0], tot)) return;
+    c->it = 0;
+    c->rho = tot[0];
+    c->rho_prev = 1.0;
+    c->rnorm = sqrt(tot[1]);
+    c->baseline = c->rnorm;
+    hist_put(c, hist, 0, c->rnorm);
+    crit_check(c, 0, c->rnorm);
+    c->done = c->stopped;
+    c->beta = safe_div(c->rho, c->rho_prev);
+}
+
+// p = z + beta p    (CgStep1, steps.py:93-119)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cg_step1_kernel(int64_t n, T* __restrict__ p, const T* __restrict__ z, const KrylovCtl* c) {
+    if (c->done) return;
+    const T beta = (T)c->beta;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = z[i] + beta * p[i];
+}
+
+// sigma = p.q; breakdown if sigma <= 0 and rho != 0 (krylov.py:64-70); alpha
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cg_sigma_kernel(int64_t n, const T* __restrict__ p, const T* __restrict__ q, KrylovCtl* c, double* part) {
+    if (c->done) return;
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += (double)p[i] * (double)q[i];
+    double v[1] = {s}, tot[1];
+    if (!grid_reduce<1>(v, part, &c->ticket[1], tot)) return;
+    c->sigma = tot[0];
+    if (c->sigma <= 0.0 && c->rho != 0.0) {
+        c->breakdown = BD_CG_SIGMA;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->alpha = safe_div(c->rho, c->sigma);
+}
+
+// x += alpha p; r -= alpha q; z = M r; rho = r.z; ||r||; it++; check   (CgStep2)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cg_step2_kernel(RowBlocks rb, T* __restrict__ x, int64_t xs, T* __restrict__ r, const T* __restrict__ p,
+                const T* __restrict__ q, T* __restrict__ z, KrylovCtl* c, double* part, double* hist) {
+    if (c->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T alpha = (T)c->alpha;
+    double rz = 0, rr = 0;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T rv = T(0);
+        if (lane < bs) {
+            const int64_t i = r0 + lane;
+            x[i * xs] = x[i * xs] + alpha * p[i];
+            rv = r[i] - alpha * q[i];
+            r[i] = rv;
+        }
+        T zv = rv;
+        if (rb.J.nblocks) {
+            zv = jacobi_row<T>(rb.J, b, bs, lane, rv);
+            if (lane < bs) z[r0 + lane] = zv;
+        }
+        rz += (double)rv * (double)zv;
+        rr += (double)rv * (double)rv;
+    }
+    double v[2] = {rz, rr}, tot[2];
+    if (!grid_reduce<2>(v, part, &c->ticket[2], tot)) return;
+    c->rho_prev = c->rho;
+    c->rho = tot[0];
+    c->it += 1;
+    c->rnorm = sqrt(tot[1]);
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+    c->done = c->stopped;
+    c->beta = safe_div(c->rho, c->rho_prev);
+}
+
+// ===========================================================================
+// BiCGSTAB (half-iteration counting, mid check on s with finalize)
+// ===========================================================================
+// cycle start: rho = rt.r; breakdown if rho == 0 with r != 0; beta
+__device__ inline void bicg_cycle_start(KrylovCtl* c, double rho_new, double rr) {
+    if (c->done) return;
+    if (rho_new == 0.0 && rr != 0.0) {  // krylov.py:227-231
+        c->breakdown = BD_RHO;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->rho = rho_new;
+    c->beta = safe_div(c->rho, c->rho_prev) * safe_div(c->alpha, c->omega);
+}
+
+// after r = b - A x: rt = b, zero p v s t y z, baseline, check(0), cycle start
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_init_kernel(int64_t n, const T* __restrict__ b, int64_t bstr, const T* __restrict__ r, T* __restrict__ rt,
+                 T* __restrict__ p, T* __restrict__ v, T* __restrict__ s, T* __restrict__ t, T* __restrict__ y,
+                 T* __restrict__ z, KrylovCtl* c, double* part, double* hist) {
+    double rr = 0, rtr = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T bv = b[i * bstr];
+        const T rv = r[i];
+        rt[i] = bv;
+        p[i] = v[i] = s[i] = t[i] = T(0);
+        if (y != p) y[i] = T(0);
+        if (z != s) z[i] = T(0);
+        rr += (double)rv * (double)rv;
+        rtr += (double)bv * (double)rv;
+    }
+    double vv[2] = {rr, rtr}, tot[2];
+    if (!grid_reduce<2>(vv, part, &c->ticket[0], tot)) return;
+    c->it = 0;
+    c->rho_prev = 1.0;
+    c->alpha = 1.0;
+    c->omega = 1.0;
+    c->rho = 0.0;
+    c->ts = c->tt = 0.0;
+    c->rnorm = sqrt(tot[0]);
+    c->baseline = c->rnorm;
+    hist_put(c, hist, 0, c->rnorm);
+    crit_check(c, 0, c->rnorm);
+    c->done = c->stopped;
+    bicg_cycle_start(c, tot[1], tot[0]);
+}
+
+// p = r + beta (p - omega v); y = M p     (BicgstabStep1, steps.py:348-378)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_step1_kernel(RowBlocks rb, const T* __restrict__ r, T* __restrict__ p, const T* __restrict__ v,
+                  T* __restrict__ y, const KrylovCtl* c) {
+    if (c->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T beta = (T)c->beta, omega = (T)c->omega;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T pv = T(0);
+        if (lane < bs) {
+            const int64_t i = r0 + lane;
+            pv = r[i] + beta * (p[i] - omega * v[i]);
+            p[i] = pv;
+        }
+        if (rb.J.nblocks) {
+            const T yv = jacobi_row<T>(rb.J, b, bs, lane, pv);
+            if (lane < bs) y[r0 + lane] = yv;
+        }
+    }
+}
+
+// gamma = rt.v; breakdown if gamma == 0 and rho != 0; alpha = rho / gamma
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_gamma_kernel(int64_t n, const T* __restrict__ rt, const T* __restrict__ v, KrylovCtl* c, double* part) {
+    if (c->done) return;
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += (double)rt[i] * (double)v[i];
+    double vv[1] = {s}, tot[1];
+    if (!grid_reduce<1>(vv, part, &c->ticket[1], tot)) return;
+    c->gamma = tot[0];
+    if (c->gamma == 0.0 && c->rho != 0.0) {  // krylov.py:235-239
+        c->breakdown = BD_GAMMA;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->alpha = safe_div(c->rho, c->gamma);
+}
+
+// s = r - alpha v; z = M s; it++; mid check on ||s||   (BicgstabStep2)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_step2_kernel(RowBlocks rb, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ s,
+                  T* __restrict__ z, KrylovCtl* c, double* part, double* hist) {
+    if (c->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T alpha = (T)c->alpha;
+    double ss = 0;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T sv = T(0);
+        if (lane < bs) {
+            const int64_t i = r0 + lane;
+            sv = r[i] - alpha * v[i];
+            s[i] = sv;
+        }
+        if (rb.J.nblocks) {
+            const T zv = jacobi_row<T>(rb.J, b, bs, lane, sv);
+            if (lane < bs) z[r0 + lane] = zv;
+        }
+        ss += (double)sv * (double)sv;
+    }
+    double vv[1] = {ss}, tot[1];
+    if (!grid_reduce<1>(vv, part, &c->ticket[2], tot)) return;
+    c->it += 1;
+    c->snorm = sqrt(tot[0]);
+    hist_put(c, hist, c->it, c->snorm);
+    crit_check(c, c->it, c->snorm);
+    if (c->stopped) {
+        // converged on ||s||: commit the pending half step (krylov.py:248-253)
+        c->mid_final = c->needs_residual;
+        c->done = 1;
+    }
+}
+
+// ts = t.s, tt = t.t; breakdown if tt == 0 and ts != 0; omega = ts / tt
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_tst_kernel(int64_t n, const T* __restrict__ t, const T* __restrict__ s, KrylovCtl* c, double* part) {
+    if (c->done) return;
+    double a = 0, bb = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double tv = t[i];
+        a += tv * (double)s[i];
+        bb += tv * tv;
+    }
+    double vv[2] = {a, bb}, tot[2];
+    if (!grid_reduce<2>(vv, part, &c->ticket[1], tot)) return;
+    c->ts = tot[0];
+    c->tt = tot[1];
+    if (c->tt == 0.0 && c->ts != 0.0) {  // krylov.py:262-265
+        c->breakdown = BD_TT;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->omega = safe_div(c->ts, c->tt);
+}
+
+// x += alpha y + omega z; r = s - omega t; it++; top check; next cycle start
+// (BicgstabStep3); or, after a mid-check stop, x += alpha y (BicgstabFinalize)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, const T* __restrict__ s,
+                  const T* __restrict__ t, const T* __restrict__ y, const T* __restrict__ z,
+                  const T* __restrict__ rt, KrylovCtl* c, double* part, double* hist) {
+    const int mid = c->mid_final;
+    if (c->done && !mid) return;
+    const T alpha = (T)c->alpha, omega = (T)c->omega;
+    double rr = 0, rtr = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (mid) {
+            x[i * xs] = x[i * xs] + alpha * y[i];
+            continue;
+        }
+        const T upd = alpha * y[i] + omega * z[i];
+        x[i * xs] = x[i * xs] + upd;
+        const T rv = s[i] - omega * t[i];
+        r[i] = rv;
+        rr += (double)rv * (double)rv;
+        rtr += (double)rt[i] * (double)rv;
+    }
+    double vv[2] = {rr, rtr}, tot[2];
+    if (!grid_reduce<2>(vv, part, &c->ticket[2], tot)) return;
+    if (mid) {
+        c->mid_final = 0;
+        return;
+    }
+    c->rho_prev = c->rho;
+    c->it += 1;
+    c->rnorm = sqrt(tot[0]);
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+    c->done = c->stopped;
+    bicg_cycle_start(c, tot[1], tot[0]);
+}
+
+// ===========================================================================
+// GMRES(k), right preconditioned, m = 1.
+// gm layout: H[(k+1) x k] row-major | cs[k] | sn[k] | gamma[k+1] | y[k]
+// ===========================================================================
+struct GmresView {
+    double* H;
+    double* cs;
+    double* sn;
+    double* g;
+    double* y;
+    int k;
+    __device__ GmresView(double* gm, int kk) : k(kk) {
+        H = gm;
+        cs = H + (size_t)(kk + 1) * kk;
+        sn = cs + kk;
+        g = sn + kk;
+        y = g + kk + 1;
+    }
+};
+
+// reset_segment (gmres.py:75-86) after r = b - A x; `first` also sets the RNR
+// baseline and runs the top-of-loop check
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_reset_kernel(int64_t n, const T* __restrict__ r, KrylovCtl* c, double* part, double* gm, double* hist,
+                   int first) {
+    if (!first && (c->stopped || c->done)) return;
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += (double)r[i] * (double)r[i];
+    double vv[1] = {s}, tot[1];
+    if (!grid_reduce<1>(vv, part, &c->ticket[0], tot)) return;
+    GmresView G(gm, c->kdim);
+    const double beta = sqrt(tot[0]);
+    for (int i = 0; i <= G.k; ++i) G.g[i] = 0.0;
+    for (int i = 0; i < G.k; ++i) G.cs[i] = G.sn[i] = 0.0;
+    G.g[0] = beta;
+    c->rnorm = beta;  // res_est
+    c->jpos = 0;
+    c->committed = 0;
+    if (first) {
+        c->it = 0;
+        c->baseline = beta;
+        if (beta == 0.0) {  // exact zero residual: declared converged (gmres.py:210-212)
+            c->stopped = 1;
+            c->stopping_id = EXACT_CONVERGENCE_ID;
+            c->finalized = 1;
+            c->rnorm = 0.0;
+            c->done = 1;
+            return;
+        }
+    }
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+}
+
+// v0 = r / beta (0 if beta == 0)
+template <typename T>
+__global__ void gmres_scale_v0_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ V, const KrylovCtl* c) {
+    if (c->stopped || c->done) return;
+    const double beta = c->rnorm;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        V[i] = beta == 0.0 ? T(0) : (T)((double)r[i] / beta);
+}
+
+// h_{0,j-1} = v_0 . w
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_dot0_kernel(int64_t n, int j, const T* __restrict__ V, const T* __restrict__ w, KrylovCtl* c, double* part,
+                  double* gm) {
+    if (c->stopped || c->done) return;
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += (double)V[i] * (double)w[i];
+    double vv[1] = {s}, tot[1];
+    if (!grid_reduce<1>(vv, part, &c->ticket[1], tot)) return;
+    GmresView G(gm, c->kdim);
+    G.H[0 * G.k + (j - 1)] = tot[0];
+}
+
+// MGS step i of Arnoldi step j: w -= h_i v_i, then h_{i+1} = v_{i+1}.w, or,
+// for i = j-1, ||w||, the Givens update and the next check (gmres.py:88-129)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_mgs_kernel(int64_t n, int j, int i, const T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* part,
+                 double* gm, double* hist) {
+    if (c->stopped || c->done) return;
+    GmresView G(gm, c->kdim);
+    const T h = (T)G.H[i * G.k + (j - 1)];
+    const T* vi = V + (int64_t)i * n;
+    const bool last = (i == j - 1);
+    const T* vn = last ? w : V + (int64_t)(i + 1) * n;
+    double s = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const T wv = w[r] - h * vi[r];
+        w[r] = wv;
+        s += (double)(last ? wv : vn[r]) * (double)wv;
+    }
+    double vv[1] = {s}, tot[1];
+    if (!grid_reduce<1>(vv, part, &c->ticket[2], tot)) return;
+    if (!last) {
+        G.H[(i + 1) * G.k + (j - 1)] = tot[0];
+        return;
+    }
+    const int col = j - 1;
+    const double hj = sqrt(tot[0]);
+    c->hnorm = hj;
+    G.H[j * G.k + col] = hj;
+    for (int q = 0; q < j - 1; ++q) {
+        const double h1 = G.H[q * G.k + col], h2 = G.H[(q + 1) * G.k + col];
+        G.H[q * G.k + col] = G.cs[q] * h1 + G.sn[q] * h2;
+        G.H[(q + 1) * G.k + col] = -G.sn[q] * h1 + G.cs[q] * h2;
+    }
+    const double h1 = G.H[col * G.k + col], h2 = G.H[j * G.k + col];
+    const double den = hypot(h1, h2);
+    const double cc = den != 0.0 ? h1 / den : 1.0, sn = den != 0.0 ? h2 / den : 0.0;
+    G.cs[col] = cc;
+    G.sn[col] = sn;
+    G.H[col * G.k + col] = den;
+    G.H[j * G.k + col] = 0.0;
+    const double gv = G.g[col];
+    G.g[col] = cc * gv;
+    G.g[j] = -sn * gv;
+    c->rnorm = fabs(G.g[j]);
+    c->jpos = j;
+    c->it += 1;
+    if (hj == 0.0) {  // happy breakdown: declared exact (gmres.py:245-248, :262-268)
+        c->stopped = 1;
+        c->stopping_id = EXACT_CONVERGENCE_ID;
+        c->finalized = 1;
+        c->rnorm = 0.0;
+        return;
+    }
+    if (j < G.k) {  // at j == k the restart recomputes the residual before the check
+        hist_put(c, hist, c->it, c->rnorm);
+        crit_check(c, c->it, c->rnorm);
+    }
+}
+
+// v_j = w / h_{j,j-1} (0 on happy breakdown)
+template <typename T>
+__global__ void gmres_normalize_kernel(int64_t n, int j, T* __restrict__ V, const T* __restrict__ w, const KrylovCtl* c) {
+    if (c->done) return;
+    if (c->stopped && c->jpos != j) return;
+    const double hj = c->hnorm;
+    T* vj = V + (int64_t)j * n;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        vj[r] = hj == 0.0 ? T(0) : (T)((double)w[r] / hj);
+}
+
+// back-solve of the rotated triangular system at jc = jpos (gmres.py:157-167)
+__global__ void gmres_backsolve_kernel(KrylovCtl* c, double* gm) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (c->done || c->committed) return;
+    GmresView G(gm, c->kdim);
+    const int jc = c->jpos;
+    const bool restart = !c->stopped && jc == G.k;
+    if (!(c->stopped || restart)) return;
+    for (int i = jc - 1; i >= 0; --i) {
+        const double d = G.H[i * G.k + i];
+        if (d == 0.0) {
+            c->breakdown = BD_HESSENBERG;
+            c->breakdown_it = c->it;
+            c->done = 1;
+            return;
+        }
+        double acc = 0.0;
+        for (int q = i + 1; q < jc; ++q) acc += G.H[i * G.k + q] * G.y[q];
+        G.y[i] = (G.g[i] - acc) / d;
+    }
+    c->committed = 1;  // combine pending
+}
+
+// x += M (V y): u = sum_i y_i v_i row-wise, then the block-Jacobi of u
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_combine_kernel(RowBlocks rb, const T* __restrict__ V, T* __restrict__ x, int64_t xs, KrylovCtl* c,
+                     const double* gm) {
+    if (c->done || !c->committed) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int jc = c->jpos;
+    const double* y = gm + (size_t)(c->kdim + 1) * c->kdim + 3 * (size_t)c->kdim + 1;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T u = T(0);
+        if (lane < bs)
+            for (int q = 0; q < jc; ++q) u += (T)y[q] * V[(int64_t)q * rb.n + r0 + lane];
+        if (rb.J.nblocks) u = jacobi_row<T>(rb.J, b, bs, lane, u);
+        if (lane < bs) x[(r0 + lane) * xs] += u;
+    }
+}
+
+// after the commit: a stopped solve is finished; a restart keeps going
+__global__ void gmres_after_commit_kernel(KrylovCtl* c) {
+    if (threadIdx.x != 0 || blockIdx.x != 0 || c->done) return;
+    if (c->committed) {
+        c->committed = 0;
+        if (c->stopped) c->done = 1;
+    } else if (c->stopped) {
+        c->done = 1;  // stopped with nothing to commit (jc = 0)
+    }
+}
+
+}  // namespace b200sp
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace b200sp;
+
+static RowBlocks make_rb(int64_t n, int64_t nb, const int32_t* starts, const int64_t* offs, const uint8_t* prec,
+                         const void* storage) {
+    return RowBlocks{n, JacobiView{nb, starts, (const long long*)offs, prec, (const unsigned char*)storage}};
+}
+
+#define KRY_LAUNCH(kernel, units, per_block, ...)                                                     \
+    do {                                                                                              \
+        kernel<<<kry_grid((units), (per_block)), KRY_BLOCK, 0, as_stream(stream)>>>(__VA_ARGS__);     \
+        count_launch();                                                                               \
+        return check_launch(#kernel);                                                                 \
+    } while (0)
+
+#define JAC_ARGS int64_t jnb, const int32_t *jstarts, const int64_t *joffs, const uint8_t *jprec, const void *jstore
+#define RB(n) make_rb((n), jnb, jstarts, joffs, jprec, jstore)
+#define RB_UNITS(n) (jnb ? jnb * 32 : ((n) + 31) / 32 * 32)
+
+extern "C" {
+
+int64_t b200sp_krylov_ctl_bytes(void) { return (int64_t)sizeof(KrylovCtl); }
+int64_t b200sp_krylov_part_elems(void) { return (int64_t)KRY_NRED * KRY_MAX_GRID; }
+
+int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,
+                           int32_t needs_residual, int32_t hist_cap, int32_t kdim, void* stream) {
+    B200SP_REQUIRE(n_crit >= 0 && n_crit <= KRY_MAX_CRIT, B200SP_EINVAL, "krylov: at most %d criteria", KRY_MAX_CRIT);
+    KrylovCtl h;
+    memset(&h, 0, sizeof(h));
+    h.n_crit = n_crit;
+    for (int i = 0; i < n_crit; ++i) {
+        h.crit_type[i] = crit_type[i];
+        h.crit_param[i] = crit_param[i];
+    }
+    h.needs_residual = needs_residual;
+    h.hist_cap = hist_cap;
+    h.kdim = kdim;
+    B200SP_CHECK_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, as_stream(stream)));
+    B200SP_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));  // &h is a stack buffer
+    return B200SP_OK;
+}
+
+// status: ints [it, stopped, stopping_id, finalized, done, breakdown, breakdown_it, jpos]
+//         doubles [baseline, rnorm, rho, alpha, omega, snorm, hnorm, sigma]
+int b200sp_krylov_status(const void* ctl, int32_t* out_i, double* out_d, void* stream) {
+    KrylovCtl h;
+    B200SP_CHECK_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, as_stream(stream)));
+    B200SP_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    const int iv[8] = {h.it, h.stopped, h.stopping_id, h.finalized, h.done, h.breakdown, h.breakdown_it, h.jpos};
+    const double dv[8] = {h.baseline, h.rnorm, h.rho, h.alpha, h.omega, h.snorm, h.hnorm, h.sigma};
+    memcpy(out_i, iv, sizeof(iv));
+    memcpy(out_d, dv, sizeof(dv));
+    return B200SP_OK;
+}
+
+// host-side stop (TimeLimit): mark stopped with the given id
+__global__ void krylov_force_stop_kernel(KrylovCtl* c, int id, int gmres) {
+    if (c->stopped || c->done) return;
+    c->stopped = 1;
+    c->stopping_id = id;
+    c->finalized = 1;
+    if (!gmres) c->done = 1;
+}
+int b200sp_krylov_force_stop(void* ctl, int32_t stopping_id, int32_t gmres, void* stream) {
+    krylov_force_stop_kernel<<<1, 1, 0, as_stream(stream)>>>((KrylovCtl*)ctl, stopping_id, gmres);
+    count_launch();
+    return check_launch("krylov_force_stop");
+}
+
+const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
+    const KrylovCtl* c = (const KrylovCtl*)ctl;
+    return which == 1 ? &c->stopped : &c->done;
+}
+
+#define KRYLOV_T(T, SUF)                                                                                          \
+    int b200sp_cg_init_##SUF(int64_t n, const T* r, T* z, T* p, JAC_ARGS, void* ctl, double* part, double* hist,  \
+                             void* stream) {                                                                      \
+        KRY_LAUNCH(cg_init_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), r, z, p, (KrylovCtl*)ctl, part, hist);       \
+    }                                                                                                             \
+    int b200sp_cg_step1_##SUF(int64_t n, T* p, const T* z, const void* ctl, void* stream) {                        \
+        KRY_LAUNCH(cg_step1_kernel<T>, n, KRY_BLOCK, n, p, z, (const KrylovCtl*)ctl);                             \
+    }                                                                                                             \
+    int b200sp_cg_sigma_##SUF(int64_t n, const T* p, const T* q, void* ctl, double* part, void* stream) {          \
+        KRY_LAUNCH(cg_sigma_kernel<T>, n, KRY_BLOCK, n, p, q, (KrylovCtl*)ctl, part);                             \
+    }                                                                                                             \
+    int b200sp_cg_step2_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* p, const T* q, T* z, JAC_ARGS,           \
+                              void* ctl, double* part, double* hist, void* stream) {                              \
+        KRY_LAUNCH(cg_step2_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), x, xs, r, p, q, z, (KrylovCtl*)ctl, part,   \
+                   hist);                                                                                         \
+    }                                                                                                             \
+    int b200sp_bicgstab_init_##SUF(int64_t n, const T* b, int64_t bs, const T* r, T* rt, T* p, T* v, T* s, T* t,   \
+                                   T* y, T* z, void* ctl, double* part, double* hist, void* stream) {             \
+        KRY_LAUNCH(bicg_init_kernel<T>, n, KRY_BLOCK, n, b, bs, r, rt, p, v, s, t, y, z, (KrylovCtl*)ctl, part,   \
+                   hist);                                                                                         \
+    }                                                                                                             \
+    int b200sp_bicgstab_step1_##SUF(int64_t n, const T* r, T* p, const T* v, T* y, JAC_ARGS, const void* ctl,     \
+                                    void* stream) {                                                               \
+        KRY_LAUNCH(bicg_step1_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), r, p, v, y, (const KrylovCtl*)ctl);       \
+    }                                                                                                             \
+    int b200sp_bicgstab_gamma_##SUF(int64_t n, const T* rt, const T* v, void* ctl, double* part, void* stream) {  \
+        KRY_LAUNCH(bicg_gamma_kernel<T>, n, KRY_BLOCK, n, rt, v, (KrylovCtl*)ctl, part);                          \
+    }                                                                                                             \
+    int b200sp_bicgstab_step2_##SUF(int64_t n, const T* r, const T* v, T* s, T* z, JAC_ARGS, void* ctl,           \
+                                    double* part, double* hist, void* stream) {                                   \
+        KRY_LAUNCH(bicg_step2_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), r, v, s, z, (KrylovCtl*)ctl, part, hist); \
+    }                                                                                                             \
+    int b200sp_bicgstab_tst_##SUF(int64_t n, const T* t, const T* s, void* ctl, double* part, void* stream) {     \
+        KRY_LAUNCH(bicg_tst_kernel<T>, n, KRY_BLOCK, n, t, s, (KrylovCtl*)ctl, part);                             \
+    }                                                                                                             \
+    int b200sp_bicgstab_step3_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* s, const T* t, const T* y,        \
+                                    const T* z, const T* rt, void* ctl, double* part, double* hist,               \
+                                    void* stream) {                                                               \
+        KRY_LAUNCH(bicg_step3_kernel<T>, n, KRY_BLOCK, n, x, xs, r, s, t, y, z, rt, (KrylovCtl*)ctl, part, hist); \
+    }                                                                                                             \
+    int b200sp_gmres_reset_##SUF(int64_t n, const T* r, void* ctl, double* part, double* gm, double* hist,        \
+                                 int32_t first, void* stream) {                                                   \
+        KRY_LAUNCH(gmres_reset_kernel<T>, n, KRY_BLOCK, n, r, (KrylovCtl*)ctl, part, gm, hist, first);            \
+    }                                                                                                             \
+    int b200sp_gmres_scale_v0_##SUF(int64_t n, const T* r, T* V, const void* ctl, void* stream) {                 \
+        KRY_LAUNCH(gmres_scale_v0_kernel<T>, n, KRY_BLOCK, n, r, V, (const KrylovCtl*)ctl);                       \
+    }                                                                                                             \
+    int b200sp_gmres_dot0_##SUF(int64_t n, int32_t j, const T* V, const T* w, void* ctl, double* part, double* gm, \
+                                void* stream) {                                                                   \
+        KRY_LAUNCH(gmres_dot0_kernel<T>, n, KRY_BLOCK, n, j, V, w, (KrylovCtl*)ctl, part, gm);                    \
+    }                                                                                                             \
+    int b200sp_gmres_mgs_##SUF(int64_t n, int32_t j, int32_t i, const T* V, T* w, void* ctl, double* part,        \
+                               double* gm, double* hist, void* stream) {                                          \
+        KRY_LAUNCH(gmres_mgs_kernel<T>, n, KRY_BLOCK, n, j, i, V, w, (KrylovCtl*)ctl, part, gm, hist);            \
+    }                                                                                                             \
+    int b200sp_gmres_normalize_##SUF(int64_t n, int32_t j, T* V, const T* w, const void* ctl, void* stream) {     \
+        KRY_LAUNCH(gmres_normalize_kernel<T>, n, KRY_BLOCK, n, j, V, w, (const KrylovCtl*)ctl);                   \
+    }                                                                                                             \
+    int b200sp_gmres_combine_##SUF(int64_t n, const T* V, T* x, int64_t xs, JAC_ARGS, void* ctl, const double* gm, \
+                                   void* stream) {                                                                \
+        KRY_LAUNCH(gmres_combine_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), V, x, xs, (KrylovCtl*)ctl, gm);        \
+    }
+
+KRYLOV_T(double, f64)
+KRYLOV_T(float, f32)
+
+int b200sp_gmres_backsolve(void* ctl, double* gm, void* stream) {
+    gmres_backsolve_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl, gm);
+    count_launch();
+    return check_launch("gmres_backsolve");
+}
+int b200sp_gmres_after_commit(void* ctl, void* stream) {
+    gmres_after_commit_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl);
+    count_launch();
+    return check_launch("gmres_after_commit");
+}
+int64_t b200sp_gmres_workspace_elems(int32_t k) { return (int64_t)(k + 1) * k + 3 * (int64_t)k + 1 + k; }
+
+}  // extern "C"

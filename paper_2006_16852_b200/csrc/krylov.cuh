@@ -1,0 +1,115 @@
+// Shared pieces of the device-resident Krylov solvers.
+//
+// A solve keeps ALL of its control state on the device (KrylovCtl): the
+// iteration counter, per-solve scalars (rho, alpha, omega, ...), the stopping
+// status and the stopping criteria. Every reduction ends in a deterministic
+// "last block" epilogue (ticket counter, partials summed in block order) that
+// also takes the solver's scalar decisions -- the reference's host-side
+// _safe_div / breakdown tests / criterion checks (src/solvers/steps.py:21-28,
+// src/solvers/krylov.py:56-76, src/stop.py:118-246) -- so a whole batch of
+// iterations runs as one CUDA graph with no host round trip.
+#pragma once
+
+#include "common.cuh"
+#include "jacobi.cuh"
+
+namespace b200sp {
+
+constexpr int KRY_BLOCK = 256;
+constexpr int KRY_MAX_GRID = kNumSMs * 8;
+constexpr int KRY_MAX_CRIT = 8;
+constexpr int KRY_NRED = 4;  // partial-sum slots per reduction
+
+enum CritType : int { CRIT_ITERATION = 1, CRIT_RNR = 2 };
+enum Breakdown : int { BD_NONE = 0, BD_CG_SIGMA = 1, BD_RHO = 2, BD_GAMMA = 3, BD_TT = 4, BD_HESSENBERG = 5 };
+constexpr int EXACT_CONVERGENCE_ID = 254;  // src/solvers/gmres.py:31
+
+struct KrylovCtl {
+    // status (m = 1): src/stop.py:30-31 STOPPING_STATUS_DTYPE
+    int it;            // completed iterations (half-iterations for BiCGSTAB)
+    int stopped;
+    int stopping_id;
+    int finalized;
+    int done;          // no more work: stopped (and committed) or breakdown
+    int breakdown;     // Breakdown code
+    int breakdown_it;  // BreakdownInfo.iteration
+    int mid_final;     // BiCGSTAB: stopped at the mid check, x += alpha y pending
+    int n_crit;
+    int needs_residual;
+    int hist_cap;
+    int jpos;          // GMRES segment position j
+    int kdim;          // GMRES restart length
+    int committed;     // GMRES: partial segment folded into x
+    int pad[2];
+    int crit_type[KRY_MAX_CRIT];
+    double crit_param[KRY_MAX_CRIT];
+    double baseline;   // ||r0||
+    double rho, rho_prev, sigma, alpha, beta, omega, gamma, ts, tt, rnorm, snorm, hnorm;
+    unsigned ticket[4];
+};
+
+// ---------------------------------------------------------------------------
+// criteria: Combined ORs the children in order; child i stamps id i+1
+// (src/stop.py:226-246); RNR stops when ||r|| <= factor * ||r0||
+// (src/stop.py:187-196); Iteration when it >= max (src/stop.py:95-106).
+// ---------------------------------------------------------------------------
+__device__ inline void crit_check(KrylovCtl* c, int it, double nrm) {
+    if (c->stopped) return;
+    for (int i = 0; i < c->n_crit; ++i) {
+        bool fire = false;
+        if (c->crit_type[i] == CRIT_ITERATION) fire = it >= (int)c->crit_param[i];
+        else if (c->crit_type[i] == CRIT_RNR) fire = nrm <= c->crit_param[i] * c->baseline;
+        if (fire) {
+            c->stopped = 1;
+            c->stopping_id = i + 1;
+            c->finalized = 1;  // solvers pass set_finalized=True
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ double safe_div(double num, double den) {
+    // num/den with 0/0 -> 0 (src/solvers/steps.py:21-28)
+    if (den == 0.0 && num == 0.0) return 0.0;
+    return num / den;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic grid reduction of NV values with a last-block epilogue.
+// Returns true in thread 0 of the last block, with the totals in `tot`.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ bool grid_reduce(double (&v)[NV], double* part, unsigned* ticket, double (&tot)[NV]) {
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ bool last;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const double s = block_sum(v[k], sh);
+        if (threadIdx.x == 0) part[k * KRY_MAX_GRID + blockIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile double*)part)[k * KRY_MAX_GRID + b];
+            tot[k] = warp_sum(s);
+        }
+    }
+    if (threadIdx.x == 0) *ticket = 0;
+    return threadIdx.x == 0;
+}
+
+inline int kry_grid(int64_t units, int per_block) {
+    int64_t g = ceil_div(units, per_block);
+    if (g > KRY_MAX_GRID) g = KRY_MAX_GRID;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+}  // namespace b200sp

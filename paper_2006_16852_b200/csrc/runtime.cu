@@ -15,6 +15,9 @@ namespace b200sp {
 
 static thread_local char g_err[512] = "";
 static std::atomic<long long> g_launches{0};
+static thread_local const int* g_guard = nullptr;
+
+const int* current_guard() { return g_guard; }
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -236,6 +239,7 @@ extern "C" {
 const char* b200sp_last_error(void) { return g_err; }
 long long b200sp_launch_count(void) { return g_launches.load(); }
 int b200sp_version(void) { return B200SP_ABI_VERSION; }
+void b200sp_set_guard(const int32_t* guard) { g_guard = guard; }
 int64_t b200sp_reduce_workspace_elems(void) { return (int64_t)kNumSMs * 4 * RED_MAX_COLS; }
 
 int b200sp_device_sync(void) {

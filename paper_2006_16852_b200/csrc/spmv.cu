@@ -21,35 +21,65 @@ namespace b200sp {
 // ===========================================================================
 // Csr, classical strategy: one sub-warp of SW lanes per row (SW = 1..32).
 // ===========================================================================
+// Each sub-warp owns U consecutive rows per step and issues the loads of all
+// U rows before any FMA: U x SW independent gathers in flight per sub-warp
+// (one row per warp leaves HBM latency exposed: the first B200 measurement of
+// the one-row variant reached 32% of peak on C2).
+template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1); };
+
 template <typename T, int SW, bool XIN>
 __global__ void __launch_bounds__(256)
 csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
                      const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
                      T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
                      const T* __restrict__ xin, int64_t xins) {
+    if (alpha.skip()) return;
+    constexpr int U = ClassicalRows<SW>::v;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & (SW - 1);
     const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
-    for (int64_t row = tid / SW; row < n; row += nsw) {
-        const int s = ld_stream(rp + row);
-        const int e = ld_stream(rp + row + 1);
-        T s0 = 0, s1 = 0;
-        int k = s + lane;
-        // two independent accumulators: two gathers in flight per lane
-        for (; k + SW < e; k += 2 * SW) {
-            const int c0 = ld_stream(ci + k), c1 = ld_stream(ci + k + SW);
-            const T v0 = ld_stream(v + k), v1 = ld_stream(v + k + SW);
-            s0 += v0 * ld_gather(b + (int64_t)c0 * bs);
-            s1 += v1 * ld_gather(b + (int64_t)c1 * bs);
+    for (int64_t row0 = (tid / SW) * U; row0 < n; row0 += nsw * U) {
+        int s[U], len[U];
+        int ptr_next = ld_stream(rp + row0);
+        int maxlen = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            s[u] = ptr_next;
+            ptr_next = (row0 + u < n) ? ld_stream(rp + row0 + u + 1) : ptr_next;
+            len[u] = ptr_next - s[u];
+            maxlen = max(maxlen, len[u]);
         }
-        if (k < e) s0 += ld_stream(v + k) * ld_gather(b + (int64_t)ld_stream(ci + k) * bs);
-        T sum = subwarp_sum<SW>(s0 + s1);
-        if (lane == 0) {
-            T r = a * sum;
-            if (XIN) r += bt * xin[row * xins];
-            x[row * xs] = r;
+        T acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = 0;
+        for (int k = lane; k < maxlen; k += SW) {
+            int c[U];
+            T vv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool ok = k < len[u];
+                c[u] = ok ? ld_stream(ci + s[u] + k) : -1;
+                vv[u] = ok ? ld_stream(v + s[u] + k) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = subwarp_sum<SW>(acc[u]);
+        if (lane < U) {
+            T mine = acc[0];
+#pragma unroll
+            for (int u = 1; u < U; ++u)
+                if (lane == u) mine = acc[u];
+            const int64_t row = row0 + lane;
+            if (row < n) {
+                T r = a * mine;
+                if (XIN) r += bt * xin[row * xins];
+                x[row * xs] = r;
+            }
         }
     }
 }
@@ -59,7 +89,7 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
                              int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be,
                              const T* xin, int64_t xins, cudaStream_t st) {
     const int block = 256;
-    int grid = grid_for(n * SW, block, 8);
+    int grid = grid_for(ceil_div(n, ClassicalRows<SW>::v) * SW, block, 8);
     if (xin)
         csr_classical_kernel<T, SW, true><<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
     else
@@ -72,7 +102,7 @@ static int csr_classical(int64_t n, const int* rp, const int* ci, const T* v, co
                          const T* xin, int64_t xins, int subwarp, void* stream) {
     if (n == 0) return B200SP_OK;
     cudaStream_t st = as_stream(stream);
-    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     switch (subwarp) {
         case 1: launch_classical<T, 1>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
         case 2: launch_classical<T, 2>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
@@ -85,6 +115,143 @@ static int csr_classical(int64_t n, const int* rp, const int* ci, const T* v, co
     }
     count_launch();
     return check_launch("csr_classical");
+}
+
+// ===========================================================================
+// Csr, stream strategy (row blocks staged through shared memory).
+// A CTA of R threads owns R consecutive rows. Their nonzeros are one
+// contiguous range; it is streamed in chunks of STREAM_CAP entries with
+// 128-bit loads (4 entries per thread per step, all independent), the
+// products v*b[c] go to shared memory, and thread t then sums row t from
+// shared memory. Every global load is coalesced and vectorised and no warp
+// reduction is needed -- the instruction count per nonzero is close to Ell's
+// while keeping the Csr layout. Rows longer than a chunk are handled by
+// accumulating across chunks (correct, but serial: skewed matrices use the
+// load-balanced strategy).
+// ===========================================================================
+template <typename T> struct StreamCap { static constexpr int v = 4096; };
+template <> struct StreamCap<float> { static constexpr int v = 8192; };
+
+template <typename T> struct Quad;
+template <> struct Quad<double> {
+    __device__ static void load(const double* p, double (&o)[4]) {
+        double2 a = ld_stream_v2(p), b = ld_stream_v2(p + 2);
+        o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+    }
+    __device__ static void store(double* s, const double (&o)[4]) {
+        reinterpret_cast<double2*>(s)[0] = make_double2(o[0], o[1]);
+        reinterpret_cast<double2*>(s)[1] = make_double2(o[2], o[3]);
+    }
+};
+template <> struct Quad<float> {
+    __device__ static void load(const float* p, float (&o)[4]) {
+        float4 a = ld_stream_v4(p);
+        o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+    }
+    __device__ static void store(float* s, const float (&o)[4]) {
+        reinterpret_cast<float4*>(s)[0] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+};
+
+template <typename T> struct StreamTpr { static constexpr int v = 2; };  // threads per row
+template <> struct StreamTpr<float> { static constexpr int v = 1; };
+
+constexpr int STREAM_NT = 256;  // threads per CTA
+template <typename T> constexpr int stream_rows() { return STREAM_NT / StreamTpr<T>::v; }
+
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(STREAM_NT)
+csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
+                  const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+                  int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+                  int CAP) {
+    if (alpha.skip()) return;
+    constexpr int TPR = StreamTpr<T>::v;
+    constexpr int NT = STREAM_NT;
+    constexpr int R = NT / TPR;
+    constexpr int UQ = 2;  // quads per thread in flight per step
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    T* s_prod = reinterpret_cast<T*>(s_raw);
+    const int t = threadIdx.x;
+    const int my_row = t / TPR, sub = t % TPR;
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    const int rows = (int)min((int64_t)R, n - r0);
+    const int row_s = my_row < rows ? ld_stream(rp + r0 + my_row) : 0;
+    const int row_e = my_row < rows ? ld_stream(rp + r0 + my_row + 1) : 0;
+    const int seg_s = ld_stream(rp + r0);
+    const int seg_e = ld_stream(rp + r0 + rows);
+    T acc0 = 0, acc1 = 0;
+    for (int64_t lo = seg_s & ~3; lo < seg_e; lo += CAP) {
+        const int64_t hi = min(lo + (int64_t)CAP, (int64_t)seg_e);
+        const int nq = (int)((hi - lo + 3) >> 2);
+        for (int q0 = t; q0 < nq; q0 += NT * UQ) {
+            int cc[UQ][4];
+            T vv[UQ][4];
+#pragma unroll
+            for (int u = 0; u < UQ; ++u) {
+                const int q = q0 + u * NT;
+                const int64_t e = lo + 4 * (int64_t)q;
+                if (q < nq && e + 4 <= hi) {
+                    int4 c4 = ld_stream_v4(ci + e);
+                    cc[u][0] = c4.x; cc[u][1] = c4.y; cc[u][2] = c4.z; cc[u][3] = c4.w;
+                    Quad<T>::load(v + e, vv[u]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool ok = q < nq && e + i < hi;
+                        cc[u][i] = ok ? ld_stream(ci + e + i) : 0;
+                        vv[u][i] = ok ? ld_stream(v + e + i) : T(0);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UQ; ++u) {
+                const int q = q0 + u * NT;
+                if (q < nq) {
+                    T p[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) p[i] = vv[u][i] * ld_gather(b + (int64_t)cc[u][i] * bs);
+                    Quad<T>::store(s_prod + 4 * q, p);
+                }
+            }
+        }
+        __syncthreads();
+        const int a0 = (int)(max((int64_t)row_s, lo) - lo), a1 = (int)(min((int64_t)row_e, hi) - lo);
+        int k = a0 + sub;
+        for (; k + TPR < a1; k += 2 * TPR) {
+            acc0 += s_prod[k];
+            acc1 += s_prod[k + TPR];
+        }
+        if (k < a1) acc0 += s_prod[k];
+        __syncthreads();
+    }
+    T sum = subwarp_sum<TPR>(acc0 + acc1);
+    if (sub == 0 && my_row < rows) {
+        const int64_t row = r0 + my_row;
+        T out = alpha.get() * sum;
+        if (XIN) out += beta.get() * xin[row * xins];
+        x[row * xs] = out;
+    }
+}
+
+template <typename T>
+static int csr_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
+                      int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
+                      const T* beta_dev, const T* xin, int64_t xins, int chunk_cap, void* stream) {
+    if (n == 0) return B200SP_OK;
+    B200SP_REQUIRE(aligned16(ci) && aligned16(v), B200SP_EINVAL, "csr stream: col_idxs/vals must be 16-byte aligned");
+    B200SP_REQUIRE(chunk_cap >= 4 && chunk_cap % 4 == 0 && chunk_cap <= StreamCap<T>::v, B200SP_EINVAL,
+                   "csr stream: chunk_cap must be a multiple of 4 in [4, %d]", StreamCap<T>::v);
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
+    const unsigned grid = (unsigned)ceil_div(n, stream_rows<T>());
+    const size_t smem = (size_t)chunk_cap * sizeof(T);
+    if (xin)
+        csr_stream_kernel<T, true><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap);
+    else
+        csr_stream_kernel<T, false><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap);
+    count_launch();
+    return check_launch("csr_stream");
 }
 
 // ===========================================================================
@@ -135,6 +302,7 @@ csr_lb_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
               int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
               const int* __restrict__ coords, int* __restrict__ carry_row,
               T* __restrict__ carry_val) {
+    if (alpha.skip()) return;
     constexpr int IPT = LbIpt<T>::v;
     constexpr int TILE = LB_BLOCK * IPT;
     __shared__ int s_rowend[TILE];
@@ -239,6 +407,7 @@ template <typename T>
 __global__ void csr_lb_fixup_kernel(int64_t n, int64_t ntiles, const int* __restrict__ carry_row,
                                     const T* __restrict__ carry_val, T* __restrict__ x, int64_t xs,
                                     Coef<T> alpha) {
+    if (alpha.skip()) return;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
     const int row = carry_row[t];
@@ -256,7 +425,7 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
                   int* carry_row, T* carry_val, void* stream) {
     if (n == 0) return B200SP_OK;
     cudaStream_t st = as_stream(stream);
-    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int64_t ntiles = ceil_div(n + nnz, lb_tile<T>());
     if (xin)
         csr_lb_kernel<T, true><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
@@ -269,66 +438,131 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
 
 // ===========================================================================
 // Coo: warp-chunked segmented reduction over the (row, col)-sorted entries.
-// Each warp owns a contiguous chunk of entries, streams it 32 entries per
-// round (coalesced), reduces equal-row runs with a shuffle scan-by-key and
-// writes every row it owns completely. Rows that straddle a chunk boundary
-// leave per-chunk partials that a fix-up pass sums in chunk order, so the
-// result is deterministic (no floating-point atomics) and needs no pre-zero
-// pass over x.
+// Each warp owns a contiguous chunk of 32*COO_E entries; every lane loads
+// COO_E consecutive entries with 128-bit streaming loads (the warp's loads
+// are fully coalesced and all independent), reduces its equal-row runs in
+// registers, and one shuffle segmented scan per chunk joins runs that cross
+// lanes. Rows owned by the chunk are written directly; rows that straddle a
+// chunk boundary leave per-chunk partials that a fix-up pass sums in chunk
+// order, so the result is deterministic (no floating-point atomics) and needs
+// no pre-zero pass over x.
 // ===========================================================================
 constexpr int COO_BLOCK = 256;
 
-template <typename T, bool XIN>
+template <typename T, bool XIN, bool VEC, int E>
 __global__ void __launch_bounds__(COO_BLOCK)
-coo_kernel(int64_t nnz, int chunk, const int* __restrict__ rows, const int* __restrict__ cols,
+coo_kernel(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
            const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
            int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
            T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    if (alpha.skip()) return;
+    constexpr int CHUNK = 32 * E;
     const int lane = threadIdx.x & 31;
     const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t e0 = c * chunk;
+    const int64_t e0 = c * CHUNK;
     if (e0 >= nnz) return;
-    const int64_t e1 = min(e0 + (int64_t)chunk, nnz);
+    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
     const int head_row = rows[e0], tail_row = rows[e1 - 1];
     const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
     const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
 
-    int run_row = INT_MIN;
-    T run = 0;
-    for (int64_t base = e0; base < e1; base += 32) {
-        const int64_t k = base + lane;
-        const bool valid = k < e1;
-        const int r = valid ? ld_stream(rows + k) : INT_MAX;
-        T p = valid ? ld_stream(vals + k) * ld_gather(b + (int64_t)ld_stream(cols + k) * bs) : T(0);
-        // inclusive scan by (sorted) key
+    const int64_t l0 = e0 + (int64_t)lane * E;
+    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
+    int r[E], cc[E];
+    T vv[E];
+    if (VEC && cnt == E) {
+        ld_stream_vec<E>(rows + l0, r);
+        ld_stream_vec<E>(cols + l0, cc);
+        ld_stream_vec<E>(vals + l0, vv);
+    } else {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            T pn = __shfl_up_sync(0xffffffffu, p, o);
-            int rn = __shfl_up_sync(0xffffffffu, r, o);
-            if (lane >= o && rn == r) p += pn;
+        for (int i = 0; i < E; ++i) {
+            const bool ok = i < cnt;
+            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
+            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
+            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
         }
-        if (r == run_row) p += run;
-        int rnext = __shfl_down_sync(0xffffffffu, r, 1);
-        if (lane == 31) rnext = (k + 1 < e1) ? rows[k + 1] : INT_MIN;
-        if (valid && k == e1 - 1) rnext = INT_MIN;
-        const bool is_end = valid && rnext != r;
-        if (is_end) {
-            const bool at_end = (k == e1 - 1);
-            const bool shared = (r == head_row && head_shared) || (at_end && tail_shared);
-            if (!shared) {
-                T out = a * p;
-                if (XIN) out += bt * xin[(int64_t)r * xins];
-                x[(int64_t)r * xs] = out;
-            } else if (r == head_row) {
-                carry_head[c] = p;
-            } else {
-                carry_tail[c] = p;
+    }
+    T p[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
+
+    // lane-local runs: the first completed run may continue from earlier
+    // lanes (needs the scan), later completed runs are final
+    int cur = r[0], first_row = INT_MIN;
+    T acc = 0, first_val = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        if (i < cnt) {
+            if (r[i] != cur) {
+                if (first_row == INT_MIN) {
+                    first_row = cur;
+                    first_val = acc;
+                } else {
+                    T out = a * acc;
+                    if (XIN) out += bt * xin[(int64_t)cur * xins];
+                    x[(int64_t)cur * xs] = out;
+                }
+                cur = r[i];
+                acc = 0;
             }
+            acc += p[i];
         }
-        run_row = __shfl_sync(0xffffffffu, is_end ? INT_MIN : r, 31);
-        run = __shfl_sync(0xffffffffu, p, 31);
+    }
+    // a lane's first run continues the previous lane's last run only if the
+    // rows match (a new row may start exactly at a lane boundary)
+    int prev_last = __shfl_up_sync(0xffffffffu, cur, 1);
+    const int next_first = __shfl_down_sync(0xffffffffu, r[0], 1);
+    const bool continues = lane > 0 && cnt > 0 && r[0] == prev_last;
+    // warp segmented inclusive scan of carry-outs; a segment starts at every
+    // lane that closed a run or does not continue its predecessor
+    T sv = acc;
+    int sf = (first_row != INT_MIN) || !continues;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T vn = __shfl_up_sync(0xffffffffu, sv, o);
+        int fn = __shfl_up_sync(0xffffffffu, sf, o);
+        if (lane >= o) {
+            if (!sf) sv += vn;
+            sf |= fn;
+        }
+    }
+    T excl = __shfl_up_sync(0xffffffffu, sv, 1);
+    if (!continues) excl = 0;
+    const int last_lane = (int)((e1 - 1 - e0) / E);  // lane holding the chunk's last entry
+    if (first_row != INT_MIN) {
+        const T val = first_val + excl;
+        if (first_row == head_row && head_shared) {
+            carry_head[c] = val;
+        } else {
+            T out = a * val;
+            if (XIN) out += bt * xin[(int64_t)first_row * xins];
+            x[(int64_t)first_row * xs] = out;
+        }
+    }
+    // last run ends exactly at this lane's boundary: complete here
+    if (cnt > 0 && lane < last_lane && next_first != cur) {
+        if (cur == head_row && head_shared) {
+            carry_head[c] = sv;
+        } else {
+            T out = a * sv;
+            if (XIN) out += bt * xin[(int64_t)cur * xins];
+            x[(int64_t)cur * xs] = out;
+        }
+    }
+    if (lane == last_lane) {
+        const bool single = head_row == tail_row;
+        if (!(tail_shared || (single && head_shared))) {
+            T out = a * sv;
+            if (XIN) out += bt * xin[(int64_t)tail_row * xins];
+            x[(int64_t)tail_row * xs] = out;
+        } else if (single) {
+            carry_head[c] = sv;
+        } else {
+            carry_tail[c] = sv;
+        }
     }
 }
 
@@ -337,6 +571,7 @@ __global__ void coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const 
                                  const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
                                  T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
                                  const T* __restrict__ xin, int64_t xins) {
+    if (alpha.skip()) return;
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
     const int64_t e0 = c * chunk, e1 = min(e0 + (int64_t)chunk, nnz);
@@ -364,20 +599,31 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
                     const T* beta_dev, const T* xin, int64_t xins, T* carry_head, T* carry_tail,
                     void* stream) {
     if (nnz == 0) return B200SP_OK;
-    B200SP_REQUIRE(chunk > 0 && chunk % 32 == 0, B200SP_EINVAL, "coo: chunk must be a positive multiple of 32");
+    B200SP_REQUIRE(chunk == 128 || chunk == 256, B200SP_EINVAL, "coo: chunk must be 128 or 256 (got %d)", chunk);
     cudaStream_t st = as_stream(stream);
-    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int64_t nchunks = ceil_div(nnz, chunk);
     const int64_t threads = nchunks * 32;
     const unsigned grid = (unsigned)ceil_div(threads, COO_BLOCK);
     const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
+    const bool vec = aligned16(rows) && aligned16(cols) && aligned16(vals);
+#define COO_LAUNCH(XI, VE)                                                                              \
+    do {                                                                                                \
+        if (chunk == 256)                                                                               \
+            coo_kernel<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, \
+                                                                 be, xin, xins, carry_head, carry_tail); \
+        else                                                                                            \
+            coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, \
+                                                                 be, xin, xins, carry_head, carry_tail); \
+    } while (0)
     if (xin) {
-        coo_kernel<T, true><<<grid, COO_BLOCK, 0, st>>>(nnz, chunk, rows, cols, vals, b, bs, x, xs, al, be, xin, xins, carry_head, carry_tail);
+        if (vec) COO_LAUNCH(true, true); else COO_LAUNCH(true, false);
         coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nnz, chunk, nchunks, rows, carry_head, carry_tail, x, xs, al, be, xin, xins);
     } else {
-        coo_kernel<T, false><<<grid, COO_BLOCK, 0, st>>>(nnz, chunk, rows, cols, vals, b, bs, x, xs, al, be, xin, xins, carry_head, carry_tail);
+        if (vec) COO_LAUNCH(false, true); else COO_LAUNCH(false, false);
         coo_fixup_kernel<T, false><<<fgrid, 256, 0, st>>>(nnz, chunk, nchunks, rows, carry_head, carry_tail, x, xs, al, be, xin, xins);
     }
+#undef COO_LAUNCH
     count_launch(2);
     return check_launch("coo_spmv");
 }
@@ -386,6 +632,7 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
 template <typename T>
 __global__ void rows_scale_kernel(int64_t count, const int* __restrict__ rows, T* __restrict__ x,
                                   int64_t xs, Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
+    if (beta.skip()) return;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     const int64_t r = rows[i];
@@ -397,9 +644,40 @@ static int rows_scale(int64_t count, const int* rows, T* x, int64_t xs, T beta, 
                       const T* xin, int64_t xins, void* stream) {
     if (count == 0) return B200SP_OK;
     rows_scale_kernel<T><<<(unsigned)ceil_div(count, 256), 256, 0, as_stream(stream)>>>(
-        count, rows, x, xs, Coef<T>{beta, beta_dev}, xin, xins);
+        count, rows, x, xs, coef(beta, beta_dev), xin, xins);
     count_launch();
     return check_launch("rows_scale");
+}
+
+// Dot product of one row stored at base, base+step, ... (len slots, padding
+// col = -1) with b: UNR independent loads in flight per thread.
+template <typename T, int UNR>
+__device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __restrict__ v, int64_t base,
+                                         int64_t step, int len, const T* __restrict__ b, int64_t bs) {
+    T acc[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc[u] = 0;
+    int k = 0;
+    for (; k + UNR <= len; k += UNR) {
+        int c[UNR];
+        T vv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            c[u] = ld_stream(ci + base + (int64_t)(k + u) * step);
+            vv[u] = ld_stream(v + base + (int64_t)(k + u) * step);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
+    }
+    for (; k < len; ++k) {
+        const int c = ld_stream(ci + base + (int64_t)k * step);
+        if (c >= 0) acc[0] += ld_stream(v + base + (int64_t)k * step) * ld_gather(b + (int64_t)c * bs);
+    }
+    T sum = acc[0];
+#pragma unroll
+    for (int u = 1; u < UNR; ++u) sum += acc[u];
+    return sum;
 }
 
 // ===========================================================================
@@ -411,23 +689,13 @@ __global__ void __launch_bounds__(256)
 ell_kernel(int64_t n, int64_t width, int64_t stride, const int* __restrict__ ci,
            const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
            int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
+    if (alpha.skip()) return;
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
          row += (int64_t)gridDim.x * blockDim.x) {
-        T s0 = 0, s1 = 0;
-        int64_t k = 0;
-        for (; k + 1 < width; k += 2) {
-            const int c0 = ld_stream(ci + k * stride + row), c1 = ld_stream(ci + (k + 1) * stride + row);
-            const T v0 = ld_stream(v + k * stride + row), v1 = ld_stream(v + (k + 1) * stride + row);
-            if (c0 >= 0) s0 += v0 * ld_gather(b + (int64_t)c0 * bs);
-            if (c1 >= 0) s1 += v1 * ld_gather(b + (int64_t)c1 * bs);
-        }
-        if (k < width) {
-            const int c0 = ld_stream(ci + k * stride + row);
-            if (c0 >= 0) s0 += ld_stream(v + k * stride + row) * ld_gather(b + (int64_t)c0 * bs);
-        }
-        T out = a * (s0 + s1);
+        const T sum = strided_dot<T, 4>(ci, v, row, stride, (int)width, b, bs);
+        T out = a * sum;
         if (XIN) out += bt * xin[row * xins];
         x[row * xs] = out;
     }
@@ -440,7 +708,7 @@ static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, con
     if (n == 0) return B200SP_OK;
     B200SP_REQUIRE(stride >= n, B200SP_EINVAL, "ell: stride %lld < rows %lld", (long long)stride, (long long)n);
     cudaStream_t st = as_stream(stream);
-    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int grid = grid_for(n, 256, 16);
     if (xin)
         ell_kernel<T, true><<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
@@ -460,6 +728,7 @@ sellp_kernel(int64_t n, int slice_size, const int* __restrict__ slice_lengths,
              const int* __restrict__ slice_sets, const int* __restrict__ ci, const T* __restrict__ v,
              const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha,
              Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
+    if (alpha.skip()) return;
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
@@ -468,21 +737,8 @@ sellp_kernel(int64_t n, int slice_size, const int* __restrict__ slice_lengths,
         const int64_t local = row - slice * slice_size;
         const int len = slice_lengths[slice];
         const int64_t base = (int64_t)slice_sets[slice] * slice_size + local;
-        T s0 = 0, s1 = 0;
-        int k = 0;
-        for (; k + 1 < len; k += 2) {
-            const int64_t i0 = base + (int64_t)k * slice_size, i1 = i0 + slice_size;
-            const int c0 = ld_stream(ci + i0), c1 = ld_stream(ci + i1);
-            const T v0 = ld_stream(v + i0), v1 = ld_stream(v + i1);
-            if (c0 >= 0) s0 += v0 * ld_gather(b + (int64_t)c0 * bs);
-            if (c1 >= 0) s1 += v1 * ld_gather(b + (int64_t)c1 * bs);
-        }
-        if (k < len) {
-            const int64_t i0 = base + (int64_t)k * slice_size;
-            const int c0 = ld_stream(ci + i0);
-            if (c0 >= 0) s0 += ld_stream(v + i0) * ld_gather(b + (int64_t)c0 * bs);
-        }
-        T out = a * (s0 + s1);
+        const T sum = strided_dot<T, 4>(ci, v, base, slice_size, len, b, bs);
+        T out = a * sum;
         if (XIN) out += bt * xin[row * xins];
         x[row * xs] = out;
     }
@@ -496,7 +752,7 @@ static int sellp_spmv(int64_t n, int slice_size, const int* sl, const int* ss, c
     if (n == 0) return B200SP_OK;
     B200SP_REQUIRE(slice_size > 0, B200SP_EINVAL, "sellp: slice_size must be positive");
     cudaStream_t st = as_stream(stream);
-    Coef<T> al{alpha, alpha_dev}, be{beta, beta_dev};
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int grid = grid_for(n, 256, 16);
     if (xin)
         sellp_kernel<T, true><<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
@@ -554,6 +810,25 @@ int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* rp, const int32_t* c
                                   const float* alpha_dev, float beta, const float* beta_dev,
                                   const float* xin, int64_t xins, int32_t subwarp, void* stream) {
     return csr_classical<float>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, subwarp, stream);
+}
+
+int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v,
+                               const double* b, int64_t bs, double* x, int64_t xs, double alpha,
+                               const double* alpha_dev, double beta, const double* beta_dev,
+                               const double* xin, int64_t xins, int32_t chunk_cap, void* stream) {
+    return csr_stream<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap, stream);
+}
+int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const float* v,
+                               const float* b, int64_t bs, float* x, int64_t xs, float alpha,
+                               const float* alpha_dev, float beta, const float* beta_dev,
+                               const float* xin, int64_t xins, int32_t chunk_cap, void* stream) {
+    return csr_stream<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap, stream);
+}
+int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
+    return value_bytes == 4 ? StreamCap<float>::v : StreamCap<double>::v;
+}
+int32_t b200sp_csr_stream_rows(int32_t value_bytes) {
+    return value_bytes == 4 ? stream_rows<float>() : stream_rows<double>();
 }
 
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes) {

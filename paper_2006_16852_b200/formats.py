@@ -379,17 +379,20 @@ class _Sparse(LinOp):
 # ---------------------------------------------------------------------------
 # Csr (src/formats.py:168-221) + strategies
 # ---------------------------------------------------------------------------
-CSR_STRATEGIES = ("classical", "load_balance", "automatic")
+CSR_STRATEGIES = ("classical", "load_balance", "stream", "automatic")
 
 
 class Csr(_Sparse):
     """Compressed sparse row with an SpMV strategy:
 
-    * ``classical``    -- sub-warp per row (sub-warp = next power of two of
-                          the longest row, capped at 32; Ginkgo's classical);
+    * ``classical``    -- sub-warp per row, several rows in flight per
+                          sub-warp (sub-warp = next power of two of
+                          mean row length / 8, capped at 32);
     * ``load_balance`` -- merge-path tiles of equal (rows + nonzeros) work
                           with a deterministic carry fix-up;
-    * ``automatic``    -- classical unless the row lengths are skewed
+    * ``stream``       -- row blocks whose nonzeros are staged through shared
+                          memory with 128-bit loads, thread-per-row reduction;
+    * ``automatic``    -- stream unless the row lengths are skewed
                           (max > 4 x mean + 64), then load_balance.
     """
 
@@ -453,8 +456,13 @@ class Csr(_Sparse):
     def strategy(self):
         return self._resolved_strategy()
 
-    def set_strategy(self, strategy):
+    def set_strategy(self, strategy, subwarp=None):
+        """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size."""
         self._set_strategy(strategy)
+        if subwarp is not None:
+            if subwarp not in (1, 2, 4, 8, 16, 32):
+                raise Unsupported("subwarp must be a power of two <= 32")
+            self._subwarp = int(subwarp)
 
     def _row_stats(self):
         if self._max_row is None:
@@ -474,13 +482,28 @@ class Csr(_Sparse):
         if n == 0:
             return "classical"
         mean = self.nnz / n
-        return "load_balance" if self._row_stats() > 4 * mean + 64 else "classical"
+        if self._row_stats() > 4 * mean + 64:
+            return "load_balance"
+        return "stream" if self._stream_ok() else "classical"
+
+    def _stream_ok(self):
+        return self._ci.data_ptr() % 16 == 0 and self._v.data_ptr() % 16 == 0
 
     def subwarp(self):
         if self._subwarp is None:
-            longest = max(1, self._row_stats())
-            self._subwarp = min(32, 1 << (longest - 1).bit_length())
+            n = self.size.rows
+            per_lane = max(1, math.ceil(self.nnz / max(n, 1) / 8))
+            self._subwarp = min(32, 1 << (per_lane - 1).bit_length())
         return self._subwarp
+
+    def stream_chunk(self):
+        """Shared-memory staging chunk (entries): one chunk holds a whole row
+        block when rows_per_CTA * longest_row fits, else the maximum."""
+        vb = self._v.element_size()
+        cap = int(_lib.query("csr_stream_capacity", vb))
+        rows = int(_lib.query("csr_stream_rows", vb))
+        need = (rows * max(1, self._row_stats()) + 4 + 3) // 4 * 4
+        return min(cap, need)
 
     def lb_plan(self):
         if self._plan is None:
@@ -515,11 +538,16 @@ class Csr(_Sparse):
     # -- kernels -------------------------------------------------------------------
     def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):
         n = self.size.rows
-        if self._resolved_strategy() == "load_balance":
+        strategy = self._resolved_strategy()
+        if strategy == "load_balance":
             coords, crow, cval = self.lb_plan()
             _lib.call("csr_spmv_lb_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(coords), ptr(crow),
                       ptr(cval), exc.stream)
+        elif strategy == "stream" and self._stream_ok():
+            _lib.call("csr_spmv_stream_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
+                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.stream_chunk(),
+                      exc.stream)
         else:
             _lib.call("csr_spmv_classical_" + suf, n, ptr(self._rp), ptr(self._ci), ptr(self._v),
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.subwarp(), exc.stream)
@@ -550,6 +578,9 @@ COO_CHUNK = 256
 
 class Coo(_Sparse):
     """Coordinate format, entries sorted by (row, col)."""
+
+    #: entries per warp chunk of the SpMV kernel (128 or 256)
+    chunk = COO_CHUNK
 
     def __init__(self, exc, size, row_idxs, col_idxs, vals, index_dtype=None, value_dtype=None):
         super().__init__(exc, size)
@@ -593,7 +624,7 @@ class Coo(_Sparse):
         """carry buffers + the list of rows that hold no entry (prefilled)."""
         if self._ws is None:
             exc = self.exec
-            nch = max(1, math.ceil(self.nnz / COO_CHUNK))
+            nch = max(1, math.ceil(self.nnz / 128))  # covers both chunk sizes
             head = torch.empty(nch, dtype=self._v.dtype, device=exc.device)
             tail = torch.empty(nch, dtype=self._v.dtype, device=exc.device)
             n = self.size.rows
@@ -613,7 +644,7 @@ class Coo(_Sparse):
         head, tail, empty, ne = self._workspace()
         if prefill and ne:
             _lib.call("rows_scale_" + suf, ne, ptr(empty), xp, xs, b_h, b_p, xin, xins, exc.stream)
-        _lib.call("coo_spmv_" + suf, self.nnz, COO_CHUNK, ptr(self._ri), ptr(self._ci), ptr(self._v),
+        _lib.call("coo_spmv_" + suf, self.nnz, self.chunk, ptr(self._ri), ptr(self._ci), ptr(self._v),
                   bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(head), ptr(tail), exc.stream)
 
     def _to_csr(self, **kw):
@@ -944,8 +975,10 @@ _FORMAT_NAMES = {"dense": Dense, "csr": Csr, "coo": Coo, "ell": Ell, "sellp": Se
 def _resolve(target):
     if isinstance(target, str):
         key = target.lower()
-        if key in ("csr_classical", "csr_lb", "csr_load_balance"):
-            return Csr, {"strategy": "classical" if key == "csr_classical" else "load_balance"}
+        named = {"csr_classical": "classical", "csr_lb": "load_balance",
+                 "csr_load_balance": "load_balance", "csr_stream": "stream"}
+        if key in named:
+            return Csr, {"strategy": named[key]}
         try:
             return _FORMAT_NAMES[key], {}
         except KeyError:

@@ -167,6 +167,21 @@ def solver_cases():
                                                         np.ones(n), 10000, 1e-8)
             out[f"gmres30_{tag}_cd_g{g}"] = solve_case(f"gmres30_{tag}_cd_g{g}", d, "gmres", pre,
                                                        np.ones(n), 10000, 1e-8, krylov_dim=30)
+    # larger systems (iteration counts / histories; SURVEY 8(c) probes)
+    for g in (32, 64, 128):
+        n, r, c, v = P.stencil3d(g, "7pt")
+        rec = solve_case(f"cg_7pt_g{g}", md(n, r, c, v), "cg", 0, np.ones(n), 10000, 1e-8)
+        if g > 32:
+            rec.pop("x")
+        out[f"cg_7pt_g{g}"] = rec
+    n, r, c, v = P.stencil3d(32, "convdiff")
+    d = md(n, r, c, v)
+    for pre in (0, 32):
+        tag = "bj32" if pre else "none"
+        for name, solver, kw in (("bicgstab", "bicgstab", {}), ("gmres30", "gmres", {"krylov_dim": 30})):
+            rec = solve_case(f"{name}_{tag}_cd_g32", d, solver, pre, np.ones(n), 10000, 1e-8, **kw)
+            rec.pop("x")
+            out[f"{name}_{tag}_cd_g32"] = rec
     # multi-column freeze (tests/test_solvers.py:218-248 pattern)
     data = random_spd(8, seed=11)
     dense = data.to_dense_array()

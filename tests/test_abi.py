@@ -16,11 +16,12 @@ LIB = os.path.join(REPO, "paper_2006_16852_b200", "libb200sp.so")
 def declared_symbols():
     text = open(HEADER).read()
     names = set(re.findall(r"\b(b200sp_[a-z0-9_]+)\s*\(", text))
-    # expand the typed conversion macro
-    macro = re.search(r"#define B200SP_CONVERT_DECL\(T, SUF\)(.*?)\n\n", text, re.S)
-    if macro:
+    # expand the typed declaration macros (T, SUF)
+    for macro in re.finditer(r"#define B200SP_[A-Z]+_DECL\(T, SUF\)(.*?)\n(?!.*\\\n)", text, re.S):
         for base in re.findall(r"b200sp_([a-z0-9_]+)_##SUF", macro.group(1)):
             names.update({f"b200sp_{base}_f64", f"b200sp_{base}_f32"})
+    for base in re.findall(r"b200sp_([a-z0-9_]+)_##SUF", text):
+        names.update({f"b200sp_{base}_f64", f"b200sp_{base}_f32"})
     return sorted(n for n in names if "##" not in n)
 
 
