@@ -375,6 +375,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--grid", type=int, default=0, help="override the stencil grid of c4/c5")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 

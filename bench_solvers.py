@@ -1,0 +1,164 @@
+"""Solver / power-law workloads for bench.py (``--workload c1|c3|c4b|c4g|c5``).
+
+  c1   CG, 2-D 5-point Poisson 256^2 (65,536 rows), rhs ones, x0 = 0, RNR 1e-8
+  c3   Csr load-balanced vs Hybrid SpMV, power law 4,194,304 rows (~16 nnz/row)
+  c4b  BiCGSTAB + block-Jacobi(32), 3-D 7-point convection-diffusion 256^3
+  c4g  GMRES(30) + block-Jacobi(32), same system
+  c5   CG, 3-D 7-point Poisson 512^3 (134,217,728 rows) on one GPU
+
+Solver workloads report ms per iteration of complete solves (device time,
+CUDA events on the solve stream, inputs resident in HBM); one step = one
+full solve from x0 = 0. e2e = the same solve through the public API with host
+b / x (H2D of b and x0, D2H of x inside the timed region).
+"""
+
+from __future__ import annotations
+
+import statistics
+import time
+
+import numpy as np
+
+from bench import METRIC, ClockSampler, Timer, allmax, barrier, bytes_csr, bytes_format, peaks
+
+
+def _solve_timer(fn, steps):
+    import torch
+
+    times = []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) * 1e-3)
+    return times, out
+
+
+def bench_solver(args, world, rank, local, kind):
+    import torch
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib, problems
+
+    exc = b2.CudaExecutor(local)
+    torch.cuda.set_device(local)
+    peak, peak_src = peaks()
+    if kind == "c1":
+        a = problems.stencil(exc, "5pt", 256)
+        fac = b2.Cg(exc, criteria=[b2.Iteration(10000), b2.ResidualNormReduction(1e-8)])
+        wl = "C1: CG, 2-D 5-point Poisson 256^2 (65,536 rows), rhs ones, x0 = 0, RNR 1e-8, fp64"
+        vec_passes = 9
+    elif kind == "c5":
+        a = problems.stencil(exc, "7pt", args.grid or 512)
+        fac = b2.Cg(exc, criteria=[b2.Iteration(20000), b2.ResidualNormReduction(1e-8)])
+        wl = f"C5: CG, 3-D 7-point Poisson {args.grid or 512}^3, rhs ones, x0 = 0, RNR 1e-8, fp64, 1 GPU"
+        vec_passes = 9
+    else:
+        g = args.grid or 256
+        a = problems.stencil(exc, "convdiff", g)
+        pre = b2.Jacobi(exc, block_size=32)
+        if kind == "c4b":
+            fac = b2.Bicgstab(exc, criteria=[b2.Iteration(20000), b2.ResidualNormReduction(1e-8)],
+                              preconditioner=pre)
+            wl = f"C4: BiCGSTAB + block-Jacobi(32), 3-D 7-point conv-diff {g}^3, rhs ones, RNR 1e-8, fp64"
+        else:
+            fac = b2.Gmres(exc, criteria=[b2.Iteration(20000), b2.ResidualNormReduction(1e-8)],
+                           preconditioner=pre, krylov_dim=30)
+            wl = f"C4: GMRES(30) + block-Jacobi(32), 3-D 7-point conv-diff {g}^3, rhs ones, RNR 1e-8, fp64"
+        vec_passes = None
+    n = a.size.rows
+    t0 = time.perf_counter()
+    solver = fac.generate(a)
+    generate_s = time.perf_counter() - t0
+    b = b2.Dense(exc, np.ones((n, 1)))
+    x = b2.Dense.zeros(exc, n, 1)
+
+    def one():
+        x.fill(0.0)
+        solver.apply(b, x)
+        return solver.last_status
+
+    for _ in range(max(1, args.warmup // 3)):
+        one()
+    barrier(world)
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        times, st = _solve_timer(one, args.steps)
+    launches = (_lib.launch_count() - launches0) // max(1, args.steps)
+    its = st.iterations
+    t = allmax(world, statistics.mean(times))
+    ms_iter = t / max(its, 1) * 1e3
+    # e2e through the public API with host operands
+    host = exc.master
+    bh = b2.Dense(host, np.ones((n, 1)))
+    xh = b2.Dense(host, np.zeros((n, 1)))
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        xh.values[...] = 0.0
+        torch.cuda.synchronize()
+        s0 = time.perf_counter()
+        solver.apply(bh, xh)
+        e2e.append(time.perf_counter() - s0)
+    e2e_t = allmax(world, statistics.mean(e2e))
+    out = {
+        "metric": METRIC, "value": round(ms_iter, 4), "unit": "ms/iter", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated stencil, b = ones, x0 = 0)",
+        "config": {"workload": wl, "rows": n, "nnz": a.nnz, "iterations": its,
+                   "converged": bool(st.converged), "generate_s": round(generate_s, 3),
+                   "l2": "working set larger than L2 (C4/C5); C1 is L2-resident (latency-bound)"},
+        "e2e": {"value": round(e2e_t / max(its, 1) * 1e3, 4), "unit": "ms/iter",
+                "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": n * 8,
+                "ms_per_step": round(e2e_t * 1e3, 3)},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if vec_passes is not None:
+        by = bytes_csr(n, a.nnz, 8) + vec_passes * n * 8
+        out["roofline"] = {"bound": "hbm", "achieved": round(by / (t / its) / 1e9, 1), "peak": peak,
+                           "unit": "GB/s", "frac": round(by / (t / its) / 1e9 / peak, 4), "traffic": None,
+                           "peak_source": peak_src, "kernel": "whole CG iteration",
+                           "bytes_per_launch": by}
+    return out
+
+
+def bench_c3(args, world, rank, local):
+    import torch
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib, problems
+
+    exc = b2.CudaExecutor(local)
+    peak, peak_src = peaks()
+    a = problems.power_law(exc, 4194304, seed=0)
+    n, nnz = a.size.rows, a.nnz
+    b = b2.Dense(exc, np.random.default_rng(0).standard_normal((n, 1)))
+    x = b2.Dense.zeros(exc, n, 1)
+    timer = Timer(exc)
+    res = {}
+    for name in ("csr_lb", "hybrid", "coo", "csr_stream"):
+        m = b2.convert(a, name)
+        m.apply(b, x)
+        ms = timer.run(lambda: m.apply(b, x), max(5, args.steps), 3)
+        t = statistics.mean(ms) * 1e-3
+        by = bytes_format(m, 8)
+        res[name] = {"us": round(t * 1e6, 1), "gbs": round(by / t / 1e9, 1),
+                     "gbs_useful": round(bytes_csr(n, nnz, 8) / t / 1e9, 1), "frac": round(by / t / 1e9 / peak, 4)}
+    head = res["csr_lb"]
+    return {"metric": METRIC, "value": head["gbs"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["us"] / 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic power law (device hash generator)",
+            "config": {"workload": "C3: Csr load-balanced SpMV, power law 4,194,304 rows, mean 16, max 50k",
+                       "rows": n, "nnz": nnz},
+            "roofline": {"bound": "hbm", "achieved": head["gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": head["frac"], "traffic": None, "peak_source": peak_src},
+            "formats": res, "gpu_launches": 2}
+
+
+def bench_workload(args, world, rank, local):
+    if args.workload == "c3":
+        return bench_c3(args, world, rank, local)
+    return bench_solver(args, world, rank, local, args.workload)

@@ -1,13 +1,14 @@
 """Device-resident solve driver: control block, batches as CUDA graphs.
 
-One DeviceRun owns the KrylovCtl block (csrc/krylov.cuh), the reduction
-partials and the optional residual-norm history of a single m = 1 solve.
-``run`` captures ``iters`` iterations of the solver body once as a CUDA graph
-(with the SpMV launch guard pointed at the solve's done/stopped flag) and
-replays it until the device reports done: one host synchronisation per batch,
-none per iteration. Iteration counts stay exact because the criteria are
-evaluated on the device at every iteration; launches after the stop are
-no-ops.
+A ``DeviceSolve`` is cached on the generated solver per (rows, value type):
+it owns the KrylovCtl block (csrc/krylov.cuh), the reduction partials, the
+optional residual-norm history, the work vectors and private copies of x and
+b. The solver body (``iters`` iterations, or one GMRES restart cycle) is
+captured ONCE as a CUDA graph -- with the SpMV launch guard pointed at the
+solve's done/stopped flag -- and replayed until the device reports done: one
+host synchronisation per batch, none per iteration, no re-capture across
+solves. Iteration counts stay exact because the criteria are evaluated on the
+device at every iteration; launches after the stop are no-ops.
 """
 
 from __future__ import annotations
@@ -19,40 +20,41 @@ import torch
 
 from .. import _lib, config
 from ..executor import ptr
+from ..formats import Dense
 from ..loggers import EventKind
-from ..stop import CRIT_ITERATION, CRIT_RNR, ResidualNormReduction
+from ..stop import CRIT_ITERATION, CRIT_RNR, CriterionArgs, ResidualNormReduction
+
+HIST_CAP = 1 << 16
 
 
-class DeviceRun:
-    def __init__(self, solver, kdim=0):
+class DeviceSolve:
+    def __init__(self, solver, n, dtype, kdim=0):
         self.solver = solver
-        exc = solver.exec
-        self.exc = exc
-        spec, self.time_child = solver.criterion_factory.device_spec()
-        self.spec = spec
+        self.exc = exc = solver.exec
+        self.n, self.dtype, self.kdim = n, dtype, kdim
         dev = exc.device
         self.ctl = torch.zeros(int(_lib.query("krylov_ctl_bytes")), dtype=torch.uint8, device=dev)
         self.part = torch.zeros(int(_lib.query("krylov_part_elems")), dtype=torch.float64, device=dev)
-        self.logging = bool(solver._log_channels)
-        cap = 0
-        if self.logging:
-            iters = [int(p) for t, p in spec if t == CRIT_ITERATION]
-            cap = (min(iters) + 2) if iters else (1 << 20)
-        self.hist = torch.zeros(max(cap, 1), dtype=torch.float64, device=dev) if cap else None
-        types = (ctypes.c_int32 * max(len(spec), 1))(*[t for t, _ in spec])
-        params = (ctypes.c_double * max(len(spec), 1))(*[p for _, p in spec])
-        needs_res = int(any(isinstance(f, ResidualNormReduction)
-                            for f in solver.criterion_factory.factories))
-        _lib.call("krylov_ctl_init", ptr(self.ctl), len(spec), ctypes.addressof(types),
-                  ctypes.addressof(params), needs_res, cap, int(kdim), exc.stream)
-        self._time_crit = None
-        if self.time_child is not None:
-            from ..stop import CriterionArgs
+        self.hist = torch.zeros(HIST_CAP, dtype=torch.float64, device=dev)
+        self.x = torch.empty((n, 1), dtype=dtype, device=dev)
+        self.b = torch.empty((n, 1), dtype=dtype, device=dev)
+        self.xd, self.bd = Dense.wrap(exc, self.x), Dense.wrap(exc, self.b)
+        self.vecs = {}
+        self.graph = None
+        self.graph_key = None
 
-            self._time_crit = solver.criterion_factory.factories[self.time_child].generate(
-                CriterionArgs(solver.a, None, None))
+    # -- work vectors -----------------------------------------------------
+    def vec(self, name, shape=None):
+        t = self.vecs.get(name)
+        if t is None:
+            t = torch.empty(shape or (self.n,), dtype=self.dtype, device=self.exc.device)
+            self.vecs[name] = t
+        return t
 
-    # -- pointers -------------------------------------------------------------
+    def dense(self, t):
+        return Dense.wrap(self.exc, t.view(-1, 1))
+
+    # -- pointers -----------------------------------------------------------
     @property
     def c(self):
         return ptr(self.ctl)
@@ -63,13 +65,35 @@ class DeviceRun:
 
     @property
     def h(self):
-        return ptr(self.hist) if self.hist is not None else 0
+        return ptr(self.hist)
 
     def guard(self, which):
         """Device address of the done (0) / stopped (1) flag."""
         return int(_lib.query("krylov_guard", self.c, which))
 
-    # -- status -------------------------------------------------------------------
+    # -- per-solve setup --------------------------------------------------------
+    def begin(self, b, x):
+        solver = self.solver
+        fac = solver.criterion_factory
+        self.spec, self.time_child = fac.device_spec()
+        self.logging = bool(solver._log_channels)
+        iters = [int(p) for t, p in self.spec if t == CRIT_ITERATION]
+        cap = (min(min(iters) + 2, HIST_CAP) if iters else HIST_CAP) if self.logging else 0
+        types = (ctypes.c_int32 * max(len(self.spec), 1))(*[t for t, _ in self.spec])
+        params = (ctypes.c_double * max(len(self.spec), 1))(*[p for _, p in self.spec])
+        needs_res = int(any(isinstance(f, ResidualNormReduction) for f in fac.factories))
+        _lib.call("krylov_ctl_init", self.c, len(self.spec), ctypes.addressof(types),
+                  ctypes.addressof(params), needs_res, cap, int(self.kdim), self.exc.stream)
+        self.time_crit = None
+        if self.time_child is not None:
+            self.time_crit = fac.factories[self.time_child].generate(CriterionArgs(solver.a, b, x))
+        self.xd.copy_from(x)
+        self.bd.copy_from(b)
+
+    def end(self, x):
+        x.copy_from(self.xd)
+
+    # -- status --------------------------------------------------------------------
     def status(self):
         iv = (ctypes.c_int32 * 8)()
         dv = (ctypes.c_double * 8)()
@@ -80,63 +104,69 @@ class DeviceRun:
         out.update({k: float(v) for k, v in zip(names_d, dv)})
         return out
 
-    # -- batches ---------------------------------------------------------------------
+    # -- batches -----------------------------------------------------------------------
     def run(self, body, iters, guard_which=0, gmres=False):
-        """Replay ``iters`` captured calls of ``body`` until the solve is done."""
+        """Replay the captured ``iters`` x ``body`` graph until done."""
         st = self.status()
         if st["done"]:
             return st
-        guard = self.guard(guard_which)
-        # one eager call to build lazily created plans/workspaces, then capture
-        _lib.query("set_guard", guard)
-        try:
-            body()
-            st = self.status()
-            if st["done"] or self._time_expired(gmres):
-                return self.status()
-            graph = torch.cuda.CUDAGraph()
-            torch.cuda.synchronize(self.exc.device)
-            with torch.cuda.graph(graph):
-                for _ in range(iters):
-                    body()
-        finally:
-            _lib.query("set_guard", 0)
+        if self.graph is None or self.graph_key != (iters, guard_which):
+            _lib.query("set_guard", self.guard(guard_which))
+            try:
+                body()  # eager pass: builds lazily created plans / workspaces
+                st = self.status()
+                if st["done"]:
+                    return st
+                graph = torch.cuda.CUDAGraph()
+                torch.cuda.synchronize(self.exc.device)
+                with torch.cuda.graph(graph):
+                    for _ in range(iters):
+                        body()
+            finally:
+                _lib.query("set_guard", 0)
+            self.graph, self.graph_key = graph, (iters, guard_which)
         while True:
-            graph.replay()
+            self.graph.replay()
             st = self.status()
             if st["done"]:
                 return st
             if self._time_expired(gmres):
-                graph.replay()  # let GMRES commit its partial segment
+                self.graph.replay()  # GMRES commits its partial segment
                 return self.status()
 
     def _time_expired(self, gmres):
-        if self._time_crit is None or not self._time_crit.expired():
+        if self.time_crit is None or not self.time_crit.expired():
             return False
         _lib.call("krylov_force_stop", self.c, self.time_child + 1, int(gmres), self.exc.stream)
         return True
 
-    # -- logger replay ----------------------------------------------------------------
+    # -- logger replay --------------------------------------------------------------------
     def replay_events(self, st):
         if not self.logging:
             return
         solver = self.solver
         final = st["it"]
-        hist = self.hist[:min(final + 1, self.hist.numel())].cpu().numpy()
+        hist = self.hist[:min(final + 1, HIST_CAP)].cpu().numpy()
         base = st["baseline"]
-        names = [type(f).__name__ for f in solver.criterion_factory.factories]
         for it in range(hist.size):
             if it > 0:
                 solver._log(EventKind.ITERATION_COMPLETE, {"iteration": it})
             with np.errstate(invalid="ignore", divide="ignore"):
                 rel = float(hist[it] / base) if base > 0 else (0.0 if hist[it] == 0 else float("inf"))
             stopped = int(st["stopped"] and it == final)
-            for (typ, _), name in zip(self.spec, names):
+            for (typ, _), f in zip(self.spec, solver.criterion_factory.factories):
                 solver._log(EventKind.CRITERION_CHECK_COMPLETED, {
-                    "criterion": name.replace("ResidualNormReduction", "ResidualNormReductionCriterion")
-                                     .replace("Iteration", "IterationCriterion"),
-                    "num_iterations": it, "num_stopped": stopped,
-                    "relative_norms": [rel] if typ == CRIT_RNR else None})
+                    "criterion": type(f).__name__ + "Criterion", "num_iterations": it,
+                    "num_stopped": stopped, "relative_norms": [rel] if typ == CRIT_RNR else None})
+
+
+def get_state(solver, n, dtype, kdim=0):
+    cache = solver.__dict__.setdefault("_device_states", {})
+    key = (n, str(dtype), kdim)
+    st = cache.get(key)
+    if st is None:
+        st = cache[key] = DeviceSolve(solver, n, dtype, kdim)
+    return st
 
 
 def batch_size(default=None):

@@ -19,8 +19,8 @@ from ..errors import ParameterError
 from ..executor import ptr
 from . import generic
 from .common import IterativeSolver, IterativeSolverFactory
-from .device import DeviceRun
-from .krylov import _dense, _vec, device_path_ok, finish_from_device, jac_args
+from .device import get_state
+from .krylov import device_path_ok, finish_from_device, jac_args
 
 DEFAULT_KRYLOV_DIM = 100
 EXACT_CONVERGENCE_ID = 254
@@ -33,24 +33,26 @@ class GmresSolver(IterativeSolver):
             raise ParameterError("krylov_dim must be >= 1")
         if not device_path_ok(self, b):
             return generic.gmres(self, b, x, k, EXACT_CONVERGENCE_ID)
-        exc, n = self.exec, self.size.rows
-        xt = x.values
-        dt = xt.dtype
-        suf = _lib.suffix(dt)
-        r, w = _vec(exc, n, dt), _vec(exc, n, dt)
-        V = torch.empty((k + 1, n), dtype=dt, device=exc.device)
+        n = self.size.rows
+        S = get_state(self, n, x.values.dtype, kdim=k)
+        suf = _lib.suffix(S.dtype)
+        exc = self.exec
         J = jac_args(self)
-        z = _vec(exc, n, dt) if J[0] else None
-        gm = torch.zeros(int(_lib.query("gmres_workspace_elems", k)), dtype=torch.float64, device=exc.device)
-        rd, wd = _dense(exc, r), _dense(exc, w)
-        zd = _dense(exc, z) if z is not None else None
-        vdense = [_dense(exc, V[i]) for i in range(k + 1)]
-        run = DeviceRun(self, kdim=k)
-        self._residual(x, b, rd)
-        _lib.call("gmres_reset_" + suf, n, ptr(r), run.c, run.p, ptr(gm), run.h, 1, exc.stream)
-        _lib.call("gmres_scale_v0_" + suf, n, ptr(r), ptr(V), run.c, exc.stream)
-        xs = xt.stride(0)
-        stopped_guard, done_guard = run.guard(1), run.guard(0)
+        r, w = S.vec("r"), S.vec("w")
+        V = S.vec("V", (k + 1, n))
+        z = S.vec("z") if J[0] else None
+        if "gm" not in S.vecs:
+            S.vecs["gm"] = torch.zeros(int(_lib.query("gmres_workspace_elems", k)), dtype=torch.float64,
+                                       device=exc.device)
+        gm = S.vecs["gm"]
+        rd, wd = S.dense(r), S.dense(w)
+        zd = S.dense(z) if z is not None else None
+        vdense = [S.dense(V[i]) for i in range(k + 1)]
+        S.begin(b, x)
+        self._residual(S.xd, S.bd, rd)
+        _lib.call("gmres_reset_" + suf, n, ptr(r), S.c, S.p, ptr(gm), S.h, 1, exc.stream)
+        _lib.call("gmres_scale_v0_" + suf, n, ptr(r), ptr(V), S.c, exc.stream)
+        stopped_guard, done_guard = S.guard(1), S.guard(0)
 
         def cycle():
             _lib.query("set_guard", stopped_guard)
@@ -60,21 +62,20 @@ class GmresSolver(IterativeSolver):
                     self.precond.apply(src, zd)
                     src = zd
                 self.a.apply(src, wd)
-                _lib.call("gmres_dot0_" + suf, n, j, ptr(V), ptr(w), run.c, run.p, ptr(gm), exc.stream)
+                _lib.call("gmres_dot0_" + suf, n, j, ptr(V), ptr(w), S.c, S.p, ptr(gm), exc.stream)
                 for i in range(j):
-                    _lib.call("gmres_mgs_" + suf, n, j, i, ptr(V), ptr(w), run.c, run.p, ptr(gm), run.h,
-                              exc.stream)
-                _lib.call("gmres_normalize_" + suf, n, j, ptr(V), ptr(w), run.c, exc.stream)
-            _lib.call("gmres_backsolve", run.c, ptr(gm), exc.stream)
-            _lib.call("gmres_combine_" + suf, n, ptr(V), ptr(xt), xs, *J, run.c, ptr(gm), exc.stream)
-            _lib.call("gmres_after_commit", run.c, exc.stream)
+                    _lib.call("gmres_mgs_" + suf, n, j, i, ptr(V), ptr(w), S.c, S.p, ptr(gm), S.h, exc.stream)
+                _lib.call("gmres_normalize_" + suf, n, j, ptr(V), ptr(w), S.c, exc.stream)
+            _lib.call("gmres_backsolve", S.c, ptr(gm), exc.stream)
+            _lib.call("gmres_combine_" + suf, n, ptr(V), ptr(S.x), 1, *J, S.c, ptr(gm), exc.stream)
+            _lib.call("gmres_after_commit", S.c, exc.stream)
             _lib.query("set_guard", done_guard)
-            self._residual(x, b, rd)
-            _lib.call("gmres_reset_" + suf, n, ptr(r), run.c, run.p, ptr(gm), run.h, 0, exc.stream)
-            _lib.call("gmres_scale_v0_" + suf, n, ptr(r), ptr(V), run.c, exc.stream)
+            self._residual(S.xd, S.bd, rd)
+            _lib.call("gmres_reset_" + suf, n, ptr(r), S.c, S.p, ptr(gm), S.h, 0, exc.stream)
+            _lib.call("gmres_scale_v0_" + suf, n, ptr(r), ptr(V), S.c, exc.stream)
 
-        st = run.run(cycle, 1, guard_which=1, gmres=True)
-        finish_from_device(self, run, st)
+        st = S.run(cycle, 1, guard_which=1, gmres=True)
+        finish_from_device(self, S, st, x)
 
 
 class Gmres(IterativeSolverFactory):
