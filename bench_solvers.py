@@ -158,7 +158,46 @@ def bench_c3(args, world, rank, local):
             "formats": res, "gpu_launches": 2}
 
 
+def bench_c5_distributed(args, world, rank, local):
+    """C5 row-partitioned CG over NCCL (torchrun, one rank per GPU): strong
+    scaling of the fixed 512^3 problem; ms per iteration, max over ranks."""
+    import torch
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200.distributed import Comm, DistCg, DistCsr
+
+    exc = b2.CudaExecutor(local)
+    torch.cuda.set_device(local)
+    g = args.grid or 512
+    comm = Comm()
+    t0 = time.perf_counter()
+    A = DistCsr.stencil(exc, comm, "7pt", g)
+    build_s = time.perf_counter() - t0
+    b = torch.ones(A.n_local, dtype=torch.float64, device=exc.device)
+    x = torch.zeros(A.n_local, dtype=torch.float64, device=exc.device)
+    solver = DistCg(A, [b2.Iteration(20000), b2.ResidualNormReduction(1e-8)])
+    for _ in range(max(1, args.warmup // 3)):
+        x.zero_()
+        solver.solve(b, x)
+    barrier(world)
+    with ClockSampler(local) as clk:
+        times, st = _solve_timer(lambda: (x.zero_(), solver.solve(b, x))[1], args.steps)
+    t = allmax(world, statistics.mean(times))
+    its = st.iterations
+    return {"metric": METRIC, "value": round(t / max(its, 1) * 1e3, 4), "unit": "ms/iter", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated 7-point Poisson, b = ones, x0 = 0)",
+            "config": {"workload": f"C5: row-partitioned CG, 3-D 7-point Poisson {g}^3, RNR 1e-8, "
+                                   f"NCCL halo + all-reduce", "iterations": its,
+                       "converged": bool(st.converged), "parallelism": f"row partition x{world}",
+                       "rows_per_rank": A.n_local, "build_s": round(build_s, 3)},
+            "gpu_launches": None, "clocks": clk.summary()}
+
+
 def bench_workload(args, world, rank, local):
     if args.workload == "c3":
         return bench_c3(args, world, rank, local)
+    if args.workload == "c5" and world > 1:
+        return bench_c5_distributed(args, world, rank, local)
     return bench_solver(args, world, rank, local, args.workload)

@@ -204,11 +204,12 @@ B200SP_CONVERT_DECL(double, f64)
 B200SP_CONVERT_DECL(float, f32)
 
 /* ---- generators (replace src/problems.py:11-45 at device scale) --------- */
-int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t n, int32_t* len, void* stream);
-int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t n, const int32_t* rp, int32_t* ci,
-                            double* v, void* stream);
-int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t n, const int32_t* rp, int32_t* ci,
-                            float* v, void* stream);
+/* rows row0 .. row0+n-1 of the global stencil (global column indices) */
+int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t row0, int64_t n, int32_t* len, void* stream);
+int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
+                            int32_t* ci, double* v, void* stream);
+int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
+                            int32_t* ci, float* v, void* stream);
 int b200sp_powerlaw_lengths(int64_t n, uint64_t seed, const double* thresholds, int32_t max_len, int32_t* len,
                             void* stream);
 int b200sp_powerlaw_fill_f64(int64_t n, uint64_t seed, const int32_t* rp, int32_t* ci, double* v, void* stream);
@@ -290,6 +291,32 @@ int b200sp_gmres_after_commit(void* ctl, void* stream);
                                    const double* gm, void* stream);
 B200SP_KRYLOV_DECL(double, f64)
 B200SP_KRYLOV_DECL(float, f32)
+
+/* ---- row-partitioned (distributed) CG ------------------------------------
+ * Each rank holds rows [lo, hi) with vector layout [owned | ghosts]; the
+ * reduction kernels of a ctl with dist = 1 park their local sums in the ctl's
+ * red[] (byte offset b200sp_krylov_red_offset()), the caller all-reduces
+ * them across ranks (NCCL) and b200sp_cg_finish runs the control step
+ * (phase 0 init, 1 sigma, 2 step2). No reference counterpart: the reference
+ * has no distributed matrix. */
+int b200sp_krylov_set_dist(void* ctl, int32_t dist, void* stream);
+int64_t b200sp_krylov_red_offset(void);
+int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream);
+int b200sp_flag_out_of_range(int64_t nnz, const int32_t* ci, int64_t lo, int64_t hi, int32_t* flag, void* stream);
+int b200sp_compact_cols(int64_t nnz, const int32_t* ci, const int32_t* flag, const int32_t* pos, int32_t* out,
+                        void* stream);
+int b200sp_map_cols(int64_t nnz, int32_t* ci, int64_t lo, int64_t hi, const int32_t* ghosts, int64_t nghost,
+                    void* stream);
+int b200sp_split_count(int64_t n, const int32_t* rp, const int32_t* ci, int32_t thr, int32_t* len_lo,
+                       int32_t* len_hi, void* stream);
+int b200sp_split_fill_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, int32_t thr,
+                          const int32_t* rp_lo, const int32_t* rp_hi, int32_t* ci_lo, double* v_lo, int32_t* ci_hi,
+                          double* v_hi, void* stream);
+int b200sp_split_fill_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, int32_t thr,
+                          const int32_t* rp_lo, const int32_t* rp_hi, int32_t* ci_lo, float* v_lo, int32_t* ci_hi,
+                          float* v_hi, void* stream);
+int b200sp_gather_f64(int64_t count, const int32_t* idx, const double* src, double* dst, void* stream);
+int b200sp_gather_f32(int64_t count, const int32_t* idx, const float* src, float* dst, void* stream);
 
 #ifdef __cplusplus
 }

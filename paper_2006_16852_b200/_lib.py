@@ -50,7 +50,7 @@ _TYPED = {
     "dense_to_csr_fill": "llplpppp",
     "csr_to_dense": "lpppplp",
     # generators
-    "stencil_fill": "ildlpppp",
+    "stencil_fill": "ildllpppp",
     "powerlaw_fill": "lupppp",
     # block-Jacobi
     "jacobi_invert": "lpppppppppidpp",
@@ -72,6 +72,9 @@ _TYPED = {
     "gmres_mgs": "lii" + "ppppppp",
     "gmres_normalize": "lipppp",
     "gmres_combine": "lppl" + "lpppp" + "ppp",
+    # distributed
+    "split_fill": "lpppippppppp",
+    "gather": "lpppp",
 }
 _UNTYPED = {
     "last_error": ("", ctypes.c_char_p),
@@ -98,7 +101,7 @@ _UNTYPED = {
     "length_histogram": ("lpipp", ctypes.c_int),
     "empty_row_flags": ("lppp", ctypes.c_int),
     "compact_flags": ("lpppp", ctypes.c_int),
-    "stencil_lengths": ("illpp", ctypes.c_int),
+    "stencil_lengths": ("illlpp", ctypes.c_int),
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
     "set_guard": ("p", None),
     "jacobi_block_sizes_sq": ("lppp", ctypes.c_int),
@@ -112,6 +115,13 @@ _UNTYPED = {
     "gmres_workspace_elems": ("i", ctypes.c_int64),
     "gmres_backsolve": ("ppp", ctypes.c_int),
     "gmres_after_commit": ("pp", ctypes.c_int),
+    "krylov_set_dist": ("pip", ctypes.c_int),
+    "krylov_red_offset": ("", ctypes.c_int64),
+    "cg_finish": ("ppip", ctypes.c_int),
+    "flag_out_of_range": ("lpllpp", ctypes.c_int),
+    "compact_cols": ("lppppp", ctypes.c_int),
+    "map_cols": ("lpllplp", ctypes.c_int),
+    "split_count": ("lppippp", ctypes.c_int),
 }
 
 _lock = threading.Lock()

@@ -38,6 +38,7 @@ struct Stencil {
     int kind;
     int64_t g;
     double conv;
+    int64_t row0;
 };
 
 __device__ __forceinline__ int stencil_len(const Stencil& s, int64_t row) {
@@ -54,16 +55,19 @@ __device__ __forceinline__ int stencil_len(const Stencil& s, int64_t row) {
     return 1 + (i > 0) + (i < g - 1) + (j > 0) + (j < g - 1) + (k > 0) + (k < g - 1);
 }
 
+// n = rows generated, starting at global row s.row0 (row-partitioned solves
+// generate only their own rows, with global column indices)
 __global__ void stencil_lengths_kernel(Stencil s, int64_t n, int* __restrict__ len) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-        len[r] = stencil_len(s, r);
+    for (int64_t lr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lr < n; lr += (int64_t)gridDim.x * blockDim.x)
+        len[lr] = stencil_len(s, s.row0 + lr);
 }
 
 template <typename T>
 __global__ void stencil_fill_kernel(Stencil s, int64_t n, const int* __restrict__ rp, int* __restrict__ ci,
                                     T* __restrict__ v) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-        int64_t o = rp[r];
+    for (int64_t lr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lr < n; lr += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = s.row0 + lr;
+        int64_t o = rp[lr];
         const int64_t g = s.g;
         if (s.kind == 0) {
             const int64_t i = r / g, j = r % g;
@@ -144,25 +148,25 @@ using namespace b200sp;
 
 extern "C" {
 
-int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t n, int32_t* len, void* stream) {
+int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t row0, int64_t n, int32_t* len, void* stream) {
     B200SP_REQUIRE(kind >= 0 && kind <= 3, B200SP_EINVAL, "stencil: unknown kind %d", kind);
     if (n == 0) return B200SP_OK;
-    stencil_lengths_kernel<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, 0.0}, n, len);
+    stencil_lengths_kernel<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, 0.0, row0}, n, len);
     count_launch();
     return check_launch("stencil_lengths");
 }
 
-int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t n, const int32_t* rp, int32_t* ci,
-                            double* v, void* stream) {
+int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
+                            int32_t* ci, double* v, void* stream) {
     if (n == 0) return B200SP_OK;
-    stencil_fill_kernel<double><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, conv}, n, rp, ci, v);
+    stencil_fill_kernel<double><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, conv, row0}, n, rp, ci, v);
     count_launch();
     return check_launch("stencil_fill");
 }
-int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t n, const int32_t* rp, int32_t* ci,
-                            float* v, void* stream) {
+int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
+                            int32_t* ci, float* v, void* stream) {
     if (n == 0) return B200SP_OK;
-    stencil_fill_kernel<float><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, conv}, n, rp, ci, v);
+    stencil_fill_kernel<float><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, conv, row0}, n, rp, ci, v);
     count_launch();
     return check_launch("stencil_fill");
 }

@@ -25,6 +25,42 @@ __device__ __forceinline__ void hist_put(const KrylovCtl* c, double* hist, int i
 // ===========================================================================
 // CG
 // ===========================================================================
+// control steps (run by the last block, or by cg_finish_kernel after the
+// cross-rank all-reduce of a distributed solve)
+__device__ inline void cg_init_ctl(KrylovCtl* c, const double* tot, double* hist) {
+    c->it = 0;
+    c->rho = tot[0];
+    c->rho_prev = 1.0;
+    c->rnorm = sqrt(tot[1]);
+    c->baseline = c->rnorm;
+    hist_put(c, hist, 0, c->rnorm);
+    crit_check(c, 0, c->rnorm);
+    c->done = c->stopped;
+    c->beta = safe_div(c->rho, c->rho_prev);
+}
+
+__device__ inline void cg_sigma_ctl(KrylovCtl* c, const double* tot) {
+    c->sigma = tot[0];
+    if (c->sigma <= 0.0 && c->rho != 0.0) {  // krylov.py:64-70
+        c->breakdown = BD_CG_SIGMA;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->alpha = safe_div(c->rho, c->sigma);
+}
+
+__device__ inline void cg_step2_ctl(KrylovCtl* c, const double* tot, double* hist) {
+    c->rho_prev = c->rho;
+    c->rho = tot[0];
+    c->it += 1;
+    c->rnorm = sqrt(tot[1]);
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+    c->done = c->stopped;
+    c->beta = safe_div(c->rho, c->rho_prev);
+}
+
 // after r = b - A x: z = M r, p = 0, rho = r.z, baseline = ||r||, check(0)
 template <typename T>
 __global__ void __launch_bounds__(KRY_BLOCK)
@@ -49,15 +85,12 @@ cg_init_kernel(RowBlocks rb, const T* __restrict__ r, T* __restrict__ z, T* __re
     }
     double v[2] = {rz, rr}, tot[2];
     if (!grid_reduce<2>(v, part, &c->ticket[0], tot)) return;
-    c->it = 0;
-    c->rho = tot[0];
-    c->rho_prev = 1.0;
-    c->rnorm = sqrt(tot[1]);
-    c->baseline = c->rnorm;
-    hist_put(c, hist, 0, c->rnorm);
-    crit_check(c, 0, c->rnorm);
-    c->done = c->stopped;
-    c->beta = safe_div(c->rho, c->rho_prev);
+    if (c->dist) {
+        c->red[0] = tot[0];
+        c->red[1] = tot[1];
+        return;
+    }
+    cg_init_ctl(c, tot, hist);
 }
 
 // p = z + beta p    (CgStep1, steps.py:93-119)
@@ -80,14 +113,11 @@ cg_sigma_kernel(int64_t n, const T* __restrict__ p, const T* __restrict__ q, Kry
         s += (double)p[i] * (double)q[i];
     double v[1] = {s}, tot[1];
     if (!grid_reduce<1>(v, part, &c->ticket[1], tot)) return;
-    c->sigma = tot[0];
-    if (c->sigma <= 0.0 && c->rho != 0.0) {
-        c->breakdown = BD_CG_SIGMA;
-        c->breakdown_it = c->it + 1;
-        c->done = 1;
+    if (c->dist) {
+        c->red[0] = tot[0];
         return;
     }
-    c->alpha = safe_div(c->rho, c->sigma);
+    cg_sigma_ctl(c, tot);
 }
 
 // x += alpha p; r -= alpha q; z = M r; rho = r.z; ||r||; it++; check   (CgStep2)
@@ -121,14 +151,22 @@ cg_step2_kernel(RowBlocks rb, T* __restrict__ x, int64_t xs, T* __restrict__ r, 
     }
     double v[2] = {rz, rr}, tot[2];
     if (!grid_reduce<2>(v, part, &c->ticket[2], tot)) return;
-    c->rho_prev = c->rho;
-    c->rho = tot[0];
-    c->it += 1;
-    c->rnorm = sqrt(tot[1]);
-    hist_put(c, hist, c->it, c->rnorm);
-    crit_check(c, c->it, c->rnorm);
-    c->done = c->stopped;
-    c->beta = safe_div(c->rho, c->rho_prev);
+    if (c->dist) {
+        c->red[0] = tot[0];
+        c->red[1] = tot[1];
+        return;
+    }
+    cg_step2_ctl(c, tot, hist);
+}
+
+// distributed solves: the control step after red[] has been all-reduced
+// (phase 0 = init, 1 = sigma, 2 = step2)
+__global__ void cg_finish_kernel(KrylovCtl* c, double* hist, int phase) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (phase != 0 && c->done) return;
+    if (phase == 0) cg_init_ctl(c, c->red, hist);
+    else if (phase == 1) cg_sigma_ctl(c, c->red);
+    else cg_step2_ctl(c, c->red, hist);
 }
 
 // ===========================================================================
@@ -688,5 +726,11 @@ int b200sp_gmres_after_commit(void* ctl, void* stream) {
     return check_launch("gmres_after_commit");
 }
 int64_t b200sp_gmres_workspace_elems(int32_t k) { return (int64_t)(k + 1) * k + 3 * (int64_t)k + 1 + k; }
+
+int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream) {
+    cg_finish_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl, hist, phase);
+    count_launch();
+    return check_launch("cg_finish");
+}
 
 }  // extern "C"

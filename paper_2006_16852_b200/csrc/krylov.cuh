@@ -46,6 +46,9 @@ struct KrylovCtl {
     double baseline;   // ||r0||
     double rho, rho_prev, sigma, alpha, beta, omega, gamma, ts, tt, rnorm, snorm, hnorm;
     unsigned ticket[4];
+    int dist;          // distributed solve: epilogues park local sums in red[]
+    int pad2;
+    double red[4];     // local reduction results, all-reduced across ranks in place
 };
 
 // ---------------------------------------------------------------------------

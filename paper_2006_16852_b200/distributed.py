@@ -1,0 +1,360 @@
+"""Row-partitioned distributed matrix and CG (one process per GPU).
+
+The reference has no distributed executor (cross-process memory
+is a non-goal; its only parallelism is ParallelExecutor's contiguous row
+blocks, src/executor.py:181-190). This module scales that same decomposition
+across GPUs:
+
+* ``Partition``  -- contiguous row blocks (plane-aligned for 3-D grids).
+* ``plan_halo``  -- ghost columns grouped by owning rank; the send lists are
+  learned with one all_gather of the (small) per-peer ghost requests.
+* ``DistCsr``    -- the rank's rows with columns renumbered to the local
+  vector layout [owned | ghosts], split into A_own and A_ghost so the
+  interior product overlaps the halo exchange:
+      halo(p) on the NCCL stream  ||  q = A_own p_own   (compute stream)
+      wait;  q += A_ghost p_ghost
+* ``DistCg``     -- the device-resident CG kernels with the reductions split
+  as local sum -> NCCL all-reduce (8-16 bytes) -> control step, two
+  all-reduces per iteration (sigma = p.q; rho = r.z with ||r||).
+Communication goes through ``Comm`` (torch.distributed; NCCL over
+NVLink/NVSwitch in production, gloo for the CPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib, config
+from .base import Dim2, LinOp
+from .executor import ptr
+from .formats import Csr, Dense, _scan
+from .problems import STENCILS
+from .solvers.common import BreakdownInfo, SolveStatus
+from .stop import CRIT_ITERATION, Combined
+
+
+# ---------------------------------------------------------------------------
+# partition + communication (host logic, CPU-testable)
+# ---------------------------------------------------------------------------
+class Partition:
+    """Contiguous row blocks of n rows over ``size`` ranks, boundaries rounded
+    to multiples of ``align`` (a grid plane) where possible."""
+
+    def __init__(self, n, size, align=1):
+        self.n, self.size = int(n), int(size)
+        units = -(-self.n // align)
+        cuts = [min(self.n, (units * p // self.size) * align) for p in range(self.size + 1)]
+        cuts[-1] = self.n
+        self.offsets = np.asarray(cuts, dtype=np.int64)
+
+    def range(self, rank):
+        return int(self.offsets[rank]), int(self.offsets[rank + 1])
+
+    def owner(self, cols):
+        return np.searchsorted(self.offsets, np.asarray(cols, dtype=np.int64), side="right") - 1
+
+
+class Comm:
+    """Collectives over torch.distributed (the default process group)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allreduce_(self, t):
+        self.dist.all_reduce(t, group=self.group)
+
+    def allgather_object(self, obj):
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def exchange(self, sends, recvs):
+        """Start point-to-point transfers; returns a handle with wait()."""
+        ops = [self.dist.P2POp(self.dist.isend, t, peer, self.group) for peer, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in recvs]
+        works = self.dist.batch_isend_irecv(ops) if ops else []
+        return _Works(works)
+
+
+class StagedComm(Comm):
+    """Comm for backends without device tensors (gloo): stage through host
+    memory. Used to test the multi-rank path with several processes sharing
+    one GPU; production runs use NCCL directly."""
+
+    def allreduce_(self, t):
+        h = t.detach().cpu()
+        self.dist.all_reduce(h, group=self.group)
+        t.copy_(h.to(t.device))
+
+    def exchange(self, sends, recvs):
+        host_recv = [(peer, torch.empty(t.shape, dtype=t.dtype)) for peer, t in recvs]
+        ops = [self.dist.P2POp(self.dist.isend, t.detach().cpu(), peer, self.group) for peer, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, h, peer, self.group) for peer, h in host_recv]
+        for w in (self.dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+        for (peer, h), (_, t) in zip(host_recv, recvs):
+            t.copy_(h.to(t.device))
+        return _Works([])
+
+
+class _Works:
+    def __init__(self, works):
+        self.works = works
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+
+
+class HaloPlan:
+    """recv: [(peer, g0, g1)] ghost segments per owning peer (sorted ghosts);
+    send: [(peer, local_idx)] owned rows each peer needs."""
+
+    def __init__(self, recv, send, n_local, n_ghost):
+        self.recv, self.send = recv, send
+        self.n_local, self.n_ghost = n_local, n_ghost
+
+    def send_is_range(self, idx):
+        return idx.size > 0 and bool(np.all(np.diff(idx) == 1))
+
+
+def plan_halo(rank, part, ghost_cols, comm):
+    """Group sorted ghost columns by owner and learn the send lists."""
+    ghost_cols = np.asarray(ghost_cols, dtype=np.int64)
+    lo, hi = part.range(rank)
+    owners = part.owner(ghost_cols)
+    recv, requests = [], {}
+    for q in np.unique(owners):
+        q = int(q)
+        seg = np.flatnonzero(owners == q)
+        recv.append((q, int(seg[0]), int(seg[-1]) + 1))
+        requests[q] = ghost_cols[seg]
+    gathered = comm.allgather_object(requests)
+    send = []
+    for p, req in enumerate(gathered):
+        if p != rank and rank in req:
+            send.append((p, np.asarray(req[rank], dtype=np.int64) - lo))
+    return HaloPlan(recv, send, hi - lo, ghost_cols.size)
+
+
+# ---------------------------------------------------------------------------
+# distributed matrix
+# ---------------------------------------------------------------------------
+class DistCsr(LinOp):
+    """This rank's rows of a row-partitioned matrix (global size n x n)."""
+
+    def __init__(self, exc, comm, part, a_own, a_ghost, plan):
+        super().__init__(exc, Dim2(part.n, part.n))
+        self.comm, self.part = comm, part
+        self.a_own, self.a_ghost, self.plan = a_own, a_ghost, plan
+        self.lo, self.hi = part.range(comm.rank)
+        dev = exc.device
+        self._send = []
+        for peer, idx in plan.send:
+            if plan.send_is_range(idx):
+                self._send.append((peer, int(idx[0]), int(idx[-1]) + 1, None, None))
+            else:
+                it = torch.from_numpy(idx.astype(np.int32)).to(dev)
+                self._send.append((peer, 0, 0, it, None))
+
+    @property
+    def n_local(self):
+        return self.plan.n_local
+
+    @property
+    def n_ext(self):
+        return self.plan.n_local + self.plan.n_ghost
+
+    @classmethod
+    def stencil(cls, exc, comm, kind, grid, value_dtype="float64", convection=0.4, strategy="automatic"):
+        """Generate this rank's rows of a stencil matrix directly on its GPU."""
+        code = STENCILS[kind]
+        n = grid * grid if code == 0 else grid ** 3
+        plane = grid if code == 0 else grid * grid
+        part = Partition(n, comm.size, align=plane)
+        lo, hi = part.range(comm.rank)
+        nl = hi - lo
+        dev = exc.device
+        lens = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+        _lib.call("stencil_lengths", code, grid, lo, nl, ptr(lens), exc.stream)
+        rp = _scan(exc, lens[:nl])
+        nnz = int(rp[-1].item())
+        vt = torch.float64 if np.dtype(value_dtype) == np.float64 else torch.float32
+        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        v = torch.empty(max(nnz, 1), dtype=vt, device=dev)
+        _lib.call("stencil_fill_" + _lib.suffix(vt), code, grid, float(convection), lo, nl, ptr(rp), ptr(ci),
+                  ptr(v), exc.stream)
+        return cls.from_local_rows(exc, comm, part, rp, ci[:nnz], v[:nnz], strategy)
+
+    @classmethod
+    def from_local_rows(cls, exc, comm, part, rp, ci, v, strategy="automatic"):
+        """Local rows with GLOBAL column indices -> renumbered, split, planned."""
+        lo, hi = part.range(comm.rank)
+        nl, nnz = hi - lo, int(ci.numel())
+        dev = exc.device
+        # ghost columns: flag, compact (device), unique (host, small)
+        flag = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        _lib.call("flag_out_of_range", nnz, ptr(ci), lo, hi, ptr(flag), exc.stream)
+        pos = _scan(exc, flag[:nnz])
+        ng_all = int(pos[-1].item())
+        gcols = torch.empty(max(ng_all, 1), dtype=torch.int32, device=dev)
+        _lib.call("compact_cols", nnz, ptr(ci), ptr(flag), ptr(pos), ptr(gcols), exc.stream)
+        ghosts = np.unique(gcols[:ng_all].cpu().numpy().astype(np.int64))
+        plan = plan_halo(comm.rank, part, ghosts, comm)
+        gdev = torch.from_numpy(ghosts.astype(np.int32)).to(dev)
+        ci = ci.clone()
+        _lib.call("map_cols", nnz, ptr(ci), lo, hi, ptr(gdev), ghosts.size, exc.stream)
+        # split into owned / ghost column blocks
+        llo = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+        lhi = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+        _lib.call("split_count", nl, ptr(rp), ptr(ci), nl, ptr(llo), ptr(lhi), exc.stream)
+        rp_lo, rp_hi = _scan(exc, llo[:nl]), _scan(exc, lhi[:nl])
+        n_lo, n_hi = int(rp_lo[-1].item()), int(rp_hi[-1].item())
+        ci_lo = torch.empty(max(n_lo, 1), dtype=torch.int32, device=dev)
+        ci_hi = torch.empty(max(n_hi, 1), dtype=torch.int32, device=dev)
+        v_lo = torch.empty(max(n_lo, 1), dtype=v.dtype, device=dev)
+        v_hi = torch.empty(max(n_hi, 1), dtype=v.dtype, device=dev)
+        _lib.call("split_fill_" + _lib.suffix(v.dtype), nl, ptr(rp), ptr(ci), ptr(v), nl, ptr(rp_lo), ptr(rp_hi),
+                  ptr(ci_lo), ptr(v_lo), ptr(ci_hi), ptr(v_hi), exc.stream)
+        a_own = Csr._from_device(exc, Dim2(nl, nl), rp_lo, ci_lo[:n_lo], v_lo[:n_lo], strategy=strategy)
+        a_gh = None
+        if ghosts.size:
+            a_gh = Csr._from_device(exc, Dim2(nl, ghosts.size), rp_hi, ci_hi[:n_hi], v_hi[:n_hi],
+                                    strategy="classical")
+        return cls(exc, comm, part, a_own, a_gh, plan)
+
+    # -- halo + product ----------------------------------------------------
+    def start_halo(self, xext):
+        """Send owned values peers need, receive ghosts into xext[n_local:]."""
+        nl = self.n_local
+        sends = []
+        for peer, a, b, idx, _ in self._send:
+            if idx is None:
+                sends.append((peer, xext[a:b]))
+            else:
+                buf = torch.empty(idx.numel(), dtype=xext.dtype, device=xext.device)
+                _lib.call("gather_" + _lib.suffix(xext.dtype), idx.numel(), ptr(idx), ptr(xext), ptr(buf),
+                          self.exec.stream)
+                sends.append((peer, buf))
+        recvs = [(peer, xext[nl + g0:nl + g1]) for peer, g0, g1 in self.plan.recv]
+        return self.comm.exchange(sends, recvs)
+
+    def apply_ext(self, xext, y, alpha=1.0, beta=None, y_in=None):
+        """y = alpha * A x + beta * y_in with x = xext[:n_local] plus ghosts."""
+        nl = self.n_local
+        exc = self.exec
+        work = self.start_halo(xext)
+        xd = Dense.wrap(exc, xext[:nl].view(-1, 1))
+        yd = Dense.wrap(exc, y.view(-1, 1))
+        if y_in is None:
+            self.a_own.apply(xd, yd) if alpha == 1.0 else self.a_own.apply_advanced(alpha, xd, 0.0, yd)
+        else:
+            from .kernels import SpmvOp
+
+            exc.run(SpmvOp(self.a_own, xd, yd, alpha=alpha, beta=beta, x_in=Dense.wrap(exc, y_in.view(-1, 1))))
+        work.wait()
+        if self.a_ghost is not None:
+            gd = Dense.wrap(exc, xext[nl:].view(-1, 1))
+            self.a_ghost.apply_advanced(alpha, gd, 1.0, yd)
+
+    def _apply_impl(self, b, x):
+        ext = torch.empty(self.n_ext, dtype=b.values.dtype, device=self.exec.device)
+        ext[:self.n_local].copy_(b.values[:, 0])
+        self.apply_ext(ext, x.values[:, 0])
+
+
+# ---------------------------------------------------------------------------
+# distributed CG
+# ---------------------------------------------------------------------------
+class DistCg:
+    """Row-partitioned CG on DistCsr (unpreconditioned), criteria
+    Iteration / ResidualNormReduction evaluated on the device from
+    all-reduced norms. ``solve`` takes this rank's slices of b and x."""
+
+    def __init__(self, a, criteria, batch=None):
+        self.a = a
+        self.exec = a.exec
+        self.factory = Combined(criteria if isinstance(criteria, (list, tuple)) else [criteria])
+        spec = self.factory.device_spec()
+        if spec is None or spec[1] is not None:
+            raise NotImplementedError("DistCg supports Iteration / ResidualNormReduction criteria")
+        self.spec = spec[0]
+        self.batch = int(batch or config.SOLVER_BATCH)
+        self.last_status = None
+        dev = self.exec.device
+        self.ctl = torch.zeros(int(_lib.query("krylov_ctl_bytes")), dtype=torch.uint8, device=dev)
+        self.part = torch.zeros(int(_lib.query("krylov_part_elems")), dtype=torch.float64, device=dev)
+        off = int(_lib.query("krylov_red_offset"))
+        self.red = self.ctl[off:off + 32].view(torch.float64)
+
+    def _status(self):
+        iv, dv = (ctypes.c_int32 * 8)(), (ctypes.c_double * 8)()
+        _lib.call("krylov_status", ptr(self.ctl), ctypes.addressof(iv), ctypes.addressof(dv), self.exec.stream)
+        return list(iv), list(dv)
+
+    def solve(self, b, x):
+        """b, x: this rank's (n_local,) device tensors; x is the initial guess."""
+        exc, A = self.exec, self.a
+        nl, dt = A.n_local, x.dtype
+        suf = _lib.suffix(dt)
+        comm = A.comm
+        types = (ctypes.c_int32 * len(self.spec))(*[t for t, _ in self.spec])
+        params = (ctypes.c_double * len(self.spec))(*[p for _, p in self.spec])
+        c = ptr(self.ctl)
+        _lib.call("krylov_ctl_init", c, len(self.spec), ctypes.addressof(types), ctypes.addressof(params), 1, 0, 0,
+                  exc.stream)
+        _lib.call("krylov_set_dist", c, 1, exc.stream)
+        r = torch.empty(nl, dtype=dt, device=exc.device)
+        q = torch.empty(nl, dtype=dt, device=exc.device)
+        pext = torch.empty(A.n_ext, dtype=dt, device=exc.device)
+        p = pext[:nl]
+        # r = b - A x  (x staged in the extended vector for its halo)
+        pext[:nl].copy_(x)
+        A.apply_ext(pext, r, alpha=-1.0, beta=1.0, y_in=b)
+        J = (0, 0, 0, 0, 0)
+        pp = self.part
+        _lib.call("cg_init_" + suf, nl, ptr(r), ptr(r), ptr(p), *J, c, ptr(pp), 0, exc.stream)
+        comm.allreduce_(self.red[:2])
+        _lib.call("cg_finish", c, 0, 0, exc.stream)
+        guard = int(_lib.query("krylov_guard", c, 0))
+        _lib.query("set_guard", guard)
+        try:
+            while True:
+                iv, _ = self._status()
+                if iv[4]:
+                    break
+                for _ in range(self.batch):
+                    _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), c, exc.stream)
+                    A.apply_ext(pext, q)
+                    _lib.call("cg_sigma_" + suf, nl, ptr(p), ptr(q), c, ptr(pp), exc.stream)
+                    comm.allreduce_(self.red[:1])
+                    _lib.call("cg_finish", c, 0, 1, exc.stream)
+                    _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(r), *J, c, ptr(pp), 0,
+                              exc.stream)
+                    comm.allreduce_(self.red[:2])
+                    _lib.call("cg_finish", c, 0, 2, exc.stream)
+        finally:
+            _lib.query("set_guard", 0)
+        iv, dv = self._status()
+        status = np.zeros(1, dtype=[("stopped", "?"), ("stopping_id", "u1"), ("finalized", "?")])
+        status["stopped"][0], status["stopping_id"][0], status["finalized"][0] = bool(iv[1]), iv[2], bool(iv[3])
+        bd = BreakdownInfo(iv[6], "non-positive p^T A p") if iv[5] else None
+        self.last_status = SolveStatus(iv[0], status, bd, self.factory.residual_criterion_ids())
+        return self.last_status
+
+
+def iteration_criteria(max_iters, factor):
+    from .stop import Iteration, ResidualNormReduction
+
+    return [Iteration(max_iters), ResidualNormReduction(factor)]
+
+
+_ = CRIT_ITERATION

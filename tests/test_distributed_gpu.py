@@ -1,0 +1,88 @@
+"""Row-partitioned CG on the device with 2 ranks sharing one GPU (gloo with
+host staging stands in for NCCL, which needs one GPU per rank): the
+distributed solve must reproduce the single-GPU CG iteration count (+-1)
+and solution, and DistCsr must reproduce the global SpMV."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, g, out_dir):
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, repo)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2006_16852_b200 as b2
+    from oracle import problems as P
+    from oracle import spmv as OS
+    from paper_2006_16852_b200.distributed import DistCg, DistCsr, StagedComm
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        exc = b2.CudaExecutor(0)
+        comm = StagedComm()
+        A = DistCsr.stencil(exc, comm, "7pt", g)
+        lo, hi = A.lo, A.hi
+        n = g ** 3
+        # SpMV vs the oracle
+        xg = np.random.default_rng(1).standard_normal(n)
+        nn, r, c, v = P.stencil3d(g, "7pt")
+        rp, ci, vals = P.to_csr(nn, r, c, v)
+        yg = OS.csr_spmv(rp, ci, vals, xg[:, None])[:, 0]
+        ext = torch.zeros(A.n_ext, dtype=torch.float64, device=exc.device)
+        ext[:A.n_local] = torch.from_numpy(xg[lo:hi]).to(exc.device)
+        y = torch.zeros(A.n_local, dtype=torch.float64, device=exc.device)
+        A.apply_ext(ext, y)
+        err = OS.rel_error_inf(y.cpu().numpy(), yg[lo:hi])
+        # distributed CG
+        b = torch.ones(A.n_local, dtype=torch.float64, device=exc.device)
+        x = torch.zeros(A.n_local, dtype=torch.float64, device=exc.device)
+        solver = DistCg(A, [b2.Iteration(1000), b2.ResidualNormReduction(1e-8)], batch=8)
+        st = solver.solve(b, x)
+        np.save(os.path.join(out_dir, f"x{rank}.npy"), x.cpu().numpy())
+        with open(os.path.join(out_dir, f"st{rank}"), "w") as f:
+            f.write(f"{lo} {hi} {st.iterations} {int(st.converged)} {err}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_cg_matches_single_gpu(tmp_path, cuda):
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import problems
+
+    g = 16
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, g, str(tmp_path)), nprocs=2, join=True)
+    parts, its = [], set()
+    for rank in range(2):
+        lo, hi, it, conv, err = (tmp_path / f"st{rank}").read_text().split()
+        assert float(err) <= 1e-14
+        assert int(conv) == 1
+        its.add(int(it))
+        parts.append(np.load(tmp_path / f"x{rank}.npy"))
+    assert len(its) == 1  # every rank took the same decisions
+    a = problems.stencil(cuda, "7pt", g)
+    x1 = b2.Dense.zeros(cuda, g ** 3, 1)
+    s = b2.Cg(cuda, criteria=[b2.Iteration(1000), b2.ResidualNormReduction(1e-8)]).generate(a)
+    s.apply(b2.Dense(cuda, np.ones((g ** 3, 1))), x1)
+    assert abs(its.pop() - s.last_status.iterations) <= 1
+    xd = np.concatenate(parts)
+    x1 = np.asarray(x1.data)[:, 0]
+    assert np.linalg.norm(xd - x1) <= 1e-7 * np.linalg.norm(x1)
