@@ -89,22 +89,24 @@ int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* row_ptrs, const int3
                                   const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
                                   const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
                                   int64_t x_in_stride, int32_t subwarp, void* stream);
-/* Csr, stream strategy: b200sp_csr_stream_rows() consecutive rows per CTA,
- * their nonzeros staged through shared memory with 128-bit loads (col_idxs /
- * vals 16-byte aligned) in chunks of chunk_cap entries (multiple of 4, at
- * most b200sp_csr_stream_capacity(); rows_per_CTA * longest_row + 4 keeps a
- * block in one chunk). Same result contract as csr_row_sums
+/* Csr, stream strategy: a CTA of 256 threads owns (256 / tpr) * rpt
+ * consecutive rows ((tpr, rpt) in {(1,1), (2,1), (4,1), (1,2), (1,4), (1,8)});
+ * their nonzeros are staged through shared memory with 128-bit loads
+ * (col_idxs / vals 16-byte aligned) in chunks of chunk_cap entries (multiple
+ * of 4, at most b200sp_csr_stream_capacity(); rows_per_CTA * longest_row + 4
+ * keeps a block in one chunk). Same result contract as csr_row_sums
  * (kernels.py:304-316). */
 int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                                const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
                                double alpha, const double* alpha_dev, double beta, const double* beta_dev,
-                               const double* x_in, int64_t x_in_stride, int32_t chunk_cap, void* stream);
+                               const double* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
+                               int32_t rpt, void* stream);
 int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                                const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride,
                                float alpha, const float* alpha_dev, float beta, const float* beta_dev,
-                               const float* x_in, int64_t x_in_stride, int32_t chunk_cap, void* stream);
+                               const float* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
+                               int32_t rpt, void* stream);
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
-int32_t b200sp_csr_stream_rows(int32_t value_bytes);
 /* Csr, load-balanced (merge-path) strategy: plan once per matrix
  * (coords: 2*(num_tiles+1) int32), workspace carry_row/carry_val: num_tiles each */
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes);

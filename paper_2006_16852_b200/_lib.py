@@ -33,7 +33,7 @@ _TYPED = {
     # SpMV
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
-    "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "ip",
+    "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
@@ -88,7 +88,6 @@ _UNTYPED = {
     "reduce_max_i32": ("lppp", ctypes.c_int),
     "csr_lb_num_tiles": ("lli", ctypes.c_int64),
     "csr_stream_capacity": ("i", ctypes.c_int32),
-    "csr_stream_rows": ("i", ctypes.c_int32),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),

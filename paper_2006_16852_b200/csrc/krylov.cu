@@ -130,7 +130,38 @@ cg_step2_kernel(RowBlocks rb, T* __restrict__ x, int64_t xs, T* __restrict__ r, 
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const T alpha = (T)c->alpha;
     double rz = 0, rr = 0;
-    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+    if (!rb.J.nblocks) {
+        // no preconditioner: plain element loop, 4 rows in flight per thread
+        const int64_t n = rb.n, st = (int64_t)gridDim.x * blockDim.x;
+        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + 3 * st < n; i += 4 * st) {
+            T pv[4], qv[4], xv[4], rv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t k = i + u * st;
+                pv[u] = p[k];
+                qv[u] = q[k];
+                xv[u] = x[k * xs];
+                rv[u] = r[k];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t k = i + u * st;
+                x[k * xs] = xv[u] + alpha * pv[u];
+                const T nr = rv[u] - alpha * qv[u];
+                r[k] = nr;
+                rr += (double)nr * (double)nr;
+            }
+        }
+        for (; i < n; i += st) {
+            x[i * xs] = x[i * xs] + alpha * p[i];
+            const T nr = r[i] - alpha * q[i];
+            r[i] = nr;
+            rr += (double)nr * (double)nr;
+        }
+        rz = rr;
+    }
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; rb.J.nblocks && b < rb.count(); b += nw) {
         int64_t r0;
         int bs;
         rb.range(b, r0, bs);

@@ -129,8 +129,7 @@ static int csr_classical(int64_t n, const int* rp, const int* ci, const T* v, co
 // accumulating across chunks (correct, but serial: skewed matrices use the
 // load-balanced strategy).
 // ===========================================================================
-template <typename T> struct StreamCap { static constexpr int v = 4096; };
-template <> struct StreamCap<float> { static constexpr int v = 8192; };
+template <typename T> struct StreamCap { static constexpr int v = 8192; };  // 64 KB / 32 KB of smem
 
 template <typename T> struct Quad;
 template <> struct Quad<double> {
@@ -153,34 +152,41 @@ template <> struct Quad<float> {
     }
 };
 
-template <typename T> struct StreamTpr { static constexpr int v = 2; };  // threads per row
-template <> struct StreamTpr<float> { static constexpr int v = 1; };
+// Shape of a CTA (256 threads): TPR threads share a row in the reduction and
+// each thread group reduces RPT rows, so a CTA owns (256 / TPR) * RPT rows.
+// Long rows (27-point) use TPR = 2; short rows (5/7-point) use RPT > 1 so a
+// CTA still streams thousands of nonzeros per staging chunk.
+constexpr int STREAM_NT = 256;
 
-constexpr int STREAM_NT = 256;  // threads per CTA
-template <typename T> constexpr int stream_rows() { return STREAM_NT / StreamTpr<T>::v; }
-
-template <typename T, bool XIN>
+template <typename T, int TPR, int RPT, bool XIN>
 __global__ void __launch_bounds__(STREAM_NT)
 csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
                   const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
                   int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
                   int CAP) {
     if (alpha.skip()) return;
-    constexpr int TPR = StreamTpr<T>::v;
     constexpr int NT = STREAM_NT;
-    constexpr int R = NT / TPR;
+    constexpr int G = NT / TPR;  // thread groups (rows reduced concurrently)
+    constexpr int R = G * RPT;
     constexpr int UQ = 2;  // quads per thread in flight per step
     extern __shared__ __align__(16) unsigned char s_raw[];
     T* s_prod = reinterpret_cast<T*>(s_raw);
     const int t = threadIdx.x;
-    const int my_row = t / TPR, sub = t % TPR;
+    const int grp = t / TPR, sub = t % TPR;
     const int64_t r0 = (int64_t)blockIdx.x * R;
     const int rows = (int)min((int64_t)R, n - r0);
-    const int row_s = my_row < rows ? ld_stream(rp + r0 + my_row) : 0;
-    const int row_e = my_row < rows ? ld_stream(rp + r0 + my_row + 1) : 0;
+    int row_s[RPT], row_e[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+        const int lr = grp + k * G;
+        row_s[k] = lr < rows ? ld_stream(rp + r0 + lr) : 0;
+        row_e[k] = lr < rows ? ld_stream(rp + r0 + lr + 1) : 0;
+    }
     const int seg_s = ld_stream(rp + r0);
     const int seg_e = ld_stream(rp + r0 + rows);
-    T acc0 = 0, acc1 = 0;
+    T acc[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) acc[k] = 0;
     for (int64_t lo = seg_s & ~3; lo < seg_e; lo += CAP) {
         const int64_t hi = min(lo + (int64_t)CAP, (int64_t)seg_e);
         const int nq = (int)((hi - lo + 3) >> 2);
@@ -216,42 +222,74 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
             }
         }
         __syncthreads();
-        const int a0 = (int)(max((int64_t)row_s, lo) - lo), a1 = (int)(min((int64_t)row_e, hi) - lo);
-        int k = a0 + sub;
-        for (; k + TPR < a1; k += 2 * TPR) {
-            acc0 += s_prod[k];
-            acc1 += s_prod[k + TPR];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int a0 = (int)(max((int64_t)row_s[r], lo) - lo), a1 = (int)(min((int64_t)row_e[r], hi) - lo);
+            T s0 = 0, s1 = 0;
+            int k = a0 + sub;
+            for (; k + TPR < a1; k += 2 * TPR) {
+                s0 += s_prod[k];
+                s1 += s_prod[k + TPR];
+            }
+            if (k < a1) s0 += s_prod[k];
+            acc[r] += s0 + s1;
         }
-        if (k < a1) acc0 += s_prod[k];
         __syncthreads();
     }
-    T sum = subwarp_sum<TPR>(acc0 + acc1);
-    if (sub == 0 && my_row < rows) {
-        const int64_t row = r0 + my_row;
-        T out = alpha.get() * sum;
-        if (XIN) out += beta.get() * xin[row * xins];
-        x[row * xs] = out;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const T sum = subwarp_sum<TPR>(acc[r]);
+        const int lr = grp + r * G;
+        if (sub == 0 && lr < rows) {
+            const int64_t row = r0 + lr;
+            T out = alpha.get() * sum;
+            if (XIN) out += beta.get() * xin[row * xins];
+            x[row * xs] = out;
+        }
     }
+}
+
+template <typename T, int TPR, int RPT>
+static void launch_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
+                          int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be, const T* xin, int64_t xins,
+                          int cap, cudaStream_t st) {
+    const unsigned grid = (unsigned)ceil_div(n, (STREAM_NT / TPR) * RPT);
+    const size_t smem = (size_t)cap * sizeof(T);
+    static bool attr_set = false;  // > 48 KB dynamic shared memory needs an opt-in
+    if (!attr_set) {
+        cudaFuncSetAttribute(csr_stream_kernel<T, TPR, RPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             StreamCap<T>::v * (int)sizeof(T));
+        cudaFuncSetAttribute(csr_stream_kernel<T, TPR, RPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             StreamCap<T>::v * (int)sizeof(T));
+        attr_set = true;
+    }
+    if (xin)
+        csr_stream_kernel<T, TPR, RPT, true><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
+    else
+        csr_stream_kernel<T, TPR, RPT, false><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
 }
 
 template <typename T>
 static int csr_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
                       int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
-                      const T* beta_dev, const T* xin, int64_t xins, int chunk_cap, void* stream) {
+                      const T* beta_dev, const T* xin, int64_t xins, int chunk_cap, int tpr, int rpt,
+                      void* stream) {
     if (n == 0) return B200SP_OK;
     B200SP_REQUIRE(aligned16(ci) && aligned16(v), B200SP_EINVAL, "csr stream: col_idxs/vals must be 16-byte aligned");
     B200SP_REQUIRE(chunk_cap >= 4 && chunk_cap % 4 == 0 && chunk_cap <= StreamCap<T>::v, B200SP_EINVAL,
                    "csr stream: chunk_cap must be a multiple of 4 in [4, %d]", StreamCap<T>::v);
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
-    const unsigned grid = (unsigned)ceil_div(n, stream_rows<T>());
-    const size_t smem = (size_t)chunk_cap * sizeof(T);
-    if (xin)
-        csr_stream_kernel<T, true><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap);
-    else
-        csr_stream_kernel<T, false><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap);
-    count_launch();
-    return check_launch("csr_stream");
+#define STREAM_CASE(TP, RP)                                                                                   \
+    if (tpr == TP && rpt == RP) {                                                                             \
+        launch_stream<T, TP, RP>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap, st);          \
+        count_launch();                                                                                       \
+        return check_launch("csr_stream");                                                                    \
+    }
+    STREAM_CASE(1, 1) STREAM_CASE(2, 1) STREAM_CASE(4, 1) STREAM_CASE(1, 2) STREAM_CASE(1, 4) STREAM_CASE(1, 8)
+#undef STREAM_CASE
+    set_error("csr stream: unsupported (threads per row, rows per thread) = (%d, %d)", tpr, rpt);
+    return B200SP_EINVAL;
 }
 
 // ===========================================================================
@@ -815,20 +853,21 @@ int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* rp, const int32_t* c
 int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v,
                                const double* b, int64_t bs, double* x, int64_t xs, double alpha,
                                const double* alpha_dev, double beta, const double* beta_dev,
-                               const double* xin, int64_t xins, int32_t chunk_cap, void* stream) {
-    return csr_stream<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap, stream);
+                               const double* xin, int64_t xins, int32_t chunk_cap, int32_t tpr, int32_t rpt,
+                               void* stream) {
+    return csr_stream<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap,
+                              tpr, rpt, stream);
 }
 int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const float* v,
                                const float* b, int64_t bs, float* x, int64_t xs, float alpha,
                                const float* alpha_dev, float beta, const float* beta_dev,
-                               const float* xin, int64_t xins, int32_t chunk_cap, void* stream) {
-    return csr_stream<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap, stream);
+                               const float* xin, int64_t xins, int32_t chunk_cap, int32_t tpr, int32_t rpt,
+                               void* stream) {
+    return csr_stream<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap,
+                             tpr, rpt, stream);
 }
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
     return value_bytes == 4 ? StreamCap<float>::v : StreamCap<double>::v;
-}
-int32_t b200sp_csr_stream_rows(int32_t value_bytes) {
-    return value_bytes == 4 ? stream_rows<float>() : stream_rows<double>();
 }
 
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes) {

@@ -456,9 +456,11 @@ class Csr(_Sparse):
     def strategy(self):
         return self._resolved_strategy()
 
-    def set_strategy(self, strategy, subwarp=None):
-        """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size."""
+    def set_strategy(self, strategy, subwarp=None, stream_shape=None):
+        """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size,
+        ``stream_shape`` = (threads per row, rows per thread) the stream one."""
         self._set_strategy(strategy)
+        self._stream_shape = tuple(stream_shape) if stream_shape is not None else None
         if subwarp is not None:
             if subwarp not in (1, 2, 4, 8, 16, 32):
                 raise Unsupported("subwarp must be a power of two <= 32")
@@ -496,14 +498,29 @@ class Csr(_Sparse):
             self._subwarp = min(32, 1 << (per_lane - 1).bit_length())
         return self._subwarp
 
-    def stream_chunk(self):
-        """Shared-memory staging chunk (entries): one chunk holds a whole row
-        block when rows_per_CTA * longest_row fits, else the maximum."""
+    def stream_config(self):
+        """(chunk entries, threads per row, rows per thread) of the stream
+        kernel: long rows share 2 threads (fp64), short rows give each thread
+        several rows so a CTA still stages thousands of nonzeros; the chunk
+        holds a whole row block when it fits."""
         vb = self._v.element_size()
+        longest = max(1, self._row_stats())
+        shape = getattr(self, "_stream_shape", None)
+        if shape is None:
+            # measured on C2 / 7-pt / 5-pt (tools/spmv_sweep.py): fp64 27-pt 1x2,
+            # 7-pt 1x2, 5-pt 1x4; fp32 27-pt 1x1
+            mean = self.nnz / max(1, self.size.rows)
+            if vb == 4 and mean >= 16:
+                shape = (1, 1)
+            elif mean < 6:
+                shape = (1, 4)
+            else:
+                shape = (1, 2)
+        tpr, rpt = shape
         cap = int(_lib.query("csr_stream_capacity", vb))
-        rows = int(_lib.query("csr_stream_rows", vb))
-        need = (rows * max(1, self._row_stats()) + 4 + 3) // 4 * 4
-        return min(cap, need)
+        rows = (256 // tpr) * rpt
+        need = (rows * longest + 4 + 3) // 4 * 4
+        return min(cap, need), tpr, rpt
 
     def lb_plan(self):
         if self._plan is None:
@@ -546,8 +563,7 @@ class Csr(_Sparse):
                       ptr(cval), exc.stream)
         elif strategy == "stream" and self._stream_ok():
             _lib.call("csr_spmv_stream_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
-                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.stream_chunk(),
-                      exc.stream)
+                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, *self.stream_config(), exc.stream)
         else:
             _lib.call("csr_spmv_classical_" + suf, n, ptr(self._rp), ptr(self._ci), ptr(self._v),
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.subwarp(), exc.stream)

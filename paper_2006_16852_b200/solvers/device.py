@@ -14,6 +14,7 @@ device at every iteration; launches after the stop are no-ops.
 from __future__ import annotations
 
 import ctypes
+import gc
 
 import numpy as np
 import torch
@@ -119,9 +120,17 @@ class DeviceSolve:
                     return st
                 graph = torch.cuda.CUDAGraph()
                 torch.cuda.synchronize(self.exc.device)
-                with torch.cuda.graph(graph):
-                    for _ in range(iters):
-                        body()
+                # relaxed mode + no GC: a collector-triggered free of a pinned
+                # host tensor (event query) must not invalidate the capture
+                gc_on = gc.isenabled()
+                gc.disable()
+                try:
+                    with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+                        for _ in range(iters):
+                            body()
+                finally:
+                    if gc_on:
+                        gc.enable()
             finally:
                 _lib.query("set_guard", 0)
             self.graph, self.graph_key = graph, (iters, guard_which)

@@ -57,6 +57,10 @@ for sw in (4, 8, 16, 32):
     variants.append((f"csr_classical_sw{sw}", m))
 variants.append(("csr_lb", b2.convert(a, "csr_lb")))
 variants.append(("csr_stream", b2.convert(a, "csr_stream")))
+for shape in ((1, 1), (2, 1), (4, 1), (1, 2), (1, 4), (1, 8)):
+    m = b2.convert(a, "csr")
+    m.set_strategy("stream", stream_shape=shape)
+    variants.append((f"csr_stream_{shape[0]}x{shape[1]}", m))
 if args.matrix == "powerlaw":
     variants = [v for v in variants if v[0] in ("csr_lb", "csr_stream", "csr_classical_sw32")]
 for ch in (128, 256):
