@@ -273,7 +273,8 @@ def bench_c2(args, world, rank, local):
                           "gflops": round(2 * nnz / t_step / 1e9, 1),
                           "frac": round(by / t_step / 1e9 / peak, 4), "bytes": by,
                           "strategy": m.strategy}
-    kern = "csr_classical_kernel" if m.strategy == "classical" else "csr_lb_kernel"
+    kern = {"classical": "csr_classical_kernel", "stream": "csr_stream_kernel",
+            "load_balance": "csr_lb_kernel"}[m.strategy]
     roofline = {"bound": "hbm", "achieved": round(by / t_step / 1e9, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(by / t_step / 1e9 / peak, 4), "traffic": traffic_from_profiles(kern),
                 "peak_source": peak_src, "kernel": kern, "bytes_per_launch": by}
