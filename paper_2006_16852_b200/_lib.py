@@ -34,6 +34,7 @@ _TYPED = {
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiip",
+    "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",

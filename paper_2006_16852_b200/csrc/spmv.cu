@@ -168,7 +168,9 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
     constexpr int NT = STREAM_NT;
     constexpr int G = NT / TPR;  // thread groups (rows reduced concurrently)
     constexpr int R = G * RPT;
-    constexpr int UQ = 2;  // quads per thread in flight per step
+    // quads per thread in flight per step; 4 measured worse (79 registers ->
+    // lower occupancy; profiles/r01_stream_sweep.txt)
+    constexpr int UQ = 2;
     extern __shared__ __align__(16) unsigned char s_raw[];
     T* s_prod = reinterpret_cast<T*>(s_raw);
     const int t = threadIdx.x;
@@ -290,6 +292,149 @@ static int csr_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, cons
 #undef STREAM_CASE
     set_error("csr stream: unsupported (threads per row, rows per thread) = (%d, %d)", tpr, rpt);
     return B200SP_EINVAL;
+}
+
+// ===========================================================================
+// Csr, stream strategy with TMA staging.
+// Same row-block decomposition as above, but the block's contiguous
+// col_idxs / vals range is moved into shared memory by the Tensor Memory
+// Accelerator (cp.async.bulk, one elected thread, completion on an mbarrier),
+// double-buffered: while the CTA reduces chunk c from shared memory, chunk
+// c+1 is already in flight. No per-thread load instructions or registers are
+// spent on the matrix stream; threads only gather x (coalesced across a warp
+// for banded rows) and accumulate their rows.
+// ===========================================================================
+constexpr int TMA_NT = 256;
+
+template <typename T, int RPT, bool XIN>
+__global__ void __launch_bounds__(TMA_NT)
+csr_tma_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
+               const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
+               Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins, int CAP) {
+    if (alpha.skip()) return;
+    constexpr int R = TMA_NT * RPT;
+    extern __shared__ __align__(128) unsigned char s_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_raw);  // 2 mbarriers
+    int* s_ci = reinterpret_cast<int*>(s_raw + 128);     // [2][CAP]
+    T* s_v = reinterpret_cast<T*>(s_raw + 128 + 2 * (size_t)CAP * sizeof(int));  // [2][CAP]
+    const int t = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    const int rows = (int)min((int64_t)R, n - r0);
+    int row_s[RPT], row_e[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+        const int lr = t + k * TMA_NT;
+        row_s[k] = lr < rows ? ld_stream(rp + r0 + lr) : 0;
+        row_e[k] = lr < rows ? ld_stream(rp + r0 + lr + 1) : 0;
+    }
+    const int64_t seg_s = ld_stream(rp + r0), seg_e = ld_stream(rp + r0 + rows);
+    const int64_t lo0 = seg_s & ~(int64_t)3;
+    const int nchunks = (int)((seg_e - lo0 + CAP - 1) / CAP);
+    if (t == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // thread 0 issues chunk c into stage c & 1 (only a multiple of 4 entries is
+    // bulk-copied; the <= 3 tail entries of the segment are read directly)
+    auto issue = [&](int c) {
+        const int64_t lo = lo0 + (int64_t)c * CAP;
+        const int64_t hi = min(lo + (int64_t)CAP, seg_e);
+        const uint32_t cnt = (uint32_t)((hi - lo) & ~(int64_t)3);
+        uint64_t* br = &bar[c & 1];
+        fence_proxy_async();
+        mbar_arrive_expect_tx(br, cnt * (uint32_t)(sizeof(int) + sizeof(T)));
+        if (cnt) {
+            tma_load_1d(s_ci + (size_t)(c & 1) * CAP, ci + lo, cnt * (uint32_t)sizeof(int), br);
+            tma_load_1d(s_v + (size_t)(c & 1) * CAP, v + lo, cnt * (uint32_t)sizeof(T), br);
+        }
+    };
+    if (t == 0) {
+        if (nchunks > 0) issue(0);
+        if (nchunks > 1) issue(1);
+    }
+    T acc[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) acc[k] = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t lo = lo0 + (int64_t)c * CAP;
+        const int64_t hi = min(lo + (int64_t)CAP, seg_e);
+        const int64_t hia = lo + ((hi - lo) & ~(int64_t)3);
+        mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
+        const int* sc = s_ci + (size_t)(c & 1) * CAP;
+        const T* sv = s_v + (size_t)(c & 1) * CAP;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int64_t a0 = max((int64_t)row_s[k], lo), a1 = min((int64_t)row_e[k], hia);
+            int e = (int)(a0 - lo);
+            const int ee = (int)(a1 - lo);
+            T s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+            for (; e + 3 < ee; e += 4) {
+                const int c0 = sc[e], c1 = sc[e + 1], c2 = sc[e + 2], c3 = sc[e + 3];
+                s0 += sv[e] * ld_gather(b + (int64_t)c0 * bs);
+                s1 += sv[e + 1] * ld_gather(b + (int64_t)c1 * bs);
+                s2 += sv[e + 2] * ld_gather(b + (int64_t)c2 * bs);
+                s3 += sv[e + 3] * ld_gather(b + (int64_t)c3 * bs);
+            }
+            for (; e < ee; ++e) s0 += sv[e] * ld_gather(b + (int64_t)sc[e] * bs);
+            // segment tail beyond the bulk-copied range
+            for (int64_t g = max(a0, hia); g < min((int64_t)row_e[k], hi); ++g)
+                s1 += ld_stream(v + g) * ld_gather(b + (int64_t)ld_stream(ci + g) * bs);
+            acc[k] += (s0 + s1) + (s2 + s3);
+        }
+        __syncthreads();  // stage (c & 1) fully consumed
+        if (t == 0 && c + 2 < nchunks) issue(c + 2);
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+        const int lr = t + k * TMA_NT;
+        if (lr < rows) {
+            const int64_t row = r0 + lr;
+            T out = alpha.get() * acc[k];
+            if (XIN) out += beta.get() * xin[row * xins];
+            x[row * xs] = out;
+        }
+    }
+}
+
+template <typename T, int RPT>
+static void launch_tma(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b, int64_t bs,
+                       T* x, int64_t xs, Coef<T> al, Coef<T> be, const T* xin, int64_t xins, int cap,
+                       cudaStream_t st) {
+    const unsigned grid = (unsigned)ceil_div(n, TMA_NT * RPT);
+    const size_t smem = 128 + 2 * (size_t)cap * (sizeof(int) + sizeof(T));
+    static bool attr_set = false;
+    if (!attr_set) {
+        const int maxb = 128 + 2 * 8192 * (int)(sizeof(int) + sizeof(T));
+        cudaFuncSetAttribute(csr_tma_kernel<T, RPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
+        cudaFuncSetAttribute(csr_tma_kernel<T, RPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
+        attr_set = true;
+    }
+    if (xin)
+        csr_tma_kernel<T, RPT, true><<<grid, TMA_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
+    else
+        csr_tma_kernel<T, RPT, false><<<grid, TMA_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
+}
+
+template <typename T>
+static int csr_tma(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b, int64_t bs, T* x,
+                   int64_t xs, T alpha, const T* alpha_dev, T beta, const T* beta_dev, const T* xin, int64_t xins,
+                   int cap, int rpt, void* stream) {
+    if (n == 0) return B200SP_OK;
+    B200SP_REQUIRE(aligned16(ci) && aligned16(v), B200SP_EINVAL, "csr tma: col_idxs/vals must be 16-byte aligned");
+    B200SP_REQUIRE(cap >= 16 && cap % 16 == 0 && cap <= 8192, B200SP_EINVAL,
+                   "csr tma: chunk must be a multiple of 16 in [16, 8192]");
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
+    switch (rpt) {
+        case 1: launch_tma<T, 1>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, st); break;
+        case 2: launch_tma<T, 2>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, st); break;
+        case 4: launch_tma<T, 4>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, st); break;
+        default: set_error("csr tma: rows per thread must be 1, 2 or 4 (got %d)", rpt); return B200SP_EINVAL;
+    }
+    count_launch();
+    return check_launch("csr_tma");
 }
 
 // ===========================================================================
@@ -865,6 +1010,20 @@ int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* rp, const 
                                void* stream) {
     return csr_stream<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap,
                              tpr, rpt, stream);
+}
+int b200sp_csr_spmv_tma_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v,
+                            const double* b, int64_t bs, double* x, int64_t xs, double alpha, const double* alpha_dev,
+                            double beta, const double* beta_dev, const double* xin, int64_t xins, int32_t chunk,
+                            int32_t rpt, void* stream) {
+    return csr_tma<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk, rpt,
+                           stream);
+}
+int b200sp_csr_spmv_tma_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const float* v,
+                            const float* b, int64_t bs, float* x, int64_t xs, float alpha, const float* alpha_dev,
+                            float beta, const float* beta_dev, const float* xin, int64_t xins, int32_t chunk,
+                            int32_t rpt, void* stream) {
+    return csr_tma<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk, rpt,
+                          stream);
 }
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
     return value_bytes == 4 ? StreamCap<float>::v : StreamCap<double>::v;

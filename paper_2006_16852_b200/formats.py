@@ -456,11 +456,16 @@ class Csr(_Sparse):
     def strategy(self):
         return self._resolved_strategy()
 
-    def set_strategy(self, strategy, subwarp=None, stream_shape=None):
+    def set_strategy(self, strategy, subwarp=None, stream_shape=None, stream_cap=None, stream_impl=None):
         """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size,
-        ``stream_shape`` = (threads per row, rows per thread) the stream one."""
+        ``stream_shape`` = (threads per row, rows per thread), ``stream_cap``
+        (entries per staging chunk) and ``stream_impl`` ("tma": bulk-copy
+        staging, "ld": 128-bit load staging) the stream one."""
         self._set_strategy(strategy)
         self._stream_shape = tuple(stream_shape) if stream_shape is not None else None
+        self._stream_cap = int(stream_cap) if stream_cap else None
+        if stream_impl is not None:
+            self._stream_impl = stream_impl
         if subwarp is not None:
             if subwarp not in (1, 2, 4, 8, 16, 32):
                 raise Unsupported("subwarp must be a power of two <= 32")
@@ -498,6 +503,17 @@ class Csr(_Sparse):
             self._subwarp = min(32, 1 << (per_lane - 1).bit_length())
         return self._subwarp
 
+    def tma_config(self):
+        """(entries per TMA stage, rows per thread) of the TMA stream kernel."""
+        shape = getattr(self, "_stream_shape", None)
+        if shape is None:
+            mean = self.nnz / max(1, self.size.rows)
+            rpt = 4 if mean < 6 else (2 if mean < 12 else 1)
+        else:
+            rpt = shape[1]
+        chunk = int(getattr(self, "_stream_cap", None) or 2048)
+        return chunk, rpt
+
     def stream_config(self):
         """(chunk entries, threads per row, rows per thread) of the stream
         kernel: long rows share 2 threads (fp64), short rows give each thread
@@ -512,12 +528,14 @@ class Csr(_Sparse):
             mean = self.nnz / max(1, self.size.rows)
             if vb == 4 and mean >= 16:
                 shape = (1, 1)
-            elif mean < 6:
+            elif mean < 12:
                 shape = (1, 4)
             else:
                 shape = (1, 2)
         tpr, rpt = shape
-        cap = int(_lib.query("csr_stream_capacity", vb))
+        # 32 KB of staging per CTA measured best (64 KB halves the CTAs per SM;
+        # profiles/r01_stream_sweep.txt)
+        cap = int(getattr(self, "_stream_cap", None) or (32768 // vb))
         rows = (256 // tpr) * rpt
         need = (rows * longest + 4 + 3) // 4 * 4
         return min(cap, need), tpr, rpt
@@ -562,8 +580,13 @@ class Csr(_Sparse):
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(coords), ptr(crow),
                       ptr(cval), exc.stream)
         elif strategy == "stream" and self._stream_ok():
-            _lib.call("csr_spmv_stream_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
-                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, *self.stream_config(), exc.stream)
+            if getattr(self, "_stream_impl", "ld") == "tma":
+                chunk, rpt = self.tma_config()
+                _lib.call("csr_spmv_tma_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
+                          bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, chunk, rpt, exc.stream)
+            else:
+                _lib.call("csr_spmv_stream_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
+                          bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, *self.stream_config(), exc.stream)
         else:
             _lib.call("csr_spmv_classical_" + suf, n, ptr(self._rp), ptr(self._ci), ptr(self._v),
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.subwarp(), exc.stream)
