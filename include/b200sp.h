@@ -100,12 +100,12 @@ int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, 
                                const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
                                double alpha, const double* alpha_dev, double beta, const double* beta_dev,
                                const double* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
-                               int32_t rpt, void* stream);
+                               int32_t rpt, int32_t gather_in_reduce, void* stream);
 int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                                const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride,
                                float alpha, const float* alpha_dev, float beta, const float* beta_dev,
                                const float* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
-                               int32_t rpt, void* stream);
+                               int32_t rpt, int32_t gather_in_reduce, void* stream);
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
 /* Csr, stream strategy with TMA staging: 256 threads x rpt (1/2/4) rows per
  * CTA; the block's col_idxs / vals range is bulk-copied (cp.async.bulk +
@@ -265,6 +265,13 @@ int b200sp_jacobi_apply_f32(int64_t nblocks, const int32_t* starts, const int64_
  *   GMRES    src/solvers/gmres.py:183-340:  per Arnoldi step j: [Jacobi], SpMV,
  *            dot0, mgs(i = 0..j-1), normalize; per cycle: backsolve, combine,
  *            after_commit, residual SpMV, reset, scale_v0 */
+/* Persistent cooperative CG for small Csr systems (one launch per solve,
+ * three grid-wide barriers per iteration; after b200sp_cg_init_*, no
+ * preconditioner, contiguous x). */
+int b200sp_cg_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals, double* x,
+                       double* r, double* p, double* q, void* ctl, double* part, double* hist, void* stream);
+int b200sp_cg_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals, float* x,
+                       float* r, float* p, float* q, void* ctl, double* part, double* hist, void* stream);
 int64_t b200sp_krylov_ctl_bytes(void);
 int64_t b200sp_krylov_part_elems(void);
 int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,

@@ -33,7 +33,7 @@ _TYPED = {
     # SpMV
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
-    "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiip",
+    "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
     "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
     "rows_scale": "lpplVpplp",
@@ -60,6 +60,7 @@ _TYPED = {
     "cg_init": "lppp" + "lpppp" + "pppp",
     "cg_step1": "lpppp",
     "cg_sigma": "lppppp",
+    "cg_coop": "lppppppppppp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
     "bicgstab_init": "lplpppppppppppp",
     "bicgstab_step1": "lpppp" + "lpppp" + "pp",

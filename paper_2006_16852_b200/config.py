@@ -18,3 +18,7 @@ DEFAULT_DEVICE = int(os.environ.get("B200SP_DEVICE", "0"))
 
 #: iterations launched per CUDA-graph batch by the device solvers
 SOLVER_BATCH = int(os.environ.get("B200SP_SOLVER_BATCH", "16"))
+
+#: unpreconditioned Csr CG up to this many rows runs as one persistent
+#: cooperative kernel (0 disables)
+CG_COOP_MAX_ROWS = int(os.environ.get("B200SP_CG_COOP_MAX_ROWS", str(1 << 20)))

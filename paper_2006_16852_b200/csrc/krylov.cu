@@ -12,6 +12,8 @@
 //   CG        src/solvers/krylov.py:36-77   + steps.py:87-158
 //   BiCGSTAB  src/solvers/krylov.py:190-271 + steps.py:238-243, :348-480
 //   GMRES     src/solvers/gmres.py:75-340
+#include <cooperative_groups.h>
+
 #include <cstring>
 
 #include "krylov.cuh"
@@ -198,6 +200,129 @@ __global__ void cg_finish_kernel(KrylovCtl* c, double* hist, int phase) {
     if (phase == 0) cg_init_ctl(c, c->red, hist);
     else if (phase == 1) cg_sigma_ctl(c, c->red);
     else cg_step2_ctl(c, c->red, hist);
+}
+
+// ===========================================================================
+// Persistent cooperative CG for small systems (C1: 65,536 rows, L2-resident):
+// the whole solve is ONE launch. Per iteration three grid-wide barriers:
+//   p = z + beta p | q = A p, sigma partials | x, r update, rr partials
+// Every block re-sums the per-block partials in the same order, so all blocks
+// compute bitwise-identical alpha / beta / stop decisions without another
+// barrier; block 0 publishes the status. Same arithmetic as the batched
+// kernels above (Csr rows summed left to right per thread).
+// ===========================================================================
+template <int NV>
+__device__ __forceinline__ void coop_block_partials(double (&v)[NV], double* part, double* sh) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const double s = block_sum(v[k], sh);
+        if (threadIdx.x == 0) part[k * KRY_MAX_GRID + blockIdx.x] = s;
+    }
+}
+template <int NV>
+__device__ __forceinline__ void coop_totals(const double* part, double (&tot)[NV], double* sh_tot) {
+    // warp 0 sums the partials in block order; broadcast through smem
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile double*)part)[k * KRY_MAX_GRID + b];
+            s = warp_sum(s);
+            if (threadIdx.x == 0) sh_tot[k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) tot[k] = sh_tot[k];
+    __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+               T* __restrict__ x, T* __restrict__ r, T* __restrict__ p, T* __restrict__ q, KrylovCtl* c,
+               double* part, double* hist) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh_tot[2];
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    // initial state comes from cg_init (run before): rho, rho_prev, beta, done
+    double rho = c->rho, beta = c->beta;
+    int it = c->it;
+    bool done = c->done;
+    while (!done) {
+        const T tb = (T)beta;
+        for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + tb * p[i];
+        grid.sync();
+        double sg = 0;
+        for (int64_t i = gt; i < n; i += gs) {
+            T s = 0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) s += av[k] * p[ci[k]];
+            q[i] = s;
+            sg += (double)p[i] * (double)s;
+        }
+        double v1[1] = {sg}, t1[1];
+        coop_block_partials<1>(v1, part, sh);
+        grid.sync();
+        coop_totals<1>(part, t1, sh_tot);
+        const double sigma = t1[0];
+        if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
+            if (gt == 0) {
+                c->sigma = sigma;
+                c->breakdown = BD_CG_SIGMA;
+                c->breakdown_it = it + 1;
+                c->done = 1;
+            }
+            break;
+        }
+        const double alpha = safe_div(rho, sigma);
+        const T ta = (T)alpha;
+        double rr = 0;
+        for (int64_t i = gt; i < n; i += gs) {
+            x[i] = x[i] + ta * p[i];
+            const T nr = r[i] - ta * q[i];
+            r[i] = nr;
+            rr += (double)nr * (double)nr;
+        }
+        double v2[1] = {rr}, t2[1];
+        coop_block_partials<1>(v2, part + 2 * KRY_MAX_GRID, sh);
+        grid.sync();
+        coop_totals<1>(part + 2 * KRY_MAX_GRID, t2, sh_tot);
+        const double rho_prev = rho;
+        rho = t2[0];
+        it += 1;
+        const double nrm = sqrt(rho);
+        // identical decision in every block (same inputs, same order)
+        bool stop = false;
+        int sid = 0;
+        for (int i = 0; i < c->n_crit && !stop; ++i) {
+            if (c->crit_type[i] == CRIT_ITERATION && it >= (int)c->crit_param[i]) stop = true, sid = i + 1;
+            else if (c->crit_type[i] == CRIT_RNR && nrm <= c->crit_param[i] * c->baseline) stop = true, sid = i + 1;
+        }
+        beta = safe_div(rho, rho_prev);
+        if (gt == 0) {
+            c->it = it;
+            c->rho_prev = rho_prev;
+            c->rho = rho;
+            c->rnorm = nrm;
+            c->sigma = sigma;
+            c->alpha = alpha;
+            c->beta = beta;
+            hist_put(c, hist, it, nrm);
+            if (stop) {
+                c->stopped = 1;
+                c->stopping_id = sid;
+                c->finalized = 1;
+                c->done = 1;
+            }
+        }
+        // no barrier needed here: every thread updates its own rows in every
+        // phase, and a partial slot is rewritten only after the next barrier,
+        // by which time every block has finished reading it
+        done = stop;
+    }
 }
 
 // ===========================================================================
@@ -757,6 +882,38 @@ int b200sp_gmres_after_commit(void* ctl, void* stream) {
     return check_launch("gmres_after_commit");
 }
 int64_t b200sp_gmres_workspace_elems(int32_t k) { return (int64_t)(k + 1) * k + 3 * (int64_t)k + 1 + k; }
+
+}  // extern "C"
+
+template <typename T>
+static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, T* p, T* q, void* ctl,
+                   double* part, double* hist, void* stream) {
+    int dev = 0, sms = 0, per_sm = 0;
+    B200SP_CHECK_CUDA(cudaGetDevice(&dev));
+    B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_coop_kernel<T>, KRY_BLOCK, 0));
+    int64_t grid = (int64_t)sms * per_sm;
+    if (grid > KRY_MAX_GRID) grid = KRY_MAX_GRID;
+    const int64_t need = ceil_div(n, KRY_BLOCK);
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    KrylovCtl* c = (KrylovCtl*)ctl;
+    void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &q, &c, &part, &hist};
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cg_coop_kernel<T>, dim3((unsigned)grid), dim3(KRY_BLOCK),
+                                                  args, 0, as_stream(stream)));
+    count_launch();
+    return B200SP_OK;
+}
+
+extern "C" {
+int b200sp_cg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
+                       double* p, double* q, void* ctl, double* part, double* hist, void* stream) {
+    return cg_coop<double>(n, rp, ci, v, x, r, p, q, ctl, part, hist, stream);
+}
+int b200sp_cg_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, float* x, float* r,
+                       float* p, float* q, void* ctl, double* part, double* hist, void* stream) {
+    return cg_coop<float>(n, rp, ci, v, x, r, p, q, ctl, part, hist, stream);
+}
 
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream) {
     cg_finish_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl, hist, phase);

@@ -158,7 +158,12 @@ template <> struct Quad<float> {
 // CTA still streams thousands of nonzeros per staging chunk.
 constexpr int STREAM_NT = 256;
 
-template <typename T, int TPR, int RPT, bool XIN>
+// GR ("gather in reduce"): stage (col, val) instead of products and gather x
+// in the thread-per-row reduction, where the lanes of a warp walk consecutive
+// rows -- for banded matrices those gathers are coalesced, while gathers in
+// the staging phase touch ~10 lines per warp instruction and saturate the
+// L1TEX LSU pipe (ncu: 85-94% busy at 47% DRAM, profiles/r01_ncu_c2_stream.txt).
+template <typename T, int TPR, int RPT, bool XIN, bool GR>
 __global__ void __launch_bounds__(STREAM_NT)
 csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
                   const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
@@ -173,6 +178,8 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
     constexpr int UQ = 2;
     extern __shared__ __align__(16) unsigned char s_raw[];
     T* s_prod = reinterpret_cast<T*>(s_raw);
+    int* s_ci = reinterpret_cast<int*>(s_raw);                             // GR only
+    T* s_v = reinterpret_cast<T*>(s_raw + (size_t)CAP * sizeof(int));      // GR only
     const int t = threadIdx.x;
     const int grp = t / TPR, sub = t % TPR;
     const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -216,10 +223,15 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
             for (int u = 0; u < UQ; ++u) {
                 const int q = q0 + u * NT;
                 if (q < nq) {
-                    T p[4];
+                    if (GR) {
+                        reinterpret_cast<int4*>(s_ci)[q] = make_int4(cc[u][0], cc[u][1], cc[u][2], cc[u][3]);
+                        Quad<T>::store(s_v + 4 * q, vv[u]);
+                    } else {
+                        T p[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) p[i] = vv[u][i] * ld_gather(b + (int64_t)cc[u][i] * bs);
-                    Quad<T>::store(s_prod + 4 * q, p);
+                        for (int i = 0; i < 4; ++i) p[i] = vv[u][i] * ld_gather(b + (int64_t)cc[u][i] * bs);
+                        Quad<T>::store(s_prod + 4 * q, p);
+                    }
                 }
             }
         }
@@ -229,11 +241,25 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
             const int a0 = (int)(max((int64_t)row_s[r], lo) - lo), a1 = (int)(min((int64_t)row_e[r], hi) - lo);
             T s0 = 0, s1 = 0;
             int k = a0 + sub;
-            for (; k + TPR < a1; k += 2 * TPR) {
-                s0 += s_prod[k];
-                s1 += s_prod[k + TPR];
+            if (GR) {
+                T s2 = 0, s3 = 0;
+                for (; k + 3 * TPR < a1; k += 4 * TPR) {
+                    const int c0 = s_ci[k], c1 = s_ci[k + TPR], c2 = s_ci[k + 2 * TPR], c3 = s_ci[k + 3 * TPR];
+                    s0 += s_v[k] * ld_gather(b + (int64_t)c0 * bs);
+                    s1 += s_v[k + TPR] * ld_gather(b + (int64_t)c1 * bs);
+                    s2 += s_v[k + 2 * TPR] * ld_gather(b + (int64_t)c2 * bs);
+                    s3 += s_v[k + 3 * TPR] * ld_gather(b + (int64_t)c3 * bs);
+                }
+                for (; k < a1; k += TPR) s0 += s_v[k] * ld_gather(b + (int64_t)s_ci[k] * bs);
+                s0 += s2;
+                s1 += s3;
+            } else {
+                for (; k + TPR < a1; k += 2 * TPR) {
+                    s0 += s_prod[k];
+                    s1 += s_prod[k + TPR];
+                }
+                if (k < a1) s0 += s_prod[k];
             }
-            if (k < a1) s0 += s_prod[k];
             acc[r] += s0 + s1;
         }
         __syncthreads();
@@ -251,30 +277,30 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
     }
 }
 
-template <typename T, int TPR, int RPT>
+template <typename T, int TPR, int RPT, bool GR>
 static void launch_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
                           int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be, const T* xin, int64_t xins,
                           int cap, cudaStream_t st) {
     const unsigned grid = (unsigned)ceil_div(n, (STREAM_NT / TPR) * RPT);
-    const size_t smem = (size_t)cap * sizeof(T);
+    const size_t per = GR ? sizeof(int) + sizeof(T) : sizeof(T);
+    const size_t smem = (size_t)cap * per;
     static bool attr_set = false;  // > 48 KB dynamic shared memory needs an opt-in
     if (!attr_set) {
-        cudaFuncSetAttribute(csr_stream_kernel<T, TPR, RPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             StreamCap<T>::v * (int)sizeof(T));
-        cudaFuncSetAttribute(csr_stream_kernel<T, TPR, RPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             StreamCap<T>::v * (int)sizeof(T));
+        const int maxb = StreamCap<T>::v * (int)per;
+        cudaFuncSetAttribute(csr_stream_kernel<T, TPR, RPT, true, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
+        cudaFuncSetAttribute(csr_stream_kernel<T, TPR, RPT, false, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
         attr_set = true;
     }
     if (xin)
-        csr_stream_kernel<T, TPR, RPT, true><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
+        csr_stream_kernel<T, TPR, RPT, true, GR><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
     else
-        csr_stream_kernel<T, TPR, RPT, false><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
+        csr_stream_kernel<T, TPR, RPT, false, GR><<<grid, STREAM_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
 }
 
 template <typename T>
 static int csr_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
                       int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
-                      const T* beta_dev, const T* xin, int64_t xins, int chunk_cap, int tpr, int rpt,
+                      const T* beta_dev, const T* xin, int64_t xins, int chunk_cap, int tpr, int rpt, int gr,
                       void* stream) {
     if (n == 0) return B200SP_OK;
     B200SP_REQUIRE(aligned16(ci) && aligned16(v), B200SP_EINVAL, "csr stream: col_idxs/vals must be 16-byte aligned");
@@ -284,7 +310,10 @@ static int csr_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, cons
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
 #define STREAM_CASE(TP, RP)                                                                                   \
     if (tpr == TP && rpt == RP) {                                                                             \
-        launch_stream<T, TP, RP>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap, st);          \
+        if (gr)                                                                                               \
+            launch_stream<T, TP, RP, true>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap, st); \
+        else                                                                                                  \
+            launch_stream<T, TP, RP, false>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, chunk_cap, st); \
         count_launch();                                                                                       \
         return check_launch("csr_stream");                                                                    \
     }
@@ -999,17 +1028,17 @@ int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* rp, const 
                                const double* b, int64_t bs, double* x, int64_t xs, double alpha,
                                const double* alpha_dev, double beta, const double* beta_dev,
                                const double* xin, int64_t xins, int32_t chunk_cap, int32_t tpr, int32_t rpt,
-                               void* stream) {
+                               int32_t gather_in_reduce, void* stream) {
     return csr_stream<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap,
-                              tpr, rpt, stream);
+                              tpr, rpt, gather_in_reduce, stream);
 }
 int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const float* v,
                                const float* b, int64_t bs, float* x, int64_t xs, float alpha,
                                const float* alpha_dev, float beta, const float* beta_dev,
                                const float* xin, int64_t xins, int32_t chunk_cap, int32_t tpr, int32_t rpt,
-                               void* stream) {
+                               int32_t gather_in_reduce, void* stream) {
     return csr_stream<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk_cap,
-                             tpr, rpt, stream);
+                             tpr, rpt, gather_in_reduce, stream);
 }
 int b200sp_csr_spmv_tma_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v,
                             const double* b, int64_t bs, double* x, int64_t xs, double alpha, const double* alpha_dev,

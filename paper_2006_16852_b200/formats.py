@@ -456,16 +456,20 @@ class Csr(_Sparse):
     def strategy(self):
         return self._resolved_strategy()
 
-    def set_strategy(self, strategy, subwarp=None, stream_shape=None, stream_cap=None, stream_impl=None):
+    def set_strategy(self, strategy, subwarp=None, stream_shape=None, stream_cap=None, stream_impl=None,
+                     gather_in_reduce=None):
         """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size,
         ``stream_shape`` = (threads per row, rows per thread), ``stream_cap``
-        (entries per staging chunk) and ``stream_impl`` ("tma": bulk-copy
-        staging, "ld": 128-bit load staging) the stream one."""
+        (entries per staging chunk), ``stream_impl`` ("tma": bulk-copy
+        staging, "ld": 128-bit load staging) and ``gather_in_reduce`` (gather
+        x row-coherently in the reduction) the stream one."""
         self._set_strategy(strategy)
         self._stream_shape = tuple(stream_shape) if stream_shape is not None else None
         self._stream_cap = int(stream_cap) if stream_cap else None
         if stream_impl is not None:
             self._stream_impl = stream_impl
+        if gather_in_reduce is not None:
+            self._stream_gr = bool(gather_in_reduce)
         if subwarp is not None:
             if subwarp not in (1, 2, 4, 8, 16, 32):
                 raise Unsupported("subwarp must be a power of two <= 32")
@@ -533,12 +537,17 @@ class Csr(_Sparse):
             else:
                 shape = (1, 2)
         tpr, rpt = shape
+        # gather-in-reduce pays off for long fp64 rows only (27-pt: 62% vs 60%;
+        # 7-pt and fp32 lose; profiles/r01_stream_sweep.txt)
+        gr_default = vb == 8 and self.nnz / max(1, self.size.rows) >= 12
+        gr = int(getattr(self, "_stream_gr", gr_default))
         # 32 KB of staging per CTA measured best (64 KB halves the CTAs per SM;
-        # profiles/r01_stream_sweep.txt)
-        cap = int(getattr(self, "_stream_cap", None) or (32768 // vb))
+        # profiles/r01_stream_sweep.txt); GR stages (col, val) = 4 + VT bytes
+        per = vb + (4 if gr else 0)
+        cap = int(getattr(self, "_stream_cap", None) or (32768 // per) // 4 * 4)
         rows = (256 // tpr) * rpt
         need = (rows * longest + 4 + 3) // 4 * 4
-        return min(cap, need), tpr, rpt
+        return min(cap, need), tpr, rpt, gr
 
     def lb_plan(self):
         if self._plan is None:

@@ -11,7 +11,7 @@ kernels, host scalars.
 
 from __future__ import annotations
 
-from .. import _lib
+from .. import _lib, config
 from ..base import Identity
 from ..executor import CudaExecutor, ptr
 from ..precond import JacobiOperator
@@ -55,6 +55,12 @@ def finish_from_device(solver, state, st, x):
 class CgSolver(IterativeSolver):
     """Preconditioned conjugate gradients (SPD systems)."""
 
+    def _coop_ok(self, J, S):
+        from ..formats import Csr
+
+        return (config.CG_COOP_MAX_ROWS > 0 and self.size.rows <= config.CG_COOP_MAX_ROWS and J[0] == 0
+                and isinstance(self.a, Csr) and S.time_child is None)
+
     def _apply_impl(self, b, x):
         if not device_path_ok(self, b):
             return generic.cg(self, b, x)
@@ -69,6 +75,13 @@ class CgSolver(IterativeSolver):
         S.begin(b, x)
         self._residual(S.xd, S.bd, rd)
         _lib.call("cg_init_" + suf, n, ptr(r), ptr(z), ptr(p), *J, S.c, S.p, S.h, exc.stream)
+
+        if self._coop_ok(J, S):
+            # small system: the whole solve is one persistent cooperative launch
+            a = self.a
+            _lib.call("cg_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(p), ptr(q),
+                      S.c, S.p, S.h, exc.stream)
+            return finish_from_device(self, S, S.status(), x)
 
         def body():
             _lib.call("cg_step1_" + suf, n, ptr(p), ptr(z), S.c, exc.stream)

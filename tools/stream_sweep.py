@@ -32,13 +32,15 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 peak, _ = peaks()
 by = bytes_csr(n, nnz, vt)
 print(f"matrix={args.matrix} g={args.grid} n={n} nnz={nnz} dtype={args.dtype}")
-cases = [("ld", s, c) for s in ((1, 1), (2, 1), (1, 2), (1, 4)) for c in (2048, 4096, 8192)]
+cases = [("ld", s, c, 0) for s in ((1, 1), (1, 2), (1, 4)) for c in (4096,)]
+cases += [("ld", s, c, 1) for s in ((1, 1), (2, 1), (1, 2), (1, 4)) for c in (1024, 2048, 2728, 4096)]
 if "--tma" in sys.argv:
-    cases += [("tma", (1, r), c) for r in (1, 2, 4) for c in (1024, 2048, 4096)]
-for impl, shape, cap in cases:
+    cases += [("tma", (1, r), c, 0) for r in (1, 2, 4) for c in (1024, 2048, 4096)]
+for impl, shape, cap, gr in cases:
     if True:
         m = b2.convert(a, "csr")
-        m.set_strategy("stream", stream_shape=shape, stream_cap=cap, stream_impl=impl)
+        m.set_strategy("stream", stream_shape=shape, stream_cap=cap, stream_impl=impl, gather_in_reduce=gr)
+        impl = impl + ("+gr" if gr else "")
         for _ in range(3):
             m.apply(b, x)
         torch.cuda.synchronize()
