@@ -7,7 +7,7 @@ Krylov ms/iteration (C1/C4/C5 workloads).
 Default workload (N=1) is BASELINE.json config C2: the 3-D 27-point stencil
 128^3 (2,097,152 rows, 55,742,968 entries), fp64. One *step* = one Csr
 (automatic strategy) SpMV x = A b through the C ABI; inputs are larger than
-L2 and L2 is additionally flushed (256 MiB write) between timed steps, each
+L2 and L2 is additionally flushed (256 MiB write, then read) between timed steps, each
 step timed with CUDA events on the launching stream. Every other format
 (Csr classical / load-balanced, Coo, Ell, Sellp, Hybrid) in fp64 and fp32 is
 timed the same way and reported under "formats". N>1: replicas (weak
@@ -181,6 +181,15 @@ class Timer:
         self.torch = torch
         self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=exc.device)
 
+    def flush(self):
+        # write a buffer larger than L2, then read it: the read evicts the
+        # dirty lines of the write here, so their write-back is not charged to
+        # the next timed kernel (tools/flush_study.py: a write-only flush
+        # adds 10-15 us of write-back to a 150 us SpMV); L2 holds none of the
+        # step's operands either way
+        self.flush_buf.fill_(1)
+        self.flush_buf.view(self.torch.int64).sum()
+
     def run(self, fn, steps, warmup):
         torch = self.torch
         for _ in range(warmup):
@@ -190,7 +199,7 @@ class Timer:
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(steps)]
         for s, e in ev:
-            self.flush_buf.fill_(1)
+            self.flush()
             s.record(stream)
             fn()
             e.record(stream)
@@ -318,7 +327,7 @@ def bench_c2(args, world, rank, local):
         "config": {"workload": "C2: Csr SpMV x = A b, 3-D 27-point stencil 128^3 "
                                "(2,097,152 rows, 55,742,968 nnz), fp64 values / int32 indices",
                    "format": f"csr ({m.strategy})", "rows": n, "nnz": nnz,
-                   "l2": "inputs larger than L2 and L2 flushed (256 MiB write) between steps",
+                   "l2": "inputs larger than L2 and L2 flushed (256 MiB write, then read back) between steps",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "gflops": round(2 * nnz / t_step / 1e9, 1),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

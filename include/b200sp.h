@@ -107,18 +107,26 @@ int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, 
                                const float* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
                                int32_t rpt, int32_t gather_in_reduce, void* stream);
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
-/* Csr, stream strategy with TMA staging: 256 threads x rpt (1/2/4) rows per
- * CTA; the block's col_idxs / vals range is bulk-copied (cp.async.bulk +
- * mbarrier, double-buffered, `chunk` entries per stage, multiple of 16, at
- * most 8192) into shared memory while the previous chunk is reduced. */
+/* Csr, stream strategy as a persistent TMA pipeline ("pipe"): one CTA per SM
+ * of `consumers` (256/512) consumer threads + 1 producer warp; tiles of
+ * consumers/tpr*rpt rows, each row reduced by `tpr` (1/2/4) threads; each
+ * tile's row_ptrs slice and col_idxs / vals range is bulk-copied
+ * (cp.async.bulk + mbarrier) into a `stages`-deep ring of shared-memory
+ * stages of `cap` entries (multiple of 4) and reduced out of shared memory.
+ * Supported (consumers, tpr, rpt): (256,1,1|2|4) (512,2,1|2) (512,4,1|2).
+ * stages * b200sp_csr_tma_stage_bytes(rows per tile) + 256 <= 226 KB. row_ptrs/col_idxs/vals 16-byte aligned. Replaces
+ * the same CsrSpmvKernel as the other Csr strategies (src/kernels.py:278-316). */
 int b200sp_csr_spmv_tma_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                             const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
                             double alpha, const double* alpha_dev, double beta, const double* beta_dev,
-                            const double* x_in, int64_t x_in_stride, int32_t chunk, int32_t rpt, void* stream);
+                            const double* x_in, int64_t x_in_stride, int32_t cap, int32_t rpt, int32_t stages,
+                            int32_t consumers, int32_t tpr, void* stream);
 int b200sp_csr_spmv_tma_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                             const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride,
                             float alpha, const float* alpha_dev, float beta, const float* beta_dev,
-                            const float* x_in, int64_t x_in_stride, int32_t chunk, int32_t rpt, void* stream);
+                            const float* x_in, int64_t x_in_stride, int32_t cap, int32_t rpt, int32_t stages,
+                            int32_t consumers, int32_t tpr, void* stream);
+int64_t b200sp_csr_tma_stage_bytes(int32_t value_bytes, int32_t rows_per_tile, int32_t cap);
 /* Csr, load-balanced (merge-path) strategy: plan once per matrix
  * (coords: 2*(num_tiles+1) int32), workspace carry_row/carry_val: num_tiles each */
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes);

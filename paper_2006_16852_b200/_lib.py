@@ -34,7 +34,7 @@ _TYPED = {
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
-    "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iip",
+    "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iiiiip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
@@ -90,6 +90,7 @@ _UNTYPED = {
     "reduce_max_i32": ("lppp", ctypes.c_int),
     "csr_lb_num_tiles": ("lli", ctypes.c_int64),
     "csr_stream_capacity": ("i", ctypes.c_int32),
+    "csr_tma_stage_bytes": ("iii", ctypes.c_int64),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),

@@ -11,6 +11,7 @@
 //   Coo  -> CooSpmvKernel / CooAdvSpmvKernel src/kernels.py:163-240
 //   Ell / Sellp / Hybrid have no reference kernel; their results
 //   are pinned through the format-independent SpMV result.
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -324,146 +325,243 @@ static int csr_stream(int64_t n, int64_t nnz, const int* rp, const int* ci, cons
 }
 
 // ===========================================================================
-// Csr, stream strategy with TMA staging.
-// Same row-block decomposition as above, but the block's contiguous
-// col_idxs / vals range is moved into shared memory by the Tensor Memory
-// Accelerator (cp.async.bulk, one elected thread, completion on an mbarrier),
-// double-buffered: while the CTA reduces chunk c from shared memory, chunk
-// c+1 is already in flight. No per-thread load instructions or registers are
-// spent on the matrix stream; threads only gather x (coalesced across a warp
-// for banded rows) and accumulate their rows.
+// Csr, stream strategy as a persistent TMA pipeline ("pipe").
+// One CTA per SM = 8 consumer warps + 1 producer warp. The matrix is cut into
+// tiles of TR = 256 * RPT consecutive rows; CTA c takes tiles c, c + grid, ...
+// (neighbouring tiles run concurrently on different SMs, so the x window they
+// gather from stays L2-resident). The producer lane bulk-copies each tile's
+// row_ptrs slice and its contiguous col_idxs / vals range into a STAGES-deep
+// ring of shared-memory stages (cp.async.bulk, completion on a `full`
+// mbarrier); consumers sum thread-per-row straight out of shared memory (lanes
+// = consecutive rows, so the x gathers of one warp instruction are coalesced
+// for banded matrices) and hand the stage back through an `empty` mbarrier.
+// No load/store instruction is spent staging the matrix -- the previous
+// register-staged kernel was L1TEX-LSU bound (ncu 85-94% busy) -- and the next
+// tiles stream in while the current one is reduced. A tile whose nonzeros
+// exceed one stage (long rows) is consumed in several chunks, rows
+// accumulating across them.
 // ===========================================================================
-constexpr int TMA_NT = 256;
+constexpr int PIPE_BAR_BYTES = 256;          // mbarriers at the front of smem
 
-template <typename T, int RPT, bool XIN>
-__global__ void __launch_bounds__(TMA_NT)
-csr_tma_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
-               const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
-               Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins, int CAP) {
+__host__ __device__ constexpr int pipe_rp_slots(int tr) { return (tr + 1 + 3) / 4 * 4; }
+
+template <typename T>
+__host__ __device__ inline int64_t pipe_stage_bytes(int tr, int cap) {
+    return (int64_t)pipe_rp_slots(tr) * 4 + (int64_t)cap * (4 + (int64_t)sizeof(T));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T, int NT, int TPR, int RPT, bool XIN>
+__global__ void __launch_bounds__(NT + 32, 1)
+csr_pipe_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
+                const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+                const T* __restrict__ xin, int64_t xins, int CAP, int STAGES) {
     if (alpha.skip()) return;
-    constexpr int R = TMA_NT * RPT;
+    constexpr int G = NT / TPR;  // rows reduced concurrently (TPR threads each)
+    constexpr int TR = G * RPT;  // rows per tile
+    constexpr int RPS = pipe_rp_slots(TR);
     extern __shared__ __align__(128) unsigned char s_raw[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(s_raw);  // 2 mbarriers
-    int* s_ci = reinterpret_cast<int*>(s_raw + 128);     // [2][CAP]
-    T* s_v = reinterpret_cast<T*>(s_raw + 128 + 2 * (size_t)CAP * sizeof(int));  // [2][CAP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_raw);
+    uint64_t* empty = full + STAGES;
+    unsigned char* stages = s_raw + PIPE_BAR_BYTES;
+    const int64_t SB = pipe_stage_bytes<T>(TR, CAP);
     const int t = threadIdx.x;
-    const int64_t r0 = (int64_t)blockIdx.x * R;
-    const int rows = (int)min((int64_t)R, n - r0);
-    int row_s[RPT], row_e[RPT];
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-        const int lr = t + k * TMA_NT;
-        row_s[k] = lr < rows ? ld_stream(rp + r0 + lr) : 0;
-        row_e[k] = lr < rows ? ld_stream(rp + r0 + lr + 1) : 0;
-    }
-    const int64_t seg_s = ld_stream(rp + r0), seg_e = ld_stream(rp + r0 + rows);
-    const int64_t lo0 = seg_s & ~(int64_t)3;
-    const int nchunks = (int)((seg_e - lo0 + CAP - 1) / CAP);
+    const int64_t ntiles = (n + TR - 1) / TR;
     if (t == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NT / 32);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    // thread 0 issues chunk c into stage c & 1 (only a multiple of 4 entries is
-    // bulk-copied; the <= 3 tail entries of the segment are read directly)
-    auto issue = [&](int c) {
-        const int64_t lo = lo0 + (int64_t)c * CAP;
-        const int64_t hi = min(lo + (int64_t)CAP, seg_e);
-        const uint32_t cnt = (uint32_t)((hi - lo) & ~(int64_t)3);
-        uint64_t* br = &bar[c & 1];
-        fence_proxy_async();
-        mbar_arrive_expect_tx(br, cnt * (uint32_t)(sizeof(int) + sizeof(T)));
-        if (cnt) {
-            tma_load_1d(s_ci + (size_t)(c & 1) * CAP, ci + lo, cnt * (uint32_t)sizeof(int), br);
-            tma_load_1d(s_v + (size_t)(c & 1) * CAP, v + lo, cnt * (uint32_t)sizeof(T), br);
+
+    if (t >= NT) {  // ---- producer warp
+        // The segment bounds of the next 32 tiles are fetched by the 32 lanes
+        // at once (one exposed row_ptrs latency per 32 tiles instead of one per
+        // tile); lane 0 then issues every copy.
+        const int lane = t - NT;
+        const int64_t stride = gridDim.x;
+        int it = 0;
+        for (int64_t base = blockIdx.x; base < ntiles; base += 32 * stride) {
+            const int64_t mine = base + lane * stride;
+            int my_s = 0, my_e = 0;
+            if (mine < ntiles) {
+                my_s = __ldg(rp + mine * TR);
+                my_e = __ldg(rp + min(mine * TR + TR, n));
+            }
+            const int batch = (int)min((int64_t)32, (ntiles - base + stride - 1) / stride);
+            for (int j = 0; j < batch; ++j) {
+                const int64_t seg_s = __shfl_sync(0xffffffffu, my_s, j);
+                const int64_t seg_e = __shfl_sync(0xffffffffu, my_e, j);
+                if (lane == 0) {
+                    const int64_t r0 = (base + j * stride) * TR;
+                    const int64_t lo0 = seg_s & ~(int64_t)3;
+                    const int nch = max(1, (int)((seg_e - lo0 + CAP - 1) / CAP));
+                    const int rpc = (int)min((int64_t)RPS, (n + 1 - r0) & ~(int64_t)3);
+                    for (int c = 0; c < nch; ++c, ++it) {
+                        const int s = it % STAGES;
+                        if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+                        const int64_t lo = lo0 + (int64_t)c * CAP;
+                        const int64_t hi = min(lo + (int64_t)CAP, seg_e);
+                        const uint32_t cnt = (uint32_t)(max(hi - lo, (int64_t)0) & ~(int64_t)3);
+                        unsigned char* st = stages + s * SB;
+                        mbar_arrive_expect_tx(&full[s], (uint32_t)rpc * 4u + cnt * (uint32_t)(4 + sizeof(T)));
+                        tma_load_1d(st, rp + r0, (uint32_t)rpc * 4u, &full[s]);
+                        if (cnt) {
+                            tma_load_1d(st + RPS * 4, ci + lo, cnt * 4u, &full[s]);
+                            tma_load_1d(st + RPS * 4 + (int64_t)CAP * 4, v + lo, cnt * (uint32_t)sizeof(T), &full[s]);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
         }
-    };
-    if (t == 0) {
-        if (nchunks > 0) issue(0);
-        if (nchunks > 1) issue(1);
+        return;
     }
-    T acc[RPT];
+
+    // ---- consumers: the TPR threads of group g reduce rows g, g + G, ... of
+    // each tile (entries interleaved across the group)
+    const int lane = t & 31;
+    const int grp = t / TPR, sub = t % TPR;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * TR;
+        const int rows = (int)min((int64_t)TR, n - r0);
+        const int rpc = (int)min((int64_t)RPS, (n + 1 - r0) & ~(int64_t)3);
+        T acc[RPT];
+        int rs[RPT], re[RPT];
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) acc[k] = 0;
-    for (int c = 0; c < nchunks; ++c) {
-        const int64_t lo = lo0 + (int64_t)c * CAP;
-        const int64_t hi = min(lo + (int64_t)CAP, seg_e);
-        const int64_t hia = lo + ((hi - lo) & ~(int64_t)3);
-        mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
-        const int* sc = s_ci + (size_t)(c & 1) * CAP;
-        const T* sv = s_v + (size_t)(c & 1) * CAP;
+        for (int k = 0; k < RPT; ++k) acc[k] = 0;
+        int nch = 1;
+        int64_t lo0 = 0, seg_e = 0;
+        for (int c = 0; c < nch; ++c, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+            const unsigned char* st = stages + s * SB;
+            const int* srp = reinterpret_cast<const int*>(st);
+            const int* sci = reinterpret_cast<const int*>(st + RPS * 4);
+            const T* sv = reinterpret_cast<const T*>(st + RPS * 4 + (int64_t)CAP * 4);
+            if (c == 0) {
+                const int64_t seg_s = srp[0];
+                seg_e = rows < rpc ? srp[rows] : __ldg(rp + r0 + rows);
+                lo0 = seg_s & ~(int64_t)3;
+                nch = max(1, (int)((seg_e - lo0 + CAP - 1) / CAP));
+#pragma unroll
+                for (int k = 0; k < RPT; ++k) {
+                    const int lr = grp + k * G;
+                    rs[k] = lr < rows ? (lr < rpc ? srp[lr] : __ldg(rp + r0 + lr)) : 0;
+                    re[k] = lr < rows ? (lr + 1 < rpc ? srp[lr + 1] : __ldg(rp + r0 + lr + 1)) : 0;
+                }
+            }
+            const int64_t lo = lo0 + (int64_t)c * CAP;
+            const int64_t hi = min(lo + (int64_t)CAP, seg_e);
+            const int64_t hia = lo + (max(hi - lo, (int64_t)0) & ~(int64_t)3);
+            int e[RPT], ee[RPT];
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                e[k] = (int)(max((int64_t)rs[k], lo) - lo) + sub;
+                ee[k] = (int)(max(min((int64_t)re[k], hia), lo) - lo);
+            }
+            // 8 (then 4) independent smem reads + x gathers in flight per row
+            // step (a predicated fixed-batch variant measured slower on every
+            // stencil: profiles/r02_pipe_sweep.txt)
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                int q = e[k];
+                const int qe = ee[k];
+                T s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+                for (; q + 7 * TPR < qe; q += 8 * TPR) {
+                    int cc[8];
+                    T vv[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) cc[i] = sci[q + i * TPR];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) vv[i] = sv[q + i * TPR] * ld_gather(b + (int64_t)cc[i] * bs);
+                    s0 += vv[0] + vv[4];
+                    s1 += vv[1] + vv[5];
+                    s2 += vv[2] + vv[6];
+                    s3 += vv[3] + vv[7];
+                }
+                for (; q + 3 * TPR < qe; q += 4 * TPR) {
+                    const int c0 = sci[q], c1 = sci[q + TPR], c2 = sci[q + 2 * TPR], c3 = sci[q + 3 * TPR];
+                    s0 += sv[q] * ld_gather(b + (int64_t)c0 * bs);
+                    s1 += sv[q + TPR] * ld_gather(b + (int64_t)c1 * bs);
+                    s2 += sv[q + 2 * TPR] * ld_gather(b + (int64_t)c2 * bs);
+                    s3 += sv[q + 3 * TPR] * ld_gather(b + (int64_t)c3 * bs);
+                }
+                for (; q < qe; q += TPR) s0 += sv[q] * ld_gather(b + (int64_t)sci[q] * bs);
+                acc[k] += (s0 + s1) + (s2 + s3);
+            }
+            if (sub == 0) {
+#pragma unroll
+                for (int k = 0; k < RPT; ++k)  // the <= 3 entries past the last bulk-copied quad of the segment
+                    for (int64_t g = max((int64_t)rs[k], hia); g < min((int64_t)re[k], hi); ++g)
+                        acc[k] += ld_stream(v + g) * ld_gather(b + (int64_t)ld_stream(ci + g) * bs);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
-            const int64_t a0 = max((int64_t)row_s[k], lo), a1 = min((int64_t)row_e[k], hia);
-            int e = (int)(a0 - lo);
-            const int ee = (int)(a1 - lo);
-            T s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-            for (; e + 3 < ee; e += 4) {
-                const int c0 = sc[e], c1 = sc[e + 1], c2 = sc[e + 2], c3 = sc[e + 3];
-                s0 += sv[e] * ld_gather(b + (int64_t)c0 * bs);
-                s1 += sv[e + 1] * ld_gather(b + (int64_t)c1 * bs);
-                s2 += sv[e + 2] * ld_gather(b + (int64_t)c2 * bs);
-                s3 += sv[e + 3] * ld_gather(b + (int64_t)c3 * bs);
+            const T sum = subwarp_sum<TPR>(acc[k]);
+            const int lr = grp + k * G;
+            if (sub == 0 && lr < rows) {
+                const int64_t row = r0 + lr;
+                T out = alpha.get() * sum;
+                if (XIN) out += beta.get() * xin[row * xins];
+                x[row * xs] = out;
             }
-            for (; e < ee; ++e) s0 += sv[e] * ld_gather(b + (int64_t)sc[e] * bs);
-            // segment tail beyond the bulk-copied range
-            for (int64_t g = max(a0, hia); g < min((int64_t)row_e[k], hi); ++g)
-                s1 += ld_stream(v + g) * ld_gather(b + (int64_t)ld_stream(ci + g) * bs);
-            acc[k] += (s0 + s1) + (s2 + s3);
-        }
-        __syncthreads();  // stage (c & 1) fully consumed
-        if (t == 0 && c + 2 < nchunks) issue(c + 2);
-    }
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-        const int lr = t + k * TMA_NT;
-        if (lr < rows) {
-            const int64_t row = r0 + lr;
-            T out = alpha.get() * acc[k];
-            if (XIN) out += beta.get() * xin[row * xins];
-            x[row * xs] = out;
         }
     }
 }
 
-template <typename T, int RPT>
-static void launch_tma(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b, int64_t bs,
-                       T* x, int64_t xs, Coef<T> al, Coef<T> be, const T* xin, int64_t xins, int cap,
+template <typename T, int NT, int TPR, int RPT>
+static int launch_pipe(int64_t n, const int* rp, const int* ci, const T* v, const T* b, int64_t bs, T* x,
+                       int64_t xs, Coef<T> al, Coef<T> be, const T* xin, int64_t xins, int cap, int stages,
                        cudaStream_t st) {
-    const unsigned grid = (unsigned)ceil_div(n, TMA_NT * RPT);
-    const size_t smem = 128 + 2 * (size_t)cap * (sizeof(int) + sizeof(T));
-    static bool attr_set = false;
-    if (!attr_set) {
-        const int maxb = 128 + 2 * 8192 * (int)(sizeof(int) + sizeof(T));
-        cudaFuncSetAttribute(csr_tma_kernel<T, RPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
-        cudaFuncSetAttribute(csr_tma_kernel<T, RPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
-        attr_set = true;
-    }
-    if (xin)
-        csr_tma_kernel<T, RPT, true><<<grid, TMA_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
-    else
-        csr_tma_kernel<T, RPT, false><<<grid, TMA_NT, smem, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap);
+    constexpr int TR = NT / TPR * RPT;
+    const int64_t smem = PIPE_BAR_BYTES + (int64_t)stages * pipe_stage_bytes<T>(TR, cap);
+    B200SP_REQUIRE(smem <= 226 * 1024, B200SP_EINVAL,
+                   "csr pipe: %d stages x %d entries need %lld bytes of shared memory (> 226 KB)", stages, cap,
+                   (long long)smem);
+    auto kern = xin ? csr_pipe_kernel<T, NT, TPR, RPT, true> : csr_pipe_kernel<T, NT, TPR, RPT, false>;
+    B200SP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = ceil_div(n, TR);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs));
+    kern<<<grid, NT + 32, (size_t)smem, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, stages);
+    return B200SP_OK;
 }
 
 template <typename T>
-static int csr_tma(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b, int64_t bs, T* x,
-                   int64_t xs, T alpha, const T* alpha_dev, T beta, const T* beta_dev, const T* xin, int64_t xins,
-                   int cap, int rpt, void* stream) {
+static int csr_pipe(int64_t n, const int* rp, const int* ci, const T* v, const T* b, int64_t bs, T* x, int64_t xs,
+                    T alpha, const T* alpha_dev, T beta, const T* beta_dev, const T* xin, int64_t xins, int cap,
+                    int rpt, int stages, int consumers, int tpr, void* stream) {
     if (n == 0) return B200SP_OK;
-    B200SP_REQUIRE(aligned16(ci) && aligned16(v), B200SP_EINVAL, "csr tma: col_idxs/vals must be 16-byte aligned");
-    B200SP_REQUIRE(cap >= 16 && cap % 16 == 0 && cap <= 8192, B200SP_EINVAL,
-                   "csr tma: chunk must be a multiple of 16 in [16, 8192]");
+    B200SP_REQUIRE(aligned16(rp) && aligned16(ci) && aligned16(v), B200SP_EINVAL,
+                   "csr pipe: row_ptrs/col_idxs/vals must be 16-byte aligned");
+    B200SP_REQUIRE(cap >= 16 && cap % 4 == 0, B200SP_EINVAL, "csr pipe: stage capacity must be a multiple of 4, >= 16");
+    B200SP_REQUIRE(stages >= 2 && stages <= 16, B200SP_EINVAL, "csr pipe: stages must be in [2, 16]");
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
-    switch (rpt) {
-        case 1: launch_tma<T, 1>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, st); break;
-        case 2: launch_tma<T, 2>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, st); break;
-        case 4: launch_tma<T, 4>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, st); break;
-        default: set_error("csr tma: rows per thread must be 1, 2 or 4 (got %d)", rpt); return B200SP_EINVAL;
+    int rc;
+#define PIPE_CASE(NT, TP, RP)                                                                                     \
+    if (consumers == NT && tpr == TP && rpt == RP)                                                                \
+        rc = launch_pipe<T, NT, TP, RP>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, stages, st); \
+    else
+    PIPE_CASE(256, 1, 1) PIPE_CASE(256, 1, 2) PIPE_CASE(256, 1, 4) PIPE_CASE(512, 2, 1) PIPE_CASE(512, 2, 2)
+    PIPE_CASE(512, 4, 1) PIPE_CASE(512, 4, 2) {
+        set_error("csr pipe: unsupported (consumer threads, threads per row, rows per thread) = (%d, %d, %d)",
+                  consumers, tpr, rpt);
+        return B200SP_EINVAL;
     }
+#undef PIPE_CASE
+    if (rc != B200SP_OK) return rc;
     count_launch();
-    return check_launch("csr_tma");
+    return check_launch("csr_pipe");
 }
 
 // ===========================================================================
@@ -1042,17 +1140,23 @@ int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* rp, const 
 }
 int b200sp_csr_spmv_tma_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v,
                             const double* b, int64_t bs, double* x, int64_t xs, double alpha, const double* alpha_dev,
-                            double beta, const double* beta_dev, const double* xin, int64_t xins, int32_t chunk,
-                            int32_t rpt, void* stream) {
-    return csr_tma<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk, rpt,
-                           stream);
+                            double beta, const double* beta_dev, const double* xin, int64_t xins, int32_t cap,
+                            int32_t rpt, int32_t stages, int32_t consumers, int32_t tpr, void* stream) {
+    (void)nnz;
+    return csr_pipe<double>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, cap, rpt, stages,
+                            consumers, tpr, stream);
 }
 int b200sp_csr_spmv_tma_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const float* v,
                             const float* b, int64_t bs, float* x, int64_t xs, float alpha, const float* alpha_dev,
-                            float beta, const float* beta_dev, const float* xin, int64_t xins, int32_t chunk,
-                            int32_t rpt, void* stream) {
-    return csr_tma<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, chunk, rpt,
-                          stream);
+                            float beta, const float* beta_dev, const float* xin, int64_t xins, int32_t cap,
+                            int32_t rpt, int32_t stages, int32_t consumers, int32_t tpr, void* stream) {
+    (void)nnz;
+    return csr_pipe<float>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, cap, rpt, stages,
+                           consumers, tpr, stream);
+}
+int64_t b200sp_csr_tma_stage_bytes(int32_t value_bytes, int32_t rows_per_tile, int32_t cap) {
+    const int tr = rows_per_tile;
+    return value_bytes == 4 ? pipe_stage_bytes<float>(tr, cap) : pipe_stage_bytes<double>(tr, cap);
 }
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
     return value_bytes == 4 ? StreamCap<float>::v : StreamCap<double>::v;

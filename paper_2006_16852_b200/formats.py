@@ -457,7 +457,7 @@ class Csr(_Sparse):
         return self._resolved_strategy()
 
     def set_strategy(self, strategy, subwarp=None, stream_shape=None, stream_cap=None, stream_impl=None,
-                     gather_in_reduce=None):
+                     gather_in_reduce=None, stream_stages=None, stream_consumers=None):
         """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size,
         ``stream_shape`` = (threads per row, rows per thread), ``stream_cap``
         (entries per staging chunk), ``stream_impl`` ("tma": bulk-copy
@@ -466,6 +466,8 @@ class Csr(_Sparse):
         self._set_strategy(strategy)
         self._stream_shape = tuple(stream_shape) if stream_shape is not None else None
         self._stream_cap = int(stream_cap) if stream_cap else None
+        self._stream_stages = int(stream_stages) if stream_stages else None
+        self._stream_consumers = int(stream_consumers) if stream_consumers else None
         if stream_impl is not None:
             self._stream_impl = stream_impl
         if gather_in_reduce is not None:
@@ -498,7 +500,7 @@ class Csr(_Sparse):
         return "stream" if self._stream_ok() else "classical"
 
     def _stream_ok(self):
-        return self._ci.data_ptr() % 16 == 0 and self._v.data_ptr() % 16 == 0
+        return self._rp.data_ptr() % 16 == 0 and self._ci.data_ptr() % 16 == 0 and self._v.data_ptr() % 16 == 0
 
     def subwarp(self):
         if self._subwarp is None:
@@ -507,16 +509,40 @@ class Csr(_Sparse):
             self._subwarp = min(32, 1 << (per_lane - 1).bit_length())
         return self._subwarp
 
+    def stream_impl(self):
+        """"tma" (persistent bulk-copy pipeline) or "ld" (register-staged CTA
+        blocks). Measured on B200 (profiles/r02_pipe_sweep.txt, clean-L2
+        timing): 27-point fp64 tma 0.728 vs ld 0.573 of the HBM roofline;
+        27-point fp32 ld 0.728 vs tma 0.673; 7-point fp64 ld 0.758 vs tma
+        0.378 -- short rows leave too few rows in flight per stage to hide the
+        x-gather latency behind 16 consumer warps."""
+        impl = getattr(self, "_stream_impl", None)
+        if impl is not None:
+            return impl
+        mean = self.nnz / max(1, self.size.rows)
+        return "tma" if self._v.element_size() == 8 and mean >= 12 else "ld"
+
     def tma_config(self):
-        """(entries per TMA stage, rows per thread) of the TMA stream kernel."""
+        """(entries per stage, rows per thread, stages, consumer threads,
+        threads per row) of the persistent TMA pipeline. Default (measured
+        best for 27-point fp64): 512 consumers, two threads per row, two rows
+        per thread group (tiles of 512 rows), stages as large as two fit."""
+        vb = self._v.element_size()
         shape = getattr(self, "_stream_shape", None)
         if shape is None:
             mean = self.nnz / max(1, self.size.rows)
-            rpt = 4 if mean < 6 else (2 if mean < 12 else 1)
-        else:
-            rpt = shape[1]
-        chunk = int(getattr(self, "_stream_cap", None) or 2048)
-        return chunk, rpt
+            shape = (2, 2) if mean >= 12 else (1, 4 if mean < 6 else 2)
+        tpr, rpt = shape
+        nt = int(getattr(self, "_stream_consumers", None) or (512 if tpr > 1 else 256))
+        rows = nt // tpr * rpt
+        budget = 220 * 1024 - 256
+        rp_bytes = ((rows + 1 + 3) // 4 * 4) * 4
+        need = (rows * max(1, self._row_stats()) + 4 + 3) // 4 * 4
+        cap_fit2 = ((budget // 2 - rp_bytes) // (4 + vb)) // 4 * 4
+        cap = int(getattr(self, "_stream_cap", None) or min(need, cap_fit2))
+        stage = rp_bytes + cap * (4 + vb)
+        stages = int(getattr(self, "_stream_stages", None) or max(2, min(4, budget // stage)))
+        return cap, rpt, stages, nt, tpr
 
     def stream_config(self):
         """(chunk entries, threads per row, rows per thread) of the stream
@@ -589,10 +615,9 @@ class Csr(_Sparse):
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(coords), ptr(crow),
                       ptr(cval), exc.stream)
         elif strategy == "stream" and self._stream_ok():
-            if getattr(self, "_stream_impl", "ld") == "tma":
-                chunk, rpt = self.tma_config()
+            if self.stream_impl() == "tma":
                 _lib.call("csr_spmv_tma_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
-                          bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, chunk, rpt, exc.stream)
+                          bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, *self.tma_config(), exc.stream)
             else:
                 _lib.call("csr_spmv_stream_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
                           bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, *self.stream_config(), exc.stream)
@@ -1027,6 +1052,8 @@ def _resolve(target):
                  "csr_load_balance": "load_balance", "csr_stream": "stream"}
         if key in named:
             return Csr, {"strategy": named[key]}
+        if key == "csr_pipe":
+            return Csr, {"strategy": "stream", "stream_impl": "tma"}
         try:
             return _FORMAT_NAMES[key], {}
         except KeyError:
@@ -1044,13 +1071,19 @@ def convert(a, target, **params):
     ``slice_size``, ``stride_factor``)."""
     cls, extra = _resolve(target)
     params = {**extra, **params}
+    impl = params.pop("stream_impl", None)
     csr_kw = {"strategy": params.pop("strategy")} if cls is Csr and "strategy" in params else {}
     if isinstance(a, Csr) and cls is Csr:
-        return Csr._from_csr(a, **csr_kw, **params)
-    csr = a._to_csr(**csr_kw)
-    if cls is Csr:
-        return csr if "exec" not in params else Csr._from_csr(csr, **params)
-    return cls._from_csr(csr, **params)
+        out = Csr._from_csr(a, **csr_kw, **params)
+    else:
+        csr = a._to_csr(**csr_kw)
+        if cls is Csr:
+            out = csr if "exec" not in params else Csr._from_csr(csr, **params)
+        else:
+            return cls._from_csr(csr, **params)
+    if impl is not None:
+        out._stream_impl = impl
+    return out
 
 
 def matrix_from_data(exc, data, fmt="csr", **params):

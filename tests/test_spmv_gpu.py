@@ -21,6 +21,11 @@ FORMATS = [
     ("csr", {"strategy": "classical"}),
     ("csr", {"strategy": "load_balance"}),
     ("csr", {"strategy": "stream"}),
+    ("csr", {"strategy": "stream", "impl": "tma"}),
+    ("csr", {"strategy": "stream", "impl": "tma", "rpt": 4, "cap": 64, "stages": 3}),
+    ("csr", {"strategy": "stream", "impl": "ld"}),
+    ("csr", {"strategy": "stream", "impl": "tma", "tpr": 4, "rpt": 2, "cap": 200, "stages": 3, "nt": 512}),
+    ("csr", {"strategy": "stream", "impl": "tma", "tpr": 2, "rpt": 1, "nt": 512}),
     ("coo", {}),
     ("ell", {}),
     ("sellp", {}),
@@ -29,12 +34,20 @@ FORMATS = [
     ("hybrid", {"strategy": "imbalance"}),
     ("hybrid", {"strategy": "col1"}),
 ]
-IDS = ["csr_classical", "csr_lb", "csr_stream", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
+IDS = ["csr_classical", "csr_lb", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
        "hybrid_col1"]
 
 
 def make(b2, exc, data, fmt, kw, dtype="float64"):
     kw = dict(kw)
+    impl = kw.pop("impl", None)
+    if impl is not None:
+        rpt, cap, stages = kw.pop("rpt", None), kw.pop("cap", None), kw.pop("stages", None)
+        nt, tpr = kw.pop("nt", None), kw.pop("tpr", 1)
+        a = b2.matrix_from_data(exc, data, fmt, value_dtype=dtype, **kw)
+        a.set_strategy(kw["strategy"], stream_impl=impl, stream_shape=(tpr, rpt or 1) if (rpt or tpr > 1) else None,
+                       stream_cap=cap, stream_stages=stages, stream_consumers=nt)
+        return a
     if fmt == "hybrid":
         s = kw.pop("strategy", None)
         kw["strategy"] = {None: None, "imbalance": b2.imbalance_limit(0.8),
@@ -174,7 +187,7 @@ def test_repeatable_bitwise(cuda):
 
     a = problems.power_law(cuda, 100000, seed=5, max_len=2000)
     b = b2.Dense(cuda, np.random.default_rng(0).standard_normal((100000, 1)))
-    for fmt in ("csr_classical", "csr_lb", "csr_stream", "coo", "ell", "sellp", "hybrid"):
+    for fmt in ("csr_classical", "csr_lb", "csr_stream", "csr_pipe", "coo", "ell", "sellp", "hybrid"):
         m = b2.convert(a, fmt)
         x1, x2 = b2.Dense.zeros(cuda, 100000, 1), b2.Dense.zeros(cuda, 100000, 1)
         m.apply(b, x1)
@@ -274,7 +287,7 @@ def test_c2_full_size_properties(cuda):
     g = 128
     cnt = [(1 + (t > 0) + (t < g - 1)) for t in (idx // (g * g), (idx // g) % g, idx % g)]
     expect = 27.0 - cnt[0] * cnt[1] * cnt[2]  # 26 - (len - 1)
-    for fmt in ("csr_classical", "csr_lb", "csr_stream", "coo", "ell", "sellp", "hybrid"):
+    for fmt in ("csr_classical", "csr_lb", "csr_stream", "csr_pipe", "coo", "ell", "sellp", "hybrid"):
         m = b2.convert(a, fmt)
         x = b2.Dense.zeros(cuda, n, 1)
         m.apply(ones, x)
@@ -284,7 +297,7 @@ def test_c2_full_size_properties(cuda):
     rp, ci, vals = P.to_csr(n, r, c, v)
     bv = np.random.default_rng(0).standard_normal((n, 1))
     ref = OS.csr_spmv(rp, ci, vals, bv)
-    for fmt in ("csr_classical", "csr_lb", "csr_stream", "coo", "ell", "sellp", "hybrid"):
+    for fmt in ("csr_classical", "csr_lb", "csr_stream", "csr_pipe", "coo", "ell", "sellp", "hybrid"):
         x = b2.Dense.zeros(cuda, n, 1)
         b2.convert(a, fmt).apply(b2.Dense(cuda, bv), x)
         assert OS.rel_error_inf(np.asarray(x.data), ref) <= 1e-14, fmt
