@@ -49,6 +49,10 @@ int b200sp_device_sync(void);
  * thread while a guard is set return immediately when *guard != 0 (device
  * flag). Solvers set it to their "done" flag around CUDA-graph batches. */
 void b200sp_set_guard(const int32_t* guard);
+/* Tuning knob for benchmark sweeps (kernel variant / launch shape by name);
+ * unset knobs keep the measured-best defaults. Not thread-safe against
+ * concurrent set calls; not needed for correct results. */
+int b200sp_set_tuning(const char* key, int32_t value);
 int64_t b200sp_reduce_workspace_elems(void);
 int64_t b200sp_scan_workspace_elems(int64_t count);
 int b200sp_exclusive_scan_i32(int64_t count, const int32_t* in, int32_t* out, long long* ws, void* stream);

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libb200sp.so")
 # type codes: l=int64 i=int32 u=uint64 p=pointer d=double V=value type of the suffix
 _P = ctypes.c_void_p
 _CT = {"l": ctypes.c_int64, "i": ctypes.c_int32, "u": ctypes.c_uint64, "p": _P,
-       "d": ctypes.c_double}
+       "d": ctypes.c_double, "s": ctypes.c_char_p}
 
 _SPMV_TAIL = "VpVppl"          # alpha, alpha_dev, beta, beta_dev, x_in, x_in_stride
 _TYPED = {
@@ -106,6 +106,7 @@ _UNTYPED = {
     "stencil_lengths": ("illlpp", ctypes.c_int),
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
     "set_guard": ("p", None),
+    "set_tuning": ("si", ctypes.c_int),
     "jacobi_block_sizes_sq": ("lppp", ctypes.c_int),
     "jacobi_pack": ("lppppppp", ctypes.c_int),
     "krylov_ctl_bytes": ("", ctypes.c_int64),
@@ -195,6 +196,11 @@ def query(name, *args):
     """Invoke a function returning a value (not an error code)."""
     _load()
     return _funcs[name](*args)
+
+
+def set_tuning(key, value):
+    """Select a kernel variant / launch shape by name (benchmark sweeps)."""
+    call("set_tuning", key.encode(), int(value))
 
 
 def launch_count():

@@ -24,6 +24,7 @@ constexpr int kWarp = 32;
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch(int n = 1);
+int tuning(const char* key, int dflt);  // b200sp_set_tuning knobs (sweeps)
 
 #define B200SP_CHECK_CUDA(expr)                                              \
     do {                                                                     \

@@ -37,6 +37,20 @@ int check_launch(const char* what) {
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Tuning knobs (kernel variants / launch shapes) for sweeps; every knob has
+// the measured-best default at its call site (tuning(key, default)).
+static constexpr int kMaxKnobs = 32;
+static char g_knob_key[kMaxKnobs][32];
+static int g_knob_val[kMaxKnobs];
+static std::atomic<int> g_knobs{0};
+
+int tuning(const char* key, int dflt) {
+    const int k = g_knobs.load(std::memory_order_acquire);
+    for (int i = 0; i < k; ++i)
+        if (std::strncmp(g_knob_key[i], key, sizeof(g_knob_key[i])) == 0) return g_knob_val[i];
+    return dflt;
+}
+
 // ---------------------------------------------------------------------------
 // exclusive scan (int32 in -> int32/int64 out, with total at out[count])
 // three phases: tile sums, single-CTA scan of tile sums, tile scan + offset
@@ -240,6 +254,21 @@ const char* b200sp_last_error(void) { return g_err; }
 long long b200sp_launch_count(void) { return g_launches.load(); }
 int b200sp_version(void) { return B200SP_ABI_VERSION; }
 void b200sp_set_guard(const int32_t* guard) { g_guard = guard; }
+
+int b200sp_set_tuning(const char* key, int32_t value) {
+    const int k = g_knobs.load(std::memory_order_acquire);
+    for (int i = 0; i < k; ++i)
+        if (std::strncmp(g_knob_key[i], key, sizeof(g_knob_key[i])) == 0) {
+            g_knob_val[i] = value;
+            return B200SP_OK;
+        }
+    B200SP_REQUIRE(k < kMaxKnobs, B200SP_EINVAL, "set_tuning: too many knobs");
+    B200SP_REQUIRE(std::strlen(key) < sizeof(g_knob_key[0]), B200SP_EINVAL, "set_tuning: key too long");
+    std::strncpy(g_knob_key[k], key, sizeof(g_knob_key[k]));
+    g_knob_val[k] = value;
+    g_knobs.store(k + 1, std::memory_order_release);
+    return B200SP_OK;
+}
 int64_t b200sp_reduce_workspace_elems(void) { return (int64_t)kNumSMs * 4 * RED_MAX_COLS; }
 
 int b200sp_device_sync(void) {

@@ -28,7 +28,9 @@ namespace b200sp {
 // the one-row variant reached 32% of peak on C2).
 template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1); };
 
-template <typename T, int SW, bool XIN>
+// L1: matrix reads allocate in L1 (a sub-warp touches only part of each
+// sector per step; the next steps re-read the rest of it from L1, not L2)
+template <typename T, int SW, bool XIN, bool L1>
 __global__ void __launch_bounds__(256)
 csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
                      const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
@@ -61,8 +63,8 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const bool ok = k < len[u];
-                c[u] = ok ? ld_stream(ci + s[u] + k) : -1;
-                vv[u] = ok ? ld_stream(v + s[u] + k) : T(0);
+                c[u] = ok ? (L1 ? __ldg(ci + s[u] + k) : ld_stream(ci + s[u] + k)) : -1;
+                vv[u] = ok ? (L1 ? __ldg(v + s[u] + k) : ld_stream(v + s[u] + k)) : T(0);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -90,11 +92,14 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
                              int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be,
                              const T* xin, int64_t xins, cudaStream_t st) {
     const int block = 256;
-    int grid = grid_for(ceil_div(n, ClassicalRows<SW>::v) * SW, block, 8);
-    if (xin)
-        csr_classical_kernel<T, SW, true><<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
-    else
-        csr_classical_kernel<T, SW, false><<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
+    // measured on B200 (profiles/r02_classical_sweep.txt): L1-allocating
+    // matrix loads lift C2 fp64 (sub-warp 4) from 0.43 to 0.85 of the HBM
+    // roofline and 7-point (sub-warp 1) from 0.27 to 0.85; two waves of CTAs
+    int grid = grid_for(ceil_div(n, ClassicalRows<SW>::v) * SW, block, tuning("classical_per_sm", 16));
+    auto kern = tuning("classical_l1", 1)
+                    ? (xin ? csr_classical_kernel<T, SW, true, true> : csr_classical_kernel<T, SW, false, true>)
+                    : (xin ? csr_classical_kernel<T, SW, true, false> : csr_classical_kernel<T, SW, false, false>);
+    kern<<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
 }
 
 template <typename T>
@@ -961,7 +966,7 @@ static int rows_scale(int64_t count, const int* rows, T* x, int64_t xs, T beta, 
 
 // Dot product of one row stored at base, base+step, ... (len slots, padding
 // col = -1) with b: UNR independent loads in flight per thread.
-template <typename T, int UNR>
+template <typename T, int UNR, bool L1 = false>
 __device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __restrict__ v, int64_t base,
                                          int64_t step, int len, const T* __restrict__ b, int64_t bs) {
     T acc[UNR];
@@ -973,8 +978,8 @@ __device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __
         T vv[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            c[u] = ld_stream(ci + base + (int64_t)(k + u) * step);
-            vv[u] = ld_stream(v + base + (int64_t)(k + u) * step);
+            c[u] = L1 ? __ldg(ci + base + (int64_t)(k + u) * step) : ld_stream(ci + base + (int64_t)(k + u) * step);
+            vv[u] = L1 ? __ldg(v + base + (int64_t)(k + u) * step) : ld_stream(v + base + (int64_t)(k + u) * step);
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
@@ -994,7 +999,7 @@ __device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __
 // Ell: column-major (stride >= n), one thread per row, padding col = -1.
 // Consecutive threads read consecutive addresses of every stored column.
 // ===========================================================================
-template <typename T, bool XIN>
+template <typename T, bool XIN, int UNR, bool L1>
 __global__ void __launch_bounds__(256)
 ell_kernel(int64_t n, int64_t width, int64_t stride, const int* __restrict__ ci,
            const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
@@ -1004,7 +1009,7 @@ ell_kernel(int64_t n, int64_t width, int64_t stride, const int* __restrict__ ci,
     const T bt = XIN ? beta.get() : T(0);
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
          row += (int64_t)gridDim.x * blockDim.x) {
-        const T sum = strided_dot<T, 4>(ci, v, row, stride, (int)width, b, bs);
+        const T sum = strided_dot<T, UNR, L1>(ci, v, row, stride, (int)width, b, bs);
         T out = a * sum;
         if (XIN) out += bt * xin[row * xins];
         x[row * xs] = out;
@@ -1019,11 +1024,11 @@ static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, con
     B200SP_REQUIRE(stride >= n, B200SP_EINVAL, "ell: stride %lld < rows %lld", (long long)stride, (long long)n);
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
-    const int grid = grid_for(n, 256, 16);
-    if (xin)
-        ell_kernel<T, true><<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
-    else
-        ell_kernel<T, false><<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
+    const int per_sm = tuning("ell_per_sm", 16);
+    const int grid = per_sm > 0 ? grid_for(n, 256, per_sm) : (int)ceil_div(n, 256);
+    auto kern = tuning("ell_l1", 0) ? (xin ? ell_kernel<T, true, 4, true> : ell_kernel<T, false, 4, true>)
+                                    : (xin ? ell_kernel<T, true, 4, false> : ell_kernel<T, false, 4, false>);
+    kern<<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
     count_launch();
     return check_launch("ell_spmv");
 }
@@ -1032,7 +1037,7 @@ static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, con
 // Sellp: slices of `slice_size` rows, each stored column-major with its own
 // length (slice_sets = exclusive prefix of slice lengths). Thread per row.
 // ===========================================================================
-template <typename T, bool XIN>
+template <typename T, bool XIN, int UNR, bool L1>
 __global__ void __launch_bounds__(256)
 sellp_kernel(int64_t n, int slice_size, const int* __restrict__ slice_lengths,
              const int* __restrict__ slice_sets, const int* __restrict__ ci, const T* __restrict__ v,
@@ -1047,7 +1052,7 @@ sellp_kernel(int64_t n, int slice_size, const int* __restrict__ slice_lengths,
         const int64_t local = row - slice * slice_size;
         const int len = slice_lengths[slice];
         const int64_t base = (int64_t)slice_sets[slice] * slice_size + local;
-        const T sum = strided_dot<T, 4>(ci, v, base, slice_size, len, b, bs);
+        const T sum = strided_dot<T, UNR, L1>(ci, v, base, slice_size, len, b, bs);
         T out = a * sum;
         if (XIN) out += bt * xin[row * xins];
         x[row * xs] = out;
@@ -1063,11 +1068,11 @@ static int sellp_spmv(int64_t n, int slice_size, const int* sl, const int* ss, c
     B200SP_REQUIRE(slice_size > 0, B200SP_EINVAL, "sellp: slice_size must be positive");
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
-    const int grid = grid_for(n, 256, 16);
-    if (xin)
-        sellp_kernel<T, true><<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
-    else
-        sellp_kernel<T, false><<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
+    const int per_sm = tuning("sellp_per_sm", 16);
+    const int grid = per_sm > 0 ? grid_for(n, 256, per_sm) : (int)ceil_div(n, 256);
+    auto kern = tuning("sellp_l1", 0) ? (xin ? sellp_kernel<T, true, 4, true> : sellp_kernel<T, false, 4, true>)
+                                      : (xin ? sellp_kernel<T, true, 4, false> : sellp_kernel<T, false, 4, false>);
+    kern<<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
     count_launch();
     return check_launch("sellp_spmv");
 }

@@ -392,7 +392,7 @@ class Csr(_Sparse):
                           with a deterministic carry fix-up;
     * ``stream``       -- row blocks whose nonzeros are staged through shared
                           memory with 128-bit loads, thread-per-row reduction;
-    * ``automatic``    -- stream unless the row lengths are skewed
+    * ``automatic``    -- classical unless the row lengths are skewed
                           (max > 4 x mean + 64), then load_balance.
     """
 
@@ -489,6 +489,11 @@ class Csr(_Sparse):
         return self._max_row
 
     def _resolved_strategy(self):
+        """automatic: load_balance for skewed row lengths (max > 4 x mean +
+        64), else classical -- with L1-allocating matrix loads the sub-warp
+        kernel is the fastest Csr SpMV measured on B200 for every stencil
+        (C2 fp64 0.85, fp32 0.74, 7-point 0.85 of the HBM roofline;
+        profiles/r02_classical_sweep.txt) ahead of the staged stream kernels."""
         if self._requested != "automatic":
             return self._requested
         n = self.size.rows
@@ -497,7 +502,7 @@ class Csr(_Sparse):
         mean = self.nnz / n
         if self._row_stats() > 4 * mean + 64:
             return "load_balance"
-        return "stream" if self._stream_ok() else "classical"
+        return "classical"
 
     def _stream_ok(self):
         return self._rp.data_ptr() % 16 == 0 and self._ci.data_ptr() % 16 == 0 and self._v.data_ptr() % 16 == 0
