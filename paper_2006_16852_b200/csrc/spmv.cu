@@ -764,46 +764,15 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
 // ===========================================================================
 constexpr int COO_BLOCK = 256;
 
-template <typename T, bool XIN, bool VEC, int E>
-__global__ void __launch_bounds__(COO_BLOCK)
-coo_kernel(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
-           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
-           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
-           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
-    if (alpha.skip()) return;
-    constexpr int CHUNK = 32 * E;
-    const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t e0 = c * CHUNK;
-    if (e0 >= nnz) return;
-    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
-    const int head_row = rows[e0], tail_row = rows[e1 - 1];
-    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
-    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
-    const T a = alpha.get();
-    const T bt = XIN ? beta.get() : T(0);
-
-    const int64_t l0 = e0 + (int64_t)lane * E;
-    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
-    int r[E], cc[E];
-    T vv[E];
-    if (VEC && cnt == E) {
-        ld_stream_vec<E>(rows + l0, r);
-        ld_stream_vec<E>(cols + l0, cc);
-        ld_stream_vec<E>(vals + l0, vv);
-    } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-            const bool ok = i < cnt;
-            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
-            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
-            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
-        }
-    }
-    T p[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
-
+// Reduce one chunk whose entries are already in registers (lane holds
+// entries l0 .. l0 + cnt - 1 of [e0, e1)); writes completed rows to x and the
+// partial sums of rows shared with neighbouring chunks to the carries.
+template <typename T, bool XIN, int E>
+__device__ __forceinline__ void coo_chunk(int64_t c, int64_t e0, int64_t e1, int lane, int cnt, const int (&r)[E],
+                                          const T (&p)[E], int head_row, int tail_row, bool head_shared,
+                                          bool tail_shared, T a, T bt, T* __restrict__ x, int64_t xs,
+                                          const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head,
+                                          T* __restrict__ carry_tail) {
     // lane-local runs: the first completed run may continue from earlier
     // lanes (needs the scan), later completed runs are final
     int cur = r[0], first_row = INT_MIN;
@@ -881,6 +850,120 @@ coo_kernel(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ co
     }
 }
 
+template <typename T, int E, bool VEC>
+__device__ __forceinline__ void coo_load(const int* __restrict__ rows, const int* __restrict__ cols,
+                                         const T* __restrict__ vals, int64_t l0, int cnt, int (&r)[E], int (&cc)[E],
+                                         T (&vv)[E]) {
+    if (VEC && cnt == E) {
+        ld_stream_vec<E>(rows + l0, r);
+        ld_stream_vec<E>(cols + l0, cc);
+        ld_stream_vec<E>(vals + l0, vv);
+    } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const bool ok = i < cnt;
+            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
+            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
+            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
+        }
+    }
+}
+
+// One chunk per warp (the grid covers every chunk).
+template <typename T, bool XIN, bool VEC, int E>
+__global__ void __launch_bounds__(COO_BLOCK)
+coo_kernel(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
+           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    if (alpha.skip()) return;
+    constexpr int CHUNK = 32 * E;
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = c * CHUNK;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
+    const int head_row = rows[e0], tail_row = rows[e1 - 1];
+    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
+    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+    const int64_t l0 = e0 + (int64_t)lane * E;
+    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
+    int r[E], cc[E];
+    T vv[E];
+    coo_load<T, E, VEC>(rows, cols, vals, l0, cnt, r, cc, vv);
+    T p[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
+    coo_chunk<T, XIN, E>(c, e0, e1, lane, cnt, r, p, head_row, tail_row, head_shared, tail_shared, alpha.get(),
+                         XIN ? beta.get() : T(0), x, xs, xin, xins, carry_head, carry_tail);
+}
+
+// Persistent warps over chunks c, c + W, ... with the next chunk's rows /
+// cols / vals loads issued before the current chunk's gathers and scan, so
+// every warp keeps a chunk of HBM reads in flight (the one-chunk-per-warp
+// grid holds a chunk only between its loads and its gathers).
+template <typename T, bool XIN, bool VEC, int E>
+__global__ void __launch_bounds__(COO_BLOCK, 2)
+coo_kernel_pf(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
+              const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+              int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+              T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    if (alpha.skip()) return;
+    constexpr int CHUNK = 32 * E;
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = (nnz + CHUNK - 1) / CHUNK;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (c >= nchunks) return;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    int r[E], cc[E];
+    T vv[E];
+    int64_t e0 = c * CHUNK;
+    int64_t l0 = e0 + (int64_t)lane * E;
+    int cnt = (int)max((int64_t)0, min((int64_t)E, min(e0 + (int64_t)CHUNK, nnz) - l0));
+    coo_load<T, E, VEC>(rows, cols, vals, l0, cnt, r, cc, vv);
+    int hprev = e0 > 0 ? __ldg(rows + e0 - 1) : INT_MIN;
+    int tnext = e0 + CHUNK < nnz ? __ldg(rows + e0 + CHUNK) : INT_MIN;
+#pragma unroll 1
+    for (; c < nchunks; c += nw) {
+        const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
+        // prefetch the next chunk of this warp
+        const int64_t c2 = c + nw;
+        const int64_t f0 = c2 * CHUNK;
+        const int64_t m0 = f0 + (int64_t)lane * E;
+        const int cnt2 = c2 < nchunks ? (int)max((int64_t)0, min((int64_t)E, min(f0 + (int64_t)CHUNK, nnz) - m0)) : 0;
+        int r2[E], cc2[E];
+        T vv2[E];
+        coo_load<T, E, VEC>(rows, cols, vals, m0, cnt2, r2, cc2, vv2);
+        const int hprev2 = c2 < nchunks ? __ldg(rows + f0 - 1) : INT_MIN;
+        const int tnext2 = c2 < nchunks && f0 + CHUNK < nnz ? __ldg(rows + f0 + CHUNK) : INT_MIN;
+        // current chunk
+        T p[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
+        const int last_lane = (int)((e1 - 1 - e0) / E);
+        const int head_row = __shfl_sync(0xffffffffu, r[0], 0);
+        int last_r = r[0];
+#pragma unroll
+        for (int i = 1; i < E; ++i)
+            if (i < cnt) last_r = r[i];
+        const int tail_row = __shfl_sync(0xffffffffu, last_r, last_lane);
+        coo_chunk<T, XIN, E>(c, e0, e1, lane, cnt, r, p, head_row, tail_row, hprev == head_row,
+                             tnext == tail_row, a, bt, x, xs, xin, xins, carry_head, carry_tail);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            r[i] = r2[i];
+            cc[i] = cc2[i];
+            vv[i] = vv2[i];
+        }
+        e0 = f0;
+        cnt = cnt2;
+        hprev = hprev2;
+        tnext = tnext2;
+    }
+}
+
 template <typename T, bool XIN>
 __global__ void coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
                                  const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
@@ -922,14 +1005,23 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
     const unsigned grid = (unsigned)ceil_div(threads, COO_BLOCK);
     const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
     const bool vec = aligned16(rows) && aligned16(cols) && aligned16(vals);
-#define COO_LAUNCH(XI, VE)                                                                              \
-    do {                                                                                                \
-        if (chunk == 256)                                                                               \
-            coo_kernel<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, \
-                                                                 be, xin, xins, carry_head, carry_tail); \
-        else                                                                                            \
-            coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, \
-                                                                 be, xin, xins, carry_head, carry_tail); \
+    const int pf = tuning("coo_prefetch", 0);
+    const unsigned pgrid = (unsigned)std::min<int64_t>(grid, (int64_t)kNumSMs * tuning("coo_per_sm", 2));
+#define COO_LAUNCH(XI, VE)                                                                                  \
+    do {                                                                                                    \
+        if (pf) {                                                                                           \
+            if (chunk == 256)                                                                               \
+                coo_kernel_pf<T, XI, VE, 8><<<pgrid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, \
+                                                                         al, be, xin, xins, carry_head, carry_tail); \
+            else                                                                                            \
+                coo_kernel_pf<T, XI, VE, 4><<<pgrid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, \
+                                                                         al, be, xin, xins, carry_head, carry_tail); \
+        } else if (chunk == 256)                                                                            \
+            coo_kernel<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,     \
+                                                                 be, xin, xins, carry_head, carry_tail);     \
+        else                                                                                                \
+            coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,     \
+                                                                 be, xin, xins, carry_head, carry_tail);     \
     } while (0)
     if (xin) {
         if (vec) COO_LAUNCH(true, true); else COO_LAUNCH(true, false);
@@ -973,6 +1065,7 @@ __device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __
 #pragma unroll
     for (int u = 0; u < UNR; ++u) acc[u] = 0;
     int k = 0;
+#pragma unroll 1
     for (; k + UNR <= len; k += UNR) {
         int c[UNR];
         T vv[UNR];
@@ -985,6 +1078,7 @@ __device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __
         for (int u = 0; u < UNR; ++u)
             if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
     }
+#pragma unroll 1
     for (; k < len; ++k) {
         const int c = ld_stream(ci + base + (int64_t)k * step);
         if (c >= 0) acc[0] += ld_stream(v + base + (int64_t)k * step) * ld_gather(b + (int64_t)c * bs);
@@ -1026,8 +1120,7 @@ static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, con
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int per_sm = tuning("ell_per_sm", 16);
     const int grid = per_sm > 0 ? grid_for(n, 256, per_sm) : (int)ceil_div(n, 256);
-    auto kern = tuning("ell_l1", 0) ? (xin ? ell_kernel<T, true, 4, true> : ell_kernel<T, false, 4, true>)
-                                    : (xin ? ell_kernel<T, true, 4, false> : ell_kernel<T, false, 4, false>);
+    auto kern = xin ? ell_kernel<T, true, 4, false> : ell_kernel<T, false, 4, false>;
     kern<<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
     count_launch();
     return check_launch("ell_spmv");
@@ -1037,26 +1130,47 @@ static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, con
 // Sellp: slices of `slice_size` rows, each stored column-major with its own
 // length (slice_sets = exclusive prefix of slice lengths). Thread per row.
 // ===========================================================================
-template <typename T, bool XIN, int UNR, bool L1>
-__global__ void __launch_bounds__(256)
+// One thread per row, no grid-stride loop (every CTA covers 256 / slice
+// rows of whole slices): fewer live registers than the grid-stride form
+// (ncu: 40 registers capped warps active at 66% vs Ell's 96%).
+// S > 0: compile-time slice size (the default 64: shifts instead of a 64-bit
+// division per row). GS: grid-stride rows (fp32) or one row per thread (fp64).
+// MINB = 8 caps registers at 32 (8 CTAs per SM): the unbounded build used
+// 56-66 registers and held warps active at 46-66% (ncu), 0.52 / 0.65 of the
+// roofline; bounded: 0.64 / 0.79 (profiles/r02_format_sweep.txt).
+template <typename T, bool XIN, int UNR, int MINB, bool GS, int S>
+__global__ void __launch_bounds__(256, MINB)
 sellp_kernel(int64_t n, int slice_size, const int* __restrict__ slice_lengths,
              const int* __restrict__ slice_sets, const int* __restrict__ ci, const T* __restrict__ v,
              const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha,
              Coef<T> beta, const T* __restrict__ xin, int64_t xins) {
     if (alpha.skip()) return;
-    const T a = alpha.get();
-    const T bt = XIN ? beta.get() : T(0);
+    const int ss = S > 0 ? S : slice_size;
+#pragma unroll 1
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
-         row += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t slice = row / slice_size;
-        const int64_t local = row - slice * slice_size;
-        const int len = slice_lengths[slice];
-        const int64_t base = (int64_t)slice_sets[slice] * slice_size + local;
-        const T sum = strided_dot<T, UNR, L1>(ci, v, base, slice_size, len, b, bs);
-        T out = a * sum;
-        if (XIN) out += bt * xin[row * xins];
+         row += GS ? (int64_t)gridDim.x * blockDim.x : n) {
+        const int64_t slice = row / ss;
+        const int local = (int)(row - slice * ss);
+        const int len = __ldg(slice_lengths + slice);
+        const int64_t base = (int64_t)__ldg(slice_sets + slice) * ss + local;
+        const T sum = strided_dot<T, UNR>(ci, v, base, ss, len, b, bs);
+        T out = alpha.get() * sum;
+        if (XIN) out += beta.get() * xin[row * xins];
         x[row * xs] = out;
     }
+}
+
+template <typename T, bool XIN, int S>
+static void launch_sellp(int64_t n, int slice_size, const int* sl, const int* ss, const int* ci, const T* v,
+                         const T* b, int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be, const T* xin,
+                         int64_t xins, cudaStream_t st) {
+    const bool gs = tuning("sellp_grid_stride", sizeof(T) == 4);
+    if (gs)
+        sellp_kernel<T, XIN, 4, 8, true, S><<<grid_for(n, 256, 16), 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs,
+                                                                                 x, xs, al, be, xin, xins);
+    else
+        sellp_kernel<T, XIN, 4, 8, false, S><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
 }
 
 template <typename T>
@@ -1068,11 +1182,13 @@ static int sellp_spmv(int64_t n, int slice_size, const int* sl, const int* ss, c
     B200SP_REQUIRE(slice_size > 0, B200SP_EINVAL, "sellp: slice_size must be positive");
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
-    const int per_sm = tuning("sellp_per_sm", 16);
-    const int grid = per_sm > 0 ? grid_for(n, 256, per_sm) : (int)ceil_div(n, 256);
-    auto kern = tuning("sellp_l1", 0) ? (xin ? sellp_kernel<T, true, 4, true> : sellp_kernel<T, false, 4, true>)
-                                      : (xin ? sellp_kernel<T, true, 4, false> : sellp_kernel<T, false, 4, false>);
-    kern<<<grid, 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins);
+    if (slice_size == 64) {
+        if (xin) launch_sellp<T, true, 64>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins, st);
+        else launch_sellp<T, false, 64>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins, st);
+    } else {
+        if (xin) launch_sellp<T, true, 0>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins, st);
+        else launch_sellp<T, false, 0>(n, slice_size, sl, ss, ci, v, b, bs, x, xs, al, be, xin, xins, st);
+    }
     count_launch();
     return check_launch("sellp_spmv");
 }
