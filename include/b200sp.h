@@ -131,21 +131,27 @@ int b200sp_csr_spmv_tma_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, con
                             const float* x_in, int64_t x_in_stride, int32_t cap, int32_t rpt, int32_t stages,
                             int32_t consumers, int32_t tpr, void* stream);
 int64_t b200sp_csr_tma_stage_bytes(int32_t value_bytes, int32_t rows_per_tile, int32_t cap);
-/* Csr, load-balanced (merge-path) strategy: plan once per matrix
- * (coords: 2*(num_tiles+1) int32), workspace carry_row/carry_val: num_tiles each */
-int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes);
-int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* row_ptrs, int32_t value_bytes, int32_t* coords,
+/* Csr, load-balanced strategy: merge-path tiles of `tile` merge items (rows +
+ * nonzeros) with a deterministic carry fix-up. mode 1: items merged
+ * thread-by-thread from shared memory (skewed rows); mode 2: the tile's rows
+ * reduced sub-warp-per-row from global memory, long rows and the carried-out
+ * row by the whole CTA. Plan once per matrix: tile = b200sp_csr_lb_tile(vb,
+ * mode), coords = 2*(num_tiles+1) int32; workspace carry_row / carry_val
+ * num_tiles each. */
+int32_t b200sp_csr_lb_tile(int32_t value_bytes, int32_t mode);
+int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t tile);
+int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* row_ptrs, int32_t tile, int32_t* coords,
                        void* stream);
 int b200sp_csr_spmv_lb_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                            const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
                            double alpha, const double* alpha_dev, double beta, const double* beta_dev,
                            const double* x_in, int64_t x_in_stride, const int32_t* coords, int32_t* carry_row,
-                           double* carry_val, void* stream);
+                           double* carry_val, int32_t tile, int32_t mode, void* stream);
 int b200sp_csr_spmv_lb_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,
                            const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride,
-                           float alpha, const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
-                           int64_t x_in_stride, const int32_t* coords, int32_t* carry_row, float* carry_val,
-                           void* stream);
+                           float alpha, const float* alpha_dev, float beta, const float* beta_dev,
+                           const float* x_in, int64_t x_in_stride, const int32_t* coords, int32_t* carry_row,
+                           float* carry_val, int32_t tile, int32_t mode, void* stream);
 /* Coo (entries sorted by row); replaces CooSpmvKernel / CooAdvSpmvKernel /
  * CooResidualKernel (kernels.py:163-275). Rows with no entry are NOT written:
  * the caller prefills them with b200sp_rows_scale_*. carry_head/carry_tail:

@@ -32,7 +32,7 @@ _TYPED = {
     "norm2": "liplpppp",
     # SpMV
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
-    "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppp",
+    "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppiip",
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
     "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iiiiip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
@@ -88,6 +88,7 @@ _UNTYPED = {
     "exclusive_scan_i32": ("lpppp", ctypes.c_int),
     "exclusive_scan_i64": ("lpppp", ctypes.c_int),
     "reduce_max_i32": ("lppp", ctypes.c_int),
+    "csr_lb_tile": ("ii", ctypes.c_int32),
     "csr_lb_num_tiles": ("lli", ctypes.c_int64),
     "csr_stream_capacity": ("i", ctypes.c_int32),
     "csr_tma_stage_bytes": ("iii", ctypes.c_int64),

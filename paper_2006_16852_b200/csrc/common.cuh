@@ -120,6 +120,7 @@ __device__ __forceinline__ void ld_stream_vec(const float* p, float (&out)[E]) {
     }
 }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+__device__ __forceinline__ bool aligned16_dev(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // Gathered vector entries: read-only path, allocate in L1 (neighbouring rows
 // of a stencil share most of their columns).

@@ -43,9 +43,12 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
     const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
-    for (int64_t row0 = (tid / SW) * U; row0 < n; row0 += nsw * U) {
+    // loop while the warp's first sub-warp has rows (uniform trip count: the
+    // sub-warp shuffles below use the full mask); later sub-warps are masked
+    const int64_t wfirst = (tid / 32) * (32 / SW) * U;
+    for (int64_t row0 = (tid / SW) * U, w0 = wfirst; w0 < n; row0 += nsw * U, w0 += nsw * U) {
         int s[U], len[U];
-        int ptr_next = ld_stream(rp + row0);
+        int ptr_next = row0 < n ? ld_stream(rp + row0) : 0;
         int maxlen = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -582,8 +585,11 @@ constexpr int LB_BLOCK = 256;
 template <typename T> struct LbIpt { static constexpr int v = 7; };
 template <> struct LbIpt<float> { static constexpr int v = 9; };
 
+// merge items (rows + nonzeros) per tile: mode 1 (item merge) is fixed by
+// its shared-memory staging arrays; mode 2 (row-parallel) takes 16384
+// (measured best of 2K/8K/16K on the stencils; knob "lb_tile")
 template <typename T>
-constexpr int lb_tile() { return LB_BLOCK * LbIpt<T>::v; }
+inline int lb_tile(int mode) { return mode == 2 ? tuning("lb_tile", 16384) : LB_BLOCK * LbIpt<T>::v; }
 
 // merge-path search: returns number of row-end items (rows) consumed at `diag`
 __device__ __forceinline__ int64_t merge_search_global(int64_t diag, const int* rp, int64_t n,
@@ -733,16 +739,143 @@ __global__ void csr_lb_fixup_kernel(int64_t n, int64_t ntiles, const int* __rest
     x[(int64_t)row * xs] += alpha.get() * sum;
 }
 
+// ---------------------------------------------------------------------------
+// Load-balanced strategy, row-parallel tile processing ("lb2"). Same
+// merge-path tiles and carry fix-up as above, but a CTA processes its tile's
+// rows directly from global memory like the classical kernel (sub-warp per
+// row with L1-allocating loads; the sub-warp width follows the tile's mean
+// row length), instead of staging products and merging item by item. Rows of
+// the tile longer than LB2_LONG entries and the carried-out last row are
+// reduced by the whole CTA. Rows whose start precedes the tile are clipped
+// to the tile's first nonzero (the fix-up adds the earlier tiles' carries).
+// ---------------------------------------------------------------------------
+constexpr int LB2_LONG = 16;  // x sub-warp width: longer rows take the CTA-wide pass
+
+template <typename T, int SW, bool XIN>
+__device__ __forceinline__ void lb2_rows(int r0, int r1, int k0, const int* __restrict__ rp,
+                                         const int* __restrict__ ci, const T* __restrict__ v,
+                                         const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
+                                         T a, T bt, const T* __restrict__ xin, int64_t xins, int* s_long,
+                                         int* s_nlong) {
+    const int lane = threadIdx.x & (SW - 1);
+    constexpr int SPW = 32 / SW;  // sub-warps per warp
+    // the trip count is uniform across a warp (the sub-warp shuffles use the
+    // full mask); rows past r1 are masked
+#pragma unroll 1
+    for (int rb = r0 + (threadIdx.x >> 5) * SPW; rb < r1; rb += LB_BLOCK / SW) {
+        const int row = rb + (threadIdx.x & 31) / SW;
+        const bool active = row < r1;
+        int s = 0, e = 0;
+        if (active) {
+            s = max(__ldg(rp + row), k0);
+            e = __ldg(rp + row + 1);
+        }
+        const bool lng = e - s > LB2_LONG * SW;
+        if (lng) {  // deferred to the CTA-wide pass
+            if (lane == 0) s_long[atomicAdd(s_nlong, 1)] = row;
+            e = s;
+        }
+        T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        int k = s + lane;
+        for (; k + 3 * SW < e; k += 4 * SW) {
+            const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + SW), c2 = __ldg(ci + k + 2 * SW),
+                      c3 = __ldg(ci + k + 3 * SW);
+            a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
+            a1 += __ldg(v + k + SW) * ld_gather(b + (int64_t)c1 * bs);
+            a2 += __ldg(v + k + 2 * SW) * ld_gather(b + (int64_t)c2 * bs);
+            a3 += __ldg(v + k + 3 * SW) * ld_gather(b + (int64_t)c3 * bs);
+        }
+        for (; k < e; k += SW) a0 += __ldg(v + k) * ld_gather(b + (int64_t)__ldg(ci + k) * bs);
+        const T sum = subwarp_sum<SW>((a0 + a1) + (a2 + a3));
+        if (active && !lng && lane == 0) {
+            T out = a * sum;
+            if (XIN) out += bt * xin[(int64_t)row * xins];
+            x[(int64_t)row * xs] = out;
+        }
+    }
+}
+
+// CTA-wide sum of entries [s, e) (result valid in thread 0)
+template <typename T>
+__device__ __forceinline__ T lb2_block_dot(int s, int e, const int* __restrict__ ci, const T* __restrict__ v,
+                                           const T* __restrict__ b, int64_t bs, T* sh) {
+    T a0 = 0, a1 = 0;
+    int k = s + threadIdx.x;
+    for (; k + LB_BLOCK < e; k += 2 * LB_BLOCK) {
+        const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + LB_BLOCK);
+        a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
+        a1 += __ldg(v + k + LB_BLOCK) * ld_gather(b + (int64_t)c1 * bs);
+    }
+    if (k < e) a0 += __ldg(v + k) * ld_gather(b + (int64_t)__ldg(ci + k) * bs);
+    return block_sum(a0 + a1, sh);
+}
+
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(LB_BLOCK)
+csr_lb2_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
+               const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+               const T* __restrict__ xin, int64_t xins, const int* __restrict__ coords, int* __restrict__ carry_row,
+               T* __restrict__ carry_val) {
+    if (alpha.skip()) return;
+    __shared__ int s_long[LB_BLOCK];
+    __shared__ int s_nlong;
+    __shared__ T s_red[LB_BLOCK / 32];
+    const int tile = blockIdx.x;
+    const int r0 = coords[2 * tile], k0 = coords[2 * tile + 1];
+    const int r1 = coords[2 * tile + 2], k1 = coords[2 * tile + 3];
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    if (threadIdx.x == 0) s_nlong = 0;
+    __syncthreads();
+    const int nrows = r1 - r0;
+    if (nrows > 0) {
+        // sub-warp width from the tile's mean row length (classical rule)
+        const int mean = (k1 - k0 + nrows - 1) / nrows;
+        const int per_lane = (mean + 7) / 8;
+        if (per_lane <= 1) lb2_rows<T, 1, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+        else if (per_lane <= 2) lb2_rows<T, 2, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+        else if (per_lane <= 4) lb2_rows<T, 4, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+        else if (per_lane <= 8) lb2_rows<T, 8, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+        else if (per_lane <= 16) lb2_rows<T, 16, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+        else lb2_rows<T, 32, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+    }
+    __syncthreads();
+    const int nlong = s_nlong;
+    for (int i = 0; i < nlong; ++i) {
+        const int row = s_long[i];
+        const T sum = lb2_block_dot(max(__ldg(rp + row), k0), __ldg(rp + row + 1), ci, v, b, bs, s_red);
+        if (threadIdx.x == 0) {
+            T out = a * sum;
+            if (XIN) out += bt * xin[(int64_t)row * xins];
+            x[(int64_t)row * xs] = out;
+        }
+    }
+    // carry-out: the entries of row r1 inside this tile
+    T carry = 0;
+    if (r1 < n) carry = lb2_block_dot(max(__ldg(rp + r1), k0), k1, ci, v, b, bs, s_red);
+    if (threadIdx.x == 0) {
+        carry_row[tile] = r1;
+        carry_val[tile] = carry;
+    }
+}
+
 template <typename T>
 static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b,
                   int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
                   const T* beta_dev, const T* xin, int64_t xins, const int* coords,
-                  int* carry_row, T* carry_val, void* stream) {
+                  int* carry_row, T* carry_val, int tile, int mode, void* stream) {
     if (n == 0) return B200SP_OK;
+    B200SP_REQUIRE(mode == 1 || mode == 2, B200SP_EINVAL, "csr lb: mode must be 1 (merge) or 2 (rows), got %d", mode);
+    B200SP_REQUIRE(tile > 0 && (mode == 2 || tile == lb_tile<T>(1)), B200SP_EINVAL,
+                   "csr lb: tile %d does not match mode %d (plan with b200sp_csr_lb_tile)", tile, mode);
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
-    const int64_t ntiles = ceil_div(n + nnz, lb_tile<T>());
-    if (xin)
+    const int64_t ntiles = ceil_div(n + nnz, tile);
+    if (mode == 2) {
+        auto k2 = xin ? csr_lb2_kernel<T, true> : csr_lb2_kernel<T, false>;
+        k2<<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row,
+                                                   carry_val);
+    } else if (xin)
         csr_lb_kernel<T, true><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
     else
         csr_lb_kernel<T, false><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
@@ -764,15 +897,46 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
 // ===========================================================================
 constexpr int COO_BLOCK = 256;
 
-// Reduce one chunk whose entries are already in registers (lane holds
-// entries l0 .. l0 + cnt - 1 of [e0, e1)); writes completed rows to x and the
-// partial sums of rows shared with neighbouring chunks to the carries.
-template <typename T, bool XIN, int E>
-__device__ __forceinline__ void coo_chunk(int64_t c, int64_t e0, int64_t e1, int lane, int cnt, const int (&r)[E],
-                                          const T (&p)[E], int head_row, int tail_row, bool head_shared,
-                                          bool tail_shared, T a, T bt, T* __restrict__ x, int64_t xs,
-                                          const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head,
-                                          T* __restrict__ carry_tail) {
+// MINB: 6 CTAs per SM (<= 40 registers) measured best for fp32 (0.70 vs
+// 0.63 of the roofline), unbounded (62 registers) for fp64 (0.645 vs 0.55).
+template <typename T, bool XIN, bool VEC, int E>
+__device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
+           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    constexpr int CHUNK = 32 * E;
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = c * CHUNK;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
+    const int head_row = rows[e0], tail_row = rows[e1 - 1];
+    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
+    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+
+    const int64_t l0 = e0 + (int64_t)lane * E;
+    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
+    int r[E], cc[E];
+    T vv[E];
+    if (VEC && cnt == E) {
+        ld_stream_vec<E>(rows + l0, r);
+        ld_stream_vec<E>(cols + l0, cc);
+        ld_stream_vec<E>(vals + l0, vv);
+    } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const bool ok = i < cnt;
+            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
+            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
+            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
+        }
+    }
+    T p[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
+
     // lane-local runs: the first completed run may continue from earlier
     // lanes (needs the scan), later completed runs are final
     int cur = r[0], first_row = INT_MIN;
@@ -850,119 +1014,23 @@ __device__ __forceinline__ void coo_chunk(int64_t c, int64_t e0, int64_t e1, int
     }
 }
 
-template <typename T, int E, bool VEC>
-__device__ __forceinline__ void coo_load(const int* __restrict__ rows, const int* __restrict__ cols,
-                                         const T* __restrict__ vals, int64_t l0, int cnt, int (&r)[E], int (&cc)[E],
-                                         T (&vv)[E]) {
-    if (VEC && cnt == E) {
-        ld_stream_vec<E>(rows + l0, r);
-        ld_stream_vec<E>(cols + l0, cc);
-        ld_stream_vec<E>(vals + l0, vv);
-    } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-            const bool ok = i < cnt;
-            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
-            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
-            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
-        }
-    }
-}
-
-// One chunk per warp (the grid covers every chunk).
+#define COO_ARGS                                                                                         \
+    int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols, const T* __restrict__ vals,   \
+        const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,   \
+        const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail
+#define COO_PASS nnz, rows, cols, vals, b, bs, x, xs, alpha, beta, xin, xins, carry_head, carry_tail
 template <typename T, bool XIN, bool VEC, int E>
-__global__ void __launch_bounds__(COO_BLOCK)
-coo_kernel(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
-           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
-           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
-           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+__global__ void __launch_bounds__(COO_BLOCK) coo_kernel(COO_ARGS) {
     if (alpha.skip()) return;
-    constexpr int CHUNK = 32 * E;
-    const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t e0 = c * CHUNK;
-    if (e0 >= nnz) return;
-    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
-    const int head_row = rows[e0], tail_row = rows[e1 - 1];
-    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
-    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
-    const int64_t l0 = e0 + (int64_t)lane * E;
-    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
-    int r[E], cc[E];
-    T vv[E];
-    coo_load<T, E, VEC>(rows, cols, vals, l0, cnt, r, cc, vv);
-    T p[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
-    coo_chunk<T, XIN, E>(c, e0, e1, lane, cnt, r, p, head_row, tail_row, head_shared, tail_shared, alpha.get(),
-                         XIN ? beta.get() : T(0), x, xs, xin, xins, carry_head, carry_tail);
+    coo_body<T, XIN, VEC, E>(COO_PASS);
 }
-
-// Persistent warps over chunks c, c + W, ... with the next chunk's rows /
-// cols / vals loads issued before the current chunk's gathers and scan, so
-// every warp keeps a chunk of HBM reads in flight (the one-chunk-per-warp
-// grid holds a chunk only between its loads and its gathers).
 template <typename T, bool XIN, bool VEC, int E>
-__global__ void __launch_bounds__(COO_BLOCK, 2)
-coo_kernel_pf(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
-              const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
-              int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
-              T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+__global__ void __launch_bounds__(COO_BLOCK, 6) coo_kernel_b6(COO_ARGS) {
     if (alpha.skip()) return;
-    constexpr int CHUNK = 32 * E;
-    const int lane = threadIdx.x & 31;
-    const int64_t nchunks = (nnz + CHUNK - 1) / CHUNK;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (c >= nchunks) return;
-    const T a = alpha.get();
-    const T bt = XIN ? beta.get() : T(0);
-    int r[E], cc[E];
-    T vv[E];
-    int64_t e0 = c * CHUNK;
-    int64_t l0 = e0 + (int64_t)lane * E;
-    int cnt = (int)max((int64_t)0, min((int64_t)E, min(e0 + (int64_t)CHUNK, nnz) - l0));
-    coo_load<T, E, VEC>(rows, cols, vals, l0, cnt, r, cc, vv);
-    int hprev = e0 > 0 ? __ldg(rows + e0 - 1) : INT_MIN;
-    int tnext = e0 + CHUNK < nnz ? __ldg(rows + e0 + CHUNK) : INT_MIN;
-#pragma unroll 1
-    for (; c < nchunks; c += nw) {
-        const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
-        // prefetch the next chunk of this warp
-        const int64_t c2 = c + nw;
-        const int64_t f0 = c2 * CHUNK;
-        const int64_t m0 = f0 + (int64_t)lane * E;
-        const int cnt2 = c2 < nchunks ? (int)max((int64_t)0, min((int64_t)E, min(f0 + (int64_t)CHUNK, nnz) - m0)) : 0;
-        int r2[E], cc2[E];
-        T vv2[E];
-        coo_load<T, E, VEC>(rows, cols, vals, m0, cnt2, r2, cc2, vv2);
-        const int hprev2 = c2 < nchunks ? __ldg(rows + f0 - 1) : INT_MIN;
-        const int tnext2 = c2 < nchunks && f0 + CHUNK < nnz ? __ldg(rows + f0 + CHUNK) : INT_MIN;
-        // current chunk
-        T p[E];
-#pragma unroll
-        for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
-        const int last_lane = (int)((e1 - 1 - e0) / E);
-        const int head_row = __shfl_sync(0xffffffffu, r[0], 0);
-        int last_r = r[0];
-#pragma unroll
-        for (int i = 1; i < E; ++i)
-            if (i < cnt) last_r = r[i];
-        const int tail_row = __shfl_sync(0xffffffffu, last_r, last_lane);
-        coo_chunk<T, XIN, E>(c, e0, e1, lane, cnt, r, p, head_row, tail_row, hprev == head_row,
-                             tnext == tail_row, a, bt, x, xs, xin, xins, carry_head, carry_tail);
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-            r[i] = r2[i];
-            cc[i] = cc2[i];
-            vv[i] = vv2[i];
-        }
-        e0 = f0;
-        cnt = cnt2;
-        hprev = hprev2;
-        tnext = tnext2;
-    }
+    coo_body<T, XIN, VEC, E>(COO_PASS);
 }
+#undef COO_ARGS
+#undef COO_PASS
 
 template <typename T, bool XIN>
 __global__ void coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
@@ -1005,23 +1073,18 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
     const unsigned grid = (unsigned)ceil_div(threads, COO_BLOCK);
     const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
     const bool vec = aligned16(rows) && aligned16(cols) && aligned16(vals);
-    const int pf = tuning("coo_prefetch", 0);
-    const unsigned pgrid = (unsigned)std::min<int64_t>(grid, (int64_t)kNumSMs * tuning("coo_per_sm", 2));
+    const int minb = tuning("coo_minb", sizeof(T) == 4 ? 6 : 1);
 #define COO_LAUNCH(XI, VE)                                                                                  \
     do {                                                                                                    \
-        if (pf) {                                                                                           \
-            if (chunk == 256)                                                                               \
-                coo_kernel_pf<T, XI, VE, 8><<<pgrid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, \
-                                                                         al, be, xin, xins, carry_head, carry_tail); \
-            else                                                                                            \
-                coo_kernel_pf<T, XI, VE, 4><<<pgrid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, \
-                                                                         al, be, xin, xins, carry_head, carry_tail); \
-        } else if (chunk == 256)                                                                            \
-            coo_kernel<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,     \
-                                                                 be, xin, xins, carry_head, carry_tail);     \
+        if (chunk == 128)                                                                                   \
+            coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
+                                                                    be, xin, xins, carry_head, carry_tail);  \
+        else if (minb == 6)                                                                                 \
+            coo_kernel_b6<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
+                                                                    be, xin, xins, carry_head, carry_tail);  \
         else                                                                                                \
-            coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,     \
-                                                                 be, xin, xins, carry_head, carry_tail);     \
+            coo_kernel<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
+                                                                    be, xin, xins, carry_head, carry_tail);  \
     } while (0)
     if (xin) {
         if (vec) COO_LAUNCH(true, true); else COO_LAUNCH(true, false);
@@ -1283,14 +1346,14 @@ int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
     return value_bytes == 4 ? StreamCap<float>::v : StreamCap<double>::v;
 }
 
-int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t value_bytes) {
-    const int tile = value_bytes == 4 ? lb_tile<float>() : lb_tile<double>();
-    return ceil_div(n + nnz, tile);
+int32_t b200sp_csr_lb_tile(int32_t value_bytes, int32_t mode) {
+    return value_bytes == 4 ? lb_tile<float>(mode) : lb_tile<double>(mode);
 }
 
-int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* rp, int32_t value_bytes,
-                       int32_t* coords, void* stream) {
-    const int tile = value_bytes == 4 ? lb_tile<float>() : lb_tile<double>();
+int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t tile) { return ceil_div(n + nnz, tile); }
+
+int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* rp, int32_t tile, int32_t* coords, void* stream) {
+    B200SP_REQUIRE(tile > 0, B200SP_EINVAL, "csr lb plan: tile must be positive");
     const int64_t ntiles = ceil_div(n + nnz, tile);
     csr_lb_plan_kernel<<<(unsigned)ceil_div(ntiles + 1, 256), 256, 0, as_stream(stream)>>>(
         n, nnz, rp, ntiles, tile, coords);
@@ -1302,16 +1365,18 @@ int b200sp_csr_spmv_lb_f64(int64_t n, int64_t nnz, const int32_t* rp, const int3
                            const double* v, const double* b, int64_t bs, double* x, int64_t xs,
                            double alpha, const double* alpha_dev, double beta,
                            const double* beta_dev, const double* xin, int64_t xins,
-                           const int32_t* coords, int32_t* carry_row, double* carry_val,
-                           void* stream) {
-    return csr_lb<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords, carry_row, carry_val, stream);
+                           const int32_t* coords, int32_t* carry_row, double* carry_val, int32_t tile,
+                           int32_t mode, void* stream) {
+    return csr_lb<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords,
+                          carry_row, carry_val, tile, mode, stream);
 }
 int b200sp_csr_spmv_lb_f32(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci,
                            const float* v, const float* b, int64_t bs, float* x, int64_t xs,
                            float alpha, const float* alpha_dev, float beta, const float* beta_dev,
                            const float* xin, int64_t xins, const int32_t* coords,
-                           int32_t* carry_row, float* carry_val, void* stream) {
-    return csr_lb<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords, carry_row, carry_val, stream);
+                           int32_t* carry_row, float* carry_val, int32_t tile, int32_t mode, void* stream) {
+    return csr_lb<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords,
+                         carry_row, carry_val, tile, mode, stream);
 }
 
 int b200sp_coo_spmv_f64(int64_t nnz, int32_t chunk, const int32_t* rows, const int32_t* cols,

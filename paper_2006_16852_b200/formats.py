@@ -457,7 +457,7 @@ class Csr(_Sparse):
         return self._resolved_strategy()
 
     def set_strategy(self, strategy, subwarp=None, stream_shape=None, stream_cap=None, stream_impl=None,
-                     gather_in_reduce=None, stream_stages=None, stream_consumers=None):
+                     gather_in_reduce=None, stream_stages=None, stream_consumers=None, lb_mode=None):
         """Switch SpMV strategy; ``subwarp`` pins the classical sub-warp size,
         ``stream_shape`` = (threads per row, rows per thread), ``stream_cap``
         (entries per staging chunk), ``stream_impl`` ("tma": bulk-copy
@@ -468,6 +468,10 @@ class Csr(_Sparse):
         self._stream_cap = int(stream_cap) if stream_cap else None
         self._stream_stages = int(stream_stages) if stream_stages else None
         self._stream_consumers = int(stream_consumers) if stream_consumers else None
+        if lb_mode is not None:
+            if lb_mode not in (1, 2):
+                raise Unsupported("lb_mode must be 1 (item merge) or 2 (row-parallel)")
+            self._lb_mode = int(lb_mode)
         if stream_impl is not None:
             self._stream_impl = stream_impl
         if gather_in_reduce is not None:
@@ -580,17 +584,30 @@ class Csr(_Sparse):
         need = (rows * longest + 4 + 3) // 4 * 4
         return min(cap, need), tpr, rpt, gr
 
+    def lb_mode(self):
+        """1 = item-level merge (skewed rows: C3 power law 0.28 vs 0.23 of the
+        roofline), 2 = row-parallel tiles (stencils: C2 fp64 0.68 vs 0.43,
+        7-point 0.85 vs 0.44; profiles/r02_lb_sweep.txt)."""
+        mode = getattr(self, "_lb_mode", None)
+        if mode is None:
+            n = self.size.rows
+            mean = self.nnz / max(n, 1)
+            mode = 1 if n and self._row_stats() > 4 * mean + 64 else 2
+        return mode
+
     def lb_plan(self):
         if self._plan is None:
             exc = self.exec
             n, nnz = self.size.rows, self.nnz
             vb = self._v.element_size()
-            nt = int(_lib.query("csr_lb_num_tiles", n, nnz, vb))
+            mode = self.lb_mode()
+            tile = int(_lib.query("csr_lb_tile", vb, mode))
+            nt = int(_lib.query("csr_lb_num_tiles", n, nnz, tile))
             coords = torch.empty(2 * (nt + 1), dtype=torch.int32, device=exc.device)
-            _lib.call("csr_lb_plan", n, nnz, ptr(self._rp), vb, ptr(coords), exc.stream)
+            _lib.call("csr_lb_plan", n, nnz, ptr(self._rp), tile, ptr(coords), exc.stream)
             carry_row = torch.empty(max(nt, 1), dtype=torch.int32, device=exc.device)
             carry_val = torch.empty(max(nt, 1), dtype=self._v.dtype, device=exc.device)
-            self._plan = (coords, carry_row, carry_val)
+            self._plan = (coords, carry_row, carry_val, tile, mode)
         return self._plan
 
     # -- attributes (reference names) --------------------------------------------
@@ -615,10 +632,10 @@ class Csr(_Sparse):
         n = self.size.rows
         strategy = self._resolved_strategy()
         if strategy == "load_balance":
-            coords, crow, cval = self.lb_plan()
+            coords, crow, cval, tile, mode = self.lb_plan()
             _lib.call("csr_spmv_lb_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),
                       bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(coords), ptr(crow),
-                      ptr(cval), exc.stream)
+                      ptr(cval), tile, mode, exc.stream)
         elif strategy == "stream" and self._stream_ok():
             if self.stream_impl() == "tma":
                 _lib.call("csr_spmv_tma_" + suf, n, self.nnz, ptr(self._rp), ptr(self._ci), ptr(self._v),

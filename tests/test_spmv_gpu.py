@@ -20,6 +20,8 @@ TOL = {"float64": 1e-14, "float32": 1e-6}
 FORMATS = [
     ("csr", {"strategy": "classical"}),
     ("csr", {"strategy": "load_balance"}),
+    ("csr", {"strategy": "load_balance", "impl": "lb1"}),
+    ("csr", {"strategy": "load_balance", "impl": "lb2"}),
     ("csr", {"strategy": "stream"}),
     ("csr", {"strategy": "stream", "impl": "tma"}),
     ("csr", {"strategy": "stream", "impl": "tma", "rpt": 4, "cap": 64, "stages": 3}),
@@ -34,13 +36,17 @@ FORMATS = [
     ("hybrid", {"strategy": "imbalance"}),
     ("hybrid", {"strategy": "col1"}),
 ]
-IDS = ["csr_classical", "csr_lb", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
+IDS = ["csr_classical", "csr_lb", "csr_lb_merge", "csr_lb_rows", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
        "hybrid_col1"]
 
 
 def make(b2, exc, data, fmt, kw, dtype="float64"):
     kw = dict(kw)
     impl = kw.pop("impl", None)
+    if impl in ("lb1", "lb2"):
+        a = b2.matrix_from_data(exc, data, fmt, value_dtype=dtype, **kw)
+        a.set_strategy("load_balance", lb_mode=int(impl[-1]))
+        return a
     if impl is not None:
         rpt, cap, stages = kw.pop("rpt", None), kw.pop("cap", None), kw.pop("stages", None)
         nt, tpr = kw.pop("nt", None), kw.pop("tpr", 1)

@@ -29,7 +29,10 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--subwarp", default="", help="comma list of classical sub-warp sizes to sweep")
 args = ap.parse_args()
 exc = b2.CudaExecutor(0)
-a = problems.stencil(exc, args.matrix, args.grid, value_dtype=args.dtype)
+if args.matrix == "powerlaw":
+    a = problems.power_law(exc, 4194304, seed=0, value_dtype=args.dtype)
+else:
+    a = problems.stencil(exc, args.matrix, args.grid, value_dtype=args.dtype)
 n = a.size.rows
 vt = 8 if args.dtype == "float64" else 4
 b = b2.Dense(exc, np.random.default_rng(0).standard_normal((n, 1)), value_dtype=args.dtype)
@@ -42,7 +45,13 @@ fmts = args.format.split(",")
 if args.subwarp:
     fmts = [f"csr_classical/{sw}" for sw in args.subwarp.split(",")]
 for fmt in fmts:
+    attrs = {}
+    if ":" in fmt:  # e.g. coo:chunk=128
+        fmt, kv = fmt.split(":")
+        attrs = {k: int(v) for k, v in (p.split("=") for p in kv.split(";"))}
     m = b2.convert(a, fmt.split("/")[0])
+    for k, v in attrs.items():
+        setattr(m, k, v)
     if "/" in fmt:
         m.set_strategy("classical", subwarp=int(fmt.split("/")[1]))
     by = bytes_format(m, vt)
@@ -50,6 +59,8 @@ for fmt in fmts:
     for combo in itertools.product(*[vals for _, vals in knobs]) if knobs else [()]:
         for (k, _), val in zip(knobs, combo):
             _lib.set_tuning(k, val)
+        if hasattr(m, "_plan"):
+            m._plan = None  # plans depend on knobs (lb_tile)
         m.apply(b, x)
         out = np.asarray(x.data).copy()
         if ref is None:
