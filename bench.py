@@ -282,8 +282,9 @@ def bench_c2(args, world, rank, local):
                           "gflops": round(2 * nnz / t_step / 1e9, 1),
                           "frac": round(by / t_step / 1e9 / peak, 4), "bytes": by,
                           "strategy": m.strategy}
-    kern = {"classical": "csr_classical_kernel", "stream": "csr_stream_kernel",
-            "load_balance": "csr_lb_kernel"}[m.strategy]
+    kern = {"classical": "csr_classical_kernel",
+            "stream": "csr_pipe_kernel" if m.stream_impl() == "tma" else "csr_stream_kernel",
+            "load_balance": "csr_lb2_kernel" if m.lb_mode() == 2 else "csr_lb_kernel"}[m.strategy]
     roofline = {"bound": "hbm", "achieved": round(by / t_step / 1e9, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(by / t_step / 1e9 / peak, 4), "traffic": traffic_from_profiles(kern),
                 "peak_source": peak_src, "kernel": kern, "bytes_per_launch": by}

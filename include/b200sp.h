@@ -331,6 +331,19 @@ int b200sp_gmres_after_commit(void* ctl, void* stream);
 B200SP_KRYLOV_DECL(double, f64)
 B200SP_KRYLOV_DECL(float, f32)
 
+/* Csr SpMV q = A p fused with the solver reduction that follows it (sub-warp
+ * per row, classical layout): phase 1 = CG sigma = p.q (replaces
+ * b200sp_cg_sigma), 2 = BiCGSTAB gamma = u.q with u = r_tilde (replaces
+ * bicgstab_gamma), 3 = BiCGSTAB ts = q.u, tt = q.q with u = s (replaces
+ * bicgstab_tst). The control step runs in the last block as in the unfused
+ * kernels (src/solvers/krylov.py:56-76, :233-265). */
+int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
+                            const double* p, double* q, const double* u, int32_t phase, int32_t subwarp, void* ctl,
+                            double* part, void* stream);
+int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
+                            const float* p, float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl,
+                            double* part, void* stream);
+
 /* ---- row-partitioned (distributed) CG ------------------------------------
  * Each rank holds rows [lo, hi) with vector layout [owned | ghosts]; the
  * reduction kernels of a ctl with dist = 1 park their local sums in the ctl's

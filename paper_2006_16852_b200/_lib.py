@@ -61,6 +61,7 @@ _TYPED = {
     "cg_step1": "lpppp",
     "cg_sigma": "lppppp",
     "cg_coop": "lppppppppppp",
+    "csr_spmv_dot": "lppppppiippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
     "bicgstab_init": "lplpppppppppppp",
     "bicgstab_step1": "lpppp" + "lpppp" + "pp",

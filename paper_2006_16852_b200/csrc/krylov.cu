@@ -341,6 +341,29 @@ __device__ inline void bicg_cycle_start(KrylovCtl* c, double rho_new, double rr)
     c->beta = safe_div(c->rho, c->rho_prev) * safe_div(c->alpha, c->omega);
 }
 
+__device__ inline void bicg_gamma_ctl(KrylovCtl* c, const double* tot) {
+    c->gamma = tot[0];
+    if (c->gamma == 0.0 && c->rho != 0.0) {  // krylov.py:235-239
+        c->breakdown = BD_GAMMA;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->alpha = safe_div(c->rho, c->gamma);
+}
+
+__device__ inline void bicg_tst_ctl(KrylovCtl* c, const double* tot) {
+    c->ts = tot[0];
+    c->tt = tot[1];
+    if (c->tt == 0.0 && c->ts != 0.0) {  // krylov.py:262-265
+        c->breakdown = BD_TT;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->omega = safe_div(c->ts, c->tt);
+}
+
 // after r = b - A x: rt = b, zero p v s t y z, baseline, check(0), cycle start
 template <typename T>
 __global__ void __launch_bounds__(KRY_BLOCK)
@@ -410,14 +433,7 @@ bicg_gamma_kernel(int64_t n, const T* __restrict__ rt, const T* __restrict__ v, 
         s += (double)rt[i] * (double)v[i];
     double vv[1] = {s}, tot[1];
     if (!grid_reduce<1>(vv, part, &c->ticket[1], tot)) return;
-    c->gamma = tot[0];
-    if (c->gamma == 0.0 && c->rho != 0.0) {  // krylov.py:235-239
-        c->breakdown = BD_GAMMA;
-        c->breakdown_it = c->it + 1;
-        c->done = 1;
-        return;
-    }
-    c->alpha = safe_div(c->rho, c->gamma);
+    bicg_gamma_ctl(c, tot);
 }
 
 // s = r - alpha v; z = M s; it++; mid check on ||s||   (BicgstabStep2)
@@ -472,15 +488,7 @@ bicg_tst_kernel(int64_t n, const T* __restrict__ t, const T* __restrict__ s, Kry
     }
     double vv[2] = {a, bb}, tot[2];
     if (!grid_reduce<2>(vv, part, &c->ticket[1], tot)) return;
-    c->ts = tot[0];
-    c->tt = tot[1];
-    if (c->tt == 0.0 && c->ts != 0.0) {  // krylov.py:262-265
-        c->breakdown = BD_TT;
-        c->breakdown_it = c->it + 1;
-        c->done = 1;
-        return;
-    }
-    c->omega = safe_div(c->ts, c->tt);
+    bicg_tst_ctl(c, tot);
 }
 
 // x += alpha y + omega z; r = s - omega t; it++; top check; next cycle start
@@ -739,6 +747,130 @@ static RowBlocks make_rb(int64_t n, int64_t nb, const int32_t* starts, const int
     return RowBlocks{n, JacobiView{nb, starts, (const long long*)offs, prec, (const unsigned char*)storage}};
 }
 
+// ===========================================================================
+// Csr SpMV with the solver's next reduction fused into its epilogue:
+//   q = A p and
+//   PH_SIGMA (CG):        sigma = p.q                -> cg_sigma_ctl
+//   PH_GAMMA (BiCGSTAB):  gamma = rt.q  (u = rt)      -> bicg_gamma_ctl
+//   PH_TST   (BiCGSTAB):  ts = q.s, tt = q.q (u = s)  -> bicg_tst_ctl
+// Rows as in the classical SpMV (sub-warp per row, L1-allocating matrix
+// loads, spmv.cu); the owner lane of a row multiplies the fresh q_i by p_i /
+// u_i, so the separate dot kernel's re-read of p and q (2n values per
+// iteration, ~9% of a 7-point CG iteration) disappears. Same ticket / block
+// order determinism as every other reduction here.
+// ===========================================================================
+enum FusedPhase : int { PH_SIGMA = 1, PH_GAMMA = 2, PH_TST = 3 };
+
+// 8 CTAs per SM (<= 32 registers): the unbounded build took 40 registers at
+// sub-warp 1 (6 CTAs per SM) and ran slower than SpMV + separate dot
+template <typename T, int SW, int PH>
+__global__ void __launch_bounds__(KRY_BLOCK, SW <= 4 ? 8 : 4)
+csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                    const T* __restrict__ p, T* __restrict__ q, const T* __restrict__ u, KrylovCtl* c,
+                    double* part) {
+    if (c->done) return;
+    constexpr int U = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & (SW - 1);
+    const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
+    double d0 = 0, d1 = 0;
+    const int64_t wfirst = (tid / 32) * (32 / SW) * U;
+    for (int64_t row0 = (tid / SW) * U, w0 = wfirst; w0 < n; row0 += nsw * U, w0 += nsw * U) {
+        int st[U], len[U];
+        int nxt = row0 < n ? __ldg(rp + row0) : 0;
+        int maxlen = 0;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            st[k] = nxt;
+            nxt = (row0 + k < n) ? __ldg(rp + row0 + k + 1) : nxt;
+            len[k] = nxt - st[k];
+            maxlen = max(maxlen, len[k]);
+        }
+        T acc[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) acc[k] = 0;
+        for (int e = lane; e < maxlen; e += SW) {
+            int cc[U];
+            T vv[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const bool ok = e < len[k];
+                cc[k] = ok ? __ldg(ci + st[k] + e) : -1;
+                vv[k] = ok ? __ldg(av + st[k] + e) : T(0);
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (cc[k] >= 0) acc[k] += vv[k] * __ldg(p + cc[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) acc[k] = subwarp_sum<SW>(acc[k]);
+        if (lane < U) {
+            T mine = acc[0];
+#pragma unroll
+            for (int k = 1; k < U; ++k)
+                if (lane == k) mine = acc[k];
+            const int64_t row = row0 + lane;
+            if (row < n) {
+                q[row] = mine;
+                if (PH == PH_SIGMA) d0 += (double)__ldg(p + row) * (double)mine;
+                if (PH == PH_GAMMA) d0 += (double)__ldg(u + row) * (double)mine;
+                if (PH == PH_TST) {
+                    d0 += (double)mine * (double)__ldg(u + row);
+                    d1 += (double)mine * (double)mine;
+                }
+            }
+        }
+    }
+    if (PH == PH_TST) {
+        double v[2] = {d0, d1}, tot[2];
+        if (!grid_reduce<2>(v, part, &c->ticket[1], tot)) return;
+        bicg_tst_ctl(c, tot);
+    } else {
+        double v[1] = {d0}, tot[1];
+        if (!grid_reduce<1>(v, part, &c->ticket[1], tot)) return;
+        if (PH == PH_SIGMA) {
+            if (c->dist) {
+                c->red[0] = tot[0];
+                return;
+            }
+            cg_sigma_ctl(c, tot);
+        } else {
+            bicg_gamma_ctl(c, tot);
+        }
+    }
+}
+
+template <typename T, int SW>
+static void launch_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
+                            int phase, KrylovCtl* c, double* part, cudaStream_t st) {
+    constexpr int U = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1);
+    const int grid = kry_grid(ceil_div(n, U) * SW, KRY_BLOCK);
+    if (phase == PH_SIGMA) csr_spmv_dot_kernel<T, SW, PH_SIGMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else if (phase == PH_GAMMA) csr_spmv_dot_kernel<T, SW, PH_GAMMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else csr_spmv_dot_kernel<T, SW, PH_TST><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+}
+
+template <typename T>
+static int csr_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
+                        int phase, int subwarp, void* ctl, double* part, void* stream) {
+    B200SP_REQUIRE(phase >= PH_SIGMA && phase <= PH_TST, B200SP_EINVAL, "csr_spmv_dot: phase must be 1..3");
+    B200SP_REQUIRE(phase == PH_SIGMA || u, B200SP_EINVAL, "csr_spmv_dot: phase %d needs the second vector", phase);
+    if (n == 0) return B200SP_OK;
+    cudaStream_t st = as_stream(stream);
+    KrylovCtl* c = (KrylovCtl*)ctl;
+    switch (subwarp) {
+        case 1: launch_spmv_dot<T, 1>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 2: launch_spmv_dot<T, 2>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 4: launch_spmv_dot<T, 4>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 8: launch_spmv_dot<T, 8>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 16: launch_spmv_dot<T, 16>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 32: launch_spmv_dot<T, 32>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        default: set_error("csr_spmv_dot: subwarp must be a power of two <= 32 (got %d)", subwarp); return B200SP_EINVAL;
+    }
+    count_launch();
+    return check_launch("csr_spmv_dot");
+}
+
 #define KRY_LAUNCH(kernel, units, per_block, ...)                                                     \
     do {                                                                                              \
         kernel<<<kry_grid((units), (per_block)), KRY_BLOCK, 0, as_stream(stream)>>>(__VA_ARGS__);     \
@@ -913,6 +1045,17 @@ int b200sp_cg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const do
 int b200sp_cg_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, float* x, float* r,
                        float* p, float* q, void* ctl, double* part, double* hist, void* stream) {
     return cg_coop<float>(n, rp, ci, v, x, r, p, q, ctl, part, hist, stream);
+}
+
+int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, const double* p,
+                            double* q, const double* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
+                            void* stream) {
+    return csr_spmv_dot<double>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
+}
+int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, const float* p,
+                            float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
+                            void* stream) {
+    return csr_spmv_dot<float>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
 }
 
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream) {

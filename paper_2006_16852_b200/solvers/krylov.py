@@ -39,6 +39,22 @@ def jac_args(solver):
     return (0, 0, 0, 0, 0)
 
 
+def fused_csr(solver):
+    """The system matrix when its SpMV can carry the next reduction in its
+    epilogue (csr_spmv_dot: Csr with the classical strategy), else None."""
+    from ..formats import Csr
+
+    a = solver.a
+    if config.FUSED_SPMV_DOT and isinstance(a, Csr) and a.strategy == "classical":
+        return a
+    return None
+
+
+def spmv_dot(S, a, suf, p, q, u, phase):
+    _lib.call("csr_spmv_dot_" + suf, a.size.rows, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(p), ptr(q),
+              ptr(u) if u is not None else 0, phase, a.subwarp(), S.c, S.p, a.exec.stream)
+
+
 def finish_from_device(solver, state, st, x):
     state.end(x)
     status = solver._new_status(1)
@@ -83,10 +99,15 @@ class CgSolver(IterativeSolver):
                       S.c, S.p, S.h, exc.stream)
             return finish_from_device(self, S, S.status(), x)
 
+        fa = fused_csr(self)
+
         def body():
             _lib.call("cg_step1_" + suf, n, ptr(p), ptr(z), S.c, exc.stream)
-            self.a.apply(pd, qd)
-            _lib.call("cg_sigma_" + suf, n, ptr(p), ptr(q), S.c, S.p, exc.stream)
+            if fa is not None:  # q = A p and sigma = p.q in one pass
+                spmv_dot(S, fa, suf, p, q, None, 1)
+            else:
+                self.a.apply(pd, qd)
+                _lib.call("cg_sigma_" + suf, n, ptr(p), ptr(q), S.c, S.p, exc.stream)
             _lib.call("cg_step2_" + suf, n, ptr(S.x), 1, ptr(r), ptr(p), ptr(q), ptr(z), *J, S.c, S.p, S.h,
                       exc.stream)
 
@@ -114,13 +135,21 @@ class BicgstabSolver(IterativeSolver):
         _lib.call("bicgstab_init_" + suf, n, ptr(S.b), 1, ptr(r), ptr(rt), ptr(p), ptr(v), ptr(s), ptr(t),
                   ptr(y), ptr(z), S.c, S.p, S.h, exc.stream)
 
+        fa = fused_csr(self)
+
         def body():
             _lib.call("bicgstab_step1_" + suf, n, ptr(r), ptr(p), ptr(v), ptr(y), *J, S.c, exc.stream)
-            self.a.apply(yd, vd)
-            _lib.call("bicgstab_gamma_" + suf, n, ptr(rt), ptr(v), S.c, S.p, exc.stream)
+            if fa is not None:  # v = A y with gamma = rt.v fused
+                spmv_dot(S, fa, suf, y, v, rt, 2)
+            else:
+                self.a.apply(yd, vd)
+                _lib.call("bicgstab_gamma_" + suf, n, ptr(rt), ptr(v), S.c, S.p, exc.stream)
             _lib.call("bicgstab_step2_" + suf, n, ptr(r), ptr(v), ptr(s), ptr(z), *J, S.c, S.p, S.h, exc.stream)
-            self.a.apply(zd, td)
-            _lib.call("bicgstab_tst_" + suf, n, ptr(t), ptr(s), S.c, S.p, exc.stream)
+            if fa is not None:  # t = A z with (t.s, t.t) fused
+                spmv_dot(S, fa, suf, z, t, s, 3)
+            else:
+                self.a.apply(zd, td)
+                _lib.call("bicgstab_tst_" + suf, n, ptr(t), ptr(s), S.c, S.p, exc.stream)
             _lib.call("bicgstab_step3_" + suf, n, ptr(S.x), 1, ptr(r), ptr(s), ptr(t), ptr(y), ptr(z), ptr(rt),
                       S.c, S.p, S.h, exc.stream)
 
