@@ -1,5 +1,4 @@
-timeout 300 python -m pytest tests/test_solvers_gpu.py -x -q > gpurun_out/t_solv.log 2>&1
-for f in 1 0; do
-  B200SP_FUSED_SPMV_DOT=$f timeout 300 python bench.py --workload c4b --no-cpu > gpurun_out/b_c4b_f$f.log 2>&1
-  B200SP_FUSED_SPMV_DOT=$f timeout 300 python bench.py --workload c5 --no-cpu --grid 256 > gpurun_out/b_c5g256_f$f.log 2>&1
-done
+timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python bench.py > gpurun_out/bench_c2.log 2>&1
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+for w in c1 c3 c4b c4g c5; do timeout 600 python bench.py --workload $w --no-cpu > gpurun_out/bench_$w.log 2>&1; done
