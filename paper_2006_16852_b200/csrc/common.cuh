@@ -182,6 +182,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// IEEE products that the compiler may not fuse into a following add
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
 // ---------------------------------------------------------------------------
 // warp reductions
 // ---------------------------------------------------------------------------

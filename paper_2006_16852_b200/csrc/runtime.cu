@@ -195,7 +195,9 @@ __global__ void add_scaled_kernel(int64_t n, int m, T alpha, const T* __restrict
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / m, j = t - i * m;
         const T a = alpha_dev ? alpha_dev[j] : alpha;
-        y[i * ys + j] = y[i * ys + j] + a * x[i * xs + j];
+        // product rounded before the add (no FMA contraction): the same two
+        // roundings as the reference's NumPy `y + a * x` (src/kernels.py:94-110)
+        y[i * ys + j] = y[i * ys + j] + mul_rn(a, x[i * xs + j]);
     }
 }
 

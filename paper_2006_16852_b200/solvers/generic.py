@@ -78,6 +78,152 @@ def cg(s, b, x):
     s._finish(it, status, breakdown)
 
 
+def fcg(s, b, x):
+    """Flexible CG (src/solvers/krylov.py:80-125; steps FcgStep1/2, steps.py:161-199)."""
+    n, m = s.size.rows, b.size.cols
+    r, z, p, q, t = (_zero(_new(b, n, m)) for _ in range(5))
+    s._residual(x, b, r)
+    prev_rho, rho_t = np.ones(m), np.zeros(m)
+    s.precond.apply(r, z)
+    rho = r.dot(z)
+    crit = s._make_criterion(b, x, initial_residual=r)
+    status = s._new_status(m)
+    it, breakdown = 0, None
+    while True:
+        all_stopped, _ = crit.check(RELATIVE_STOPPING_ID, True, status, Updater(it, residual=r, solution=x))
+        if all_stopped:
+            break
+        act = _cols(status)
+        beta = safe_div(rho_t, prev_rho)
+        for j in act:  # p = z + (rho_t / prev_rho) p
+            pj = p.column(j)
+            pj.scale(float(beta[j]))
+            pj.add_scaled(1.0, z.column(j))
+        s.a.apply(p, q)
+        sigma = p.dot(q)
+        running = ~status.data["stopped"]
+        if ((sigma <= 0) & (rho != 0) & running).any():
+            breakdown = BreakdownInfo(it + 1, "non-positive p^T A p")
+            break
+        alpha = safe_div(rho, sigma)
+        for j in act:  # x += alpha p; t = (r - alpha q) - r; r = r - alpha q
+            x.column(j).add_scaled(float(alpha[j]), p.column(j))
+            tj, rj = t.column(j), r.column(j)
+            tj.copy_from(rj)
+            rj.add_scaled(-float(alpha[j]), q.column(j))
+            tj.scale(-1.0)
+            tj.add_scaled(1.0, rj)
+        prev_rho = rho
+        s.precond.apply(r, z)
+        rho = r.dot(z)
+        rho_t = t.dot(z)
+        it += 1
+        s._log_iteration(it)
+    s._finish(it, status, breakdown)
+
+
+def _residual_nonzero(r, cols):
+    return any(float(r.column(int(j)).norm2()[0]) != 0.0 for j in cols)
+
+
+def cgs(s, b, x):
+    """Conjugate gradient squared (src/solvers/krylov.py:128-187; steps
+    CgsStep1/2/3, steps.py:246-345): two SpMVs per cycle, a criterion check
+    after each half."""
+    n, m = s.size.rows, b.size.cols
+    r = _new(b, n, m)
+    r.copy_from(b)
+    rt = _new(b, n, m)
+    rt.copy_from(b)
+    p, q, u, u_hat, v_hat, t = (_zero(_new(b, n, m)) for _ in range(6))
+    w = _zero(_new(b, n, m))
+    prev_rho, alpha = np.ones(m), np.zeros(m)
+    s.a.apply_advanced(-1.0, x, 1.0, r)
+    crit = s._make_criterion(b, x, initial_residual=r)
+    status = s._new_status(m)
+    it, breakdown = 0, None
+    while True:
+        all_stopped, _ = crit.check(RELATIVE_STOPPING_ID, True, status, Updater(it, residual=r, solution=x))
+        if all_stopped:
+            break
+        act = _cols(status)
+        running = ~status.data["stopped"]
+        rho = rt.dot(r)
+        zero_rho = (rho == 0) & running
+        if zero_rho.any() and _residual_nonzero(r, np.flatnonzero(zero_rho)):
+            breakdown = BreakdownInfo(it + 1, "rho = 0")
+            break
+        beta = safe_div(rho, prev_rho)
+        for j in act:  # u = r + beta q; p = u + beta (q + beta p)
+            bj = float(beta[j])
+            uj, pj = u.column(j), p.column(j)
+            uj.copy_from(q.column(j))
+            uj.scale(bj)
+            uj.add_scaled(1.0, r.column(j))
+            pj.scale(bj)
+            pj.add_scaled(1.0, q.column(j))
+            pj.scale(bj)
+            pj.add_scaled(1.0, uj)
+        s.precond.apply(p, t)
+        s.a.apply(t, v_hat)
+        gamma = rt.dot(v_hat)
+        if ((gamma == 0) & (rho != 0) & running).any():
+            breakdown = BreakdownInfo(it + 1, "r_tld^T A p = 0")
+            break
+        a_new = safe_div(rho, gamma)
+        for j in act:  # q = u - alpha v_hat; w = u + q
+            alpha[j] = a_new[j]
+            qj, wj = q.column(j), w.column(j)
+            qj.copy_from(u.column(j))
+            qj.add_scaled(-float(alpha[j]), v_hat.column(j))
+            wj.copy_from(u.column(j))
+            wj.add_scaled(1.0, qj)
+        it += 1
+        s._log_iteration(it)
+        all_stopped, _ = crit.check(RELATIVE_STOPPING_ID, True, status, Updater(it, residual=r, solution=x))
+        if all_stopped:
+            break
+        act = _cols(status)
+        s.precond.apply(w, u_hat)
+        s.a.apply(u_hat, t)
+        for j in act:  # r -= alpha t; x += alpha u_hat
+            r.column(j).add_scaled(-float(alpha[j]), t.column(j))
+            x.column(j).add_scaled(float(alpha[j]), u_hat.column(j))
+        prev_rho = rho
+        it += 1
+        s._log_iteration(it)
+    s._finish(it, status, breakdown)
+
+
+def ir(s, b, x):
+    """Iterative refinement x <- x + S(b - A x) (src/solvers/ir.py:13-46)."""
+    n, m = s.size.rows, b.size.cols
+    # d is the inner operator's initial guess: zero on the first iteration
+    # (the reference's np.empty arena hands out zeroed pages here; verified
+    # bitwise against a zero-filled run), the previous correction afterwards
+    r, d = _new(b, n, m), _zero(_new(b, n, m))
+    inner = s.params["inner_op"]
+    s._residual(x, b, r)
+    crit = s._make_criterion(b, x, initial_residual=r)
+    status = s._new_status(m)
+    it = 0
+    while True:
+        all_stopped, _ = crit.check(RELATIVE_STOPPING_ID, True, status, Updater(it, residual=r, solution=x))
+        if all_stopped:
+            break
+        act = _cols(status)
+        inner.apply(r, d)
+        if len(act) == m:
+            x.add_scaled(1.0, d)
+        else:  # freeze stopped columns
+            for j in act:
+                x.column(j).add_scaled(1.0, d.column(j))
+        s._residual(x, b, r)
+        it += 1
+        s._log_iteration(it)
+    s._finish(it, status, None)
+
+
 def bicgstab(s, b, x):
     n, m = s.size.rows, b.size.cols
     r = _new(b, n, m)

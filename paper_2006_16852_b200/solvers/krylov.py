@@ -1,4 +1,4 @@
-"""CG and BiCGSTAB (reference src/solvers/krylov.py:36-77, :190-271).
+"""CG, BiCGSTAB, FCG and CGS (reference src/solvers/krylov.py:36-271).
 
 Single right-hand side with device-evaluable criteria (Iteration,
 ResidualNormReduction, TimeLimit) and an Identity or block-Jacobi
@@ -157,8 +157,32 @@ class BicgstabSolver(IterativeSolver):
         finish_from_device(self, S, st, x)
 
 
+class FcgSolver(IterativeSolver):
+    """Flexible CG (src/solvers/krylov.py:80-125): host-controlled loop over
+    device kernels (generic.fcg)."""
+
+    def _apply_impl(self, b, x):
+        return generic.fcg(self, b, x)
+
+
+class CgsSolver(IterativeSolver):
+    """Conjugate gradient squared (src/solvers/krylov.py:128-187):
+    host-controlled loop over device kernels (generic.cgs)."""
+
+    def _apply_impl(self, b, x):
+        return generic.cgs(self, b, x)
+
+
 class Cg(IterativeSolverFactory):
     solver_cls = CgSolver
+
+
+class Fcg(IterativeSolverFactory):
+    solver_cls = FcgSolver
+
+
+class Cgs(IterativeSolverFactory):
+    solver_cls = CgsSolver
 
 
 class Bicgstab(IterativeSolverFactory):

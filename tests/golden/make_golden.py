@@ -25,6 +25,7 @@ sys.path.insert(0, REPO)
 import opalg  # noqa: E402  (the reference)
 from opalg import (Bicgstab, Cg, Coo, Csr, Dense, Dim2, Gmres, Iteration, Jacobi,  # noqa: E402
                    MatrixData, ResidualNormReduction)
+from opalg.solvers import Cgs, Fcg, Ir  # noqa: E402
 from opalg.problems import (convection_diffusion, five_point_poisson, random_sparse,  # noqa: E402
                             random_spd, tridiagonal)
 from opalg.stop import Criterion, CriterionFactory  # noqa: E402
@@ -123,9 +124,11 @@ def solve_case(name, data, solver, precond, b, crit_iters, factor, **kw):
     x = Dense.zeros(REF, n, bd.size.cols)
     hist = _HistoryFactory()
     crits = [Iteration(crit_iters), ResidualNormReduction(factor), hist]
-    fac = {"cg": Cg, "bicgstab": Bicgstab, "gmres": Gmres}[solver]
+    fac = {"cg": Cg, "bicgstab": Bicgstab, "gmres": Gmres, "fcg": Fcg, "cgs": Cgs, "ir": Ir}[solver]
     pre = Jacobi(REF, block_size=precond) if precond else None
-    s = fac(REF, criteria=crits, preconditioner=pre, **kw).generate(a)
+    if pre is not None:
+        kw["preconditioner"] = pre
+    s = fac(REF, criteria=crits, **kw).generate(a)
     s.apply(bd, x)
     st = s.last_status
     true_r = bd.data - data.to_dense_array() @ x.data if n <= 5000 else None
@@ -198,6 +201,40 @@ def solver_cases():
     return out
 
 
+def solver_ext_cases():
+    """Fcg / Cgs / Ir (SURVEY 8(f) #4): iteration counts, histories, x."""
+    out = {}
+    n, r, c, v = P.stencil3d(16, "7pt")
+    d = md(n, r, c, v)
+    for pre in (0, 32):
+        tag = "bj32" if pre else "none"
+        out[f"fcg_{tag}_7pt_g16"] = solve_case(f"fcg_{tag}_7pt_g16", d, "fcg", pre, np.ones(n), 10000, 1e-8)
+    n, r, c, v = P.stencil3d(12, "convdiff")
+    d = md(n, r, c, v)
+    for pre in (0, 32):
+        tag = "bj32" if pre else "none"
+        out[f"cgs_{tag}_cd_g12"] = solve_case(f"cgs_{tag}_cd_g12", d, "cgs", pre, np.ones(n), 10000, 1e-8)
+    # Ir with an inner CG of 4 iterations, and with a block-Jacobi inner operator
+    n, r, c, v = P.stencil3d(12, "7pt")
+    d = md(n, r, c, v)
+    out["ir_cg4_7pt_g12"] = solve_case("ir_cg4_7pt_g12", d, "ir", 0, np.ones(n), 10000, 1e-8,
+                                       inner=Cg(REF, criteria=[Iteration(4)]))
+    n, r, c, v = P.stencil3d(12, "convdiff")
+    d = md(n, r, c, v)
+    out["ir_bj32_cd_g12"] = solve_case("ir_bj32_cd_g12", d, "ir", 0, np.ones(n), 10000, 1e-8,
+                                       inner=Jacobi(REF, block_size=32))
+    # multi-column freeze through Fcg and Cgs
+    data = random_spd(8, seed=11)
+    dense = data.to_dense_array()
+    w, vecs = np.linalg.eigh(dense)
+    b2 = np.stack([dense @ vecs[:, 0], np.ones(8)], axis=1)
+    out["fcg_freeze"] = solve_case("fcg_freeze", data.canonicalize(), "fcg", 0, b2, 60, 1e-10)
+    data = random_sparse(100, density=0.1, seed=6)
+    b = np.random.default_rng(6).standard_normal(100)
+    out["cgs_rand100"] = solve_case("cgs_rand100", data.canonicalize(), "cgs", 0, b, 3000, 1e-12)
+    return out
+
+
 def jacobi_cases():
     out = {}
     n, r, c, v = P.stencil3d(8, "convdiff")
@@ -251,6 +288,10 @@ def save(name, cases):
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["ext"]:
+        save("solvers_ext.npz", solver_ext_cases())
+        sys.exit(0)
+    save("solvers_ext.npz", solver_ext_cases())
     save("spmv.npz", spmv_cases())
     save("misc.npz", misc_cases())
     save("jacobi.npz", jacobi_cases())

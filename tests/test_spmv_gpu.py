@@ -332,6 +332,9 @@ def test_dense_blas(cuda):
     np.testing.assert_allclose(x.norm2(), np.sqrt((xv * xv).sum(axis=0)), rtol=1e-14)
     y.add_scaled(0.7, x)
     y.add_scaled(-0.7, x)
-    assert np.abs(np.asarray(y.data) - yv).max() <= 1e-15 * np.abs(yv).max()
+    # bitwise the reference's NumPy `y += a * x` (product rounded, then added)
+    ref = yv + 0.7 * xv
+    ref = ref + (-0.7) * xv
+    np.testing.assert_array_equal(np.asarray(y.data), ref)
     y.scale(b2.Dense(cuda, [[2.0, -1.0]]))
-    np.testing.assert_allclose(np.asarray(y.data), yv * [2.0, -1.0], rtol=1e-15)
+    np.testing.assert_array_equal(np.asarray(y.data), ref * [2.0, -1.0])
