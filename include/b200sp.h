@@ -344,6 +344,19 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* row_ptrs, const int32_t* c
                             const float* p, float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl,
                             double* part, void* stream);
 
+/* ---- Matrix Market reader (host code; reference src/mmio.py:38-126) ------
+ * b200sp_mm_header parses the header and size line of the file image `buf`:
+ * info[7] = {array?, symmetric?, rows, cols, entries, body offset, size-line
+ * number}; b200sp_mm_count sizes the output (symmetric mirrors included);
+ * b200sp_mm_parse fills 0-based int64 rows / cols and vals (array files:
+ * vals only, column-major) with `threads` host threads (<= 0: all cores).
+ * Errors: B200SP_EINVAL = ParseError with *err_line the reference's 1-based
+ * line number, B200SP_EUNSUPPORTED = Unsupported; same messages. */
+int b200sp_mm_header(const char* buf, int64_t len, int64_t* info, int64_t* err_line);
+int b200sp_mm_count(const char* buf, int64_t len, const int64_t* info, int32_t threads, int64_t* out_count);
+int b200sp_mm_parse(const char* buf, int64_t len, const int64_t* info, int32_t threads, int64_t* rows,
+                    int64_t* cols, double* vals, int64_t capacity, int64_t* out_count, int64_t* err_line);
+
 /* ---- row-partitioned (distributed) CG ------------------------------------
  * Each rank holds rows [lo, hi) with vector layout [owned | ghosts]; the
  * reduction kernels of a ctl with dist = 1 park their local sums in the ctl's

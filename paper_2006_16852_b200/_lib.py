@@ -109,6 +109,9 @@ _UNTYPED = {
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
     "set_guard": ("p", None),
     "set_tuning": ("si", ctypes.c_int),
+    "mm_header": ("plpp", ctypes.c_int),
+    "mm_count": ("plpip", ctypes.c_int),
+    "mm_parse": ("plpippplpp", ctypes.c_int),
     "jacobi_block_sizes_sq": ("lppp", ctypes.c_int),
     "jacobi_pack": ("lppppppp", ctypes.c_int),
     "krylov_ctl_bytes": ("", ctypes.c_int64),
