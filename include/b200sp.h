@@ -344,6 +344,21 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* row_ptrs, const int32_t* c
                             const float* p, float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl,
                             double* part, void* stream);
 
+/* ---- device assembly of coordinate triples (reference MatrixData.canonicalize,
+ * src/formats.py:40-53, bit for bit) ------------------------------------------
+ * int64 rows / cols and fp64 values (any order, duplicates allowed, indices
+ * pre-validated) -> (row, col)-sorted unique int32 rows / cols and values of
+ * the suffix type; *nnz_out (device int32) = number of unique coordinates.
+ * Stable LSD radix sort of row * ncols + col; duplicate groups summed
+ * 0.0 + v1 + v2 ... in input order when the input has any duplicate. */
+int64_t b200sp_assemble_workspace_bytes(int64_t count);
+int b200sp_assemble_coo_f64(int64_t count, const int64_t* rows, const int64_t* cols, const double* vals,
+                            int64_t nrows, int64_t ncols, int32_t* rows_out, int32_t* cols_out, double* vals_out,
+                            int32_t* nnz_out, void* ws, void* stream);
+int b200sp_assemble_coo_f32(int64_t count, const int64_t* rows, const int64_t* cols, const double* vals,
+                            int64_t nrows, int64_t ncols, int32_t* rows_out, int32_t* cols_out, float* vals_out,
+                            int32_t* nnz_out, void* ws, void* stream);
+
 /* ---- Matrix Market reader (host code; reference src/mmio.py:38-126) ------
  * b200sp_mm_header parses the header and size line of the file image `buf`:
  * info[7] = {array?, symmetric?, rows, cols, entries, body offset, size-line

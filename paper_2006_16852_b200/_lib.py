@@ -77,6 +77,7 @@ _TYPED = {
     "gmres_combine": "lppl" + "lpppp" + "ppp",
     # distributed
     "split_fill": "lpppippppppp",
+    "assemble_coo": "lpppllppppp",
     "gather": "lpppp",
 }
 _UNTYPED = {
@@ -109,6 +110,7 @@ _UNTYPED = {
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
     "set_guard": ("p", None),
     "set_tuning": ("si", ctypes.c_int),
+    "assemble_workspace_bytes": ("l", ctypes.c_int64),
     "mm_header": ("plpp", ctypes.c_int),
     "mm_count": ("plpip", ctypes.c_int),
     "mm_parse": ("plpippplpp", ctypes.c_int),

@@ -371,7 +371,7 @@ csr_pipe_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
     constexpr int G = NT / TPR;  // rows reduced concurrently (TPR threads each)
     constexpr int TR = G * RPT;  // rows per tile
     constexpr int RPS = pipe_rp_slots(TR);
-    extern __shared__ __align__(128) unsigned char s_raw[];
+    extern __shared__ __align__(16) unsigned char s_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(s_raw);
     uint64_t* empty = full + STAGES;
     unsigned char* stages = s_raw + PIPE_BAR_BYTES;

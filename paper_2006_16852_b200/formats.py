@@ -382,6 +382,38 @@ class _Sparse(LinOp):
 CSR_STRATEGIES = ("classical", "load_balance", "stream", "automatic")
 
 
+def assemble_device(exc, data, vt):
+    """MatrixData -> canonical (row, col)-sorted int32 rows / cols and values
+    on the device (csrc/assemble.cu): the reference's canonicalize
+    (src/formats.py:40-53) bit for bit -- stable sort by (row, col),
+    duplicates summed in input order -- so Csr.from_data never sorts on the
+    host. Index ranges are validated first (the reference's Csr/Coo checks)."""
+    n, m = data.size
+    k = data.nnz
+    if k:
+        if int(data.rows.min()) < 0 or int(data.rows.max()) >= n:
+            raise DimensionMismatch("row index out of range")
+        if int(data.cols.min()) < 0 or int(data.cols.max()) >= m:
+            raise DimensionMismatch("column index out of range")
+    if k >= 2 ** 31 - 1:
+        raise Unsupported("more than 2^31-1 stored entries need 64-bit indices")
+    dev = exc.device
+    tv = _torch_vt(vt)
+    rows_o = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    cols_o = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    vals_o = torch.empty(max(k, 1), dtype=tv, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    if k:
+        r = torch.from_numpy(np.ascontiguousarray(data.rows, dtype=np.int64)).to(dev)
+        c = torch.from_numpy(np.ascontiguousarray(data.cols, dtype=np.int64)).to(dev)
+        v = torch.from_numpy(np.ascontiguousarray(data.vals, dtype=np.float64)).to(dev)
+        ws = torch.empty(int(_lib.query("assemble_workspace_bytes", k)), dtype=torch.uint8, device=dev)
+        _lib.call("assemble_coo_" + _lib.suffix(tv), k, ptr(r), ptr(c), ptr(v), n, m, ptr(rows_o), ptr(cols_o),
+                  ptr(vals_o), ptr(cnt), ptr(ws), exc.stream)
+    nnz = int(cnt.item())
+    return rows_o[:nnz], cols_o[:nnz], vals_o[:nnz]
+
+
 class Csr(_Sparse):
     """Compressed sparse row with an SpMV strategy:
 
@@ -434,14 +466,16 @@ class Csr(_Sparse):
 
     @classmethod
     def _from_host_data(cls, exc, data, value_dtype=None, index_dtype=None):
+        """Device assembly: raw triples go to the GPU once, where they are
+        canonicalised bit-exactly (assemble_device) and compressed."""
         _require_cuda(exc)
         _check_index_dtype(index_dtype)
-        data = data.canonicalize()
         n = data.size.rows
-        counts = np.bincount(data.rows, minlength=n) if data.nnz else np.zeros(n, np.int64)
-        rp = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(counts, out=rp[1:])
-        return cls(exc, data.size, rp, data.cols, data.vals, value_dtype=value_dtype)
+        vt = _np_vt(value_dtype or config.DEFAULT_VALUE_DTYPE)
+        ri, ci, v = assemble_device(exc, data, vt)
+        rp = torch.empty(n + 1, dtype=torch.int32, device=exc.device)
+        _lib.call("coo_to_csr_ptrs", int(v.numel()), n, ptr(ri), ptr(rp), exc.stream)
+        return cls._from_device(exc, data.size, rp, ci, v)
 
     # -- strategy ----------------------------------------------------------------
     def _set_strategy(self, strategy):

@@ -235,6 +235,29 @@ def solver_ext_cases():
     return out
 
 
+def assemble_cases():
+    """MatrixData.canonicalize on unsorted triples with duplicates (device
+    assembly parity): several sizes, a lone -0.0, exact cancellations."""
+    out = {}
+    rng = np.random.default_rng(21)
+    for name, (nr, nc, k) in {"small": (7, 5, 40), "mid": (300, 200, 20000), "wide": (3, 100000, 50000),
+                              "tall": (70000, 3, 60000), "nodup": (1000, 1000, 0)}.items():
+        if name == "nodup":
+            idx = rng.choice(1000 * 1000, 5000, replace=False)
+            r, c = idx // 1000, idx % 1000
+        else:
+            r = rng.integers(0, nr, k)
+            c = rng.integers(0, nc, k)
+        v = rng.standard_normal(r.size) * 10.0 ** rng.integers(-8, 8, r.size)
+        v[::97] = -0.0
+        if name == "mid":
+            v[1::50] = -v[0::50][: v[1::50].size]  # exact cancellations where coordinates repeat
+        d = MatrixData(Dim2(nr, nc), r, c, v).canonicalize()
+        out[name] = {"size": np.array([nr, nc]), "rows_in": r, "cols_in": c, "vals_in": v,
+                     "rows": d.rows, "cols": d.cols, "vals": d.vals}
+    return out
+
+
 def jacobi_cases():
     out = {}
     n, r, c, v = P.stencil3d(8, "convdiff")
@@ -291,6 +314,10 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["ext"]:
         save("solvers_ext.npz", solver_ext_cases())
         sys.exit(0)
+    if sys.argv[1:] == ["assemble"]:
+        save("assemble.npz", assemble_cases())
+        sys.exit(0)
+    save("assemble.npz", assemble_cases())
     save("solvers_ext.npz", solver_ext_cases())
     save("spmv.npz", spmv_cases())
     save("misc.npz", misc_cases())
