@@ -359,6 +359,37 @@ int b200sp_assemble_coo_f32(int64_t count, const int64_t* rows, const int64_t* c
                             int64_t nrows, int64_t ncols, int32_t* rows_out, int32_t* cols_out, float* vals_out,
                             int32_t* nnz_out, void* ws, void* stream);
 
+/* ---- ParILU(0) + sparse triangular solves (reference src/precond.py:211-426,
+ * src/solvers/triangular.py:18-155) -----------------------------------------
+ * ilu_counts: per-row entries with col <= i (L) and col >= i (U); *nodiag =
+ * first row without a stored diagonal (init INT_MAX). diag: first stored
+ * diagonal per row, *zero = first row whose diagonal is 0 or missing (init
+ * INT_MAX). ilu_fill: L / U patterns (row pointers from exclusive scans of
+ * the counts), original values al / au and the initial iterate (l = a / a_jj,
+ * l_ii = 1; u = a). parilu_sweep: one Jacobi-style fixed-point sweep from
+ * (lold, uold) into (lnew, unew); lrow / urow from csr_rows. trs: sync-free
+ * substitution of one column, lower (forward) or upper (backward); diag NULL
+ * = unit diagonal; `ready` (n int32, zero at creation) and a fresh `epoch`
+ * per call; `ticket` = one int32 of scratch. */
+int b200sp_ilu_counts(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, int32_t* lcnt, int32_t* ucnt,
+                      int32_t* nodiag, void* stream);
+int b200sp_csr_rows(int64_t n, const int32_t* row_ptrs, int32_t* row_of_entry, void* stream);
+#define B200SP_ILU_DECL(T, SUF)                                                                                     \
+    int b200sp_diag_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* diag, int32_t* zero,      \
+                          void* stream);                                                                           \
+    int b200sp_ilu_fill_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, const T* diag,          \
+                              const int32_t* lrp, const int32_t* urp, int32_t* lci, T* al, T* lv, int32_t* uci,    \
+                              T* au, T* uv, void* stream);                                                         \
+    int b200sp_parilu_sweep_##SUF(int64_t n, int64_t nl, int64_t nu, const int32_t* lrow, const int32_t* lrp,       \
+                                  const int32_t* lci, const T* al, const T* lold, T* lnew, const int32_t* urow,    \
+                                  const int32_t* urp, const int32_t* uci, const T* au, const T* uold, T* unew,     \
+                                  void* stream);                                                                   \
+    int b200sp_trs_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, const T* diag,               \
+                         int32_t lower, const T* b, int64_t bs, T* x, int64_t xs, int32_t* ready, int32_t epoch,   \
+                         int32_t* ticket, void* stream);
+B200SP_ILU_DECL(double, f64)
+B200SP_ILU_DECL(float, f32)
+
 /* ---- Matrix Market reader (host code; reference src/mmio.py:38-126) ------
  * b200sp_mm_header parses the header and size line of the file image `buf`:
  * info[7] = {array?, symmetric?, rows, cols, entries, body offset, size-line

@@ -78,6 +78,10 @@ _TYPED = {
     # distributed
     "split_fill": "lpppippppppp",
     "assemble_coo": "lpppllppppp",
+    "diag": "lpppppp",
+    "ilu_fill": "lppppppppppppp",
+    "parilu_sweep": "lllppppppppppppp",
+    "trs": "lppppiplplpipp",
     "gather": "lpppp",
 }
 _UNTYPED = {
@@ -111,6 +115,8 @@ _UNTYPED = {
     "set_guard": ("p", None),
     "set_tuning": ("si", ctypes.c_int),
     "assemble_workspace_bytes": ("l", ctypes.c_int64),
+    "ilu_counts": ("lpppppp", ctypes.c_int),
+    "csr_rows": ("lppp", ctypes.c_int),
     "mm_header": ("plpp", ctypes.c_int),
     "mm_count": ("plpip", ctypes.c_int),
     "mm_parse": ("plpippplpp", ctypes.c_int),

@@ -151,3 +151,126 @@ class Jacobi(LinOpFactory):
             offs = (off64[:nb] * 8).contiguous()
             storage = inv64.view(torch.uint8)
         return JacobiOperator(exc, a.size, starts, offs, prec[:nb], storage, cond[:nb])
+
+
+# ---------------------------------------------------------------------------
+# ParILU(0) + ILU preconditioner (reference src/precond.py:211-426)
+# ---------------------------------------------------------------------------
+class IluFactors:
+    """Level-0 incomplete factors: unit-lower L and upper U, both Csr with the
+    sparsity of tril / triu of A (diagonals stored explicitly)."""
+
+    def __init__(self, l, u):  # noqa: E741 (reference field names)
+        self.l, self.u = l, u
+
+    def defect_on_pattern(self, a):
+        """Frobenius norm of (L U - A) restricted to the sparsity of A."""
+        lu = self.l.to_data().to_dense_array() @ self.u.to_data().to_dense_array()
+        ad = a.to_data()
+        return float(np.linalg.norm(lu[ad.rows, ad.cols] - ad.vals))
+
+
+def parilu_generate(a, sweeps=5):
+    """Approximate ILU(0) factors after ``sweeps`` Jacobi-style fixed-point
+    sweeps (csrc/ilu.cu); ``sweeps=0`` returns the scaled triangles of A."""
+    from .formats import _scan
+
+    csr = a if isinstance(a, Csr) else convert(a, "csr")
+    exc = csr.exec
+    _require_cuda(exc)
+    n = csr.size.rows
+    dev = exc.device
+    vt = csr._v.dtype
+    suf = _lib.suffix(vt)
+    from .solvers.triangular import INT_MAX, extract_diagonal
+
+    diag, bad = extract_diagonal(csr)
+    if bad != INT_MAX:
+        raise Singular(f"zero diagonal at row {bad}")
+    lcnt = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    ucnt = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    nodiag = torch.full((1,), INT_MAX, dtype=torch.int32, device=dev)
+    _lib.call("ilu_counts", n, ptr(csr._rp), ptr(csr._ci), ptr(lcnt), ptr(ucnt), ptr(nodiag), exc.stream)
+    lrp, urp = _scan(exc, lcnt[:n]), _scan(exc, ucnt[:n])
+    nl, nu = int(lrp[-1].item()), int(urp[-1].item())
+    lci = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+    uci = torch.empty(max(nu, 1), dtype=torch.int32, device=dev)
+    al, lv, lv2 = (torch.empty(max(nl, 1), dtype=vt, device=dev) for _ in range(3))
+    au, uv, uv2 = (torch.empty(max(nu, 1), dtype=vt, device=dev) for _ in range(3))
+    _lib.call("ilu_fill_" + suf, n, ptr(csr._rp), ptr(csr._ci), ptr(csr._v), ptr(diag), ptr(lrp), ptr(urp),
+              ptr(lci), ptr(al), ptr(lv), ptr(uci), ptr(au), ptr(uv), exc.stream)
+    if sweeps:
+        lrow = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+        urow = torch.empty(max(nu, 1), dtype=torch.int32, device=dev)
+        _lib.call("csr_rows", n, ptr(lrp), ptr(lrow), exc.stream)
+        _lib.call("csr_rows", n, ptr(urp), ptr(urow), exc.stream)
+        for _ in range(int(sweeps)):
+            _lib.call("parilu_sweep_" + suf, n, nl, nu, ptr(lrow), ptr(lrp), ptr(lci), ptr(al), ptr(lv), ptr(lv2),
+                      ptr(urow), ptr(urp), ptr(uci), ptr(au), ptr(uv), ptr(uv2), exc.stream)
+            lv, lv2 = lv2, lv
+            uv, uv2 = uv2, uv
+    lower = Csr._from_device(exc, csr.size, lrp, lci[:nl], lv[:nl])
+    upper = Csr._from_device(exc, csr.size, urp, uci[:nu], uv[:nu])
+    return IluFactors(lower, upper)
+
+
+class ParIlu(LinOpFactory):
+    """Factorization factory producing :class:`IluFactors`."""
+
+    def __init__(self, exc, sweeps=5):
+        super().__init__(exc)
+        self.sweeps = sweeps
+
+    def _validate(self, a):
+        if not a.size.square:
+            raise DimensionMismatch("factorization needs a square matrix")
+
+    def _generate(self, a):
+        return parilu_generate(a, self.sweeps)
+
+
+class IluPreconditioner(LinOp):
+    """z = U^-1 (L^-1 r) through the configured triangular solvers."""
+
+    def __init__(self, l_solver, u_solver):
+        super().__init__(l_solver.exec, l_solver.size)
+        self.l_solver = l_solver
+        self.u_solver = u_solver
+
+    def _apply_impl(self, b, x):
+        tmp = b.like(*b.values.shape)
+        self.l_solver.apply(b, tmp)
+        self.u_solver.apply(tmp, x)
+
+    def clone_to(self, target):
+        return IluPreconditioner(self.l_solver.clone_to(target), self.u_solver.clone_to(target))
+
+
+class Ilu(LinOpFactory):
+    """ILU preconditioner factory: ``generate`` takes the system matrix
+    (factors via ParILU) or pre-generated :class:`IluFactors`; the factor
+    solvers default to the direct triangular solvers."""
+
+    def __init__(self, exc, l_solver_factory=None, u_solver_factory=None, sweeps=5):
+        from .solvers.triangular import LowerTrs, UpperTrs
+
+        super().__init__(exc)
+        self.l_solver_factory = l_solver_factory or LowerTrs(exc, unit_diagonal=True)
+        self.u_solver_factory = u_solver_factory or UpperTrs(exc)
+        self.sweeps = sweeps
+
+    def _validate(self, a):
+        if isinstance(a, IluFactors):
+            return
+        if not a.size.square:
+            raise DimensionMismatch("ILU needs a square matrix")
+
+    def generate(self, system_matrix):
+        if isinstance(system_matrix, IluFactors):
+            f = system_matrix
+            return IluPreconditioner(self.l_solver_factory.generate(f.l), self.u_solver_factory.generate(f.u))
+        return super().generate(system_matrix)
+
+    def _generate(self, a):
+        f = parilu_generate(a, self.sweeps)
+        return IluPreconditioner(self.l_solver_factory.generate(f.l), self.u_solver_factory.generate(f.u))

@@ -258,6 +258,52 @@ def assemble_cases():
     return out
 
 
+def ilu_cases():
+    """ParIlu factors (several sweep counts), triangular solves and
+    ILU-preconditioned solves (SURVEY 8(f) #3)."""
+    from opalg.precond import Ilu, ParIlu
+    from opalg.solvers import LowerTrs, UpperTrs
+
+    out = {}
+    rng = np.random.default_rng(31)
+    mats = {"cd5": P.stencil3d(5, "convdiff"), "p2d8": P.five_point(8)}
+    d = random_sparse(40, density=0.15, seed=7).canonicalize()
+    mats["rand40"] = (40, d.rows, d.cols, d.vals)
+    for name, (n, r, c, v) in mats.items():
+        a = Csr.from_data(REF, md(n, r, c, v))
+        for sw in (0, 1, 3, 2 * n):
+            f = ParIlu(REF, sweeps=sw).generate(a)
+            out[f"parilu_{name}_s{sw}"] = {
+                "l_rp": f.l.row_ptrs, "l_ci": f.l.col_idxs, "l_v": f.l.vals,
+                "u_rp": f.u.row_ptrs, "u_ci": f.u.col_idxs, "u_v": f.u.vals,
+                "defect": np.array(f.defect_on_pattern(a)), "sweeps": np.array(sw)}
+        f = ParIlu(REF, sweeps=2 * n).generate(a)
+        b = rng.standard_normal((n, 2))
+        xl = Dense.zeros(REF, n, 2)
+        LowerTrs(REF, unit_diagonal=True).generate(f.l).apply(Dense(REF, b), xl)
+        xu = Dense.zeros(REF, n, 2)
+        UpperTrs(REF).generate(f.u).apply(Dense(REF, b), xu)
+        xz = Dense.zeros(REF, n, 2)
+        Ilu(REF, sweeps=2 * n).generate(a).apply(Dense(REF, b), xz)
+        out[f"trs_{name}"] = {"b": b, "xl": xl.data.copy(), "xu": xu.data.copy(), "xilu": xz.data.copy()}
+    # ILU-preconditioned Krylov solves (5 sweeps, the default)
+    for name, kind, solver in (("cg_ilu_7pt_g8", "7pt", "cg"), ("bicgstab_ilu_cd_g8", "convdiff", "bicgstab"),
+                               ("gmres_ilu_cd_g8", "convdiff", "gmres")):
+        n, r, c, v = P.stencil3d(8, kind)
+        a = Csr.from_data(REF, md(n, r, c, v))
+        fac = {"cg": Cg, "bicgstab": Bicgstab, "gmres": Gmres}[solver]
+        hist = _HistoryFactory()
+        s = fac(REF, criteria=[Iteration(1000), ResidualNormReduction(1e-10), hist],
+                preconditioner=Ilu(REF)).generate(a)
+        x = Dense.zeros(REF, n, 1)
+        s.apply(Dense(REF, np.ones((n, 1))), x)
+        st = s.last_status
+        print(f"  {name}: iterations={st.iterations}")
+        out[name] = {"iterations": np.array(st.iterations), "stopping_id": np.array(st.stopping_id),
+                     "x": x.data.copy(), "history": np.array(hist.rows)}
+    return out
+
+
 def jacobi_cases():
     out = {}
     n, r, c, v = P.stencil3d(8, "convdiff")
@@ -313,6 +359,9 @@ def save(name, cases):
 if __name__ == "__main__":
     if sys.argv[1:] == ["ext"]:
         save("solvers_ext.npz", solver_ext_cases())
+        sys.exit(0)
+    if sys.argv[1:] == ["ilu"]:
+        save("ilu.npz", ilu_cases())
         sys.exit(0)
     if sys.argv[1:] == ["assemble"]:
         save("assemble.npz", assemble_cases())
