@@ -812,7 +812,7 @@ __device__ __forceinline__ T lb2_block_dot(int s, int e, const int* __restrict__
 
 template <typename T, bool XIN>
 __global__ void __launch_bounds__(LB_BLOCK)
-csr_lb2_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
+csr_lb2_kernel(int64_t n, int64_t ntiles, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
                const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
                const T* __restrict__ xin, int64_t xins, const int* __restrict__ coords, int* __restrict__ carry_row,
                T* __restrict__ carry_val) {
@@ -820,42 +820,44 @@ csr_lb2_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
     __shared__ int s_long[LB_BLOCK];
     __shared__ int s_nlong;
     __shared__ T s_red[LB_BLOCK / 32];
-    const int tile = blockIdx.x;
-    const int r0 = coords[2 * tile], k0 = coords[2 * tile + 1];
-    const int r1 = coords[2 * tile + 2], k1 = coords[2 * tile + 3];
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
-    if (threadIdx.x == 0) s_nlong = 0;
-    __syncthreads();
-    const int nrows = r1 - r0;
-    if (nrows > 0) {
-        // sub-warp width from the tile's mean row length (classical rule)
-        const int mean = (k1 - k0 + nrows - 1) / nrows;
-        const int per_lane = (mean + 7) / 8;
-        if (per_lane <= 1) lb2_rows<T, 1, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-        else if (per_lane <= 2) lb2_rows<T, 2, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-        else if (per_lane <= 4) lb2_rows<T, 4, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-        else if (per_lane <= 8) lb2_rows<T, 8, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-        else if (per_lane <= 16) lb2_rows<T, 16, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-        else lb2_rows<T, 32, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-    }
-    __syncthreads();
-    const int nlong = s_nlong;
-    for (int i = 0; i < nlong; ++i) {
-        const int row = s_long[i];
-        const T sum = lb2_block_dot(max(__ldg(rp + row), k0), __ldg(rp + row + 1), ci, v, b, bs, s_red);
-        if (threadIdx.x == 0) {
-            T out = a * sum;
-            if (XIN) out += bt * xin[(int64_t)row * xins];
-            x[(int64_t)row * xs] = out;
+    // persistent CTAs over equal-work tiles (no last-wave tail)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int r0 = coords[2 * tile], k0 = coords[2 * tile + 1];
+        const int r1 = coords[2 * tile + 2], k1 = coords[2 * tile + 3];
+        if (threadIdx.x == 0) s_nlong = 0;
+        __syncthreads();
+        const int nrows = r1 - r0;
+        if (nrows > 0) {
+            // sub-warp width from the tile's mean row length (classical rule)
+            const int mean = (k1 - k0 + nrows - 1) / nrows;
+            const int per_lane = (mean + 7) / 8;
+            if (per_lane <= 1) lb2_rows<T, 1, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 2) lb2_rows<T, 2, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 4) lb2_rows<T, 4, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 8) lb2_rows<T, 8, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 16) lb2_rows<T, 16, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else lb2_rows<T, 32, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
         }
-    }
-    // carry-out: the entries of row r1 inside this tile
-    T carry = 0;
-    if (r1 < n) carry = lb2_block_dot(max(__ldg(rp + r1), k0), k1, ci, v, b, bs, s_red);
-    if (threadIdx.x == 0) {
-        carry_row[tile] = r1;
-        carry_val[tile] = carry;
+        __syncthreads();
+        const int nlong = s_nlong;
+        for (int i = 0; i < nlong; ++i) {
+            const int row = s_long[i];
+            const T sum = lb2_block_dot(max(__ldg(rp + row), k0), __ldg(rp + row + 1), ci, v, b, bs, s_red);
+            if (threadIdx.x == 0) {
+                T out = a * sum;
+                if (XIN) out += bt * xin[(int64_t)row * xins];
+                x[(int64_t)row * xs] = out;
+            }
+        }
+        // carry-out: the entries of row r1 inside this tile
+        T carry = 0;
+        if (r1 < n) carry = lb2_block_dot(max(__ldg(rp + r1), k0), k1, ci, v, b, bs, s_red);
+        if (threadIdx.x == 0) {
+            carry_row[tile] = r1;
+            carry_val[tile] = carry;
+        }
     }
 }
 
@@ -873,8 +875,9 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
     const int64_t ntiles = ceil_div(n + nnz, tile);
     if (mode == 2) {
         auto k2 = xin ? csr_lb2_kernel<T, true> : csr_lb2_kernel<T, false>;
-        k2<<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row,
-                                                   carry_val);
+        const unsigned g2 = (unsigned)std::min<int64_t>(ntiles, (int64_t)kNumSMs * tuning("lb2_per_sm", 1 << 20));  // one CTA per tile measured best (0.66 vs 0.51 persistent)
+        k2<<<g2, LB_BLOCK, 0, st>>>(n, ntiles, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row,
+                                    carry_val);
     } else if (xin)
         csr_lb_kernel<T, true><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
     else
@@ -1032,6 +1035,97 @@ __global__ void __launch_bounds__(COO_BLOCK, 6) coo_kernel_b6(COO_ARGS) {
 #undef COO_ARGS
 #undef COO_PASS
 
+// Entry-interleaved variant ("seg"): lane l of step s takes entry
+// e0 + 32 s + l of the warp's 256-entry chunk, so every load and every x
+// gather of a warp instruction covers 32 consecutive entries (~1 stencil
+// row: a few sectors instead of the ~32 the lane-contiguous layout touches
+// -- ncu: L1TEX 79% busy there). Rows are joined by a shuffle segmented
+// scan per step (keys sorted, so "same row as lane - o" delimits segments)
+// and a warp-uniform carry between steps. Chunking, carries and the fix-up
+// pass are exactly those of the lane-contiguous kernel.
+template <typename T, bool XIN>
+__global__ void __launch_bounds__(COO_BLOCK)
+coo_kernel_seg(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols, const T* __restrict__ vals,
+               const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+               const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    if (alpha.skip()) return;
+    constexpr int STEPS = 8;
+    constexpr int CHUNK = 32 * STEPS;
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = c * CHUNK;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
+    const int head_row = __ldg(rows + e0), tail_row = __ldg(rows + e1 - 1);
+    const bool head_shared = e0 > 0 && __ldg(rows + e0 - 1) == head_row;
+    const bool tail_shared = e1 < nnz && __ldg(rows + e1) == tail_row;
+    const bool single = head_row == tail_row;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    int rr[STEPS], cc[STEPS];
+    T vv[STEPS];
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) {
+        const int64_t e = e0 + s * 32 + lane;
+        const bool ok = e < e1;
+        rr[s] = ok ? __ldg(rows + e) : INT_MAX;
+        cc[s] = ok ? __ldg(cols + e) : 0;
+        vv[s] = ok ? __ldg(vals + e) : T(0);
+    }
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) vv[s] = rr[s] != INT_MAX ? vv[s] * ld_gather(b + (int64_t)cc[s] * bs) : T(0);
+    auto emit = [&](int row, T val) {  // a row completed inside this chunk (not the tail)
+        if (row == head_row && head_shared) {
+            carry_head[c] = val;
+        } else {
+            T out = a * val;
+            if (XIN) out += bt * xin[(int64_t)row * xins];
+            x[(int64_t)row * xs] = out;
+        }
+    };
+    int carry_r = INT_MIN;
+    T carry_v = 0;
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) {
+        const int r = rr[s];
+        T val = vv[s];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T vn = __shfl_up_sync(0xffffffffu, val, o);
+            const int rn = __shfl_up_sync(0xffffffffu, r, o);
+            if (lane >= o && rn == r) val += vn;
+        }
+        const int r0 = __shfl_sync(0xffffffffu, r, 0);
+        if (r0 == INT_MAX) break;  // step past the chunk end (warp-uniform)
+        if (carry_r != INT_MIN) {
+            if (r0 == carry_r) {
+                if (r == carry_r) val += carry_v;
+            } else if (lane == 0) {
+                emit(carry_r, carry_v);
+            }
+        }
+        const int rnext = __shfl_down_sync(0xffffffffu, r, 1);
+        const unsigned valid = __ballot_sync(0xffffffffu, r != INT_MAX);
+        const int last = 31 - __clz(valid);
+        const bool end = r != INT_MAX && (lane == last || rnext != r);
+        // the segment ending at the last valid lane continues as the carry
+        carry_r = __shfl_sync(0xffffffffu, r, last);
+        carry_v = __shfl_sync(0xffffffffu, val, last);
+        if (end && lane != last) emit(r, val);
+    }
+    if (lane == 0) {  // the tail row
+        if (!(tail_shared || (single && head_shared))) {
+            T out = a * carry_v;
+            if (XIN) out += bt * xin[(int64_t)tail_row * xins];
+            x[(int64_t)tail_row * xs] = out;
+        } else if (single) {
+            carry_head[c] = carry_v;
+        } else {
+            carry_tail[c] = carry_v;
+        }
+    }
+}
+
 template <typename T, bool XIN>
 __global__ void coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
                                  const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
@@ -1074,9 +1168,13 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
     const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
     const bool vec = aligned16(rows) && aligned16(cols) && aligned16(vals);
     const int minb = tuning("coo_minb", sizeof(T) == 4 ? 6 : 1);
+    const int seg = tuning("coo_seg", 0) && chunk == 256;
 #define COO_LAUNCH(XI, VE)                                                                                  \
     do {                                                                                                    \
-        if (chunk == 128)                                                                                   \
+        if (seg)                                                                                            \
+            coo_kernel_seg<T, XI><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, be,   \
+                                                              xin, xins, carry_head, carry_tail);           \
+        else if (chunk == 128)                                                                              \
             coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
                                                                     be, xin, xins, carry_head, carry_tail);  \
         else if (minb == 6)                                                                                 \

@@ -338,3 +338,32 @@ def test_dense_blas(cuda):
     np.testing.assert_array_equal(np.asarray(y.data), ref)
     y.scale(b2.Dense(cuda, [[2.0, -1.0]]))
     np.testing.assert_array_equal(np.asarray(y.data), ref * [2.0, -1.0])
+
+
+@pytest.mark.parametrize("knob,val", [("coo_seg", 1), ("coo_minb", 6)])
+def test_coo_kernel_variants(cuda, golden_spmv, knob, val):
+    """Every Coo kernel variant (b200sp_set_tuning) reproduces the reference,
+    including rows spanning many chunks and empty rows."""
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib
+
+    default = {"coo_seg": 0, "coo_minb": 1}[knob]
+    _lib.set_tuning(knob, val)
+    try:
+        for name, g in golden_spmv.items():
+            for dtype in ("float64", "float32"):
+                a = make(b2, cuda, golden_data(b2, g), "coo", {}, dtype)
+                x = b2.Dense(cuda, np.full(g["b"].shape, 7.0), value_dtype=dtype)
+                a.apply(b2.Dense(cuda, g["b"], value_dtype=dtype), x)
+                ref = g["x_csr"]
+                if dtype == "float32":
+                    n = int(g["n"])
+                    rp = OS.csr_from_triples(n, g["rows"], g["cols"], g["vals"])
+                    ref = OS.csr_spmv(rp, g["cols"], g["vals"].astype(np.float32).astype(np.float64),
+                                      g["b"].astype(np.float32).astype(np.float64))
+                assert OS.rel_error_inf(np.asarray(x.data), ref) <= TOL[dtype], (name, dtype)
+        test_long_rows_straddling_tiles_and_chunks(cuda, "coo", {})
+        test_fused_residual(cuda, golden_spmv, "coo", {})
+        test_advanced_apply_matches_reference(cuda, golden_spmv, "coo", {})
+    finally:
+        _lib.set_tuning(knob, default)
