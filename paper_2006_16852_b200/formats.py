@@ -20,6 +20,7 @@ import math
 import numpy as np
 
 from . import _lib, config
+from .loggers import EventKind
 from .base import Dim2, LinOp
 from .errors import DimensionMismatch, Unsupported
 from .executor import CudaExecutor, DeviceView, HostExecutor, ptr
@@ -660,6 +661,113 @@ class Csr(_Sparse):
     @property
     def vals(self):
         return DeviceView(self._v)
+
+    # -- host operands: pipelined transfers -----------------------------------------
+    #: row chunks of the pipelined host apply (0 disables it)
+    HOST_PIPELINE_CHUNKS = 8  # 4 / 8 / 16 measured 0.626 / 0.568 / 0.649 ms on C2 (link ceiling 0.38)
+
+    def apply(self, b, x):
+        """x <- A b. With both operands in host (pinned) memory, a single column
+        and the row-parallel classical strategy, the transfers are pipelined
+        with the SpMV: b goes up in chunks on one copy stream, each row chunk
+        starts as soon as every b entry its columns reach has arrived (column
+        range per chunk, planned once), and x comes down chunk by chunk on a
+        second copy stream -- H2D and D2H overlap each other and the kernels
+        instead of running back to back (same results: rows are independent)."""
+        if not self._pipeline_ok(b, x):
+            return super().apply(b, x)
+        self._check_usable()
+        self._check_conformal(b, x)
+        self._log(EventKind.LINOP_APPLY_STARTED, {"op": type(self).__name__, "uid": self.uid})
+        self._pipelined_apply(b, x)
+        self._log(EventKind.LINOP_APPLY_COMPLETED, {"op": type(self).__name__, "uid": self.uid})
+
+    def _pipeline_ok(self, b, x):
+        from .executor import HostExecutor
+
+        return (self.HOST_PIPELINE_CHUNKS > 0 and isinstance(getattr(b, "exec", None), HostExecutor)
+                and isinstance(getattr(x, "exec", None), HostExecutor) and b.exec.pinned
+                and getattr(b, "is_dense", False) and getattr(x, "is_dense", False)
+                and b.size.cols == 1 and x.size.cols == 1 and self.size.rows >= (1 << 16)
+                and self._resolved_strategy() == "classical"
+                and np.dtype(b.dtype) == self.value_dtype and np.dtype(x.dtype) == self.value_dtype)
+
+    def _pipeline_plan(self):
+        plan = getattr(self, "_pplan", None)
+        if plan is None:
+            n = self.size.rows
+            k = self.HOST_PIPELINE_CHUNKS
+            bounds = [n * j // k for j in range(k + 1)]
+            rp = self._rp.cpu().numpy()
+            ci = self._ci
+            need = []  # highest column each row chunk reads
+            for j in range(k):
+                lo, hi = int(rp[bounds[j]]), int(rp[bounds[j + 1]])
+                need.append(int(ci[lo:hi].max().item()) if hi > lo else -1)
+            m = self.size.cols
+            cb = [m * j // k for j in range(k + 1)]  # b chunks
+            # b chunk index whose arrival completes columns [0, need]
+            wait = [next(i for i in range(k) if cb[i + 1] > nd) if nd >= 0 else -1 for nd in need]
+            dev = self.exec.device
+            plan = {"rows": bounds, "cols": cb, "wait": wait,
+                    "s_in": torch.cuda.Stream(dev), "s_out": torch.cuda.Stream(dev),
+                    "b": torch.empty(m, dtype=self._v.dtype, device=dev),
+                    "x": torch.empty(n, dtype=self._v.dtype, device=dev)}
+            self._pplan = plan
+        return plan
+
+    def _pipelined_apply(self, b, x):
+        """Replays a CUDA graph of the whole chunked pipeline (captured once per
+        pair of host buffers: one launch instead of ~4 per chunk)."""
+        P = self._pipeline_plan()
+        bh = torch.from_numpy(np.asarray(b.values).reshape(-1))
+        xh = torch.from_numpy(np.asarray(x.values).reshape(-1))
+        key = (bh.data_ptr(), xh.data_ptr())
+        graphs = P.setdefault("graphs", {})
+        g = graphs.get(key)
+        if g is None:
+            if len(graphs) >= 4:
+                graphs.clear()
+            torch.cuda.synchronize(self.exec.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._pipeline_issue(P, bh, xh)
+            graphs[key] = g
+        g.replay()
+        torch.cuda.current_stream(self.exec.device).synchronize()
+
+    def _pipeline_issue(self, P, bh, xh):
+        exc = self.exec
+        k = len(P["wait"])
+        bd, xd = P["b"], P["x"]
+        cur = torch.cuda.current_stream(exc.device)
+        s_in, s_out = P["s_in"], P["s_out"]
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        ev_in = []
+        with torch.cuda.stream(s_in):
+            for i in range(k):
+                lo, hi = P["cols"][i], P["cols"][i + 1]
+                bd[lo:hi].copy_(bh[lo:hi], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_in)
+                ev_in.append(e)
+        suf = _lib.suffix(self._v.dtype)
+        isz = self._v.element_size()
+        sw = self.subwarp()
+        for j in range(k):
+            r0, r1 = P["rows"][j], P["rows"][j + 1]
+            if P["wait"][j] >= 0:
+                cur.wait_event(ev_in[P["wait"][j]])
+            _lib.call("csr_spmv_classical_" + suf, r1 - r0, self._rp.data_ptr() + 4 * r0, ptr(self._ci), ptr(self._v),
+                      ptr(bd), 1, xd.data_ptr() + isz * r0, 1, 1.0, 0, 0.0, 0, 0, 0, sw, cur.cuda_stream)
+            e = torch.cuda.Event()
+            e.record(cur)
+            s_out.wait_event(e)
+            with torch.cuda.stream(s_out):
+                xh[r0:r1].copy_(xd[r0:r1], non_blocking=True)
+        cur.wait_stream(s_in)
+        cur.wait_stream(s_out)
 
     # -- kernels -------------------------------------------------------------------
     def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins):

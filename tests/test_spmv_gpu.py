@@ -367,3 +367,29 @@ def test_coo_kernel_variants(cuda, golden_spmv, knob, val):
         test_advanced_apply_matches_reference(cuda, golden_spmv, "coo", {})
     finally:
         _lib.set_tuning(knob, default)
+
+
+@pytest.mark.parametrize("kind", ["27pt", "random"])
+def test_pipelined_host_apply_bitwise(cuda, host, kind):
+    """Host operands on a large Csr take the chunked transfer/compute
+    pipeline; results are bitwise those of the device-resident apply."""
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import problems
+
+    if kind == "27pt":
+        a = problems.stencil(cuda, "27pt", 64)
+    else:
+        n, rng = 70000, np.random.default_rng(4)
+        rows = np.repeat(np.arange(n), 8)
+        data = b2.MatrixData((n, n), rows, rng.integers(0, n, rows.size), rng.standard_normal(rows.size))
+        a = b2.matrix_from_data(cuda, data, "csr")
+    n = a.size.rows
+    assert a._pipeline_ok(b2.Dense(host, np.zeros((n, 1))), b2.Dense(host, np.zeros((n, 1))))
+    bv = np.random.default_rng(1).standard_normal((n, 1))
+    xh = b2.Dense(host, np.full((n, 1), 3.0))
+    a.apply(b2.Dense(host, bv), xh)
+    xd = b2.Dense.zeros(cuda, n, 1)
+    a.apply(b2.Dense(cuda, bv), xd)
+    np.testing.assert_array_equal(np.asarray(xh.data), np.asarray(xd.data))
+    a.apply(b2.Dense(host, 2 * bv), xh)  # plan and buffers reused
+    np.testing.assert_array_equal(np.asarray(xh.data), 2 * np.asarray(xd.data))
