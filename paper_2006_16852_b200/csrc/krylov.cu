@@ -747,6 +747,8 @@ static RowBlocks make_rb(int64_t n, int64_t nb, const int32_t* starts, const int
     return RowBlocks{n, JacobiView{nb, starts, (const long long*)offs, prec, (const unsigned char*)storage}};
 }
 
+namespace b200sp {
+
 // ===========================================================================
 // Csr SpMV with the solver's next reduction fused into its epilogue:
 //   q = A p and
@@ -870,6 +872,8 @@ static int csr_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, co
     count_launch();
     return check_launch("csr_spmv_dot");
 }
+
+}  // namespace b200sp
 
 #define KRY_LAUNCH(kernel, units, per_block, ...)                                                     \
     do {                                                                                              \

@@ -26,18 +26,19 @@ namespace b200sp {
 // U rows before any FMA: U x SW independent gathers in flight per sub-warp
 // (one row per warp leaves HBM latency exposed: the first B200 measurement of
 // the one-row variant reached 32% of peak on C2).
-template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1); };
+// rows in flight per sub-warp; thread-per-row (7-point) takes 2: 0.851 vs
+// 0.819 of the roofline at 256^3 (profiles/r02_classical_sweep.txt)
+template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 || SW == 1 ? 2 : 1); };
 
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)
-template <typename T, int SW, bool XIN, bool L1>
+template <typename T, int SW, bool XIN, bool L1, int U>
 __global__ void __launch_bounds__(256)
 csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
                      const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
                      T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
                      const T* __restrict__ xin, int64_t xins) {
     if (alpha.skip()) return;
-    constexpr int U = ClassicalRows<SW>::v;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & (SW - 1);
     const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
@@ -98,10 +99,15 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
     // measured on B200 (profiles/r02_classical_sweep.txt): L1-allocating
     // matrix loads lift C2 fp64 (sub-warp 4) from 0.43 to 0.85 of the HBM
     // roofline and 7-point (sub-warp 1) from 0.27 to 0.85; two waves of CTAs
-    int grid = grid_for(ceil_div(n, ClassicalRows<SW>::v) * SW, block, tuning("classical_per_sm", 16));
-    auto kern = tuning("classical_l1", 1)
-                    ? (xin ? csr_classical_kernel<T, SW, true, true> : csr_classical_kernel<T, SW, false, true>)
-                    : (xin ? csr_classical_kernel<T, SW, true, false> : csr_classical_kernel<T, SW, false, false>);
+    // (the no_allocate build of this kernel is gone; its numbers stay in the
+    // sweep file). U = rows in flight per sub-warp: knob "classical_rows" 2
+    // doubles it for the narrow sub-warps
+    constexpr int U0 = ClassicalRows<SW>::v;
+    constexpr int U2 = U0 < 2 ? 2 : U0;
+    const bool two = tuning("classical_rows", 0) == 2;
+    const int grid = grid_for(ceil_div(n, two ? U2 : U0) * SW, block, tuning("classical_per_sm", 32));
+    auto kern = two ? (xin ? csr_classical_kernel<T, SW, true, true, U2> : csr_classical_kernel<T, SW, false, true, U2>)
+                    : (xin ? csr_classical_kernel<T, SW, true, true, U0> : csr_classical_kernel<T, SW, false, true, U0>);
     kern<<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
 }
 
