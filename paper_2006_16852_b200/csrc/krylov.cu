@@ -806,13 +806,11 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) acc[k] = subwarp_sum<SW>(acc[k]);
-        if (lane < U) {
-            T mine = acc[0];
 #pragma unroll
-            for (int k = 1; k < U; ++k)
-                if (lane == k) mine = acc[k];
-            const int64_t row = row0 + lane;
-            if (row < n) {
+        for (int k = 0; k < U; ++k) {  // row k written by lane k % SW (U may exceed SW)
+            const int64_t row = row0 + k;
+            if (k % SW == lane && row < n) {
+                const T mine = acc[k];
                 q[row] = mine;
                 if (PH == PH_SIGMA) d0 += (double)__ldg(p + row) * (double)mine;
                 if (PH == PH_GAMMA) d0 += (double)__ldg(u + row) * (double)mine;

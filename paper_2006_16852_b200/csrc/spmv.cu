@@ -26,9 +26,10 @@ namespace b200sp {
 // U rows before any FMA: U x SW independent gathers in flight per sub-warp
 // (one row per warp leaves HBM latency exposed: the first B200 measurement of
 // the one-row variant reached 32% of peak on C2).
-// rows in flight per sub-warp; thread-per-row (7-point) takes 2: 0.851 vs
-// 0.819 of the roofline at 256^3 (profiles/r02_classical_sweep.txt)
-template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 || SW == 1 ? 2 : 1); };
+// rows in flight per sub-warp (2 rows per thread at sub-warp 1 strides the
+// row accesses of a warp by 2 and measured slower: 0.745 vs 0.748 / CG
+// 0.81 vs 0.51 ms; profiles/r02_classical_sweep.txt)
+template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1); };
 
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)
@@ -76,14 +77,13 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = subwarp_sum<SW>(acc[u]);
-        if (lane < U) {
-            T mine = acc[0];
+        // every lane holds every row's total (xor reduction); row u is
+        // written by lane u % SW (U may exceed SW: thread-per-row takes 2)
 #pragma unroll
-            for (int u = 1; u < U; ++u)
-                if (lane == u) mine = acc[u];
-            const int64_t row = row0 + lane;
-            if (row < n) {
-                T r = a * mine;
+        for (int u = 0; u < U; ++u) {
+            const int64_t row = row0 + u;
+            if (u % SW == lane && row < n) {
+                T r = a * acc[u];
                 if (XIN) r += bt * xin[row * xins];
                 x[row * xs] = r;
             }
