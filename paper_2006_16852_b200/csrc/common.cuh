@@ -119,6 +119,33 @@ __device__ __forceinline__ void ld_stream_vec(const float* p, float (&out)[E]) {
         out[i] = q.x; out[i + 1] = q.y; out[i + 2] = q.z; out[i + 3] = q.w;
     }
 }
+// the same with L1-allocating loads: when a lane's 16-byte pieces leave the
+// other half of each 32-byte sector to its next instruction, no_allocate would
+// fetch every sector twice from L2
+template <int E>
+__device__ __forceinline__ void ld_cached_vec(const int* p, int (&out)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; i += 4) {
+        int4 q = __ldg(reinterpret_cast<const int4*>(p + i));
+        out[i] = q.x; out[i + 1] = q.y; out[i + 2] = q.z; out[i + 3] = q.w;
+    }
+}
+template <int E>
+__device__ __forceinline__ void ld_cached_vec(const double* p, double (&out)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; i += 2) {
+        double2 q = __ldg(reinterpret_cast<const double2*>(p + i));
+        out[i] = q.x; out[i + 1] = q.y;
+    }
+}
+template <int E>
+__device__ __forceinline__ void ld_cached_vec(const float* p, float (&out)[E]) {
+#pragma unroll
+    for (int i = 0; i < E; i += 4) {
+        float4 q = __ldg(reinterpret_cast<const float4*>(p + i));
+        out[i] = q.x; out[i + 1] = q.y; out[i + 2] = q.z; out[i + 3] = q.w;
+    }
+}
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 __device__ __forceinline__ bool aligned16_dev(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 

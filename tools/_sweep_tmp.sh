@@ -1,3 +1,4 @@
-timeout 600 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
-timeout 300 python tools/knob_sweep.py --matrix 7pt --grid 256 --format csr_classical --knobs "classical_per_sm=16,32" > gpurun_out/knobs17.txt 2>&1
-timeout 300 python bench.py --workload c5 --grid 256 --no-cpu > gpurun_out/b_c5g256.log 2>&1
+timeout 300 python -m pytest tests/test_spmv_gpu.py -q -x -k "coo or hybrid" > gpurun_out/t_coo.log 2>&1
+timeout 200 python tools/knob_sweep.py --format coo,hybrid --knobs "coo_minb=1,6" > gpurun_out/knobs18.txt 2>&1
+timeout 200 python tools/knob_sweep.py --dtype float32 --format coo --knobs "coo_minb=1,6" >> gpurun_out/knobs18.txt 2>&1
+timeout 200 python tools/knob_sweep.py --matrix powerlaw --format coo,hybrid >> gpurun_out/knobs18.txt 2>&1
