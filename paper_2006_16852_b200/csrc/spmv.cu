@@ -757,7 +757,7 @@ __global__ void csr_lb_fixup_kernel(int64_t n, int64_t ntiles, const int* __rest
 // ---------------------------------------------------------------------------
 constexpr int LB2_LONG = 16;  // x sub-warp width: longer rows take the CTA-wide pass
 
-template <typename T, int SW, bool XIN>
+template <typename T, int SW, bool XIN, bool UNR4>
 __device__ __forceinline__ void lb2_rows(int r0, int r1, int k0, const int* __restrict__ rp,
                                          const int* __restrict__ ci, const T* __restrict__ v,
                                          const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
@@ -783,7 +783,7 @@ __device__ __forceinline__ void lb2_rows(int r0, int r1, int k0, const int* __re
         }
         T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
         int k = s + lane;
-        for (; k + 3 * SW < e; k += 4 * SW) {
+        for (; UNR4 && k + 3 * SW < e; k += 4 * SW) {
             const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + SW), c2 = __ldg(ci + k + 2 * SW),
                       c3 = __ldg(ci + k + 3 * SW);
             a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
@@ -791,7 +791,10 @@ __device__ __forceinline__ void lb2_rows(int r0, int r1, int k0, const int* __re
             a2 += __ldg(v + k + 2 * SW) * ld_gather(b + (int64_t)c2 * bs);
             a3 += __ldg(v + k + 3 * SW) * ld_gather(b + (int64_t)c3 * bs);
         }
-        for (; k < e; k += SW) a0 += __ldg(v + k) * ld_gather(b + (int64_t)__ldg(ci + k) * bs);
+        for (; k < e; k += SW) {
+            int c0 = __ldg(ci + k);
+            a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
+        }
         const T sum = subwarp_sum<SW>((a0 + a1) + (a2 + a3));
         if (active && !lng && lane == 0) {
             T out = a * sum;
@@ -816,7 +819,7 @@ __device__ __forceinline__ T lb2_block_dot(int s, int e, const int* __restrict__
     return block_sum(a0 + a1, sh);
 }
 
-template <typename T, bool XIN>
+template <typename T, bool XIN, bool UNR4>
 __global__ void __launch_bounds__(LB_BLOCK)
 csr_lb2_kernel(int64_t n, int64_t ntiles, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
                const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
@@ -839,12 +842,12 @@ csr_lb2_kernel(int64_t n, int64_t ntiles, const int* __restrict__ rp, const int*
             // sub-warp width from the tile's mean row length (classical rule)
             const int mean = (k1 - k0 + nrows - 1) / nrows;
             const int per_lane = (mean + 7) / 8;
-            if (per_lane <= 1) lb2_rows<T, 1, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 2) lb2_rows<T, 2, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 4) lb2_rows<T, 4, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 8) lb2_rows<T, 8, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 16) lb2_rows<T, 16, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else lb2_rows<T, 32, XIN>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            if (per_lane <= 1) lb2_rows<T, 1, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 2) lb2_rows<T, 2, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 4) lb2_rows<T, 4, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 8) lb2_rows<T, 8, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else if (per_lane <= 16) lb2_rows<T, 16, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+            else lb2_rows<T, 32, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
         }
         __syncthreads();
         const int nlong = s_nlong;
@@ -880,7 +883,9 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int64_t ntiles = ceil_div(n + nnz, tile);
     if (mode == 2) {
-        auto k2 = xin ? csr_lb2_kernel<T, true> : csr_lb2_kernel<T, false>;
+        // fp64: one entry per step (27-pt 0.686 vs 0.653, 7-pt 0.848 vs 0.804); fp32: 4 (0.620 vs 0.571)
+        auto k2 = tuning("lb2_unroll", sizeof(T) == 8 ? 1 : 4) == 4 ? (xin ? csr_lb2_kernel<T, true, true> : csr_lb2_kernel<T, false, true>)
+                                                : (xin ? csr_lb2_kernel<T, true, false> : csr_lb2_kernel<T, false, false>);
         const unsigned g2 = (unsigned)std::min<int64_t>(ntiles, (int64_t)kNumSMs * tuning("lb2_per_sm", 1 << 20));  // one CTA per tile measured best (0.66 vs 0.51 persistent)
         k2<<<g2, LB_BLOCK, 0, st>>>(n, ntiles, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row,
                                     carry_val);

@@ -1,4 +1,3 @@
-timeout 300 python -m pytest tests/test_spmv_gpu.py -q -x -k "coo or hybrid" > gpurun_out/t_coo.log 2>&1
-timeout 200 python tools/knob_sweep.py --format coo,hybrid --knobs "coo_minb=1,6" > gpurun_out/knobs18.txt 2>&1
-timeout 200 python tools/knob_sweep.py --dtype float32 --format coo --knobs "coo_minb=1,6" >> gpurun_out/knobs18.txt 2>&1
-timeout 200 python tools/knob_sweep.py --matrix powerlaw --format coo,hybrid >> gpurun_out/knobs18.txt 2>&1
+timeout 200 python tools/knob_sweep.py --format csr_lb --knobs "lb2_unroll=4,1 lb_tile=16384,32768,65536" > gpurun_out/knobs19.txt 2>&1
+timeout 200 python tools/knob_sweep.py --dtype float32 --format csr_lb --knobs "lb2_unroll=4,1 lb_tile=16384,65536" >> gpurun_out/knobs19.txt 2>&1
+timeout 300 python tools/knob_sweep.py --matrix 7pt --grid 256 --format csr_lb --knobs "lb2_unroll=4,1 lb_tile=16384,65536" >> gpurun_out/knobs19.txt 2>&1
