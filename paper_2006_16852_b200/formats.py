@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import copy
 import math
+import threading
 
 import numpy as np
 
@@ -383,6 +384,9 @@ class _Sparse(LinOp):
 CSR_STRATEGIES = ("classical", "load_balance", "stream", "automatic")
 
 
+_PIPELINE_LOCK = threading.Lock()
+
+
 def assemble_device(exc, data, vt):
     """MatrixData -> canonical (row, col)-sorted int32 rows / cols and values
     on the device (csrc/assemble.cu): the reference's canonicalize
@@ -679,7 +683,8 @@ class Csr(_Sparse):
         self._check_usable()
         self._check_conformal(b, x)
         self._log(EventKind.LINOP_APPLY_STARTED, {"op": type(self).__name__, "uid": self.uid})
-        self._pipelined_apply(b, x)
+        with _PIPELINE_LOCK:  # the plan's device buffers / graphs are shared
+            self._pipelined_apply(b, x)
         self._log(EventKind.LINOP_APPLY_COMPLETED, {"op": type(self).__name__, "uid": self.uid})
 
     def _pipeline_ok(self, b, x):

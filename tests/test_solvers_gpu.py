@@ -373,3 +373,31 @@ def test_jacobi_singular_block_raises(cuda):
     a = b2.matrix_from_data(cuda, data, "csr")
     with pytest.raises(b2.Singular):
         b2.Jacobi(cuda, block_size=2).generate(a)
+
+
+def test_concurrent_applies_of_one_solver(cuda):
+    """concurrent applies of one operator to disjoint outputs
+    are safe: two host threads share one generated CG."""
+    import threading
+
+    import paper_2006_16852_b200 as b2
+
+    n, r, c, v = P.stencil3d(16, "7pt")
+    a = system(b2, cuda, n, r, c, v)
+    s = b2.Cg(cuda, criteria=[b2.Iteration(1000), b2.ResidualNormReduction(1e-10)]).generate(a)
+    rhs = [np.random.default_rng(k).standard_normal((n, 1)) for k in range(4)]
+    out = [None] * 4
+
+    def work(k):
+        x = b2.Dense.zeros(cuda, n, 1)
+        s.apply(b2.Dense(cuda, rhs[k]), x)
+        out[k] = np.asarray(x.data)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    m = csr_host(n, r, c, v)
+    for k in range(4):
+        assert true_rel_residual(m, out[k][:, 0], rhs[k][:, 0]) <= 1e-9
