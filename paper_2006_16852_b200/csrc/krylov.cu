@@ -212,29 +212,41 @@ __global__ void cg_finish_kernel(KrylovCtl* c, double* hist, int phase) {
 // kernels above (Csr rows summed left to right per thread).
 // ===========================================================================
 template <int NV>
-__device__ __forceinline__ void coop_block_partials(double (&v)[NV], double* part, double* sh) {
+__device__ __forceinline__ void coop_block_partials(double (&v)[NV], double* part, double* sh, double* sh_tot) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
         const double s = block_sum(v[k], sh);
-        if (threadIdx.x == 0) part[k * KRY_MAX_GRID + blockIdx.x] = s;
+        if (threadIdx.x == 0) {
+            if (gridDim.x == 1) sh_tot[k] = s;  // one block: the total stays on chip
+            else part[k * KRY_MAX_GRID + blockIdx.x] = s;
+        }
     }
 }
 template <int NV>
 __device__ __forceinline__ void coop_totals(const double* part, double (&tot)[NV], double* sh_tot) {
     // warp 0 sums the partials in block order; broadcast through smem
-    if (threadIdx.x < 32) {
+    if (gridDim.x > 1) {
+        if (threadIdx.x < 32) {
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            double s = 0;
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile double*)part)[k * KRY_MAX_GRID + b];
-            s = warp_sum(s);
-            if (threadIdx.x == 0) sh_tot[k] = s;
+            for (int k = 0; k < NV; ++k) {
+                double s = 0;
+                for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile double*)part)[k * KRY_MAX_GRID + b];
+                s = warp_sum(s);
+                if (threadIdx.x == 0) sh_tot[k] = s;
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; ++k) tot[k] = sh_tot[k];
     __syncthreads();
+}
+
+// grid-wide barrier; a one-block grid (tiny systems) only needs the block
+// barrier (cooperative grid.sync costs microseconds even then)
+__device__ __forceinline__ void coop_sync(cooperative_groups::grid_group& grid) {
+    if (gridDim.x == 1) __syncthreads();
+    else grid.sync();
 }
 
 template <typename T>
@@ -255,7 +267,7 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
     while (!done) {
         const T tb = (T)beta;
         for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + tb * p[i];
-        grid.sync();
+        coop_sync(grid);
         double sg = 0;
         for (int64_t i = gt; i < n; i += gs) {
             T s = 0;
@@ -264,8 +276,8 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
             sg += (double)p[i] * (double)s;
         }
         double v1[1] = {sg}, t1[1];
-        coop_block_partials<1>(v1, part, sh);
-        grid.sync();
+        coop_block_partials<1>(v1, part, sh, sh_tot);
+        coop_sync(grid);
         coop_totals<1>(part, t1, sh_tot);
         const double sigma = t1[0];
         if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
@@ -287,8 +299,8 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
             rr += (double)nr * (double)nr;
         }
         double v2[1] = {rr}, t2[1];
-        coop_block_partials<1>(v2, part + 2 * KRY_MAX_GRID, sh);
-        grid.sync();
+        coop_block_partials<1>(v2, part + 2 * KRY_MAX_GRID, sh, sh_tot);
+        coop_sync(grid);
         coop_totals<1>(part + 2 * KRY_MAX_GRID, t2, sh_tot);
         const double rho_prev = rho;
         rho = t2[0];

@@ -137,3 +137,45 @@ def choose_format(a, candidates=("csr", "csr_lb", "ell", "sellp", "hybrid", "coo
     res = (best, convert(csr, best), times)
     a._auto_format = res
     return res
+
+
+OVERHEAD_SCHEMA = "opalg-bench/overhead/v1"
+OVERHEAD_SOLVERS = ("bicgstab", "cg", "cgs", "fcg", "gmres")
+
+
+def run_overhead(solvers=OVERHEAD_SOLVERS, iters=1000, runs=20, krylov_dim=100, executor=None):
+    """The paper's framework-overhead microbenchmark (PAPER.md:1789-1816;
+    reference src/bench.py:253-291): time per iteration of each solver on a
+    1x1 Coo system with b = NaN and only an Iteration criterion, so every
+    control branch runs with negligible kernel work. Wall clock around the
+    public apply (device-resident solvers: the device loop and its host
+    batch synchronisations included)."""
+    import time
+
+    from .executor import CudaExecutor
+    from .formats import Coo
+    from .solvers import SOLVER_FACTORIES
+    from .stop import Iteration
+
+    exc = executor or CudaExecutor()
+    results = {}
+    for name in solvers:
+        kw = {"krylov_dim": krylov_dim} if name == "gmres" else {}
+        a = Coo(exc, (1, 1), [0], [0], [1.0])
+        solver = SOLVER_FACTORIES[name](exc, criteria=[Iteration(iters)], **kw).generate(a)
+        per_run = []
+        for r in range(runs + 1):
+            b = Dense(exc, [[float("nan")]])
+            x = Dense.zeros(exc, 1, 1)
+            t0 = time.perf_counter_ns()
+            solver.apply(b, x)
+            dt = (time.perf_counter_ns() - t0) / iters
+            if solver.last_status.iterations != iters:
+                raise OpalgError(f"{name}: expected {iters} iterations, got {solver.last_status.iterations}")
+            if r:  # the first run captures the CUDA graphs
+                per_run.append(dt)
+        results[name] = {"iterations": iters, "runs": runs,
+                         "time_per_iteration_us": float(np.mean(per_run)) / 1000.0}
+    times = [v["time_per_iteration_us"] for v in results.values()]
+    return {"schema": OVERHEAD_SCHEMA, "solvers": results,
+            "max_over_min": float(max(times) / min(times)) if times else None}

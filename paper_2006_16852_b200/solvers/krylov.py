@@ -72,10 +72,22 @@ class CgSolver(IterativeSolver):
     """Preconditioned conjugate gradients (SPD systems)."""
 
     def _coop_ok(self, J, S):
-        from ..formats import Csr
+        from ..formats import _Sparse
 
         return (config.CG_COOP_MAX_ROWS > 0 and self.size.rows <= config.CG_COOP_MAX_ROWS and J[0] == 0
-                and isinstance(self.a, Csr) and S.time_child is None)
+                and isinstance(self.a, _Sparse) and S.time_child is None)
+
+    def _coop_csr(self):
+        """The system as Csr for the cooperative kernel (other sparse formats
+        are converted once; their row sums run in the same entry order)."""
+        from ..formats import Csr, convert
+
+        if isinstance(self.a, Csr):
+            return self.a
+        c = getattr(self, "_coop_csr_cache", None)
+        if c is None:
+            c = self._coop_csr_cache = convert(self.a, "csr")
+        return c
 
     def _apply_impl(self, b, x):
         if not device_path_ok(self, b):
@@ -94,7 +106,7 @@ class CgSolver(IterativeSolver):
 
         if self._coop_ok(J, S):
             # small system: the whole solve is one persistent cooperative launch
-            a = self.a
+            a = self._coop_csr()
             _lib.call("cg_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(p), ptr(q),
                       S.c, S.p, S.h, exc.stream)
             return finish_from_device(self, S, S.status(), x)
