@@ -588,8 +588,14 @@ static int csr_pipe(int64_t n, const int* rp, const int* ci, const T* v, const T
 // fix-up pass. Work per CTA is bounded regardless of row-length skew.
 // ===========================================================================
 constexpr int LB_BLOCK = 256;
-template <typename T> struct LbIpt { static constexpr int v = 7; };
-template <> struct LbIpt<float> { static constexpr int v = 9; };
+#ifndef LB_IPT_F64
+#define LB_IPT_F64 7
+#endif
+#ifndef LB_IPT_F32
+#define LB_IPT_F32 9
+#endif
+template <typename T> struct LbIpt { static constexpr int v = LB_IPT_F64; };
+template <> struct LbIpt<float> { static constexpr int v = LB_IPT_F32; };
 
 // merge items (rows + nonzeros) per tile: mode 1 (item merge) is fixed by
 // its shared-memory staging arrays; mode 2 (row-parallel) takes 16384
