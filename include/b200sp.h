@@ -306,6 +306,8 @@ int b200sp_gmres_after_commit(void* ctl, void* stream);
                              double* hist, void* stream);                                                          \
     int b200sp_cg_step1_##SUF(int64_t n, T* p, const T* z, const void* ctl, void* stream);                         \
     int b200sp_cg_sigma_##SUF(int64_t n, const T* p, const T* q, void* ctl, double* part, void* stream);            \
+    int b200sp_fcg_step2_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* p, const T* q, T* t, T* z,              \
+                               B200SP_JAC_DECL, void* ctl, double* part, double* hist, void* stream);             \
     int b200sp_cg_step2_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* p, const T* q, T* z, B200SP_JAC_DECL,     \
                               void* ctl, double* part, double* hist, void* stream);                                \
     int b200sp_bicgstab_init_##SUF(int64_t n, const T* b, int64_t bs, const T* r, T* rt, T* p, T* v, T* s, T* t,    \
@@ -413,6 +415,10 @@ int b200sp_mm_parse(const char* buf, int64_t len, const int64_t* info, int32_t t
 int b200sp_krylov_set_dist(void* ctl, int32_t dist, void* stream);
 int64_t b200sp_krylov_red_offset(void);
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream);
+/* FCG (src/solvers/krylov.py:80-125) reuses cg_init / cg_step1 / the fused
+ * SpMV + sigma; fcg_init_ctl seeds rho_t = 0 after cg_init, fcg_step2 also
+ * forms t = r_new - r_old and reduces (r.z, t.z, r.r). */
+int b200sp_fcg_init_ctl(void* ctl, void* stream);
 int b200sp_flag_out_of_range(int64_t nnz, const int32_t* ci, int64_t lo, int64_t hi, int32_t* flag, void* stream);
 int b200sp_compact_cols(int64_t nnz, const int32_t* ci, const int32_t* flag, const int32_t* pos, int32_t* out,
                         void* stream);

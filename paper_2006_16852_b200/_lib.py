@@ -63,6 +63,7 @@ _TYPED = {
     "cg_coop": "lppppppppppp",
     "csr_spmv_dot": "lppppppiippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
+    "fcg_step2": "lplppppp" + "lpppp" + "pppp",
     "bicgstab_init": "lplpppppppppppp",
     "bicgstab_step1": "lpppp" + "lpppp" + "pp",
     "bicgstab_gamma": "lppppp",
@@ -117,6 +118,7 @@ _UNTYPED = {
     "assemble_workspace_bytes": ("l", ctypes.c_int64),
     "ilu_counts": ("lpppppp", ctypes.c_int),
     "csr_rows": ("lppp", ctypes.c_int),
+    "fcg_init_ctl": ("pp", ctypes.c_int),
     "mm_header": ("plpp", ctypes.c_int),
     "mm_count": ("plpip", ctypes.c_int),
     "mm_parse": ("plpippplpp", ctypes.c_int),

@@ -192,6 +192,65 @@ cg_step2_kernel(RowBlocks rb, T* __restrict__ x, int64_t xs, T* __restrict__ r, 
     cg_step2_ctl(c, tot, hist);
 }
 
+// ===========================================================================
+// FCG (src/solvers/krylov.py:80-125; FcgStep1 = CgStep1 with beta =
+// rho_t / prev_rho, FcgStep2 steps.py:167-199). Step 1 and the fused SpMV +
+// sigma are CG's; step 2 also forms t = r_new - r_old and reduces
+// (r.z, t.z, r.r) for rho, rho_t and the criterion.
+// ===========================================================================
+__global__ void fcg_init_ctl_kernel(KrylovCtl* c) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {  // fcg_init: prev_rho = 1, rho_t = 0
+        c->rho_t = 0.0;
+        c->beta = safe_div(0.0, c->rho_prev);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+fcg_step2_kernel(RowBlocks rb, T* __restrict__ x, int64_t xs, T* __restrict__ r, const T* __restrict__ p,
+                 const T* __restrict__ q, T* __restrict__ t, T* __restrict__ z, KrylovCtl* c, double* part,
+                 double* hist) {
+    if (c->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T alpha = (T)c->alpha;
+    double rz = 0, tz = 0, rr = 0;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T rv = T(0), tv = T(0);
+        if (lane < bs) {
+            const int64_t i = r0 + lane;
+            x[i * xs] = x[i * xs] + mul_rn(alpha, p[i]);
+            const T ro = r[i];
+            rv = ro - mul_rn(alpha, q[i]);
+            tv = rv - ro;
+            t[i] = tv;
+            r[i] = rv;
+        }
+        T zv = rv;
+        if (rb.J.nblocks) {
+            zv = jacobi_row<T>(rb.J, b, bs, lane, rv);
+            if (lane < bs) z[r0 + lane] = zv;
+        }
+        rz += (double)rv * (double)zv;
+        tz += (double)tv * (double)zv;
+        rr += (double)rv * (double)rv;
+    }
+    double v[3] = {rz, tz, rr}, tot[3];
+    if (!grid_reduce<3>(v, part, &c->ticket[2], tot)) return;
+    c->rho_prev = c->rho;
+    c->rho = tot[0];
+    c->rho_t = tot[1];
+    c->it += 1;
+    c->rnorm = sqrt(tot[2]);
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+    c->done = c->stopped;
+    c->beta = safe_div(c->rho_t, c->rho_prev);
+}
+
 // distributed solves: the control step after red[] has been all-reduced
 // (phase 0 = init, 1 = sigma, 2 = step2)
 __global__ void cg_finish_kernel(KrylovCtl* c, double* hist, int phase) {
@@ -962,6 +1021,11 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
     int b200sp_cg_sigma_##SUF(int64_t n, const T* p, const T* q, void* ctl, double* part, void* stream) {          \
         KRY_LAUNCH(cg_sigma_kernel<T>, n, KRY_BLOCK, n, p, q, (KrylovCtl*)ctl, part);                             \
     }                                                                                                             \
+    int b200sp_fcg_step2_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* p, const T* q, T* t, T* z, JAC_ARGS,    \
+                               void* ctl, double* part, double* hist, void* stream) {                             \
+        KRY_LAUNCH(fcg_step2_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), x, xs, r, p, q, t, z, (KrylovCtl*)ctl, part, \
+                   hist);                                                                                         \
+    }                                                                                                             \
     int b200sp_cg_step2_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* p, const T* q, T* z, JAC_ARGS,           \
                               void* ctl, double* part, double* hist, void* stream) {                              \
         KRY_LAUNCH(cg_step2_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), x, xs, r, p, q, z, (KrylovCtl*)ctl, part,   \
@@ -1070,6 +1134,12 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* rp, const int32_t* ci, con
                             float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
                             void* stream) {
     return csr_spmv_dot<float>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
+}
+
+int b200sp_fcg_init_ctl(void* ctl, void* stream) {
+    fcg_init_ctl_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl);
+    count_launch();
+    return check_launch("fcg_init_ctl");
 }
 
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream) {

@@ -49,6 +49,7 @@ struct KrylovCtl {
     int dist;          // distributed solve: epilogues park local sums in red[]
     int pad2;
     double red[4];     // local reduction results, all-reduced across ranks in place
+    double rho_t;      // FCG: t.z with t = r_new - r_old (src/solvers/krylov.py:80-125)
 };
 
 // ---------------------------------------------------------------------------

@@ -170,11 +170,41 @@ class BicgstabSolver(IterativeSolver):
 
 
 class FcgSolver(IterativeSolver):
-    """Flexible CG (src/solvers/krylov.py:80-125): host-controlled loop over
-    device kernels (generic.fcg)."""
+    """Flexible CG (src/solvers/krylov.py:80-125). Device-resident like CG:
+    cg_init + fcg_init_ctl, then batches of cg_step1 -> SpMV + sigma ->
+    fcg_step2 (t = r_new - r_old, rho = r.z, rho_t = t.z, ||r||, check);
+    the host-controlled loop (generic.fcg) otherwise."""
 
     def _apply_impl(self, b, x):
-        return generic.fcg(self, b, x)
+        if not device_path_ok(self, b):
+            return generic.fcg(self, b, x)
+        n = self.size.rows
+        S = get_state(self, n, x.values.dtype)
+        suf = _lib.suffix(S.dtype)
+        exc = self.exec
+        J = jac_args(self)
+        r, p, q, t = S.vec("r"), S.vec("p"), S.vec("q"), S.vec("t")
+        z = r if J[0] == 0 else S.vec("z")
+        rd, pd, qd, td = S.dense(r), S.dense(p), S.dense(q), S.dense(t)
+        S.begin(b, x)
+        self._residual(S.xd, S.bd, rd)
+        td.fill(0.0)
+        _lib.call("cg_init_" + suf, n, ptr(r), ptr(z), ptr(p), *J, S.c, S.p, S.h, exc.stream)
+        _lib.call("fcg_init_ctl", S.c, exc.stream)
+        fa = fused_csr(self)
+
+        def body():
+            _lib.call("cg_step1_" + suf, n, ptr(p), ptr(z), S.c, exc.stream)
+            if fa is not None:
+                spmv_dot(S, fa, suf, p, q, None, 1)
+            else:
+                self.a.apply(pd, qd)
+                _lib.call("cg_sigma_" + suf, n, ptr(p), ptr(q), S.c, S.p, exc.stream)
+            _lib.call("fcg_step2_" + suf, n, ptr(S.x), 1, ptr(r), ptr(p), ptr(q), ptr(t), ptr(z), *J, S.c, S.p,
+                      S.h, exc.stream)
+
+        st = S.run(body, batch_size())
+        finish_from_device(self, S, st, x)
 
 
 class CgsSolver(IterativeSolver):
