@@ -320,6 +320,12 @@ int b200sp_gmres_after_commit(void* ctl, void* stream);
     int b200sp_bicgstab_tst_##SUF(int64_t n, const T* t, const T* s, void* ctl, double* part, void* stream);        \
     int b200sp_bicgstab_step3_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* s, const T* t, const T* y,         \
                                     const T* z, const T* rt, void* ctl, double* part, double* hist, void* stream); \
+    int b200sp_cgs_step1_##SUF(int64_t n, const T* r, const T* q, T* u, T* p, T* ph, B200SP_JAC_DECL,             \
+                               const void* ctl, void* stream);                                                     \
+    int b200sp_cgs_step2_##SUF(int64_t n, const T* u, const T* vh, T* q, T* w, T* uh, B200SP_JAC_DECL,            \
+                               const void* ctl, void* stream);                                                     \
+    int b200sp_cgs_step3_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* t, const T* uh, const T* rt, void* ctl, \
+                               double* part, double* hist, void* stream);                                          \
     int b200sp_gmres_reset_##SUF(int64_t n, const T* r, void* ctl, double* part, double* gm, double* hist,          \
                                  int32_t first, void* stream);                                                     \
     int b200sp_gmres_scale_v0_##SUF(int64_t n, const T* r, T* V, const void* ctl, void* stream);                   \
@@ -419,6 +425,9 @@ int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream);
  * SpMV + sigma; fcg_init_ctl seeds rho_t = 0 after cg_init, fcg_step2 also
  * forms t = r_new - r_old and reduces (r.z, t.z, r.r). */
 int b200sp_fcg_init_ctl(void* ctl, void* stream);
+/* CGS (src/solvers/krylov.py:128-187) reuses bicgstab_init and the gamma
+ * SpMV epilogue; cgs_mid is the mid-cycle check on the unchanged ||r||. */
+int b200sp_cgs_mid(void* ctl, double* hist, void* stream);
 int b200sp_flag_out_of_range(int64_t nnz, const int32_t* ci, int64_t lo, int64_t hi, int32_t* flag, void* stream);
 int b200sp_compact_cols(int64_t nnz, const int32_t* ci, const int32_t* flag, const int32_t* pos, int32_t* out,
                         void* stream);

@@ -64,6 +64,9 @@ _TYPED = {
     "csr_spmv_dot": "lppppppiippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
     "fcg_step2": "lplppppp" + "lpppp" + "pppp",
+    "cgs_step1": "lppppp" + "lpppp" + "pp",
+    "cgs_step2": "lppppp" + "lpppp" + "pp",
+    "cgs_step3": "lplpppppppp",
     "bicgstab_init": "lplpppppppppppp",
     "bicgstab_step1": "lpppp" + "lpppp" + "pp",
     "bicgstab_gamma": "lppppp",
@@ -119,6 +122,7 @@ _UNTYPED = {
     "ilu_counts": ("lpppppp", ctypes.c_int),
     "csr_rows": ("lppp", ctypes.c_int),
     "fcg_init_ctl": ("pp", ctypes.c_int),
+    "cgs_mid": ("ppp", ctypes.c_int),
     "mm_header": ("plpp", ctypes.c_int),
     "mm_count": ("plpip", ctypes.c_int),
     "mm_parse": ("plpippplpp", ctypes.c_int),

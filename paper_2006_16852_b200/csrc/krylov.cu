@@ -601,6 +601,118 @@ bicg_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, c
 }
 
 // ===========================================================================
+// CGS (src/solvers/krylov.py:128-187; steps.py:246-345). Initialisation is
+// BiCGSTAB's (rt = b, workspace zeroed, rho = rt.r, beta = rho / 1); the
+// first SpMV carries gamma = rt.v_hat (BiCGSTAB's gamma control: breakdown,
+// alpha = rho / gamma); the mid check sees the unchanged ||r||; step 3 ends
+// in the top-of-loop check followed by the next rho = rt.r.
+// ===========================================================================
+__device__ inline void cgs_cycle_start(KrylovCtl* c, double rho_new, double rr) {
+    if (c->done) return;
+    if (rho_new == 0.0 && rr != 0.0) {  // krylov.py:155-158
+        c->breakdown = BD_RHO;
+        c->breakdown_it = c->it + 1;
+        c->done = 1;
+        return;
+    }
+    c->rho = rho_new;
+    c->beta = safe_div(c->rho, c->rho_prev);
+}
+
+// u = r + beta q; p = u + beta (q + beta p); ph = M p      (CgsStep1)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cgs_step1_kernel(RowBlocks rb, const T* __restrict__ r, const T* __restrict__ q, T* __restrict__ u, T* __restrict__ p,
+                 T* __restrict__ ph, const KrylovCtl* c) {
+    if (c->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T beta = (T)c->beta;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T pv = T(0);
+        if (lane < bs) {
+            const int64_t i = r0 + lane;
+            const T qv = q[i];
+            const T uv = r[i] + mul_rn(beta, qv);
+            u[i] = uv;
+            pv = uv + mul_rn(beta, qv + mul_rn(beta, p[i]));
+            p[i] = pv;
+        }
+        if (rb.J.nblocks) {
+            const T yv = jacobi_row<T>(rb.J, b, bs, lane, pv);
+            if (lane < bs) ph[r0 + lane] = yv;
+        }
+    }
+}
+
+// q = u - alpha v_hat; w = u + q; uh = M w      (CgsStep2)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cgs_step2_kernel(RowBlocks rb, const T* __restrict__ u, const T* __restrict__ vh, T* __restrict__ q, T* __restrict__ w,
+                 T* __restrict__ uh, const KrylovCtl* c) {
+    if (c->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T alpha = (T)c->alpha;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < rb.count(); b += nw) {
+        int64_t r0;
+        int bs;
+        rb.range(b, r0, bs);
+        T wv = T(0);
+        if (lane < bs) {
+            const int64_t i = r0 + lane;
+            const T uv = u[i];
+            const T qv = uv - mul_rn(alpha, vh[i]);
+            q[i] = qv;
+            wv = uv + qv;
+            w[i] = wv;
+        }
+        if (rb.J.nblocks) {
+            const T yv = jacobi_row<T>(rb.J, b, bs, lane, wv);
+            if (lane < bs) uh[r0 + lane] = yv;
+        }
+    }
+}
+
+// mid check: it++, criteria on the unchanged ||r|| (krylov.py:171-176)
+__global__ void cgs_mid_kernel(KrylovCtl* c, double* hist) {
+    if (threadIdx.x != 0 || blockIdx.x != 0 || c->done) return;
+    c->it += 1;
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+    c->done = c->stopped;
+}
+
+// r -= alpha t; x += alpha uh; it++; top check; next rho = rt.r  (CgsStep3)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cgs_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, const T* __restrict__ t,
+                 const T* __restrict__ uh, const T* __restrict__ rt, KrylovCtl* c, double* part, double* hist) {
+    if (c->done) return;
+    const T alpha = (T)c->alpha;
+    double rr = 0, rtr = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T rv = r[i] - mul_rn(alpha, t[i]);
+        r[i] = rv;
+        x[i * xs] = x[i * xs] + mul_rn(alpha, uh[i]);
+        rr += (double)rv * (double)rv;
+        rtr += (double)rt[i] * (double)rv;
+    }
+    double vv[2] = {rr, rtr}, tot[2];
+    if (!grid_reduce<2>(vv, part, &c->ticket[2], tot)) return;
+    c->rho_prev = c->rho;
+    c->it += 1;
+    c->rnorm = sqrt(tot[0]);
+    hist_put(c, hist, c->it, c->rnorm);
+    crit_check(c, c->it, c->rnorm);
+    c->done = c->stopped;
+    cgs_cycle_start(c, tot[1], tot[0]);
+}
+
+// ===========================================================================
 // GMRES(k), right preconditioned, m = 1.
 // gm layout: H[(k+1) x k] row-major | cs[k] | sn[k] | gamma[k+1] | y[k]
 // ===========================================================================
@@ -1055,6 +1167,18 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
                                     void* stream) {                                                               \
         KRY_LAUNCH(bicg_step3_kernel<T>, n, KRY_BLOCK, n, x, xs, r, s, t, y, z, rt, (KrylovCtl*)ctl, part, hist); \
     }                                                                                                             \
+    int b200sp_cgs_step1_##SUF(int64_t n, const T* r, const T* q, T* u, T* p, T* ph, JAC_ARGS, const void* ctl,   \
+                               void* stream) {                                                                    \
+        KRY_LAUNCH(cgs_step1_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), r, q, u, p, ph, (const KrylovCtl*)ctl);     \
+    }                                                                                                             \
+    int b200sp_cgs_step2_##SUF(int64_t n, const T* u, const T* vh, T* q, T* w, T* uh, JAC_ARGS, const void* ctl,  \
+                               void* stream) {                                                                    \
+        KRY_LAUNCH(cgs_step2_kernel<T>, RB_UNITS(n), KRY_BLOCK, RB(n), u, vh, q, w, uh, (const KrylovCtl*)ctl);    \
+    }                                                                                                             \
+    int b200sp_cgs_step3_##SUF(int64_t n, T* x, int64_t xs, T* r, const T* t, const T* uh, const T* rt, void* ctl, \
+                               double* part, double* hist, void* stream) {                                        \
+        KRY_LAUNCH(cgs_step3_kernel<T>, n, KRY_BLOCK, n, x, xs, r, t, uh, rt, (KrylovCtl*)ctl, part, hist);        \
+    }                                                                                                             \
     int b200sp_gmres_reset_##SUF(int64_t n, const T* r, void* ctl, double* part, double* gm, double* hist,        \
                                  int32_t first, void* stream) {                                                   \
         KRY_LAUNCH(gmres_reset_kernel<T>, n, KRY_BLOCK, n, r, (KrylovCtl*)ctl, part, gm, hist, first);            \
@@ -1134,6 +1258,12 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* rp, const int32_t* ci, con
                             float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
                             void* stream) {
     return csr_spmv_dot<float>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
+}
+
+int b200sp_cgs_mid(void* ctl, double* hist, void* stream) {
+    cgs_mid_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl, hist);
+    count_launch();
+    return check_launch("cgs_mid");
 }
 
 int b200sp_fcg_init_ctl(void* ctl, void* stream) {

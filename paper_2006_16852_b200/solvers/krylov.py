@@ -208,11 +208,47 @@ class FcgSolver(IterativeSolver):
 
 
 class CgsSolver(IterativeSolver):
-    """Conjugate gradient squared (src/solvers/krylov.py:128-187):
-    host-controlled loop over device kernels (generic.cgs)."""
+    """Conjugate gradient squared (src/solvers/krylov.py:128-187), two
+    SpMVs per cycle and a check after each half. Device-resident: BiCGSTAB's
+    init, cgs_step1 (u, p, ph = M p) -> SpMV + gamma -> cgs_step2 (q, w,
+    uh = M w) -> mid check -> SpMV -> cgs_step3 (r, x, ||r||, next rho);
+    the host-controlled loop (generic.cgs) otherwise."""
 
     def _apply_impl(self, b, x):
-        return generic.cgs(self, b, x)
+        if not device_path_ok(self, b):
+            return generic.cgs(self, b, x)
+        n = self.size.rows
+        S = get_state(self, n, x.values.dtype)
+        suf = _lib.suffix(S.dtype)
+        exc = self.exec
+        J = jac_args(self)
+        r, rt, p, q, u, vh, t = (S.vec(k) for k in ("r", "rt", "p", "q", "u", "vh", "t"))
+        w = S.vec("w")
+        ph = p if J[0] == 0 else S.vec("ph")
+        uh = w if J[0] == 0 else S.vec("uh")
+        rd, phd, vhd, uhd, td = S.dense(r), S.dense(ph), S.dense(vh), S.dense(uh), S.dense(t)
+        S.begin(b, x)
+        self._residual(S.xd, S.bd, rd)
+        # rt = b, p q u uh vh t = 0, baseline / check(0), rho = rt.r, beta
+        _lib.call("bicgstab_init_" + suf, n, ptr(S.b), 1, ptr(r), ptr(rt), ptr(p), ptr(q), ptr(u), ptr(t),
+                  ptr(uh), ptr(vh), S.c, S.p, S.h, exc.stream)
+        fa = fused_csr(self)
+
+        def body():
+            _lib.call("cgs_step1_" + suf, n, ptr(r), ptr(q), ptr(u), ptr(p), ptr(ph), *J, S.c, exc.stream)
+            if fa is not None:  # v_hat = A ph with gamma = rt.v_hat fused
+                spmv_dot(S, fa, suf, ph, vh, rt, 2)
+            else:
+                self.a.apply(phd, vhd)
+                _lib.call("bicgstab_gamma_" + suf, n, ptr(rt), ptr(vh), S.c, S.p, exc.stream)
+            _lib.call("cgs_step2_" + suf, n, ptr(u), ptr(vh), ptr(q), ptr(w), ptr(uh), *J, S.c, exc.stream)
+            _lib.call("cgs_mid", S.c, S.h, exc.stream)
+            self.a.apply(uhd, td)
+            _lib.call("cgs_step3_" + suf, n, ptr(S.x), 1, ptr(r), ptr(t), ptr(uh), ptr(rt), S.c, S.p, S.h,
+                      exc.stream)
+
+        st = S.run(body, max(1, batch_size() // 2))
+        finish_from_device(self, S, st, x)
 
 
 class Cg(IterativeSolverFactory):
