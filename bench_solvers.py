@@ -195,7 +195,28 @@ def bench_c5_distributed(args, world, rank, local):
             "gpu_launches": None, "clocks": clk.summary()}
 
 
+PAPER_OVERHEAD_V100_US = {"bicgstab": 1.26, "cg": 1.28, "cgs": 1.00, "fcg": 1.45, "gmres": 1.51}
+
+
+def bench_overhead(args, world, rank, local):
+    """The paper's framework-overhead microbenchmark: us per iteration on a 1x1
+    Coo system with b = NaN and Iteration(1000) (reference src/bench.py:253-291)."""
+    from paper_2006_16852_b200 import CudaExecutor
+    from paper_2006_16852_b200.profile import run_overhead
+
+    res = run_overhead(iters=1000, runs=max(3, min(args.steps, 20)), executor=CudaExecutor(local))
+    per = {k: round(v["time_per_iteration_us"], 3) for k, v in res["solvers"].items()}
+    return {"metric": "framework overhead per iteration (1x1 system, b = NaN)", "value": per["cg"],
+            "unit": "us/iter", "n_gpus": 1, "steps": args.steps, "warmup": 1, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "1x1 Coo [[1.0]], b = NaN",
+            "config": {"workload": "PAPER.md:1789-1816 overhead benchmark", "solvers_us_per_iter": per,
+                       "paper_v100_us_per_iter": PAPER_OVERHEAD_V100_US},
+            "gpu_launches": None}
+
+
 def bench_workload(args, world, rank, local):
+    if args.workload == "overhead":
+        return bench_overhead(args, world, rank, local)
     if args.workload == "c3":
         return bench_c3(args, world, rank, local)
     if args.workload == "c5" and world > 1:
