@@ -14,6 +14,8 @@ b / x (H2D of b and x0, D2H of x inside the timed region).
 
 from __future__ import annotations
 
+import os
+
 import statistics
 import time
 
@@ -220,5 +222,15 @@ def bench_workload(args, world, rank, local):
     if args.workload == "c3":
         return bench_c3(args, world, rank, local)
     if args.workload == "c5" and world > 1:
+        return bench_c5_distributed(args, world, rank, local)
+    if args.workload == "c5d":  # the distributed solver, also at one rank (NCCL world of 1)
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
         return bench_c5_distributed(args, world, rank, local)
     return bench_solver(args, world, rank, local, args.workload)
