@@ -401,3 +401,89 @@ def test_concurrent_applies_of_one_solver(cuda):
     m = csr_host(n, r, c, v)
     for k in range(4):
         assert true_rel_residual(m, out[k][:, 0], rhs[k][:, 0]) <= 1e-9
+
+
+class _ResidualAgreement:
+    """Recurrence vs true residual norms at consistent checks (the
+    reference's tests/test_solvers.py:251-279 probe)."""
+
+    def __init__(self, dense, b, even_only=False):
+        self.dense, self.b, self.even_only = dense, b, even_only
+        self.rows = []
+
+    def check(self, stopping_id, set_finalized, status, updater):
+        if self.even_only and updater.num_iterations % 2 == 1:
+            return False, False
+        true_r = None
+        if updater.solution is not None:
+            true_r = np.linalg.norm(self.b - self.dense @ np.asarray(updater.solution.data)[:, 0])
+        if updater.residual is not None:
+            rec = float(np.linalg.norm(np.asarray(updater.residual.data)))
+        elif updater.residual_norm is not None:
+            rec = float(updater.residual_norm[0])
+        else:
+            return False, False
+        self.rows.append((rec, true_r))
+        return False, False
+
+
+def _probe_factory(b2, probe):
+    class ProbeCrit(b2.stop.Criterion):
+        def check(self, stopping_id, set_finalized, status, updater):
+            return probe.check(stopping_id, set_finalized, status, updater)
+
+    class ProbeFactory(b2.stop.CriterionFactory):
+        def generate(self, args):
+            return ProbeCrit()
+
+    return ProbeFactory()
+
+
+@pytest.mark.parametrize("name,tol", [("cg", 1e-6), ("fcg", 1e-6), ("cgs", 1e-6), ("bicgstab", 1e-6)])
+def test_recurrence_residual_tracks_true_residual(cuda, name, tol):
+    """Reference tests/test_solvers.py:282-306 (user-defined criterion: the
+    host-controlled loop over device kernels)."""
+    import paper_2006_16852_b200 as b2
+
+    data = random_spd(40, seed=12) if name in ("cg", "fcg") else random_sparse(40, density=0.2, seed=12)
+    dense = data.to_dense_array()
+    a = b2.matrix_from_data(cuda, data, "csr")
+    bv = np.random.default_rng(12).standard_normal(40)
+    b = b2.Dense.vector(cuda, bv)
+    x = b2.Dense.zeros(cuda, 40, 1)
+    probe = _ResidualAgreement(dense, bv.copy(), even_only=(name == "bicgstab"))
+    s = b2.SOLVER_FACTORIES[name](cuda, criteria=[b2.Iteration(25), _probe_factory(b2, probe)]).generate(a)
+    s.apply(b, x)
+    assert probe.rows
+    bn = np.linalg.norm(bv)
+    for rec, true_r in probe.rows:
+        if true_r is None or true_r <= 1e-8 * bn:
+            continue
+        assert abs(rec - true_r) <= tol * max(true_r, 1e-300)
+
+
+def test_gmres_rotation_residual_matches_true_residual(cuda):
+    """Reference tests/test_solvers.py:309-333: the Givens estimate equals the
+    true residual of the iterate committed at the stop."""
+    import paper_2006_16852_b200 as b2
+
+    data = random_sparse(40, density=0.2, seed=12)
+    dense = data.to_dense_array()
+    bv = np.random.default_rng(12).standard_normal(40)
+    for j in (1, 3, 7, 12, 20):
+        a = b2.matrix_from_data(cuda, data, "csr")
+        x = b2.Dense.zeros(cuda, 40, 1)
+        est = {}
+
+        class Probe:
+            def check(self, stopping_id, set_finalized, status, updater):
+                est[updater.num_iterations] = float(updater.residual_norm[0])
+                return False, False
+
+        s = b2.Gmres(cuda, criteria=[b2.Iteration(j), _probe_factory(b2, Probe())], krylov_dim=50).generate(a)
+        s.apply(b2.Dense.vector(cuda, bv), x)
+        true_r = np.linalg.norm(bv - dense @ np.asarray(x.data)[:, 0])
+        if true_r > 1e-10 * np.linalg.norm(bv):
+            # + 1e-14 ||b||: near 1e-8 ||b|| the evaluation of b - A x itself
+            # carries ~eps ||A|| ||x|| of rounding (j = 20 differs by 4.6e-16)
+            assert abs(est[j] - true_r) <= 1e-8 * true_r + 1e-14 * np.linalg.norm(bv), j
