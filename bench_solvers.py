@@ -160,6 +160,75 @@ def bench_c3(args, world, rank, local):
             "formats": res, "gpu_launches": 2}
 
 
+def _dist_breakdown(A, comm, solver, world, reps=30):
+    """Per-iteration pieces of the distributed CG, each timed alone with CUDA
+    events (max over ranks): the communication-free iteration (step1, owned
+    and ghost SpMV, sigma, step2 on a criterion-free control block), one halo
+    exchange, one 8-byte all-reduce. iteration - compute = the communication
+    the overlap does not hide."""
+    import ctypes
+
+    import torch
+
+    from paper_2006_16852_b200 import _lib
+    from paper_2006_16852_b200.executor import ptr
+
+    exc = A.exec
+    nl, dt = A.n_local, torch.float64
+    suf = "f64"
+    pext = torch.ones(A.n_ext, dtype=dt, device=exc.device)
+    p, q, r, x = pext[:nl], torch.zeros(nl, dtype=dt, device=exc.device), torch.ones(nl, dtype=dt, device=exc.device), \
+        torch.zeros(nl, dtype=dt, device=exc.device)
+    ctl = torch.zeros(int(_lib.query("krylov_ctl_bytes")), dtype=torch.uint8, device=exc.device)
+    part = torch.zeros(int(_lib.query("krylov_part_elems")), dtype=torch.float64, device=exc.device)
+    t0, p0 = (ctypes.c_int32 * 1)(), (ctypes.c_double * 1)()
+    _lib.call("krylov_ctl_init", ptr(ctl), 0, ctypes.addressof(t0), ctypes.addressof(p0), 1, 0, 0, exc.stream)
+    J = (0, 0, 0, 0, 0)
+
+    class _NoHalo:  # the same kernels as the solve, without the exchange
+        def __getattr__(self, k):
+            return getattr(A, k)
+
+        def start_halo(self, xext):
+            class _W:
+                def wait(self):
+                    pass
+            return _W()
+
+    view = solver.__class__.__new__(solver.__class__)
+    view.__dict__.update(solver.__dict__)
+    view.a = _NoHalo()
+
+    def compute():
+        _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), ptr(ctl), exc.stream)
+        view._spmv_sigma(pext, p, q, ptr(ctl), part, suf)
+        _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(r), *J, ptr(ctl), ptr(part), 0,
+                  exc.stream)
+
+    def halo():
+        A.start_halo(pext).wait()
+
+    red = torch.zeros(1, dtype=torch.float64, device=exc.device)
+
+    def allreduce():
+        comm.allreduce_(red)
+
+    out = {}
+    for name, fn in (("compute_ms", compute), ("halo_ms", halo), ("allreduce_ms", allreduce)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        out[name] = round(allmax(world, s.elapsed_time(e) / reps), 4)
+    return out
+
+
 def bench_c5_distributed(args, world, rank, local):
     """C5 row-partitioned CG over NCCL (torchrun, one rank per GPU): strong
     scaling of the fixed 512^3 problem; ms per iteration, max over ranks."""
@@ -186,6 +255,9 @@ def bench_c5_distributed(args, world, rank, local):
         times, st = _solve_timer(lambda: (x.zero_(), solver.solve(b, x))[1], args.steps)
     t = allmax(world, statistics.mean(times))
     its = st.iterations
+    brk = _dist_breakdown(A, comm, solver, world)
+    brk["iteration_ms"] = round(t / max(its, 1) * 1e3, 4)
+    brk["exposed_comm_ms"] = round(brk["iteration_ms"] - brk["compute_ms"], 4)
     return {"metric": METRIC, "value": round(t / max(its, 1) * 1e3, 4), "unit": "ms/iter", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -193,7 +265,7 @@ def bench_c5_distributed(args, world, rank, local):
             "config": {"workload": f"C5: row-partitioned CG, 3-D 7-point Poisson {g}^3, RNR 1e-8, "
                                    f"NCCL halo + all-reduce", "iterations": its,
                        "converged": bool(st.converged), "parallelism": f"row partition x{world}",
-                       "rows_per_rank": A.n_local, "build_s": round(build_s, 3)},
+                       "rows_per_rank": A.n_local, "build_s": round(build_s, 3), "breakdown": brk},
             "gpu_launches": None, "clocks": clk.summary()}
 
 

@@ -343,7 +343,9 @@ B200SP_KRYLOV_DECL(float, f32)
  * per row, classical layout): phase 1 = CG sigma = p.q (replaces
  * b200sp_cg_sigma), 2 = BiCGSTAB gamma = u.q with u = r_tilde (replaces
  * bicgstab_gamma), 3 = BiCGSTAB ts = q.u, tt = q.q with u = s (replaces
- * bicgstab_tst). The control step runs in the last block as in the unfused
+ * bicgstab_tst), 4 = distributed CG ghost block: q += A p (p = the ghost
+ * vector) and sigma = u.q with u = the owned p. The control step (or, with a
+ * distributed ctl, the parking of the local sum) runs in the last block as in the unfused
  * kernels (src/solvers/krylov.py:56-76, :233-265). */
 int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
                             const double* p, double* q, const double* u, int32_t phase, int32_t subwarp, void* ctl,

@@ -944,7 +944,9 @@ namespace b200sp {
 // iteration, ~9% of a 7-point CG iteration) disappears. Same ticket / block
 // order determinism as every other reduction here.
 // ===========================================================================
-enum FusedPhase : int { PH_SIGMA = 1, PH_GAMMA = 2, PH_TST = 3 };
+// PH_SIGMA_ACC (distributed CG, ghost block): q += A_ghost p_ghost and
+// sigma = u.q with u = the owned p (the SpMV input is the ghost vector)
+enum FusedPhase : int { PH_SIGMA = 1, PH_GAMMA = 2, PH_TST = 3, PH_SIGMA_ACC = 4 };
 
 // 8 CTAs per SM (<= 32 registers): the unbounded build took 40 registers at
 // sub-warp 1 (6 CTAs per SM) and ran slower than SpMV + separate dot
@@ -993,7 +995,11 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
         for (int k = 0; k < U; ++k) {  // row k written by lane k % SW (U may exceed SW)
             const int64_t row = row0 + k;
             if (k % SW == lane && row < n) {
-                const T mine = acc[k];
+                T mine = acc[k];
+                if (PH == PH_SIGMA_ACC) {
+                    mine += q[row];
+                    d0 += (double)__ldg(u + row) * (double)mine;
+                }
                 q[row] = mine;
                 if (PH == PH_SIGMA) d0 += (double)__ldg(p + row) * (double)mine;
                 if (PH == PH_GAMMA) d0 += (double)__ldg(u + row) * (double)mine;
@@ -1011,7 +1017,7 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
     } else {
         double v[1] = {d0}, tot[1];
         if (!grid_reduce<1>(v, part, &c->ticket[1], tot)) return;
-        if (PH == PH_SIGMA) {
+        if (PH == PH_SIGMA || PH == PH_SIGMA_ACC) {
             if (c->dist) {
                 c->red[0] = tot[0];
                 return;
@@ -1030,13 +1036,14 @@ static void launch_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av
     const int grid = kry_grid(ceil_div(n, U) * SW, KRY_BLOCK);
     if (phase == PH_SIGMA) csr_spmv_dot_kernel<T, SW, PH_SIGMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
     else if (phase == PH_GAMMA) csr_spmv_dot_kernel<T, SW, PH_GAMMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else if (phase == PH_SIGMA_ACC) csr_spmv_dot_kernel<T, SW, PH_SIGMA_ACC><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
     else csr_spmv_dot_kernel<T, SW, PH_TST><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
 }
 
 template <typename T>
 static int csr_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
                         int phase, int subwarp, void* ctl, double* part, void* stream) {
-    B200SP_REQUIRE(phase >= PH_SIGMA && phase <= PH_TST, B200SP_EINVAL, "csr_spmv_dot: phase must be 1..3");
+    B200SP_REQUIRE(phase >= PH_SIGMA && phase <= PH_SIGMA_ACC, B200SP_EINVAL, "csr_spmv_dot: phase must be 1..4");
     B200SP_REQUIRE(phase == PH_SIGMA || u, B200SP_EINVAL, "csr_spmv_dot: phase %d needs the second vector", phase);
     if (n == 0) return B200SP_OK;
     cudaStream_t st = as_stream(stream);

@@ -295,6 +295,31 @@ class DistCg:
         off = int(_lib.query("krylov_red_offset"))
         self.red = self.ctl[off:off + 32].view(torch.float64)
 
+    def _spmv_sigma(self, pext, p, q, c, pp, suf):
+        """q = A p with the local sigma = p.q parked for the all-reduce. With
+        classical-strategy blocks the reduction rides in an SpMV epilogue
+        (csr_spmv_dot): the owned block's when there are no ghosts, else the
+        ghost block's accumulate-and-dot pass after the halo lands (the owned
+        SpMV still overlaps the exchange); otherwise SpMV + cg_sigma."""
+        from .solvers.krylov import fused_csr_ok
+
+        A, exc = self.a, self.exec
+        nl = A.n_local
+        own, gh = A.a_own, A.a_ghost
+        if not (config.FUSED_SPMV_DOT and fused_csr_ok(own) and (gh is None or fused_csr_ok(gh))):
+            A.apply_ext(pext, q)
+            _lib.call("cg_sigma_" + suf, nl, ptr(p), ptr(q), c, ptr(pp), exc.stream)
+            return
+        if gh is None:
+            _lib.call("csr_spmv_dot_" + suf, nl, ptr(own._rp), ptr(own._ci), ptr(own._v), ptr(p), ptr(q), 0, 1,
+                      own.subwarp(), c, ptr(pp), exc.stream)
+            return
+        work = A.start_halo(pext)
+        own.apply(Dense.wrap(exc, pext[:nl].view(-1, 1)), Dense.wrap(exc, q.view(-1, 1)))
+        work.wait()
+        _lib.call("csr_spmv_dot_" + suf, nl, ptr(gh._rp), ptr(gh._ci), ptr(gh._v), ptr(pext[nl:]), ptr(q), ptr(p),
+                  4, gh.subwarp(), c, ptr(pp), exc.stream)
+
     def _status(self):
         iv, dv = (ctypes.c_int32 * 8)(), (ctypes.c_double * 8)()
         _lib.call("krylov_status", ptr(self.ctl), ctypes.addressof(iv), ctypes.addressof(dv), self.exec.stream)
@@ -333,8 +358,7 @@ class DistCg:
                     break
                 for _ in range(self.batch):
                     _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), c, exc.stream)
-                    A.apply_ext(pext, q)
-                    _lib.call("cg_sigma_" + suf, nl, ptr(p), ptr(q), c, ptr(pp), exc.stream)
+                    self._spmv_sigma(pext, p, q, c, pp, suf)
                     comm.allreduce_(self.red[:1])
                     _lib.call("cg_finish", c, 0, 1, exc.stream)
                     _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(r), *J, c, ptr(pp), 0,

@@ -39,15 +39,19 @@ def jac_args(solver):
     return (0, 0, 0, 0, 0)
 
 
-def fused_csr(solver):
-    """The system matrix when its SpMV can carry the next reduction in its
-    epilogue (csr_spmv_dot: Csr with the classical strategy), else None."""
+def fused_csr_ok(a):
+    """True when ``a``'s SpMV can carry a reduction in its epilogue
+    (csr_spmv_dot: Csr with the classical strategy)."""
     from ..formats import Csr
 
+    return isinstance(a, Csr) and a.strategy == "classical"
+
+
+def fused_csr(solver):
+    """The system matrix when its SpMV can carry the next reduction in its
+    epilogue, else None."""
     a = solver.a
-    if config.FUSED_SPMV_DOT and isinstance(a, Csr) and a.strategy == "classical":
-        return a
-    return None
+    return a if config.FUSED_SPMV_DOT and fused_csr_ok(a) else None
 
 
 def spmv_dot(S, a, suf, p, q, u, phase):
