@@ -710,7 +710,14 @@ class Csr(_Sparse):
                 lo, hi = int(rp[bounds[j]]), int(rp[bounds[j + 1]])
                 need.append(int(ci[lo:hi].max().item()) if hi > lo else -1)
             m = self.size.cols
-            cb = [m * j // k for j in range(k + 1)]  # b chunks
+            # b chunk i ends right after the highest column row chunk i reads
+            # (running max), so row chunk j waits only for b chunks 0..j --
+            # not for the next one, as equal b chunks would for a band
+            cb, hi = [0], 0
+            for j in range(k - 1):
+                hi = min(m, max(hi, need[j] + 1, cb[-1]))
+                cb.append(hi)
+            cb.append(m)
             # b chunk index whose arrival completes columns [0, need]
             wait = [next(i for i in range(k) if cb[i + 1] > nd) if nd >= 0 else -1 for nd in need]
             dev = self.exec.device
