@@ -118,6 +118,27 @@ def bench_solver(args, world, rank, local, kind):
                 "ms_per_step": round(e2e_t * 1e3, 3)},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    if vec_passes is None:  # C4: bytes per counted iteration from the kernels' traffic
+        spmv = bytes_csr(n, a.nnz, 8)
+        jac = int(solver.precond._storage.numel()) * solver.precond._storage.element_size() + 2 * n * 8
+        if kind == "c4b":
+            # one cycle = two counted half-iterations: 2 SpMV (+ the fused
+            # second-vector reads) + 2 Jacobi applies + 19 vector passes
+            by_it = (2 * spmv + 2 * jac + 19 * n * 8) / 2
+            label = "BiCGSTAB half-iteration (2 SpMV + 2 block-Jacobi + 19n vector values per cycle)"
+        else:
+            # GMRES step j: SpMV + Jacobi + the reference ledger for m = 1
+            # (src/solvers/gmres.py:238-242), averaged over the run's steps
+            k = 30
+            tot = 0.0
+            for it in range(1, its + 1):
+                j = (it - 1) % k + 1
+                tot += ((7 * n + 5) + (j - 1) * (4 * n + 4)) * 8 + 8 + ((3 * n + 8) + (j - 1) * (n + 2)) * 8 + 8
+            by_it = spmv + jac + tot / max(its, 1)
+            label = "GMRES(30) step (SpMV + block-Jacobi + reference MGS ledger, run average)"
+        out["roofline"] = {"bound": "hbm", "achieved": round(by_it / (t / its) / 1e9, 1), "peak": peak,
+                           "unit": "GB/s", "frac": round(by_it / (t / its) / 1e9 / peak, 4), "traffic": None,
+                           "peak_source": peak_src, "kernel": label, "bytes_per_launch": int(by_it)}
     if vec_passes is not None:
         by = bytes_csr(n, a.nnz, 8) + vec_passes * n * 8
         out["roofline"] = {"bound": "hbm", "achieved": round(by / (t / its) / 1e9, 1), "peak": peak,
