@@ -378,6 +378,50 @@ def bench_reference(args):
     }
 
 
+def c5_sub(args, world, rank, local, head):
+    """C5 (3-D 7-point Poisson 512^3, CG to 1e-8) alongside the C2 line, so a
+    plain `bench.py --gpus N` run also records the CG ms/iteration at N GPUs:
+    single-GPU CG at N = 1, the row-partitioned NCCL CG (strong scaling,
+    with the exposed-communication breakdown) at N > 1. Guarded: an error
+    is reported in the sub-object, and a watchdog prints the C2 line and
+    exits if the sub-measurement does not finish in time."""
+    import types
+
+    sub_args = types.SimpleNamespace(**vars(args))
+    sub_args.steps, sub_args.warmup, sub_args.grid = 2, 3, args.grid or 512
+    timer = threading.Timer(float(os.environ.get("B200SP_C5_TIMEOUT", "300")), _c5_watchdog,
+                            args=(rank, head))
+    timer.daemon = True
+    timer.start()
+    try:
+        from bench_solvers import bench_c5_distributed, bench_solver
+
+        if world > 1:
+            r = bench_c5_distributed(sub_args, world, rank, local)
+        else:
+            r = bench_solver(sub_args, world, rank, local, "c5")
+        keep = {"workload": r["config"]["workload"], "n_gpus": world, "ms_per_iter": r["value"],
+                "iterations": r["config"]["iterations"], "converged": r["config"]["converged"],
+                "scaling": "strong", "timed_solves": sub_args.steps}
+        if "breakdown" in r["config"]:
+            keep["breakdown"] = r["config"]["breakdown"]
+        if r.get("roofline"):
+            keep["frac_of_hbm_peak"] = r["roofline"]["frac"]
+        return keep
+    except Exception as e:  # noqa: BLE001 -- the C2 line must still be printed
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    finally:
+        timer.cancel()
+
+
+def _c5_watchdog(rank, head):
+    if rank == 0:
+        head = dict(head)
+        head["c5_cg"] = {"error": "timeout"}
+        print(json.dumps(head), flush=True)
+    os._exit(0)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -387,6 +431,8 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--grid", type=int, default=0, help="override the stencil grid of c4/c5")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="c2 only: skip the C5 CG sub-measurement (distributed at N > 1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -400,6 +446,8 @@ def main():
     world, rank, local = dist_setup()
     if args.workload == "c2":
         out = bench_c2(args, world, rank, local)
+        if not args.no_c5:
+            out["c5_cg"] = c5_sub(args, world, rank, local, out)
     else:
         from bench_solvers import bench_workload  # solver workloads
 
