@@ -1237,6 +1237,8 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
     if (grid > KRY_MAX_GRID) grid = KRY_MAX_GRID;
     const int64_t need = ceil_div(n, KRY_BLOCK);
     if (grid > need) grid = need;
+    const int cap = tuning("coop_blocks", 0);  // sweep knob: fewer blocks = cheaper grid barriers
+    if (cap > 0 && grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &q, &c, &part, &hist};
