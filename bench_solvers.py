@@ -118,6 +118,15 @@ def bench_solver(args, world, rank, local, kind):
                 "ms_per_step": round(e2e_t * 1e3, 3)},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    # the paper-comparable figure: the reference's traffic model (src/model.py,
+    # COO-unpreconditioned ledger) per iteration over the measured time
+    from paper_2006_16852_b200.model import per_iteration_bytes
+
+    sname = {"c1": "cg", "c5": "cg", "c4b": "bicgstab", "c4g": "gmres"}[kind]
+    mb = per_iteration_bytes(sname, n, a.nnz, its, krylov_dim=30 if kind == "c4g" else 100)
+    out["model_traffic"] = {"source": "src/model.py ledger (reference solver loop, COO, no preconditioner)",
+                            "bytes_per_iter": int(mb), "GBps": round(mb / (t / its) / 1e9, 1),
+                            "frac_of_peak": round(mb / (t / its) / 1e9 / peak, 4)}
     if vec_passes is None:  # C4: bytes per counted iteration from the kernels' traffic
         spmv = bytes_csr(n, a.nnz, 8)
         jac = int(solver.precond._storage.numel()) * solver.precond._storage.element_size() + 2 * n * 8
