@@ -36,8 +36,57 @@ def stencil(exc, kind, grid, value_dtype="float64", convection=0.4, strategy="au
     return Csr._from_device(exc, Dim2(n, n), rp, ci, v, strategy=strategy)
 
 
-def five_point_poisson(exc, grid, **kw):
-    return stencil(exc, "5pt", grid, **kw)
+# ---------------------------------------------------------------------------
+# the reference's host generators (src/problems.py:11-58), same triples in the
+# same (non-canonical) order, vectorised
+# ---------------------------------------------------------------------------
+def tridiagonal(n, lower=-1.0, diag=2.0, upper=-1.0):
+    """MatrixData of tridiag(lower, diag, upper); per row: lower, diagonal,
+    upper, zero off-diagonals omitted (src/problems.py:11-19)."""
+    from .formats import MatrixData
+
+    i = np.arange(n, dtype=np.int64)
+    cols = np.stack([i - 1, i, i + 1], axis=1)
+    vals = np.broadcast_to(np.array([lower, diag, upper], dtype=np.float64), (n, 3))
+    keep = np.stack([(i > 0) & (lower != 0.0), np.ones(n, bool), (i < n - 1) & (upper != 0.0)], axis=1)
+    rows = np.repeat(i, 3).reshape(n, 3)
+    return MatrixData(Dim2(n, n), rows[keep], cols[keep], vals[keep])
+
+
+def five_point_poisson(grid):
+    """MatrixData of the 5-point Laplacian on a grid x grid mesh (diagonal 4,
+    neighbours -1); per row: diagonal, then (-1,0), (1,0), (0,-1), (0,1)
+    (src/problems.py:22-39)."""
+    from .formats import MatrixData
+
+    n = grid * grid
+    me = np.arange(n, dtype=np.int64)
+    i, j = me // grid, me % grid
+    cols = np.stack([me, me - grid, me + grid, me - 1, me + 1], axis=1)
+    vals = np.broadcast_to(np.array([4.0, -1.0, -1.0, -1.0, -1.0]), (n, 5))
+    keep = np.stack([np.ones(n, bool), i > 0, i < grid - 1, j > 0, j < grid - 1], axis=1)
+    rows = np.repeat(me, 5).reshape(n, 5)
+    return MatrixData(Dim2(n, n), rows[keep], cols[keep], vals[keep])
+
+
+def convection_diffusion(n, convection=0.4):
+    """1-D convection-diffusion: tridiag(-1 - c, 2, -1 + c) (src/problems.py:42-45)."""
+    return tridiagonal(n, lower=-1.0 - convection, diag=2.0, upper=-1.0 + convection)
+
+
+def random_sparse(n, density=0.1, seed=0, diag_dominant=True):
+    """Seeded random matrix with a full diagonal, optionally strictly
+    diagonally dominant (src/problems.py:48-58)."""
+    from .formats import MatrixData
+
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n, n)) < density
+    np.fill_diagonal(mask, True)
+    dense = np.where(mask, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+    if diag_dominant:
+        off = np.abs(dense).sum(axis=1) - np.abs(np.diag(dense))
+        np.fill_diagonal(dense, off + 1.0)
+    return MatrixData.from_dense_array(dense)
 
 
 def power_law(exc, n, seed=0, max_len=50000, c=5.5154, value_dtype="float64", strategy="automatic"):
