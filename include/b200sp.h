@@ -189,6 +189,12 @@ int b200sp_sellp_spmv_f32(int64_t n, int32_t slice_size, const int32_t* slice_le
                           const float* x_in, int64_t x_in_stride, void* stream);
 
 /* Dense operator times one column (DenseSpmvKernel, kernels.py:319-332) */
+/* matrix-free tridiagonal stencil x = tridiag(l, c, r) b on (n, m) row-major
+ * blocks (StencilMatrix; StencilApplyKernel, src/kernels.py:335-363) */
+int b200sp_stencil3_apply_f64(int64_t n, int32_t m, double l, double c, double r, const double* b, int64_t bs,
+                              double* x, int64_t xs, void* stream);
+int b200sp_stencil3_apply_f32(int64_t n, int32_t m, float l, float c, float r, const float* b, int64_t bs,
+                              float* x, int64_t xs, void* stream);
 int b200sp_dense_spmv_f64(int64_t n, int64_t k, const double* a, int64_t a_stride, const double* b, int64_t b_stride,
                          double* x, int64_t x_stride, void* stream);
 int b200sp_dense_spmv_f32(int64_t n, int64_t k, const float* a, int64_t a_stride, const float* b, int64_t b_stride,

@@ -40,6 +40,7 @@ _TYPED = {
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
     "sellp_spmv": "lippppplpl" + _SPMV_TAIL + "p",
     "dense_spmv": "llplplplp",
+    "stencil3_apply": "liVVVplplp",
     # conversions
     "csr_to_ell": "lpppllppp",
     "csr_to_sellp": "lpppippppp",

@@ -1374,6 +1374,24 @@ static int sellp_spmv(int64_t n, int slice_size, const int* sl, const int* ss, c
 }
 
 // ===========================================================================
+// Matrix-free tridiagonal stencil (StencilMatrix; StencilApplyKernel,
+// src/kernels.py:335-363): x_i = c b_i, then += l b_{i-1}, then += r b_{i+1},
+// each product rounded before its add as in the reference's NumPy passes.
+// ===========================================================================
+template <typename T>
+__global__ void stencil3_kernel(int64_t n, int m, T l, T c, T r, const T* __restrict__ b, int64_t bs,
+                                T* __restrict__ x, int64_t xs) {
+    const int64_t tot = n * m;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / m, j = t - i * m;
+        T v = mul_rn(c, b[i * bs + j]);
+        if (i > 0) v = v + mul_rn(l, b[(i - 1) * bs + j]);
+        if (i < n - 1) v = v + mul_rn(r, b[(i + 1) * bs + j]);
+        x[i * xs + j] = v;
+    }
+}
+
+// ===========================================================================
 // Dense (n, k) row-major times b: warp per row (DenseSpmvKernel,
 // src/kernels.py:319-332; small operators only, not a performance target)
 // ===========================================================================
@@ -1548,6 +1566,20 @@ int b200sp_sellp_spmv_f32(int64_t n, int32_t slice_size, const int32_t* slice_le
     return sellp_spmv<float>(n, slice_size, slice_lengths, slice_sets, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, stream);
 }
 
+int b200sp_stencil3_apply_f64(int64_t n, int32_t m, double l, double c, double r, const double* b, int64_t bs,
+                              double* x, int64_t xs, void* stream) {
+    if (n == 0) return B200SP_OK;
+    stencil3_kernel<double><<<grid_for(n * m, 256, 8), 256, 0, as_stream(stream)>>>(n, m, l, c, r, b, bs, x, xs);
+    count_launch();
+    return check_launch("stencil3_apply");
+}
+int b200sp_stencil3_apply_f32(int64_t n, int32_t m, float l, float c, float r, const float* b, int64_t bs,
+                              float* x, int64_t xs, void* stream) {
+    if (n == 0) return B200SP_OK;
+    stencil3_kernel<float><<<grid_for(n * m, 256, 8), 256, 0, as_stream(stream)>>>(n, m, l, c, r, b, bs, x, xs);
+    count_launch();
+    return check_launch("stencil3_apply");
+}
 int b200sp_dense_spmv_f64(int64_t n, int64_t k, const double* a, int64_t as, const double* b, int64_t bs,
                          double* x, int64_t xs, void* stream) {
     return dense_spmv<double>(n, k, a, as, b, bs, x, xs, stream);

@@ -318,3 +318,56 @@ class DeviceView:
 
     def __abs__(self):
         return abs(self.numpy())
+
+
+class StorageMode(Enum):
+    OWNING = "owning"
+    VIEW = "view"
+
+
+class Array:
+    """Fixed-size buffer resident on one executor (src/executor.py:270-334):
+    a torch tensor on a CudaExecutor, a (pinned) ndarray on the host arena.
+    Owning arrays hold their own storage; views alias caller memory and never
+    release it; ``copy_to`` is always a deep, owning copy."""
+
+    def __init__(self, exc, size=None, data=None, mode=StorageMode.OWNING, dtype=None):
+        self.exec = exc
+        self.mode = mode
+        dt = np.dtype(dtype or (getattr(data, "dtype", None) if data is not None else None)
+                      or config.DEFAULT_VALUE_DTYPE)
+        if data is not None:
+            if isinstance(exc, CudaExecutor):
+                src = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.asarray(data, dtype=dt))
+                t = src.to(exc.device)
+                # owning: never alias the caller's buffer
+                self.data = t.clone() if mode is StorageMode.OWNING and t.data_ptr() == src.data_ptr() else t
+            else:
+                arr = np.asarray(data, dtype=dt)
+                self.data = arr.copy() if mode is StorageMode.OWNING else arr
+        else:
+            self.data = (torch.empty(int(size), dtype=_torch_dtype(dt), device=exc.device)
+                         if isinstance(exc, CudaExecutor) else exc.alloc(int(size), dt))
+
+    @classmethod
+    def view(cls, exc, size, buffer):
+        """Non-owning view over the first ``size`` elements of ``buffer``."""
+        buf = buffer.reshape(-1) if hasattr(buffer, "reshape") else np.asarray(buffer).reshape(-1)
+        n = buf.numel() if isinstance(buf, torch.Tensor) else buf.size
+        if size > n:
+            raise OpalgError("view exceeds the underlying buffer")
+        obj = cls.__new__(cls)
+        obj.exec, obj.mode, obj.data = exc, StorageMode.VIEW, buf[:size]
+        return obj
+
+    def __len__(self):
+        return int(self.data.numel() if isinstance(self.data, torch.Tensor) else self.data.size)
+
+    def copy_to(self, target):
+        """Deep copy onto ``target`` (always owning; the source is unchanged)."""
+        out = Array(target, size=len(self), dtype=str(self.data.dtype).replace("torch.", ""))
+        if isinstance(out.data, torch.Tensor):
+            out.data.copy_(torch.as_tensor(self.data).to(out.data.device))
+        else:
+            out.data[...] = self.data.cpu().numpy() if isinstance(self.data, torch.Tensor) else self.data
+        return out

@@ -1216,6 +1216,46 @@ class Hybrid(_Sparse):
 
 
 # ---------------------------------------------------------------------------
+# StencilMatrix (src/formats.py:268-298): matrix-free tridiagonal operator
+# ---------------------------------------------------------------------------
+class StencilMatrix(LinOp):
+    """Matrix-free 3-point stencil operator (tridiagonal action) on the
+    device; converts to Csr only, like the reference."""
+
+    def __init__(self, exc, n, left, center, right, value_dtype=None):
+        _require_cuda(exc)
+        super().__init__(exc, Dim2(n, n))
+        vt = _np_vt(value_dtype or config.DEFAULT_VALUE_DTYPE)
+        self.coefficients = np.asarray([left, center, right], dtype=vt)
+
+    def _apply_impl(self, b, x):
+        bt, xt = b.values, x.values
+        l, c, r = (float(v) for v in self.coefficients)
+        _lib.call("stencil3_apply_" + _lib.suffix(xt.dtype), xt.shape[0], xt.shape[1], l, c, r, ptr(bt),
+                  bt.stride(0), ptr(xt), xt.stride(0), self.exec.stream)
+
+    def to_data(self):
+        from .problems import tridiagonal
+
+        left, center, right = (float(v) for v in self.coefficients)
+        n = self.size.rows
+        i = np.arange(n, dtype=np.int64)
+        cols = np.stack([i - 1, i, i + 1], axis=1)
+        vals = np.broadcast_to(np.array([left, center, right]), (n, 3))
+        keep = np.stack([i > 0, np.ones(n, bool), i < n - 1], axis=1)
+        return MatrixData(self.size, np.repeat(i, 3).reshape(n, 3)[keep], cols[keep], vals[keep])
+
+    def convert_to(self, kind, **kw):
+        if kind is Csr or (isinstance(kind, str) and kind.lower() == "csr"):
+            return Csr.from_data(self.exec, self.to_data(), value_dtype=self.coefficients.dtype)
+        raise Unsupported("stencil matrices only convert to CSR")
+
+    def clone_to(self, target):
+        return StencilMatrix(target, self.size.rows, *map(float, self.coefficients),
+                             value_dtype=self.coefficients.dtype)
+
+
+# ---------------------------------------------------------------------------
 # conversions (src/formats.py:301-329)
 # ---------------------------------------------------------------------------
 _FORMAT_NAMES = {"dense": Dense, "csr": Csr, "coo": Coo, "ell": Ell, "sellp": Sellp, "hybrid": Hybrid}

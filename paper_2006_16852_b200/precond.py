@@ -24,6 +24,31 @@ from .formats import Csr, _require_cuda, convert
 MAX_BLOCK = 32
 
 
+def gauss_jordan_inverse(block, exc=None):
+    """Explicit inverse of a dense block by Gauss-Jordan elimination with
+    partial pivoting (src/precond.py:28-46), computed by the device
+    generation kernel -- bit-identical to the reference -- or None when a
+    pivot vanishes. Blocks are limited to 32 rows on this backend."""
+    from .executor import CudaExecutor
+    from .formats import MatrixData
+
+    blk = np.asarray(block, dtype=np.float64)
+    bs = blk.shape[0]
+    if blk.ndim != 2 or blk.shape[1] != bs:
+        raise DimensionMismatch("gauss_jordan_inverse needs a square block")
+    if bs > MAX_BLOCK:
+        raise Unsupported(f"blocks are limited to {MAX_BLOCK} rows on this backend")
+    if bs == 0:
+        return np.zeros((0, 0))
+    exc = exc or CudaExecutor()
+    a = Csr.from_data(exc, MatrixData.from_dense_array(blk))
+    try:
+        op = Jacobi(exc, block_size=bs).generate(a)
+    except Singular:
+        return None
+    return op.stored_inverse(0).astype(np.float64)
+
+
 def uniform_block_boundaries(n, block_size):
     """Block start rows for uniform blocks (last block may be smaller)."""
     return list(range(0, n, int(block_size)))
