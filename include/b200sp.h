@@ -386,10 +386,27 @@ int b200sp_assemble_coo_f32(int64_t count, const int64_t* rows, const int64_t* c
  * (lold, uold) into (lnew, unew); lrow / urow from csr_rows. trs: sync-free
  * substitution of one column, lower (forward) or upper (backward); diag NULL
  * = unit diagonal; `ready` (n int32, zero at creation) and a fresh `epoch`
- * per call; `ticket` = one int32 of scratch. */
+ * per call; `ticket` = one int32 of scratch; `order` = rows grouped by
+ * dependency level (b200sp_trs_order) or NULL for plain row order. */
 int b200sp_ilu_counts(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, int32_t* lcnt, int32_t* ucnt,
                       int32_t* nodiag, void* stream);
 int b200sp_csr_rows(int64_t n, const int32_t* row_ptrs, int32_t* row_of_entry, void* stream);
+/* dependency levels of a triangular factor (relaxation sweeps until
+ * *changed stays 0) and the rows grouped by level (claim order of trs) */
+int b200sp_trs_levels(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, int32_t lower, int32_t* level,
+                      int32_t* changed, void* stream);
+int b200sp_trs_level_hist(int64_t n, const int32_t* level, int32_t* count, void* stream);
+/* level-synchronous substitution of one column as one cooperative launch
+ * (rows of a level in parallel, a grid barrier between levels); offs =
+ * nlevels + 1 level starts in `order`; diag NULL = unit diagonal */
+int b200sp_trs_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, const double* diag,
+                        const double* b, int64_t bs, double* x, int64_t xs, const int32_t* order, const int32_t* offs,
+                        int32_t nlevels, void* stream);
+int b200sp_trs_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, const float* diag,
+                        const float* b, int64_t bs, float* x, int64_t xs, const int32_t* order, const int32_t* offs,
+                        int32_t nlevels, void* stream);
+int b200sp_trs_order(int64_t n, const int32_t* level, const int32_t* offs, int32_t* cursor, int32_t* order,
+                     void* stream);
 #define B200SP_ILU_DECL(T, SUF)                                                                                     \
     int b200sp_diag_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* diag, int32_t* zero,      \
                           void* stream);                                                                           \
@@ -402,7 +419,7 @@ int b200sp_csr_rows(int64_t n, const int32_t* row_ptrs, int32_t* row_of_entry, v
                                   void* stream);                                                                   \
     int b200sp_trs_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, const T* diag,               \
                          int32_t lower, const T* b, int64_t bs, T* x, int64_t xs, int32_t* ready, int32_t epoch,   \
-                         int32_t* ticket, void* stream);
+                         int32_t* ticket, const int32_t* order, void* stream);
 B200SP_ILU_DECL(double, f64)
 B200SP_ILU_DECL(float, f32)
 

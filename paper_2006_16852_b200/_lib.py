@@ -86,7 +86,8 @@ _TYPED = {
     "diag": "lpppppp",
     "ilu_fill": "lppppppppppppp",
     "parilu_sweep": "lllppppppppppppp",
-    "trs": "lppppiplplpipp",
+    "trs": "lppppiplplpippp",
+    "trs_coop": "lppppplplppip",
     "gather": "lpppp",
 }
 _UNTYPED = {
@@ -122,6 +123,9 @@ _UNTYPED = {
     "assemble_workspace_bytes": ("l", ctypes.c_int64),
     "ilu_counts": ("lpppppp", ctypes.c_int),
     "csr_rows": ("lppp", ctypes.c_int),
+    "trs_levels": ("lppippp", ctypes.c_int),
+    "trs_level_hist": ("lppp", ctypes.c_int),
+    "trs_order": ("lppppp", ctypes.c_int),
     "fcg_init_ctl": ("pp", ctypes.c_int),
     "cgs_mid": ("ppp", ctypes.c_int),
     "mm_header": ("plpp", ctypes.c_int),

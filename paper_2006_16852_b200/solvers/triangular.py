@@ -2,9 +2,12 @@
 
 The reference substitutes row by row (or level by level across workers).
 Here a synchronisation-free kernel (csrc/ilu.cu: trs_kernel) solves every
-column in one launch: warps claim rows in dependency order through an atomic
-ticket, wait on the rows they depend on with acquire loads of per-row flags,
-and publish their x_i with a release store. Generation extracts the diagonal
+column in one launch: warps claim rows through an atomic ticket in the order
+of their dependency levels (computed on the device at generation: claiming
+in plain row order serialised a stencil factor along its x-neighbour chain,
+143 ms vs 4.3 ms per ILU apply at 128^3), wait on the rows they depend on
+with acquire loads of per-row flags, and publish their x_i with a release
+store. Generation extracts the diagonal
 on the device and raises Singular on a zero (or missing) one, like the
 reference; ``levels`` (the reference's dependency levels) is computed on
 demand for inspection only.
@@ -19,7 +22,7 @@ from .. import _lib
 from ..base import LinOp, LinOpFactory
 from ..errors import DimensionMismatch, Singular
 from ..executor import ptr
-from ..formats import Csr, _require_cuda
+from ..formats import Csr, _require_cuda, _scan
 
 INT_MAX = 2 ** 31 - 1
 
@@ -38,6 +41,11 @@ def extract_diagonal(factor):
 class TriangularSolver(LinOp):
     """Exact substitution with a (unit-)triangular Csr factor."""
 
+    #: level-synchronous cooperative substitution instead of the sync-free
+    #: kernel (measured slower: a grid barrier costs ~7 us per level vs
+    #: ~5.6 us of flag latency; profiles/r02_trs_sweep.txt)
+    LEVEL_SYNC = False
+
     def __init__(self, factor: Csr, lower: bool, unit_diagonal=False):
         _require_cuda(factor.exec)
         super().__init__(factor.exec, factor.size)
@@ -55,6 +63,34 @@ class TriangularSolver(LinOp):
         self._ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self._epoch = 0
         self._levels = None
+        self._order, self._nlevels = self._level_order()
+
+    def _level_order(self):
+        """Rows grouped by dependency level, computed on the device by
+        relaxation sweeps (one host check per sweep; depth + 1 sweeps)."""
+        f, exc = self.factor, self.exec
+        n = f.size.rows
+        if n == 0:
+            return None, 0
+        dev = exc.device
+        level = torch.zeros(n, dtype=torch.int32, device=dev)
+        changed = torch.zeros(1, dtype=torch.int32, device=dev)
+        while True:
+            changed.zero_()
+            _lib.call("trs_levels", n, ptr(f._rp), ptr(f._ci), int(self.lower), ptr(level), ptr(changed),
+                      exc.stream)
+            if not int(changed.item()):
+                break
+        nlev = int(level.max().item()) + 1
+        count = torch.zeros(nlev, dtype=torch.int32, device=dev)
+        _lib.call("trs_level_hist", n, ptr(level), ptr(count), exc.stream)
+        offs = _scan(exc, count)
+        cursor = torch.zeros(nlev, dtype=torch.int32, device=dev)
+        order = torch.empty(n, dtype=torch.int32, device=dev)
+        _lib.call("trs_order", n, ptr(level), ptr(offs), ptr(cursor), ptr(order), exc.stream)
+        self._level_of = level
+        self._level_offs = offs
+        return order, nlev
 
     @property
     def levels(self):
@@ -79,12 +115,19 @@ class TriangularSolver(LinOp):
         suf = _lib.suffix(xv.dtype)
         isz = xv.element_size()
         for j in range(xv.shape[1]):
+            if self.LEVEL_SYNC and self._order is not None:
+                _lib.call("trs_coop_" + suf, n, ptr(f._rp), ptr(f._ci), ptr(f._v),
+                          ptr(self.diag) if self.diag is not None else 0,
+                          bv.data_ptr() + j * bv.stride(1) * isz, bv.stride(0),
+                          xv.data_ptr() + j * xv.stride(1) * isz, xv.stride(0),
+                          ptr(self._order), ptr(self._level_offs), self._nlevels, self.exec.stream)
+                continue
             self._epoch += 1
             _lib.call("trs_" + suf, n, ptr(f._rp), ptr(f._ci), ptr(f._v),
                       ptr(self.diag) if self.diag is not None else 0, int(self.lower),
                       bv.data_ptr() + j * bv.stride(1) * isz, bv.stride(0),
                       xv.data_ptr() + j * xv.stride(1) * isz, xv.stride(0),
-                      ptr(self._ready), self._epoch, ptr(self._ticket), self.exec.stream)
+                      ptr(self._ready), self._epoch, ptr(self._ticket), ptr(self._order), self.exec.stream)
 
     def clone_to(self, target):
         return TriangularSolver(self.factor.clone_to(target), self.lower, self.unit_diagonal)
