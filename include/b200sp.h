@@ -111,13 +111,14 @@ int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, 
                                const float* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
                                int32_t rpt, int32_t gather_in_reduce, void* stream);
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
-/* Csr, stream strategy as a persistent TMA pipeline ("pipe"): one CTA per SM
+/* Csr, stream strategy as a persistent TMA pipeline ("pipe"): one or two CTAs per SM
  * of `consumers` (256/512) consumer threads + 1 producer warp; tiles of
  * consumers/tpr*rpt rows, each row reduced by `tpr` (1/2/4) threads; each
  * tile's row_ptrs slice and col_idxs / vals range is bulk-copied
  * (cp.async.bulk + mbarrier) into a `stages`-deep ring of shared-memory
  * stages of `cap` entries (multiple of 4) and reduced out of shared memory.
- * Supported (consumers, tpr, rpt): (256,1,1|2|4) (512,2,1|2) (512,4,1|2).
+ * Supported (consumers, tpr, rpt): (256,1,1|2|4) (256,2,1|2) (512,2,1|2) (512,4,1|2).
+ * Two CTAs per SM run when 2 x stages x stage bytes fits (tuning "pipe_ctas").
  * stages * b200sp_csr_tma_stage_bytes(rows per tile) + 256 <= 226 KB. row_ptrs/col_idxs/vals 16-byte aligned. Replaces
  * the same CsrSpmvKernel as the other Csr strategies (src/kernels.py:278-316). */
 int b200sp_csr_spmv_tma_f64(int64_t n, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idxs,

@@ -545,7 +545,10 @@ static int launch_pipe(int64_t n, const int* rp, const int* ci, const T* v, cons
     auto kern = xin ? csr_pipe_kernel<T, NT, TPR, RPT, true> : csr_pipe_kernel<T, NT, TPR, RPT, false>;
     B200SP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t ntiles = ceil_div(n, TR);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs));
+    // CTAs per SM: 2 when two stage rings fit (more consumer warps to hide
+    // the gather latency), knob "pipe_ctas" to force
+    const int per_sm = tuning("pipe_ctas", smem * 2 <= 226 * 1024 ? 2 : 1);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm));
     kern<<<grid, NT + 32, (size_t)smem, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, stages);
     return B200SP_OK;
 }
@@ -566,7 +569,8 @@ static int csr_pipe(int64_t n, const int* rp, const int* ci, const T* v, const T
     if (consumers == NT && tpr == TP && rpt == RP)                                                                \
         rc = launch_pipe<T, NT, TP, RP>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, cap, stages, st); \
     else
-    PIPE_CASE(256, 1, 1) PIPE_CASE(256, 1, 2) PIPE_CASE(256, 1, 4) PIPE_CASE(512, 2, 1) PIPE_CASE(512, 2, 2)
+    PIPE_CASE(256, 1, 1) PIPE_CASE(256, 1, 2) PIPE_CASE(256, 1, 4) PIPE_CASE(256, 2, 1) PIPE_CASE(256, 2, 2)
+    PIPE_CASE(512, 2, 1) PIPE_CASE(512, 2, 2)
     PIPE_CASE(512, 4, 1) PIPE_CASE(512, 4, 2) {
         set_error("csr pipe: unsupported (consumer threads, threads per row, rows per thread) = (%d, %d, %d)",
                   consumers, tpr, rpt);

@@ -545,6 +545,10 @@ class Csr(_Sparse):
         mean = self.nnz / n
         if self._row_stats() > 4 * mean + 64:
             return "load_balance"
+        # fp32 with long rows: the TMA pipeline with two CTAs per SM measured
+        # 0.759 vs the classical kernel's 0.72 on C2 (profiles/r02_pipe_sweep.txt)
+        if self._v.element_size() == 4 and mean >= 12 and self._stream_ok() and n >= (1 << 16):
+            return "stream"
         return "classical"
 
     def _stream_ok(self):
@@ -568,7 +572,7 @@ class Csr(_Sparse):
         if impl is not None:
             return impl
         mean = self.nnz / max(1, self.size.rows)
-        return "tma" if self._v.element_size() == 8 and mean >= 12 else "ld"
+        return "tma" if mean >= 12 else "ld"
 
     def tma_config(self):
         """(entries per stage, rows per thread, stages, consumer threads,
@@ -577,9 +581,12 @@ class Csr(_Sparse):
         per thread group (tiles of 512 rows), stages as large as two fit."""
         vb = self._v.element_size()
         shape = getattr(self, "_stream_shape", None)
+        mean = self.nnz / max(1, self.size.rows)
         if shape is None:
-            mean = self.nnz / max(1, self.size.rows)
-            shape = (2, 2) if mean >= 12 else (1, 4 if mean < 6 else 2)
+            # fp64 long rows: 512 consumers, 2 threads x 2 rows (0.727); fp32
+            # long rows: 256 consumers, thread per row, whole-tile stages, two
+            # CTAs per SM (0.759)
+            shape = ((2, 2) if vb == 8 else (1, 1)) if mean >= 12 else (1, 4 if mean < 6 else 2)
         tpr, rpt = shape
         nt = int(getattr(self, "_stream_consumers", None) or (512 if tpr > 1 else 256))
         rows = nt // tpr * rpt
@@ -589,7 +596,9 @@ class Csr(_Sparse):
         cap_fit2 = ((budget // 2 - rp_bytes) // (4 + vb)) // 4 * 4
         cap = int(getattr(self, "_stream_cap", None) or min(need, cap_fit2))
         stage = rp_bytes + cap * (4 + vb)
-        stages = int(getattr(self, "_stream_stages", None) or max(2, min(4, budget // stage)))
+        # two stages per CTA: three measured slower everywhere (the ring only
+        # has to cover one tile of latency); two CTAs per SM when they fit
+        stages = int(getattr(self, "_stream_stages", None) or 2)
         return cap, rpt, stages, nt, tpr
 
     def stream_config(self):
