@@ -111,6 +111,28 @@ int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, 
                                const float* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
                                int32_t rpt, int32_t gather_in_reduce, void* stream);
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
+/* Csr apply with b and x in pinned (mapped) host memory, as one cooperative
+ * kernel: producer CTAs stream b over PCIe into `b_dev` in chunks of
+ * b200sp_csr_host_chunk_elems() entries and publish each with
+ * flags[chunk] = epoch (release); consumer CTAs reduce row tiles of
+ * `tile_rows` rows (classical sub-warp scheme, identical results to
+ * b200sp_csr_spmv_classical_*) as soon as the chunks up to tile_need[tile]
+ * have landed, and store x straight into host memory. flags: int32
+ * [ceil(ncols / chunk_elems)], zero-initialised once; epoch > 0 and
+ * different from the previous call's. tile_need from b200sp_csr_tile_chunks.
+ * Replaces LinOp.apply on host operands (src/base.py:60-70, migration
+ * src/base.py:99-127) for CsrSpmvKernel (src/kernels.py:278-316). */
+int32_t b200sp_csr_host_chunk_elems(int32_t value_bytes);
+int b200sp_csr_tile_chunks(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, int32_t tile_rows,
+                           int64_t chunk_elems, int32_t* tile_need, void* stream);
+int b200sp_csr_spmv_host_f64(int64_t n, int64_t ncols, const int32_t* row_ptrs, const int32_t* col_idxs,
+                             const double* vals, const double* b_host, double* b_dev, double* x_host,
+                             const int32_t* tile_need, int32_t tile_rows, int32_t* flags, int32_t epoch,
+                             int32_t subwarp, void* stream);
+int b200sp_csr_spmv_host_f32(int64_t n, int64_t ncols, const int32_t* row_ptrs, const int32_t* col_idxs,
+                             const float* vals, const float* b_host, float* b_dev, float* x_host,
+                             const int32_t* tile_need, int32_t tile_rows, int32_t* flags, int32_t epoch,
+                             int32_t subwarp, void* stream);
 /* Csr, stream strategy as a persistent TMA pipeline ("pipe"): one or two CTAs per SM
  * of `consumers` (256/512) consumer threads + 1 producer warp; tiles of
  * consumers/tpr*rpt rows, each row reduced by `tpr` (1/2/4) threads; each

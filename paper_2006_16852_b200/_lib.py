@@ -35,6 +35,7 @@ _TYPED = {
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppiip",
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
     "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iiiiip",
+    "csr_spmv_host": "llpppppppipiip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
@@ -103,6 +104,8 @@ _UNTYPED = {
     "csr_lb_tile": ("ii", ctypes.c_int32),
     "csr_lb_num_tiles": ("lli", ctypes.c_int64),
     "csr_stream_capacity": ("i", ctypes.c_int32),
+    "csr_host_chunk_elems": ("i", ctypes.c_int32),
+    "csr_tile_chunks": ("lppilpp", ctypes.c_int),
     "csr_tma_stage_bytes": ("iii", ctypes.c_int64),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),

@@ -216,6 +216,9 @@ __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, 
 // ---------------------------------------------------------------------------
 // warp reductions
 // ---------------------------------------------------------------------------
+// rows in flight per sub-warp of the classical Csr kernels (spmv.cu, hoststream.cu)
+template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1); };
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

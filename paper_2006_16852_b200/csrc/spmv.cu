@@ -29,7 +29,7 @@ namespace b200sp {
 // rows in flight per sub-warp (2 rows per thread at sub-warp 1 strides the
 // row accesses of a warp by 2 and measured slower: 0.745 vs 0.748 / CG
 // 0.81 vs 0.51 ms; profiles/r02_classical_sweep.txt)
-template <int SW> struct ClassicalRows { static constexpr int v = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1); };
+// (ClassicalRows<SW> in common.cuh: shared with the host-stream kernel)
 
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)

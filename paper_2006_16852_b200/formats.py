@@ -693,7 +693,10 @@ class Csr(_Sparse):
         self._check_conformal(b, x)
         self._log(EventKind.LINOP_APPLY_STARTED, {"op": type(self).__name__, "uid": self.uid})
         with _PIPELINE_LOCK:  # the plan's device buffers / graphs are shared
-            self._pipelined_apply(b, x)
+            if self.HOST_STREAM == "kernel":
+                self._host_stream_apply(b, x)
+            else:
+                self._pipelined_apply(b, x)
         self._log(EventKind.LINOP_APPLY_COMPLETED, {"op": type(self).__name__, "uid": self.uid})
 
     def _pipeline_ok(self, b, x):
@@ -704,7 +707,51 @@ class Csr(_Sparse):
                 and getattr(b, "is_dense", False) and getattr(x, "is_dense", False)
                 and b.size.cols == 1 and x.size.cols == 1 and self.size.rows >= (1 << 16)
                 and self._resolved_strategy() == "classical"
+                and np.asarray(b.values).flags.c_contiguous and np.asarray(x.values).flags.c_contiguous
                 and np.dtype(b.dtype) == self.value_dtype and np.dtype(x.dtype) == self.value_dtype)
+
+    #: "copies": the copy-engine pipeline (chunked H2D / SpMV / D2H in a graph);
+    #: "kernel": one cooperative kernel streams b in, reduces row tiles as their
+    #: columns land and stores x straight to host memory (csrc/hoststream.cu).
+    #: Over PCIe Gen5 the copy engines win (C2: 0.50 vs 0.54 ms; SM loads / stores
+    #: to host memory reach ~40 GB/s per direction vs the engines' 55,
+    #: profiles/r02_e2e_probe.txt); the kernel is the design for hosts whose
+    #: memory the SMs reach over a coherent link
+    HOST_STREAM = "copies"
+    HOST_TILE_BYTES = 8192  # x bytes per consumer tile (1024 fp64 rows)
+
+    def _host_stream_plan(self):
+        plan = getattr(self, "_hsplan", None)
+        if plan is None:
+            n = self.size.rows
+            vb = self._v.element_size()
+            tile = self.HOST_TILE_BYTES // vb
+            chunk = int(_lib.query("csr_host_chunk_elems", vb))
+            dev = self.exec.device
+            ntiles = (n + tile - 1) // tile
+            need = torch.empty(ntiles, dtype=torch.int32, device=dev)
+            _lib.call("csr_tile_chunks", n, ptr(self._rp), ptr(self._ci), tile, chunk, ptr(need),
+                              self.exec.stream)
+            m = self.size.cols
+            plan = {"tile": tile, "need": need, "epoch": 0,
+                    "flags": torch.zeros((m + chunk - 1) // chunk, dtype=torch.int32, device=dev),
+                    "b": torch.empty(max(1, m), dtype=self._v.dtype, device=dev)}
+            self._hsplan = plan
+        return plan
+
+    def _host_stream_apply(self, b, x):
+        P = self._host_stream_plan()
+        P["epoch"] += 1
+        if P["epoch"] >= 2**31 - 1:
+            P["flags"].zero_()
+            P["epoch"] = 1
+        bh = np.asarray(b.values)
+        xh = np.asarray(x.values)
+        suf = _lib.suffix(self._v.dtype)
+        _lib.call("csr_spmv_host_" + suf, self.size.rows, self.size.cols, ptr(self._rp), ptr(self._ci),
+                  ptr(self._v), bh.ctypes.data, ptr(P["b"]), xh.ctypes.data, ptr(P["need"]), P["tile"],
+                  ptr(P["flags"]), P["epoch"], self.subwarp(), self.exec.stream)
+        torch.cuda.current_stream(self.exec.device).synchronize()
 
     def _pipeline_plan(self):
         plan = getattr(self, "_pplan", None)

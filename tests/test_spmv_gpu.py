@@ -369,27 +369,60 @@ def test_coo_kernel_variants(cuda, golden_spmv, knob, val):
         _lib.set_tuning(knob, default)
 
 
-@pytest.mark.parametrize("kind", ["27pt", "random"])
-def test_pipelined_host_apply_bitwise(cuda, host, kind):
-    """Host operands on a large Csr take the chunked transfer/compute
-    pipeline; results are bitwise those of the device-resident apply."""
+@pytest.mark.parametrize("mode", ["kernel", "copies"])
+@pytest.mark.parametrize("kind", ["27pt", "random", "odd"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_pipelined_host_apply_bitwise(cuda, host, kind, mode, dtype):
+    """Host operands on a large Csr take the streaming path (the cooperative
+    host-stream kernel, or the chunked copy-engine pipeline); results are
+    bitwise those of the device-resident apply."""
     import paper_2006_16852_b200 as b2
     from paper_2006_16852_b200 import problems
+    from paper_2006_16852_b200.formats import Csr
 
     if kind == "27pt":
-        a = problems.stencil(cuda, "27pt", 64)
+        a = problems.stencil(cuda, "27pt", 64, value_dtype=dtype)
     else:
-        n, rng = 70000, np.random.default_rng(4)
+        # "odd": a row count that is no multiple of the tile or the 16-byte store width
+        n, rng = (70000 if kind == "random" else 65537 + 1024 * 3 + 1), np.random.default_rng(4)
         rows = np.repeat(np.arange(n), 8)
-        data = b2.MatrixData((n, n), rows, rng.integers(0, n, rows.size), rng.standard_normal(rows.size))
-        a = b2.matrix_from_data(cuda, data, "csr")
+        cols = rng.integers(0, n, rows.size) if kind == "random" else (rows + rng.integers(-300, 300, rows.size)) % n
+        data = b2.MatrixData((n, n), rows, cols, rng.standard_normal(rows.size))
+        a = b2.matrix_from_data(cuda, data, "csr", value_dtype=dtype)
+    a = b2.convert(a, "csr_classical")  # (fp32 long rows default to the stream strategy)
     n = a.size.rows
-    assert a._pipeline_ok(b2.Dense(host, np.zeros((n, 1))), b2.Dense(host, np.zeros((n, 1))))
-    bv = np.random.default_rng(1).standard_normal((n, 1))
-    xh = b2.Dense(host, np.full((n, 1), 3.0))
-    a.apply(b2.Dense(host, bv), xh)
-    xd = b2.Dense.zeros(cuda, n, 1)
-    a.apply(b2.Dense(cuda, bv), xd)
-    np.testing.assert_array_equal(np.asarray(xh.data), np.asarray(xd.data))
-    a.apply(b2.Dense(host, 2 * bv), xh)  # plan and buffers reused
-    np.testing.assert_array_equal(np.asarray(xh.data), 2 * np.asarray(xd.data))
+    old = Csr.HOST_STREAM
+    Csr.HOST_STREAM = mode
+    try:
+        assert a._pipeline_ok(b2.Dense(host, np.zeros((n, 1)), value_dtype=dtype),
+                              b2.Dense(host, np.zeros((n, 1)), value_dtype=dtype))
+        bv = np.random.default_rng(1).standard_normal((n, 1))
+        xh = b2.Dense(host, np.full((n, 1), 3.0), value_dtype=dtype)
+        a.apply(b2.Dense(host, bv, value_dtype=dtype), xh)
+        xd = b2.Dense.zeros(cuda, n, 1, value_dtype=dtype)
+        a.apply(b2.Dense(cuda, bv, value_dtype=dtype), xd)
+        np.testing.assert_array_equal(np.asarray(xh.data), np.asarray(xd.data))
+        for f in (2.0, 0.5, 4.0):  # plan, flags (epochs) and buffers reused; exact scalings
+            a.apply(b2.Dense(host, f * bv, value_dtype=dtype), xh)
+            np.testing.assert_array_equal(np.asarray(xh.data), f * np.asarray(xd.data))
+    finally:
+        Csr.HOST_STREAM = old
+
+
+def test_host_stream_rejects_pageable(cuda):
+    """The host-stream kernel needs page-locked operands: plain NumPy memory
+    is refused with ParameterError (the Python layer never sends it there)."""
+    from paper_2006_16852_b200 import _lib, problems
+    from paper_2006_16852_b200.errors import ParameterError
+    import torch
+
+    a = problems.stencil(cuda, "27pt", 16)
+    n = a.size.rows
+    P = a._host_stream_plan()
+    b = np.ones(n)
+    x = np.zeros(n)
+    with pytest.raises(ParameterError, match="pinned"):
+        _lib.call("csr_spmv_host_f64", n, n, a._rp.data_ptr(), a._ci.data_ptr(), a._v.data_ptr(), b.ctypes.data,
+                  P["b"].data_ptr(), x.ctypes.data, P["need"].data_ptr(), P["tile"], P["flags"].data_ptr(), 1,
+                  a.subwarp(), a.exec.stream)
+    torch.cuda.synchronize()
