@@ -1149,31 +1149,73 @@ coo_kernel_seg(int64_t nnz, const int* __restrict__ rows, const int* __restrict_
     }
 }
 
+// Carry fix-up: the owner of a row shared by several chunks (the chunk holding
+// the row's first entries) adds the head partials of the chunks that follow
+// it in chunk order. Chains of up to COO_FIX_SERIAL chunks are summed by the
+// owner thread; a longer chain (a row of thousands of entries: the power
+// law's 50k rows span ~200 chunks and serialised this pass for ~110 us) is
+// summed by the owner's whole warp, lanes striding over the chain and a
+// shuffle tree combining them (deterministic: the order depends only on the
+// chain length).
+constexpr int COO_FIX_SERIAL = 32;
+
 template <typename T, bool XIN>
-__global__ void coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
-                                 const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
-                                 T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
-                                 const T* __restrict__ xin, int64_t xins) {
+__global__ void __launch_bounds__(256)
+coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
+                 const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
+                 T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+                 const T* __restrict__ xin, int64_t xins) {
     if (alpha.skip()) return;
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nchunks) return;
-    const int64_t e0 = c * chunk, e1 = min(e0 + (int64_t)chunk, nnz);
-    const int head_row = rows[e0], tail_row = rows[e1 - 1];
-    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
-    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
-    const bool single = head_row == tail_row;
-    if (!tail_shared || (single && head_shared)) return;  // not the owner of a shared row
-    T sum = single ? carry_head[c] : carry_tail[c];
-    for (int64_t u = c + 1; u < nchunks; ++u) {
-        sum += carry_head[u];
-        const int64_t f0 = u * chunk, f1 = min(f0 + (int64_t)chunk, nnz);
-        const bool u_single = rows[f0] == rows[f1 - 1];
-        const bool u_tail_shared = f1 < nnz && rows[f1] == rows[f1 - 1];
-        if (!(u_single && u_tail_shared)) break;
+    const int lane = threadIdx.x & 31;
+    bool is_long = false, single = false;
+    int tail_row = 0;
+    if (c < nchunks) {
+        const int64_t e0 = c * chunk, e1 = min(e0 + (int64_t)chunk, nnz);
+        const int head_row = rows[e0];
+        tail_row = rows[e1 - 1];
+        const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
+        const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+        single = head_row == tail_row;
+        if (tail_shared && !(single && head_shared)) {  // owner of a shared row
+            const int64_t probe = c + COO_FIX_SERIAL + 1;
+            is_long = probe < nchunks && rows[probe * chunk] == tail_row;
+            if (!is_long) {
+                T sum = single ? carry_head[c] : carry_tail[c];
+                for (int64_t u = c + 1; u < nchunks; ++u) {
+                    sum += carry_head[u];
+                    const int64_t f0 = u * chunk, f1 = min(f0 + (int64_t)chunk, nnz);
+                    const bool u_single = rows[f0] == rows[f1 - 1];
+                    const bool u_tail_shared = f1 < nnz && rows[f1] == rows[f1 - 1];
+                    if (!(u_single && u_tail_shared)) break;
+                }
+                T out = alpha.get() * sum;
+                if (XIN) out += beta.get() * xin[(int64_t)tail_row * xins];
+                x[(int64_t)tail_row * xs] = out;
+            }
+        }
     }
-    T out = alpha.get() * sum;
-    if (XIN) out += beta.get() * xin[(int64_t)tail_row * xins];
-    x[(int64_t)tail_row * xs] = out;
+    // long chains: the owner's warp sums them (every lane is still here)
+    unsigned longs = __ballot_sync(0xffffffffu, is_long);
+    while (longs) {
+        const int src = __ffs(longs) - 1;
+        longs &= longs - 1;
+        const int64_t oc = __shfl_sync(0xffffffffu, c, src);
+        const int row = __shfl_sync(0xffffffffu, tail_row, src);
+        T acc = 0;
+        // the chain: every later chunk whose first entry is still in `row`
+        for (int64_t u = oc + 1 + lane;; u += 32) {
+            const bool in = u < nchunks && rows[u * chunk] == row;
+            if (in) acc += carry_head[u];
+            if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;
+        }
+        acc = warp_sum(acc);
+        if (lane == src) {
+            T out = alpha.get() * ((single ? carry_head[oc] : carry_tail[oc]) + acc);
+            if (XIN) out += beta.get() * xin[(int64_t)row * xins];
+            x[(int64_t)row * xs] = out;
+        }
+    }
 }
 
 template <typename T>
