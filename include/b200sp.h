@@ -160,8 +160,13 @@ int64_t b200sp_csr_tma_stage_bytes(int32_t value_bytes, int32_t rows_per_tile, i
  * reduced sub-warp-per-row from global memory, long rows and the carried-out
  * row by the whole CTA. Plan once per matrix: tile = b200sp_csr_lb_tile(vb,
  * mode), coords = 2*(num_tiles+1) int32; workspace carry_row / carry_val
- * num_tiles each. */
+ * num_tiles each. mode 3 ("nnz split", skewed rows): warp chunks of
+ * tile = b200sp_csr_lb_tile(vb, 3) nonzeros reduced like Coo, rows derived
+ * from row_ptrs; coords = the chunk start rows from b200sp_csr_seg_plan
+ * (nchunks + 1 int32, nchunks = ceil(nnz / tile)), carry_row = nchunks int32
+ * (chunk tail rows), carry_val = 2 * nchunks values. */
 int32_t b200sp_csr_lb_tile(int32_t value_bytes, int32_t mode);
+int b200sp_csr_seg_plan(int64_t n, int64_t nnz, const int32_t* row_ptrs, int32_t* chunk_rows, void* stream);
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t tile);
 int b200sp_csr_lb_plan(int64_t n, int64_t nnz, const int32_t* row_ptrs, int32_t tile, int32_t* coords,
                        void* stream);

@@ -108,6 +108,7 @@ _UNTYPED = {
     "csr_tile_chunks": ("lppilpp", ctypes.c_int),
     "csr_tma_stage_bytes": ("iii", ctypes.c_int64),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
+    "csr_seg_plan": ("llppp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),
     "coo_to_csr_ptrs": ("llppp", ctypes.c_int),

@@ -921,48 +921,17 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
 // ===========================================================================
 constexpr int COO_BLOCK = 256;
 
-// MINB: 6 CTAs per SM (<= 40 registers) measured best for fp32 (0.70 vs
-// 0.63 of the roofline), unbounded (62 registers) for fp64 (0.645 vs 0.55).
-template <typename T, bool XIN, bool VEC, int E>
-__device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
-           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
-           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
-           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
-    constexpr int CHUNK = 32 * E;
+// The segmented reduction of one warp chunk (shared by Coo and the Csr
+// nnz-split strategy): r[i] / p[i] = row and product of the lane's entries
+// (r = INT_MAX past the chunk end), head/tail = rows of the chunk's first /
+// last entry and whether they continue into the previous / next chunk.
+template <typename T, bool XIN, int E>
+__device__ __forceinline__ void coo_segments(int64_t c, int64_t e0, int64_t e1, int cnt, const int (&r)[E],
+                                             const T (&p)[E], int head_row, int tail_row, bool head_shared,
+                                             bool tail_shared, T a, T bt, T* __restrict__ x, int64_t xs,
+                                             const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head,
+                                             T* __restrict__ carry_tail) {
     const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t e0 = c * CHUNK;
-    if (e0 >= nnz) return;
-    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
-    const int head_row = rows[e0], tail_row = rows[e1 - 1];
-    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
-    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
-    const T a = alpha.get();
-    const T bt = XIN ? beta.get() : T(0);
-
-    const int64_t l0 = e0 + (int64_t)lane * E;
-    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
-    int r[E], cc[E];
-    T vv[E];
-    if (VEC && cnt == E) {
-        // streaming loads measured best on C2 (0.646 vs 0.623 with
-        // L1-allocating ones; the power law prefers L1: 0.39 vs 0.36)
-        ld_stream_vec<E>(rows + l0, r);
-        ld_stream_vec<E>(cols + l0, cc);
-        ld_stream_vec<E>(vals + l0, vv);
-    } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-            const bool ok = i < cnt;
-            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
-            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
-            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
-        }
-    }
-    T p[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
-
     // lane-local runs: the first completed run may continue from earlier
     // lanes (needs the scan), later completed runs are final
     int cur = r[0], first_row = INT_MIN;
@@ -1038,6 +1007,51 @@ __device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ ro
             carry_tail[c] = sv;
         }
     }
+}
+
+// MINB: 6 CTAs per SM (<= 40 registers) measured best for fp32 (0.70 vs
+// 0.63 of the roofline), unbounded (62 registers) for fp64 (0.645 vs 0.55).
+template <typename T, bool XIN, bool VEC, int E>
+__device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
+           const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
+           int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
+           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    constexpr int CHUNK = 32 * E;
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = c * CHUNK;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
+    const int head_row = rows[e0], tail_row = rows[e1 - 1];
+    const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
+    const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+
+    const int64_t l0 = e0 + (int64_t)lane * E;
+    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
+    int r[E], cc[E];
+    T vv[E];
+    if (VEC && cnt == E) {
+        // streaming loads measured best on C2 (0.646 vs 0.623 with
+        // L1-allocating ones; the power law prefers L1: 0.39 vs 0.36)
+        ld_stream_vec<E>(rows + l0, r);
+        ld_stream_vec<E>(cols + l0, cc);
+        ld_stream_vec<E>(vals + l0, vv);
+    } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const bool ok = i < cnt;
+            r[i] = ok ? ld_stream(rows + l0 + i) : INT_MAX;
+            cc[i] = ok ? ld_stream(cols + l0 + i) : 0;
+            vv[i] = ok ? ld_stream(vals + l0 + i) : T(0);
+        }
+    }
+    T p[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
+    coo_segments<T, XIN, E>(c, e0, e1, cnt, r, p, head_row, tail_row, head_shared, tail_shared, a, bt, x, xs,
+                            xin, xins, carry_head, carry_tail);
 }
 
 #define COO_ARGS                                                                                         \
@@ -1159,10 +1173,25 @@ coo_kernel_seg(int64_t nnz, const int* __restrict__ rows, const int* __restrict_
 // chain length).
 constexpr int COO_FIX_SERIAL = 32;
 
-template <typename T, bool XIN>
+// rows of a chunk's first / last entry: read from the Coo row indices, or
+// (Csr nnz-split) from the plan's chunk start rows and the kernel's tail rows
+struct CooChunkRows {
+    const int* rows;
+    int chunk;
+    int64_t nnz;
+    __device__ int head(int64_t c) const { return rows[c * chunk]; }
+    __device__ int tail(int64_t c) const { return rows[min((c + 1) * chunk, nnz) - 1]; }
+};
+struct CsrChunkRows {
+    const int* srow;
+    const int* ctail;
+    __device__ int head(int64_t c) const { return srow[c]; }
+    __device__ int tail(int64_t c) const { return ctail[c]; }
+};
+
+template <typename T, bool XIN, class Rows>
 __global__ void __launch_bounds__(256)
-coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict__ rows,
-                 const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
+coo_fixup_kernel(int64_t nchunks, Rows R, const T* __restrict__ carry_head, const T* __restrict__ carry_tail,
                  T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
                  const T* __restrict__ xin, int64_t xins) {
     if (alpha.skip()) return;
@@ -1171,22 +1200,21 @@ coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict_
     bool is_long = false, single = false;
     int tail_row = 0;
     if (c < nchunks) {
-        const int64_t e0 = c * chunk, e1 = min(e0 + (int64_t)chunk, nnz);
-        const int head_row = rows[e0];
-        tail_row = rows[e1 - 1];
-        const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
-        const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
+        const int head_row = R.head(c);
+        tail_row = R.tail(c);
+        const bool head_shared = c > 0 && R.tail(c - 1) == head_row;
+        const bool tail_shared = c + 1 < nchunks && R.head(c + 1) == tail_row;
         single = head_row == tail_row;
         if (tail_shared && !(single && head_shared)) {  // owner of a shared row
             const int64_t probe = c + COO_FIX_SERIAL + 1;
-            is_long = probe < nchunks && rows[probe * chunk] == tail_row;
+            is_long = probe < nchunks && R.head(probe) == tail_row;
             if (!is_long) {
                 T sum = single ? carry_head[c] : carry_tail[c];
                 for (int64_t u = c + 1; u < nchunks; ++u) {
                     sum += carry_head[u];
-                    const int64_t f0 = u * chunk, f1 = min(f0 + (int64_t)chunk, nnz);
-                    const bool u_single = rows[f0] == rows[f1 - 1];
-                    const bool u_tail_shared = f1 < nnz && rows[f1] == rows[f1 - 1];
+                    const int u_tail = R.tail(u);
+                    const bool u_single = R.head(u) == u_tail;
+                    const bool u_tail_shared = u + 1 < nchunks && R.head(u + 1) == u_tail;
                     if (!(u_single && u_tail_shared)) break;
                 }
                 T out = alpha.get() * sum;
@@ -1205,7 +1233,7 @@ coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict_
         T acc = 0;
         // the chain: every later chunk whose first entry is still in `row`
         for (int64_t u = oc + 1 + lane;; u += 32) {
-            const bool in = u < nchunks && rows[u * chunk] == row;
+            const bool in = u < nchunks && R.head(u) == row;
             if (in) acc += carry_head[u];
             if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;
         }
@@ -1216,6 +1244,163 @@ coo_fixup_kernel(int64_t nnz, int chunk, int64_t nchunks, const int* __restrict_
             x[(int64_t)row * xs] = out;
         }
     }
+}
+
+// ===========================================================================
+// Csr, load-balanced strategy mode 3 ("nnz split"): the Coo kernel's warp
+// chunks of 32 x SEG_E consecutive nonzeros, with each entry's row derived
+// from the row pointers instead of read from a row-index array. The plan
+// holds the row of every chunk's first entry (srow[c]); a lane binary-
+// searches its first entry's row inside [srow[c], srow[c+1]] and walks
+// row_ptrs from there. Empty rows are written by the lane whose entry starts
+// the next non-empty row
+// (trailing ones by the last lane). Chunk carries and the fix-up are the
+// Coo ones (the kernel records each chunk's tail row for the fix-up). For
+// skewed row lengths (the C3 power law): every warp gets the same number
+// of nonzeros and all of a lane's gathers are independent.
+// ===========================================================================
+constexpr int SEG_E = 8;
+constexpr int SEG_CHUNK = 32 * SEG_E;
+
+// srow[c] = row of chunk c's first entry; srow[nchunks] = n
+__global__ void csr_seg_plan_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, int64_t nchunks,
+                                    int* __restrict__ srow) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > nchunks) return;
+    if (t == nchunks) {
+        srow[t] = (int)n;
+        return;
+    }
+    const int64_t e = t * SEG_CHUNK;
+    int64_t lo = 0, hi = n - 1;  // largest row r with rp[r] <= e
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (rp[mid] <= e) lo = mid;
+        else hi = mid - 1;
+    }
+    srow[t] = (int)lo;
+}
+
+template <typename T, bool XIN, bool VEC>
+__global__ void __launch_bounds__(COO_BLOCK)
+csr_seg_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
+               const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
+               Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins, const int* __restrict__ srow,
+               int* __restrict__ ctail, T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+    if (alpha.skip()) return;
+    constexpr int E = SEG_E;
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = c * SEG_CHUNK;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(e0 + (int64_t)SEG_CHUNK, nnz);
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
+    auto write_empty = [&](int64_t q) {
+        T out = a * T(0);
+        if (XIN) out += bt * xin[q * xins];
+        x[q * xs] = out;
+    };
+    const int64_t l0 = e0 + (int64_t)lane * E;
+    const int cnt = (int)max((int64_t)0, min((int64_t)E, e1 - l0));
+    int cc[E];
+    T vv[E];
+    if (VEC && cnt == E) {
+        ld_cached_vec<E>(ci + l0, cc);  // L1-allocating: measured better on the power law (as Coo)
+        ld_cached_vec<E>(v + l0, vv);
+    } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const bool ok = i < cnt;
+            cc[i] = ok ? __ldg(ci + l0 + i) : 0;
+            vv[i] = ok ? __ldg(v + l0 + i) : T(0);
+        }
+    }
+    T p[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) p[i] = i < cnt ? vv[i] * ld_gather(b + (int64_t)cc[i] * bs) : T(0);
+
+    // rows of the lane's entries: binary search for the first one inside the
+    // chunk's row range, then a walk over row_ptrs (L1 hits, issued while the
+    // gathers are in flight). Measured alternatives (profiles/r02_c3_lb3.txt):
+    // a per-lane start-row plan (0.5 B per nonzero) 444 vs 433 us on C3, a
+    // shuffle search over a 32-row window 521 us
+    const int head_row = srow[c];
+    int r[E];
+    int cur = head_row;
+    if (cnt > 0) {
+        int lo = head_row, hi = min(srow[c + 1], (int)n - 1);
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(rp + mid) <= l0) lo = mid;
+            else hi = mid - 1;
+        }
+        cur = lo;
+        if (__ldg(rp + cur) == l0)  // the empty rows just before a row starting here
+            for (int q = cur - 1; q >= 0 && __ldg(rp + q) == l0; --q) write_empty(q);
+        int nend = __ldg(rp + cur + 1);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            if (i < cnt) {
+                const int e = (int)(l0 + i);
+                while (e >= nend) {
+                    ++cur;
+                    nend = __ldg(rp + cur + 1);
+                    if (nend <= e) write_empty(cur);
+                }
+                r[i] = cur;
+            } else {
+                r[i] = INT_MAX;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) r[i] = INT_MAX;
+    }
+    const int last_lane = (int)((e1 - 1 - e0) / E);
+    const int tail_row = __shfl_sync(0xffffffffu, cur, last_lane);
+    const bool head_shared = e0 > 0 && __ldg(rp + head_row) < e0;
+    const bool tail_shared = e1 < nnz && __ldg(rp + tail_row + 1) > e1;
+    if (lane == last_lane) {
+        ctail[c] = tail_row;
+        if (e1 == nnz)
+            for (int64_t q = (int64_t)tail_row + 1; q < n; ++q) write_empty(q);  // trailing empty rows
+    }
+    coo_segments<T, XIN, E>(c, e0, e1, cnt, r, p, head_row, tail_row, head_shared, tail_shared, a, bt, x, xs,
+                            xin, xins, carry_head, carry_tail);
+}
+
+template <typename T>
+static int csr_seg(int64_t n, int64_t nnz, const int* rp, const int* ci, const T* v, const T* b, int64_t bs, T* x,
+                   int64_t xs, T alpha, const T* alpha_dev, T beta, const T* beta_dev, const T* xin, int64_t xins,
+                   const int* srow, int* ctail, T* carry, int tile, void* stream) {
+    if (n == 0) return B200SP_OK;
+    B200SP_REQUIRE(tile == SEG_CHUNK, B200SP_EINVAL, "csr lb mode 3: tile must be %d (got %d)", SEG_CHUNK, tile);
+    B200SP_REQUIRE(nnz < INT_MAX - SEG_CHUNK, B200SP_EINVAL, "csr lb mode 3: nnz must fit int32 entry indices");
+    if (nnz == 0)  // every row empty: the classical kernel writes alpha * 0 + beta * x_in
+        return csr_classical<T>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, 1, stream);
+    cudaStream_t st = as_stream(stream);
+    Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
+    const int64_t nchunks = ceil_div(nnz, SEG_CHUNK);
+    T* carry_head = carry;
+    T* carry_tail = carry + nchunks;
+    const unsigned grid = (unsigned)ceil_div(nchunks * 32, COO_BLOCK);
+    const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
+    const bool vec = aligned16(ci) && aligned16(v);
+    const CsrChunkRows R{srow, ctail};
+#define SEG_LAUNCH(XI, VE)                                                                                   \
+    csr_seg_kernel<T, XI, VE><<<grid, COO_BLOCK, 0, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, \
+                                                          srow, ctail, carry_head, carry_tail)
+    if (xin) {
+        if (vec) SEG_LAUNCH(true, true); else SEG_LAUNCH(true, false);
+        coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nchunks, R, carry_head, carry_tail, x, xs, al, be, xin, xins);
+    } else {
+        if (vec) SEG_LAUNCH(false, true); else SEG_LAUNCH(false, false);
+        coo_fixup_kernel<T, false><<<fgrid, 256, 0, st>>>(nchunks, R, carry_head, carry_tail, x, xs, al, be, xin, xins);
+    }
+#undef SEG_LAUNCH
+    count_launch(2);
+    return check_launch("csr_seg");
 }
 
 template <typename T>
@@ -1251,10 +1436,10 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
     } while (0)
     if (xin) {
         if (vec) COO_LAUNCH(true, true); else COO_LAUNCH(true, false);
-        coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nnz, chunk, nchunks, rows, carry_head, carry_tail, x, xs, al, be, xin, xins);
+        coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nchunks, CooChunkRows{rows, chunk, nnz}, carry_head, carry_tail, x, xs, al, be, xin, xins);
     } else {
         if (vec) COO_LAUNCH(false, true); else COO_LAUNCH(false, false);
-        coo_fixup_kernel<T, false><<<fgrid, 256, 0, st>>>(nnz, chunk, nchunks, rows, carry_head, carry_tail, x, xs, al, be, xin, xins);
+        coo_fixup_kernel<T, false><<<fgrid, 256, 0, st>>>(nchunks, CooChunkRows{rows, chunk, nnz}, carry_head, carry_tail, x, xs, al, be, xin, xins);
     }
 #undef COO_LAUNCH
     count_launch(2);
@@ -1528,7 +1713,17 @@ int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
 }
 
 int32_t b200sp_csr_lb_tile(int32_t value_bytes, int32_t mode) {
+    if (mode == 3) return SEG_CHUNK;
     return value_bytes == 4 ? lb_tile<float>(mode) : lb_tile<double>(mode);
+}
+
+int b200sp_csr_seg_plan(int64_t n, int64_t nnz, const int32_t* rp, int32_t* chunk_rows, void* stream) {
+    if (n == 0) return B200SP_OK;
+    const int64_t nchunks = ceil_div(nnz, SEG_CHUNK);
+    csr_seg_plan_kernel<<<(unsigned)ceil_div(nchunks + 1, 256), 256, 0, as_stream(stream)>>>(n, nnz, rp, nchunks,
+                                                                                           chunk_rows);
+    count_launch();
+    return check_launch("csr_seg_plan");
 }
 
 int64_t b200sp_csr_lb_num_tiles(int64_t n, int64_t nnz, int32_t tile) { return ceil_div(n + nnz, tile); }
@@ -1548,6 +1743,9 @@ int b200sp_csr_spmv_lb_f64(int64_t n, int64_t nnz, const int32_t* rp, const int3
                            const double* beta_dev, const double* xin, int64_t xins,
                            const int32_t* coords, int32_t* carry_row, double* carry_val, int32_t tile,
                            int32_t mode, void* stream) {
+    if (mode == 3)
+        return csr_seg<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords,
+                               carry_row, carry_val, tile, stream);
     return csr_lb<double>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords,
                           carry_row, carry_val, tile, mode, stream);
 }
@@ -1556,6 +1754,9 @@ int b200sp_csr_spmv_lb_f32(int64_t n, int64_t nnz, const int32_t* rp, const int3
                            float alpha, const float* alpha_dev, float beta, const float* beta_dev,
                            const float* xin, int64_t xins, const int32_t* coords,
                            int32_t* carry_row, float* carry_val, int32_t tile, int32_t mode, void* stream) {
+    if (mode == 3)
+        return csr_seg<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords,
+                              carry_row, carry_val, tile, stream);
     return csr_lb<float>(n, nnz, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, coords,
                          carry_row, carry_val, tile, mode, stream);
 }

@@ -508,8 +508,8 @@ class Csr(_Sparse):
         self._stream_stages = int(stream_stages) if stream_stages else None
         self._stream_consumers = int(stream_consumers) if stream_consumers else None
         if lb_mode is not None:
-            if lb_mode not in (1, 2):
-                raise Unsupported("lb_mode must be 1 (item merge) or 2 (row-parallel)")
+            if lb_mode not in (1, 2, 3):
+                raise Unsupported("lb_mode must be 1 (item merge), 2 (row-parallel) or 3 (nnz split)")
             self._lb_mode = int(lb_mode)
         if stream_impl is not None:
             self._stream_impl = stream_impl
@@ -633,14 +633,15 @@ class Csr(_Sparse):
         return min(cap, need), tpr, rpt, gr
 
     def lb_mode(self):
-        """1 = item-level merge (skewed rows: C3 power law 0.28 vs 0.23 of the
-        roofline), 2 = row-parallel tiles (stencils: C2 fp64 0.68 vs 0.43,
-        7-point 0.85 vs 0.44; profiles/r02_lb_sweep.txt)."""
+        """1 = item-level merge, 2 = row-parallel tiles (stencils: C2 fp64 0.68
+        vs 0.43, 7-point 0.85 vs 0.44; profiles/r02_lb_sweep.txt), 3 = nnz
+        split with Coo-style warp chunks (skewed rows: C3 power law 433 us vs
+        497 us merge, 617 us row-parallel; profiles/r02_c3_lb3.txt)."""
         mode = getattr(self, "_lb_mode", None)
         if mode is None:
             n = self.size.rows
             mean = self.nnz / max(n, 1)
-            mode = 1 if n and self._row_stats() > 4 * mean + 64 else 2
+            mode = 3 if n and self._row_stats() > 4 * mean + 64 else 2
         return mode
 
     def lb_plan(self):
@@ -650,6 +651,14 @@ class Csr(_Sparse):
             vb = self._v.element_size()
             mode = self.lb_mode()
             tile = int(_lib.query("csr_lb_tile", vb, mode))
+            if mode == 3:  # nnz split: chunk start rows, chunk tail rows, head + tail carries
+                nt = (nnz + tile - 1) // tile
+                coords = torch.empty(nt + 1, dtype=torch.int32, device=exc.device)
+                _lib.call("csr_seg_plan", n, nnz, ptr(self._rp), ptr(coords), exc.stream)
+                carry_row = torch.empty(max(nt, 1), dtype=torch.int32, device=exc.device)
+                carry_val = torch.empty(max(2 * nt, 1), dtype=self._v.dtype, device=exc.device)
+                self._plan = (coords, carry_row, carry_val, tile, mode)
+                return self._plan
             nt = int(_lib.query("csr_lb_num_tiles", n, nnz, tile))
             coords = torch.empty(2 * (nt + 1), dtype=torch.int32, device=exc.device)
             _lib.call("csr_lb_plan", n, nnz, ptr(self._rp), tile, ptr(coords), exc.stream)

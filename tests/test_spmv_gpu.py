@@ -22,6 +22,7 @@ FORMATS = [
     ("csr", {"strategy": "load_balance"}),
     ("csr", {"strategy": "load_balance", "impl": "lb1"}),
     ("csr", {"strategy": "load_balance", "impl": "lb2"}),
+    ("csr", {"strategy": "load_balance", "impl": "lb3"}),
     ("csr", {"strategy": "stream"}),
     ("csr", {"strategy": "stream", "impl": "tma"}),
     ("csr", {"strategy": "stream", "impl": "tma", "rpt": 4, "cap": 64, "stages": 3}),
@@ -36,14 +37,14 @@ FORMATS = [
     ("hybrid", {"strategy": "imbalance"}),
     ("hybrid", {"strategy": "col1"}),
 ]
-IDS = ["csr_classical", "csr_lb", "csr_lb_merge", "csr_lb_rows", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
+IDS = ["csr_classical", "csr_lb", "csr_lb_merge", "csr_lb_rows", "csr_lb_nnz", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
        "hybrid_col1"]
 
 
 def make(b2, exc, data, fmt, kw, dtype="float64"):
     kw = dict(kw)
     impl = kw.pop("impl", None)
-    if impl in ("lb1", "lb2"):
+    if impl in ("lb1", "lb2", "lb3"):
         a = b2.matrix_from_data(exc, data, fmt, value_dtype=dtype, **kw)
         a.set_strategy("load_balance", lb_mode=int(impl[-1]))
         return a
