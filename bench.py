@@ -405,6 +405,7 @@ def c5_sub(args, world, rank, local, head):
                 "scaling": "strong", "timed_solves": sub_args.steps}
         if "breakdown" in r["config"]:
             keep["breakdown"] = r["config"]["breakdown"]
+            keep["halo"] = r["config"].get("halo")
         if r.get("roofline"):
             keep["frac_of_hbm_peak"] = r["roofline"]["frac"]
         return keep

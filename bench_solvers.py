@@ -243,8 +243,14 @@ def _dist_breakdown(A, comm, solver, world, reps=30):
     def allreduce():
         comm.allreduce_(red)
 
+    cases = [("compute_ms", compute), ("halo_ms", halo), ("allreduce_ms", allreduce)]
+    peer = getattr(A, "_peer_halo", {}).get(torch.float64)
+    if peer is not None:  # the halo the solve used: peer stores fused into step1 + the flag wait
+        cases += [("step1_ms", lambda: _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), ptr(ctl), exc.stream)),
+                  ("step1_peer_put_wait_ms", lambda: (peer.step1(nl, p, r, ptr(ctl), suf, exc.stream),
+                                                      peer.wait(ptr(ctl), exc.stream)))]
     out = {}
-    for name, fn in (("compute_ms", compute), ("halo_ms", halo), ("allreduce_ms", allreduce)):
+    for name, fn in cases:
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -293,7 +299,8 @@ def bench_c5_distributed(args, world, rank, local):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated 7-point Poisson, b = ones, x0 = 0)",
             "config": {"workload": f"C5: row-partitioned CG, 3-D 7-point Poisson {g}^3, RNR 1e-8, "
-                                   f"NCCL halo + all-reduce", "iterations": its,
+                                   f"{'peer-memory' if solver.halo == 'peer' else 'NCCL'} halo + NCCL all-reduce",
+                       "halo": solver.halo, "iterations": its,
                        "converged": bool(st.converged), "parallelism": f"row partition x{world}",
                        "rows_per_rank": A.n_local, "build_s": round(build_s, 3), "breakdown": brk},
             "gpu_launches": None, "clocks": clk.summary()}

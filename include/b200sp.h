@@ -473,6 +473,22 @@ int b200sp_mm_parse(const char* buf, int64_t len, const int64_t* info, int32_t t
  * has no distributed matrix. */
 int b200sp_krylov_set_dist(void* ctl, int32_t dist, void* stream);
 int64_t b200sp_krylov_red_offset(void);
+/* Peer-memory halo for the distributed CG (CUDA IPC over NVLink/NVSwitch):
+ * cg_step1_put = CgStep1 (p = z + beta p, steps.py:93-119) that also stores
+ * local rows [lo[k], hi[k]) into dst[k] (a peer's ghost slots, mapped) and,
+ * once every CTA's stores are out, writes epoch to flag[k] (this rank's slot
+ * in the peer's flag array; release, system scope). ticket: one zeroed
+ * uint32. peer_wait: a one-thread kernel returning once every flags[k] >=
+ * epoch (acquire) -- order the ghost SpMV after it. Both skip when the
+ * solve is done. At most b200sp_peer_max() puts, twice that many waits. */
+int32_t b200sp_peer_max(void);
+int b200sp_cg_step1_put_f64(int64_t n, double* p, const double* z, const void* ctl, int32_t nput, const int64_t* lo,
+                            const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,
+                            uint32_t* ticket, void* stream);
+int b200sp_cg_step1_put_f32(int64_t n, float* p, const float* z, const void* ctl, int32_t nput, const int64_t* lo,
+                            const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,
+                            uint32_t* ticket, void* stream);
+int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream);
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream);
 /* FCG (src/solvers/krylov.py:80-125) reuses cg_init / cg_step1 / the fused
  * SpMV + sigma; fcg_init_ctl seeds rho_t = 0 after cg_init, fcg_step2 also

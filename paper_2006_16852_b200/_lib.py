@@ -61,6 +61,7 @@ _TYPED = {
     # Krylov (JAC = l p p p p)
     "cg_init": "lppp" + "lpppp" + "pppp",
     "cg_step1": "lpppp",
+    "cg_step1_put": "lpppippppipp",
     "cg_sigma": "lppppp",
     "cg_coop": "lppppppppppp",
     "csr_spmv_dot": "lppppppiippp",
@@ -109,6 +110,8 @@ _UNTYPED = {
     "csr_tma_stage_bytes": ("iii", ctypes.c_int64),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_seg_plan": ("llppp", ctypes.c_int),
+    "peer_max": ("", ctypes.c_int32),
+    "peer_wait": ("pipip", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),
     "coo_to_csr_ptrs": ("llppp", ctypes.c_int),

@@ -26,3 +26,7 @@ CG_COOP_MAX_ROWS = int(os.environ.get("B200SP_CG_COOP_MAX_ROWS", str(1 << 20)))
 #: CG / BiCGSTAB on a classical-strategy Csr fuse the reduction after each
 #: SpMV into its epilogue (csr_spmv_dot); False runs SpMV + dot kernels
 FUSED_SPMV_DOT = os.environ.get("B200SP_FUSED_SPMV_DOT", "1") != "0"
+# distributed CG halo: "auto" = peer memory (CUDA IPC) under NCCL when every
+# send is a row range, "1" = force it (also over gloo: ranks sharing one GPU),
+# "0" = NCCL send/recv
+PEER_HALO = os.environ.get("B200SP_PEER_HALO", "auto")

@@ -83,6 +83,75 @@ __global__ void gather_kernel(int64_t count, const int* __restrict__ idx, const 
 
 __global__ void krylov_set_dist_kernel(KrylovCtl* c, int dist) { c->dist = dist; }
 
+// ---------------------------------------------------------------------------
+// Halo exchange through peer memory (CUDA IPC; NVLink / NVSwitch between
+// GPUs). The CG step that updates p (CgStep1, steps.py:93-119) also stores
+// each boundary row it produces straight into the ghost slots of the
+// neighbour that needs it, so the exchange rides on the kernel that
+// computes the values -- no pack, no separate transfer. The grid's last CTA
+// (ticket) then raises this rank's flag in every destination's flag array
+// (release at system scope). A destination's ghost SpMV is ordered after a
+// one-thread wait kernel that acquires its flags. Sends must be row ranges
+// (slab partitions); buffer reuse across iterations is ordered by the two
+// all-reduces every iteration performs.
+// ---------------------------------------------------------------------------
+constexpr int PEER_MAX = 4;
+struct PeerPut {
+    int n;
+    int64_t lo[PEER_MAX], hi[PEER_MAX];  // local rows [lo, hi) go to ...
+    void* dst[PEER_MAX];                 // ... the peer's ghost slots (mapped peer memory)
+    int* flag[PEER_MAX];                 // this rank's flag slot in the peer's flag array
+};
+struct PeerWait {
+    int n;
+    const int* flag[2 * PEER_MAX];
+};
+
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+cg_step1_put_kernel(int64_t n, T* __restrict__ p, const T* __restrict__ z, const KrylovCtl* c, PeerPut pp,
+                    int epoch, unsigned* ticket) {
+    if (c->done) return;
+    const T beta = (T)c->beta;
+    bool wrote = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = z[i] + beta * p[i];
+        p[i] = v;
+#pragma unroll
+        for (int k = 0; k < PEER_MAX; ++k)
+            if (k < pp.n && i >= pp.lo[k] && i < pp.hi[k]) {
+                static_cast<T*>(pp.dst[k])[i - pp.lo[k]] = v;
+                wrote = true;
+            }
+    }
+    if (wrote) __threadfence_system();  // this thread's peer stores before the CTA's arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        if (t == gridDim.x - 1) {  // every CTA's stores are out: raise the flags
+            __threadfence_system();
+            *ticket = 0;
+            for (int k = 0; k < pp.n; ++k) st_release_sys(pp.flag[k], epoch);
+        }
+    }
+}
+
+__global__ void peer_wait_kernel(const KrylovCtl* c, PeerWait w, int epoch) {
+    if (c->done) return;
+    for (int k = 0; k < w.n; ++k)
+        while (ld_acquire_sys(w.flag[k]) < epoch) __nanosleep(256);
+}
+
 }  // namespace b200sp
 
 using namespace b200sp;
@@ -135,5 +204,44 @@ int b200sp_krylov_set_dist(void* ctl, int32_t dist, void* stream) {
     return check_launch("krylov_set_dist");
 }
 int64_t b200sp_krylov_red_offset(void) { return (int64_t)offsetof(KrylovCtl, red); }
+
+int32_t b200sp_peer_max(void) { return PEER_MAX; }
+
+#define PEER_PUT_DEF(SUF, T)                                                                                  \
+    int b200sp_cg_step1_put_##SUF(int64_t n, T* p, const T* z, const void* ctl, int32_t nput, const int64_t* lo, \
+                                  const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,     \
+                                  uint32_t* ticket, void* stream) {                                             \
+        B200SP_REQUIRE(nput >= 0 && nput <= PEER_MAX, B200SP_EINVAL, "cg_step1_put: at most %d peers (got %d)", \
+                       PEER_MAX, nput);                                                                         \
+        B200SP_REQUIRE(epoch > 0, B200SP_EINVAL, "cg_step1_put: epoch must be positive");                       \
+        if (n <= 0) return B200SP_OK;                                                                           \
+        PeerPut pp{};                                                                                           \
+        pp.n = nput;                                                                                            \
+        for (int k = 0; k < nput; ++k) {                                                                        \
+            pp.lo[k] = lo[k];                                                                                   \
+            pp.hi[k] = hi[k];                                                                                   \
+            pp.dst[k] = dst[k];                                                                                 \
+            pp.flag[k] = flag[k];                                                                               \
+        }                                                                                                       \
+        cg_step1_put_kernel<T><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(n, p, z, (const KrylovCtl*)ctl, \
+                                                                                    pp, epoch, ticket);         \
+        count_launch();                                                                                         \
+        return check_launch("cg_step1_put");                                                                    \
+    }
+PEER_PUT_DEF(f64, double)
+PEER_PUT_DEF(f32, float)
+#undef PEER_PUT_DEF
+
+int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream) {
+    B200SP_REQUIRE(nwait >= 0 && nwait <= 2 * PEER_MAX, B200SP_EINVAL, "peer_wait: at most %d flags (got %d)",
+                   2 * PEER_MAX, nwait);
+    if (nwait == 0) return B200SP_OK;
+    PeerWait w{};
+    w.n = nwait;
+    for (int k = 0; k < nwait; ++k) w.flag[k] = flags[k];
+    peer_wait_kernel<<<1, 1, 0, as_stream(stream)>>>((const KrylovCtl*)ctl, w, epoch);
+    count_launch();
+    return check_launch("peer_wait");
+}
 
 }  // extern "C"

@@ -16,6 +16,9 @@ across GPUs:
 * ``DistCg``     -- the device-resident CG kernels with the reductions split
   as local sum -> NCCL all-reduce (8-16 bytes) -> control step, two
   all-reduces per iteration (sigma = p.q; rho = r.z with ||r||).
+* ``PeerHalo``   -- the halo as peer-memory stores fused into the step that
+  produces p (CUDA IPC over NVLink/NVSwitch), used instead of NCCL
+  send/recv when the partition allows it.
 Communication goes through ``Comm`` (torch.distributed; NCCL over
 NVLink/NVSwitch in production, gloo for the CPU tests).
 """
@@ -272,6 +275,87 @@ class DistCsr(LinOp):
 
 
 # ---------------------------------------------------------------------------
+# halo through peer memory
+# ---------------------------------------------------------------------------
+class PeerHalo:
+    """The halo exchange as peer-memory stores fused into the CG step that
+    produces the values (b200sp_cg_step1_put): every rank exports its
+    extended vector [owned | ghosts] and a flag array through CUDA IPC (one
+    all_gather of the handles), opens the buffers of the ranks it sends to
+    (peer access over NVLink / NVSwitch is enabled on open), and then
+    writes its boundary rows straight into their ghost slots while updating
+    p, raising its flag in their flag arrays when the kernel's stores are
+    out. The receiver orders its ghost SpMV after b200sp_peer_wait on the
+    flags of the ranks it receives from. No NCCL call, no pack/unpack.
+
+    Valid when every send is a row range (slab partitions) and at most
+    b200sp_peer_max() peers are involved; the iteration's all-reduces order
+    the reuse of the ghost slots from one exchange to the next."""
+
+    def __init__(self, A, dtype):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        comm, exc = A.comm, A.exec
+        dev = exc.device
+        self.A = A
+        self.pext = torch.zeros(A.n_ext, dtype=dtype, device=dev)
+        self.flags = torch.zeros(max(comm.size, 1), dtype=torch.int32, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        mine = {"pext": reduce_tensor(self.pext), "flags": reduce_tensor(self.flags), "nl": A.n_local,
+                "g0": {int(peer): int(g0) for peer, g0, _ in A.plan.recv}}
+        every = comm.allgather_object(mine)
+        self._remote = []  # keep the mapped peer buffers alive
+        lo, hi, dst, flg = [], [], [], []
+        esz = self.pext.element_size()
+        for peer, a, b, idx, _ in A._send:
+            info = every[peer]
+            fn, args = info["pext"]
+            rp_ = fn(*args)
+            fn, args = info["flags"]
+            rf = fn(*args)
+            self._remote.append((rp_, rf))
+            g0 = info["g0"][comm.rank]
+            lo.append(a)
+            hi.append(b)
+            dst.append(rp_.data_ptr() + (info["nl"] + g0) * esz)
+            flg.append(rf.data_ptr() + 4 * comm.rank)
+        k = len(lo)
+        self.nput = k
+        self.lo = (ctypes.c_int64 * max(k, 1))(*lo)
+        self.hi = (ctypes.c_int64 * max(k, 1))(*hi)
+        self.dst = (ctypes.c_void_p * max(k, 1))(*dst)
+        self.flag = (ctypes.c_void_p * max(k, 1))(*flg)
+        waits = [self.flags.data_ptr() + 4 * int(peer) for peer, _, _ in A.plan.recv]
+        self.nwait = len(waits)
+        self.waits = (ctypes.c_void_p * max(self.nwait, 1))(*waits)
+        self.epoch = 0
+        torch.cuda.synchronize(dev)
+
+    @staticmethod
+    def usable(A):
+        """Every send a row range, few enough peers, mode allows it."""
+        mode = config.PEER_HALO
+        if mode == "0" or A.comm.size < 2:
+            return False
+        if mode != "1" and str(A.comm.dist.get_backend(A.comm.group)).lower() != "nccl":
+            return False
+        pmax = int(_lib.query("peer_max"))
+        ranges = all(idx is None for _, _, _, idx, _ in A._send)
+        return ranges and len(A._send) <= pmax and len(A.plan.recv) <= 2 * pmax
+
+    def step1(self, nl, p, z, ctl, suf, stream):
+        """p = z + beta p, boundary rows stored into the peers' ghost slots."""
+        self.epoch += 1
+        _lib.call("cg_step1_put_" + suf, nl, ptr(p), ptr(z), ctl, self.nput, ctypes.addressof(self.lo),
+                  ctypes.addressof(self.hi), ctypes.addressof(self.dst), ctypes.addressof(self.flag), self.epoch,
+                  ptr(self.ticket), stream)
+
+    def wait(self, ctl, stream):
+        _lib.call("peer_wait", ctl, self.nwait, ctypes.addressof(self.waits), self.epoch, stream)
+
+
+# ---------------------------------------------------------------------------
 # distributed CG
 # ---------------------------------------------------------------------------
 class DistCg:
@@ -294,6 +378,25 @@ class DistCg:
         self.part = torch.zeros(int(_lib.query("krylov_part_elems")), dtype=torch.float64, device=dev)
         off = int(_lib.query("krylov_red_offset"))
         self.red = self.ctl[off:off + 32].view(torch.float64)
+
+    def _spmv_sigma_peer(self, peer, pext, p, q, c, pp, suf):
+        """q = A p, sigma parked; the ghosts arrive by peer stores from the
+        neighbours' step1: owned SpMV, wait for the flags, ghost SpMV."""
+        from .solvers.krylov import fused_csr_ok
+
+        A, exc = self.a, self.exec
+        nl = A.n_local
+        own, gh = A.a_own, A.a_ghost
+        own.apply(Dense.wrap(exc, pext[:nl].view(-1, 1)), Dense.wrap(exc, q.view(-1, 1)))
+        peer.wait(c, exc.stream)
+        if gh is None:
+            _lib.call("cg_sigma_" + suf, nl, ptr(p), ptr(q), c, ptr(pp), exc.stream)
+        elif config.FUSED_SPMV_DOT and fused_csr_ok(gh):
+            _lib.call("csr_spmv_dot_" + suf, nl, ptr(gh._rp), ptr(gh._ci), ptr(gh._v), ptr(pext[nl:]), ptr(q),
+                      ptr(p), 4, gh.subwarp(), c, ptr(pp), exc.stream)
+        else:
+            gh.apply_advanced(1.0, Dense.wrap(exc, pext[nl:].view(-1, 1)), 1.0, Dense.wrap(exc, q.view(-1, 1)))
+            _lib.call("cg_sigma_" + suf, nl, ptr(p), ptr(q), c, ptr(pp), exc.stream)
 
     def _spmv_sigma(self, pext, p, q, c, pp, suf):
         """q = A p with the local sigma = p.q parked for the all-reduce. With
@@ -339,7 +442,16 @@ class DistCg:
         _lib.call("krylov_set_dist", c, 1, exc.stream)
         r = torch.empty(nl, dtype=dt, device=exc.device)
         q = torch.empty(nl, dtype=dt, device=exc.device)
-        pext = torch.empty(A.n_ext, dtype=dt, device=exc.device)
+        peer = None
+        if PeerHalo.usable(A):
+            peer = getattr(A, "_peer_halo", {}).get(dt)
+            if peer is None:  # collective: every rank builds it on its first solve of this dtype
+                peer = PeerHalo(A, dt)
+                A.__dict__.setdefault("_peer_halo", {})[dt] = peer
+            pext = peer.pext
+        else:
+            pext = torch.empty(A.n_ext, dtype=dt, device=exc.device)
+        self.halo = "peer" if peer is not None else "nccl"
         p = pext[:nl]
         # r = b - A x  (x staged in the extended vector for its halo)
         pext[:nl].copy_(x)
@@ -357,8 +469,12 @@ class DistCg:
                 if iv[4]:
                     break
                 for _ in range(self.batch):
-                    _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), c, exc.stream)
-                    self._spmv_sigma(pext, p, q, c, pp, suf)
+                    if peer is not None:
+                        peer.step1(nl, p, r, c, suf, exc.stream)
+                        self._spmv_sigma_peer(peer, pext, p, q, c, pp, suf)
+                    else:
+                        _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), c, exc.stream)
+                        self._spmv_sigma(pext, p, q, c, pp, suf)
                     comm.allreduce_(self.red[:1])
                     _lib.call("cg_finish", c, 0, 1, exc.stream)
                     _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(r), *J, c, ptr(pp), 0,

@@ -21,8 +21,10 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, g, out_dir):
+def _worker(rank, world, port, g, out_dir, halo="0"):
     import sys
+
+    os.environ["B200SP_PEER_HALO"] = halo  # read at package import
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, repo)
@@ -57,24 +59,34 @@ def _worker(rank, world, port, g, out_dir):
         solver = DistCg(A, [b2.Iteration(1000), b2.ResidualNormReduction(1e-8)], batch=8)
         st = solver.solve(b, x)
         np.save(os.path.join(out_dir, f"x{rank}.npy"), x.cpu().numpy())
+        x2 = torch.zeros(A.n_local, dtype=torch.float64, device=exc.device)
+        st2 = solver.solve(b, x2)  # again: the peer buffers, flags and epochs are reused
+        same = bool(torch.equal(x, x2)) and st2.iterations == st.iterations
         with open(os.path.join(out_dir, f"st{rank}"), "w") as f:
-            f.write(f"{lo} {hi} {st.iterations} {int(st.converged)} {err}")
+            f.write(f"{lo} {hi} {st.iterations} {int(st.converged)} {err} {solver.halo} {int(same)}")
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_cg_matches_single_gpu(tmp_path, cuda):
+@pytest.mark.parametrize("world,halo", [(2, "0"), (2, "1"), (3, "1")], ids=["2rank-staged", "2rank-peer", "3rank-peer"])
+def test_multi_rank_cg_matches_single_gpu(tmp_path, cuda, world, halo):
+    """halo "1": the ghosts travel by peer stores fused into the p update
+    (CUDA IPC between the ranks' processes; with one GPU they map the same
+    device) and the ghost SpMV waits on the flags -- the NVLink path of a
+    multi-GPU run, minus the link."""
     import paper_2006_16852_b200 as b2
     from paper_2006_16852_b200 import problems
 
     g = 16
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, g, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, port, g, str(tmp_path), halo), nprocs=world, join=True)
     parts, its = [], set()
-    for rank in range(2):
-        lo, hi, it, conv, err = (tmp_path / f"st{rank}").read_text().split()
+    for rank in range(world):
+        lo, hi, it, conv, err, used, same = (tmp_path / f"st{rank}").read_text().split()
         assert float(err) <= 1e-14
         assert int(conv) == 1
+        assert used == ("peer" if halo == "1" else "nccl")
+        assert int(same) == 1
         its.add(int(it))
         parts.append(np.load(tmp_path / f"x{rank}.npy"))
     assert len(its) == 1  # every rank took the same decisions
