@@ -249,6 +249,9 @@ def _dist_breakdown(A, comm, solver, world, reps=30):
         cases += [("step1_ms", lambda: _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), ptr(ctl), exc.stream)),
                   ("step1_peer_put_wait_ms", lambda: (peer.step1(nl, p, r, ptr(ctl), suf, exc.stream),
                                                       peer.wait(ptr(ctl), exc.stream)))]
+    pred = getattr(A, "_peer_reduce", None)
+    if pred is not None:
+        cases.append(("peer_allreduce_ms", lambda: pred.allreduce_(red, exc.stream)))
     out = {}
     for name, fn in cases:
         for _ in range(3):

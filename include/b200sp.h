@@ -489,6 +489,14 @@ int b200sp_cg_step1_put_f32(int64_t n, float* p, const float* z, const void* ctl
                             const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,
                             uint32_t* ticket, void* stream);
 int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream);
+/* All-reduce (sum) of red[0..k), k <= 4, across `world` <= 8 ranks through
+ * peer memory: slots[j] = rank j's slot array (2 * world * 4 doubles, zeroed
+ * once; mapped), flags[j] = rank j's int32 flag array (world entries, zeroed
+ * once); epoch increases by one per call on every rank. Sums in rank order:
+ * identical on every rank. One thread; replaces the 8-32 byte NCCL
+ * all-reduces of the distributed CG. */
+int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, double* const* slots,
+                          int32_t* const* flags, int32_t epoch, void* stream);
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream);
 /* FCG (src/solvers/krylov.py:80-125) reuses cg_init / cg_step1 / the fused
  * SpMV + sigma; fcg_init_ctl seeds rho_t = 0 after cg_init, fcg_step2 also

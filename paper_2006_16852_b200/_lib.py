@@ -112,6 +112,7 @@ _UNTYPED = {
     "csr_seg_plan": ("llppp", ctypes.c_int),
     "peer_max": ("", ctypes.c_int32),
     "peer_wait": ("pipip", ctypes.c_int),
+    "peer_allreduce": ("piiippip", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),
     "coo_to_csr_ptrs": ("llppp", ctypes.c_int),

@@ -146,6 +146,41 @@ cg_step1_put_kernel(int64_t n, T* __restrict__ p, const T* __restrict__ z, const
     }
 }
 
+// All-reduce of the k <= 4 local sums parked in ctl.red, through peer
+// memory: one thread stores them into slot [parity][rank] of every rank's
+// slot array (its own included), raises its flag there, waits for every
+// rank's flag and sums the slots in rank order -- the same order on every
+// rank, so every rank gets the identical result (as with NCCL). Slots are
+// double-buffered by epoch parity: a rank can only write epoch e+1 after
+// every rank raised e+1's predecessor flag, i.e. finished reading epoch e-1.
+constexpr int PEER_RED_MAX = 8;
+struct PeerRed {
+    int world, rank;
+    double* slots[PEER_RED_MAX];  // every rank's slot array (mapped; own local)
+    int* flags[PEER_RED_MAX];     // every rank's flag array
+};
+
+__global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch) {
+    const int par = epoch & 1;
+    double v[4];
+    for (int i = 0; i < k; ++i) v[i] = red[i];
+    for (int j = 0; j < pr.world; ++j) {
+        double* dst = pr.slots[j] + ((size_t)par * pr.world + pr.rank) * 4;
+        for (int i = 0; i < k; ++i) dst[i] = v[i];
+    }
+    __threadfence_system();
+    for (int j = 0; j < pr.world; ++j) st_release_sys(pr.flags[j] + pr.rank, epoch);
+    const int* mine = pr.flags[pr.rank];
+    for (int j = 0; j < pr.world; ++j)
+        while (ld_acquire_sys(mine + j) < epoch) __nanosleep(64);
+    const volatile double* sl = pr.slots[pr.rank] + (size_t)par * pr.world * 4;
+    for (int i = 0; i < k; ++i) {
+        double s = 0;
+        for (int j = 0; j < pr.world; ++j) s += sl[j * 4 + i];
+        red[i] = s;
+    }
+}
+
 __global__ void peer_wait_kernel(const KrylovCtl* c, PeerWait w, int epoch) {
     if (c->done) return;
     for (int k = 0; k < w.n; ++k)
@@ -231,6 +266,24 @@ int32_t b200sp_peer_max(void) { return PEER_MAX; }
 PEER_PUT_DEF(f64, double)
 PEER_PUT_DEF(f32, float)
 #undef PEER_PUT_DEF
+
+int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, double* const* slots,
+                          int32_t* const* flags, int32_t epoch, void* stream) {
+    B200SP_REQUIRE(k >= 1 && k <= 4, B200SP_EINVAL, "peer_allreduce: 1..4 values (got %d)", k);
+    B200SP_REQUIRE(world >= 1 && world <= PEER_RED_MAX && rank >= 0 && rank < world, B200SP_EINVAL,
+                   "peer_allreduce: world must be 1..%d (got %d, rank %d)", PEER_RED_MAX, world, rank);
+    B200SP_REQUIRE(epoch > 0, B200SP_EINVAL, "peer_allreduce: epoch must be positive");
+    PeerRed pr{};
+    pr.world = world;
+    pr.rank = rank;
+    for (int j = 0; j < world; ++j) {
+        pr.slots[j] = slots[j];
+        pr.flags[j] = flags[j];
+    }
+    peer_allreduce_kernel<<<1, 1, 0, as_stream(stream)>>>(red, k, pr, epoch);
+    count_launch();
+    return check_launch("peer_allreduce");
+}
 
 int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream) {
     B200SP_REQUIRE(nwait >= 0 && nwait <= 2 * PEER_MAX, B200SP_EINVAL, "peer_wait: at most %d flags (got %d)",

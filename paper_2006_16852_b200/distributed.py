@@ -355,6 +355,48 @@ class PeerHalo:
         _lib.call("peer_wait", ctl, self.nwait, ctypes.addressof(self.waits), self.epoch, stream)
 
 
+class PeerReduce:
+    """The CG's 8-32 byte all-reduces through peer memory
+    (b200sp_peer_allreduce): every rank maps every other rank's slot and flag
+    arrays once; a call is one single-thread kernel that stores the local sums
+    into every rank's slots, raises its flags and sums the slots in rank
+    order after every flag has arrived -- identical results on every rank,
+    no NCCL launch."""
+
+    def __init__(self, comm, dev):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        w = comm.size
+        self.world, self.rank = w, comm.rank
+        self.slots = torch.zeros(2 * w * 4, dtype=torch.float64, device=dev)
+        self.flags = torch.zeros(w, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        every = comm.allgather_object({"slots": reduce_tensor(self.slots), "flags": reduce_tensor(self.flags)})
+        self._remote, sl, fl = [], [], []
+        for j, info in enumerate(every):
+            if j == comm.rank:
+                sl.append(self.slots.data_ptr())
+                fl.append(self.flags.data_ptr())
+                continue
+            fn, args = info["slots"]
+            ts = fn(*args)
+            fn, args = info["flags"]
+            tf = fn(*args)
+            self._remote.append((ts, tf))
+            sl.append(ts.data_ptr())
+            fl.append(tf.data_ptr())
+        self.sl = (ctypes.c_void_p * w)(*sl)
+        self.fl = (ctypes.c_void_p * w)(*fl)
+        self.epoch = 0
+        torch.cuda.synchronize(dev)
+
+    def allreduce_(self, t, stream):
+        """Sum a float64 device tensor of 1..4 values across the ranks, in place."""
+        self.epoch += 1
+        _lib.call("peer_allreduce", ptr(t), t.numel(), self.world, self.rank, ctypes.addressof(self.sl),
+                  ctypes.addressof(self.fl), self.epoch, stream)
+
+
 # ---------------------------------------------------------------------------
 # distributed CG
 # ---------------------------------------------------------------------------
@@ -452,6 +494,19 @@ class DistCg:
         else:
             pext = torch.empty(A.n_ext, dtype=dt, device=exc.device)
         self.halo = "peer" if peer is not None else "nccl"
+        red = None  # the all-reduces ride on peer memory too when the halo does
+        if peer is not None and comm.size <= 8:
+            red = getattr(A, "_peer_reduce", None)
+            if red is None:
+                red = PeerReduce(comm, exc.device)
+                A.__dict__["_peer_reduce"] = red
+        self.reduce = "peer" if red is not None else "nccl"
+
+        def allreduce(k):
+            if red is not None:
+                red.allreduce_(self.red[:k], exc.stream)
+            else:
+                comm.allreduce_(self.red[:k])
         p = pext[:nl]
         # r = b - A x  (x staged in the extended vector for its halo)
         pext[:nl].copy_(x)
@@ -459,7 +514,7 @@ class DistCg:
         J = (0, 0, 0, 0, 0)
         pp = self.part
         _lib.call("cg_init_" + suf, nl, ptr(r), ptr(r), ptr(p), *J, c, ptr(pp), 0, exc.stream)
-        comm.allreduce_(self.red[:2])
+        allreduce(2)
         _lib.call("cg_finish", c, 0, 0, exc.stream)
         guard = int(_lib.query("krylov_guard", c, 0))
         _lib.query("set_guard", guard)
@@ -475,11 +530,11 @@ class DistCg:
                     else:
                         _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), c, exc.stream)
                         self._spmv_sigma(pext, p, q, c, pp, suf)
-                    comm.allreduce_(self.red[:1])
+                    allreduce(1)
                     _lib.call("cg_finish", c, 0, 1, exc.stream)
                     _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(r), *J, c, ptr(pp), 0,
                               exc.stream)
-                    comm.allreduce_(self.red[:2])
+                    allreduce(2)
                     _lib.call("cg_finish", c, 0, 2, exc.stream)
         finally:
             _lib.query("set_guard", 0)

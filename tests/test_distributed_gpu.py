@@ -63,7 +63,7 @@ def _worker(rank, world, port, g, out_dir, halo="0"):
         st2 = solver.solve(b, x2)  # again: the peer buffers, flags and epochs are reused
         same = bool(torch.equal(x, x2)) and st2.iterations == st.iterations
         with open(os.path.join(out_dir, f"st{rank}"), "w") as f:
-            f.write(f"{lo} {hi} {st.iterations} {int(st.converged)} {err} {solver.halo} {int(same)}")
+            f.write(f"{lo} {hi} {st.iterations} {int(st.converged)} {err} {solver.halo}/{solver.reduce} {int(same)}")
     finally:
         dist.destroy_process_group()
 
@@ -85,7 +85,7 @@ def test_multi_rank_cg_matches_single_gpu(tmp_path, cuda, world, halo):
         lo, hi, it, conv, err, used, same = (tmp_path / f"st{rank}").read_text().split()
         assert float(err) <= 1e-14
         assert int(conv) == 1
-        assert used == ("peer" if halo == "1" else "nccl")
+        assert used == ("peer/peer" if halo == "1" else "nccl/nccl")
         assert int(same) == 1
         its.add(int(it))
         parts.append(np.load(tmp_path / f"x{rank}.npy"))
