@@ -90,3 +90,33 @@ def test_partition_alignment_and_owner():
     assert list(p.owner([0, 64 * 512 * 512 - 1, 64 * 512 * 512, 512 ** 3 - 1])) == [0, 0, 1, 7]
     q = Partition(10, 3)
     assert q.offsets[0] == 0 and q.offsets[-1] == 10 and np.all(np.diff(q.offsets) >= 3)
+
+
+def test_peer_halo_eligibility(monkeypatch):
+    """The peer-memory halo is used for row-range sends with few neighbours,
+    automatically only under NCCL (gloo needs B200SP_PEER_HALO=1)."""
+    import types
+
+    import numpy as np
+
+    from paper_2006_16852_b200 import config
+    from paper_2006_16852_b200.distributed import HaloPlan, PeerHalo
+
+    def fake(backend, sends, nrecv=2, size=3):
+        dist = types.SimpleNamespace(get_backend=lambda group=None: backend)
+        comm = types.SimpleNamespace(dist=dist, group=None, size=size, rank=1)
+        plan = HaloPlan([(p, 0, 4) for p in range(nrecv)], [], 10, 8)
+        return types.SimpleNamespace(comm=comm, plan=plan, _send=sends)
+
+    ranges = [(0, 0, 4, None, None), (2, 6, 10, None, None)]
+    indexed = [(0, 0, 0, np.arange(3), None)]
+    monkeypatch.setattr(config, "PEER_HALO", "auto")
+    assert PeerHalo.usable(fake("nccl", ranges))
+    assert not PeerHalo.usable(fake("gloo", ranges))
+    assert not PeerHalo.usable(fake("nccl", indexed))
+    assert not PeerHalo.usable(fake("nccl", ranges * 3))  # more puts than b200sp_peer_max()
+    assert not PeerHalo.usable(fake("nccl", ranges, size=1))
+    monkeypatch.setattr(config, "PEER_HALO", "1")
+    assert PeerHalo.usable(fake("gloo", ranges))
+    monkeypatch.setattr(config, "PEER_HALO", "0")
+    assert not PeerHalo.usable(fake("nccl", ranges))
