@@ -183,16 +183,18 @@ int b200sp_csr_spmv_lb_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, cons
 /* Coo (entries sorted by row); replaces CooSpmvKernel / CooAdvSpmvKernel /
  * CooResidualKernel (kernels.py:163-275). Rows with no entry are NOT written:
  * the caller prefills them with b200sp_rows_scale_*. carry_head/carry_tail:
- * ceil(nnz/chunk) values each. */
+ * ceil(nnz/chunk) values each; chunk_rows (optional, NULL allowed): 2 *
+ * ceil(nnz/chunk) int32, 8-byte aligned -- the kernel records each chunk's
+ * first / last row there so the carry fix-up reads them contiguously. */
 int b200sp_coo_spmv_f64(int64_t nnz, int32_t chunk, const int32_t* row_idxs, const int32_t* col_idxs,
                         const double* vals, const double* b, int64_t b_stride, double* x, int64_t x_stride,
                         double alpha, const double* alpha_dev, double beta, const double* beta_dev,
-                        const double* x_in, int64_t x_in_stride, double* carry_head, double* carry_tail,
+                        const double* x_in, int64_t x_in_stride, double* carry_head, double* carry_tail, int32_t* chunk_rows,
                         void* stream);
 int b200sp_coo_spmv_f32(int64_t nnz, int32_t chunk, const int32_t* row_idxs, const int32_t* col_idxs,
                         const float* vals, const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
                         const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
-                        int64_t x_in_stride, float* carry_head, float* carry_tail, void* stream);
+                        int64_t x_in_stride, float* carry_head, float* carry_tail, int32_t* chunk_rows, void* stream);
 int b200sp_rows_scale_f64(int64_t count, const int32_t* rows, double* x, int64_t x_stride, double beta,
                           const double* beta_dev, const double* x_in, int64_t x_in_stride, void* stream);
 int b200sp_rows_scale_f32(int64_t count, const int32_t* rows, float* x, int64_t x_stride, float beta,

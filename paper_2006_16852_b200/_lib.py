@@ -36,7 +36,7 @@ _TYPED = {
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
     "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iiiiip",
     "csr_spmv_host": "llpppppppipiip",
-    "coo_spmv": "lipppplpl" + _SPMV_TAIL + "ppp",
+    "coo_spmv": "lipppplpl" + _SPMV_TAIL + "pppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
     "sellp_spmv": "lippppplpl" + _SPMV_TAIL + "p",

@@ -1015,7 +1015,7 @@ template <typename T, bool XIN, bool VEC, int E>
 __device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
            const T* __restrict__ vals, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
            int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
-           T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+           T* __restrict__ carry_head, T* __restrict__ carry_tail, int2* __restrict__ chunk_rows) {
     constexpr int CHUNK = 32 * E;
     const int lane = threadIdx.x & 31;
     const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1023,6 +1023,7 @@ __device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ ro
     if (e0 >= nnz) return;
     const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
     const int head_row = rows[e0], tail_row = rows[e1 - 1];
+    if (chunk_rows && lane == 0) chunk_rows[c] = make_int2(head_row, tail_row);  // for the fix-up
     const bool head_shared = e0 > 0 && rows[e0 - 1] == head_row;
     const bool tail_shared = e1 < nnz && rows[e1] == tail_row;
     const T a = alpha.get();
@@ -1057,8 +1058,9 @@ __device__ __forceinline__ void coo_body(int64_t nnz, const int* __restrict__ ro
 #define COO_ARGS                                                                                         \
     int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols, const T* __restrict__ vals,   \
         const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,   \
-        const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail
-#define COO_PASS nnz, rows, cols, vals, b, bs, x, xs, alpha, beta, xin, xins, carry_head, carry_tail
+        const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail,        \
+        int2* __restrict__ chunk_rows
+#define COO_PASS nnz, rows, cols, vals, b, bs, x, xs, alpha, beta, xin, xins, carry_head, carry_tail, chunk_rows
 template <typename T, bool XIN, bool VEC, int E>
 __global__ void __launch_bounds__(COO_BLOCK) coo_kernel(COO_ARGS) {
     if (alpha.skip()) return;
@@ -1084,7 +1086,8 @@ template <typename T, bool XIN>
 __global__ void __launch_bounds__(COO_BLOCK)
 coo_kernel_seg(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols, const T* __restrict__ vals,
                const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
-               const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail) {
+               const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail,
+               int2* __restrict__ chunk_rows) {
     if (alpha.skip()) return;
     constexpr int STEPS = 8;
     constexpr int CHUNK = 32 * STEPS;
@@ -1097,6 +1100,7 @@ coo_kernel_seg(int64_t nnz, const int* __restrict__ rows, const int* __restrict_
     const bool head_shared = e0 > 0 && __ldg(rows + e0 - 1) == head_row;
     const bool tail_shared = e1 < nnz && __ldg(rows + e1) == tail_row;
     const bool single = head_row == tail_row;
+    if (chunk_rows && lane == 0) chunk_rows[c] = make_int2(head_row, tail_row);
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
     int rr[STEPS], cc[STEPS];
@@ -1181,6 +1185,11 @@ struct CooChunkRows {
     int64_t nnz;
     __device__ int head(int64_t c) const { return rows[c * chunk]; }
     __device__ int tail(int64_t c) const { return rows[min((c + 1) * chunk, nnz) - 1]; }
+};
+struct PairChunkRows {  // (head, tail) per chunk, recorded by the Coo kernel
+    const int2* cr;
+    __device__ int head(int64_t c) const { return cr[c].x; }
+    __device__ int tail(int64_t c) const { return cr[c].y; }
 };
 struct CsrChunkRows {
     const int* srow;
@@ -1407,7 +1416,7 @@ template <typename T>
 static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, const T* vals,
                     const T* b, int64_t bs, T* x, int64_t xs, T alpha, const T* alpha_dev, T beta,
                     const T* beta_dev, const T* xin, int64_t xins, T* carry_head, T* carry_tail,
-                    void* stream) {
+                    int32_t* chunk_rows_ws, void* stream) {
     if (nnz == 0) return B200SP_OK;
     B200SP_REQUIRE(chunk == 128 || chunk == 256, B200SP_EINVAL, "coo: chunk must be 128 or 256 (got %d)", chunk);
     cudaStream_t st = as_stream(stream);
@@ -1419,28 +1428,44 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
     const bool vec = aligned16(rows) && aligned16(cols) && aligned16(vals);
     const int minb = tuning("coo_minb", sizeof(T) == 4 ? 6 : 1);
     const int seg = tuning("coo_seg", 0) && chunk == 256;
+    int2* crows = reinterpret_cast<int2*>(chunk_rows_ws);
+    B200SP_REQUIRE(!crows || (reinterpret_cast<uintptr_t>(crows) & 7) == 0, B200SP_EINVAL,
+                   "coo: chunk_rows must be 8-byte aligned");
 #define COO_LAUNCH(XI, VE)                                                                                  \
     do {                                                                                                    \
         if (seg)                                                                                            \
             coo_kernel_seg<T, XI><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, be,   \
-                                                              xin, xins, carry_head, carry_tail);           \
+                                                              xin, xins, carry_head, carry_tail, crows);    \
         else if (chunk == 128)                                                                              \
             coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
-                                                                    be, xin, xins, carry_head, carry_tail);  \
+                                                                    be, xin, xins, carry_head, carry_tail, crows); \
         else if (minb == 6)                                                                                 \
             coo_kernel_b6<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
-                                                                    be, xin, xins, carry_head, carry_tail);  \
+                                                                    be, xin, xins, carry_head, carry_tail, crows); \
         else                                                                                                \
             coo_kernel<T, XI, VE, 8><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
-                                                                    be, xin, xins, carry_head, carry_tail);  \
+                                                                    be, xin, xins, carry_head, carry_tail, crows); \
+    } while (0)
+    // the fix-up reads each chunk's (head, tail) rows from the kernel's record
+    // when given the workspace (2 ints per chunk, contiguous) instead of
+    // strided row-index loads (C3: 76 MB of scattered sectors, 32 us)
+#define COO_FIXUP(XI)                                                                                       \
+    do {                                                                                                    \
+        if (crows)                                                                                          \
+            coo_fixup_kernel<T, XI><<<fgrid, 256, 0, st>>>(nchunks, PairChunkRows{crows}, carry_head, carry_tail, \
+                                                           x, xs, al, be, xin, xins);                       \
+        else                                                                                                \
+            coo_fixup_kernel<T, XI><<<fgrid, 256, 0, st>>>(nchunks, CooChunkRows{rows, chunk, nnz}, carry_head, \
+                                                           carry_tail, x, xs, al, be, xin, xins);           \
     } while (0)
     if (xin) {
         if (vec) COO_LAUNCH(true, true); else COO_LAUNCH(true, false);
-        coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nchunks, CooChunkRows{rows, chunk, nnz}, carry_head, carry_tail, x, xs, al, be, xin, xins);
+        COO_FIXUP(true);
     } else {
         if (vec) COO_LAUNCH(false, true); else COO_LAUNCH(false, false);
-        coo_fixup_kernel<T, false><<<fgrid, 256, 0, st>>>(nchunks, CooChunkRows{rows, chunk, nnz}, carry_head, carry_tail, x, xs, al, be, xin, xins);
+        COO_FIXUP(false);
     }
+#undef COO_FIXUP
 #undef COO_LAUNCH
     count_launch(2);
     return check_launch("coo_spmv");
@@ -1765,15 +1790,15 @@ int b200sp_coo_spmv_f64(int64_t nnz, int32_t chunk, const int32_t* rows, const i
                         const double* vals, const double* b, int64_t bs, double* x, int64_t xs,
                         double alpha, const double* alpha_dev, double beta, const double* beta_dev,
                         const double* xin, int64_t xins, double* carry_head, double* carry_tail,
-                        void* stream) {
-    return coo_spmv<double>(nnz, chunk, rows, cols, vals, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, carry_head, carry_tail, stream);
+                        int32_t* chunk_rows, void* stream) {
+    return coo_spmv<double>(nnz, chunk, rows, cols, vals, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, carry_head, carry_tail, chunk_rows, stream);
 }
 int b200sp_coo_spmv_f32(int64_t nnz, int32_t chunk, const int32_t* rows, const int32_t* cols,
                         const float* vals, const float* b, int64_t bs, float* x, int64_t xs,
                         float alpha, const float* alpha_dev, float beta, const float* beta_dev,
                         const float* xin, int64_t xins, float* carry_head, float* carry_tail,
-                        void* stream) {
-    return coo_spmv<float>(nnz, chunk, rows, cols, vals, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, carry_head, carry_tail, stream);
+                        int32_t* chunk_rows, void* stream) {
+    return coo_spmv<float>(nnz, chunk, rows, cols, vals, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, carry_head, carry_tail, chunk_rows, stream);
 }
 
 int b200sp_rows_scale_f64(int64_t count, const int32_t* rows, double* x, int64_t xs, double beta,

@@ -941,6 +941,7 @@ class Coo(_Sparse):
             nch = max(1, math.ceil(self.nnz / 128))  # covers both chunk sizes
             head = torch.empty(nch, dtype=self._v.dtype, device=exc.device)
             tail = torch.empty(nch, dtype=self._v.dtype, device=exc.device)
+            crows = torch.empty(2 * nch, dtype=torch.int32, device=exc.device)  # per chunk (head, tail) rows
             n = self.size.rows
             rp = torch.empty(n + 1, dtype=torch.int32, device=exc.device)
             _lib.call("coo_to_csr_ptrs", self.nnz, n, ptr(self._ri), ptr(rp), exc.stream)
@@ -950,16 +951,16 @@ class Coo(_Sparse):
             ne = int(pos[-1].item())
             empty = torch.empty(max(ne, 1), dtype=torch.int32, device=exc.device)
             _lib.call("compact_flags", n, ptr(flags), ptr(pos), ptr(empty), exc.stream)
-            self._ws = (head, tail, empty, ne)
+            self._ws = (head, tail, empty, ne, crows)
         return self._ws
 
     def _launch_column(self, exc, suf, bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins,
                        prefill=True):
-        head, tail, empty, ne = self._workspace()
+        head, tail, empty, ne, crows = self._workspace()
         if prefill and ne:
             _lib.call("rows_scale_" + suf, ne, ptr(empty), xp, xs, b_h, b_p, xin, xins, exc.stream)
         _lib.call("coo_spmv_" + suf, self.nnz, self.chunk, ptr(self._ri), ptr(self._ci), ptr(self._v),
-                  bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(head), ptr(tail), exc.stream)
+                  bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, ptr(head), ptr(tail), ptr(crows), exc.stream)
 
     def _to_csr(self, **kw):
         exc = self.exec
