@@ -320,12 +320,13 @@ int b200sp_jacobi_apply_f32(int64_t nblocks, const int32_t* starts, const int64_
  *            dot0, mgs(i = 0..j-1), normalize; per cycle: backsolve, combine,
  *            after_commit, residual SpMV, reset, scale_v0 */
 /* Persistent cooperative CG for small Csr systems (one launch per solve,
- * three grid-wide barriers per iteration; after b200sp_cg_init_*, no
- * preconditioner, contiguous x). */
+ * two grid-wide barriers per iteration: the p update is recomputed inside
+ * the SpMV and written to the other of p / p2, n values each; after
+ * b200sp_cg_init_* (which fills p), no preconditioner, contiguous x). */
 int b200sp_cg_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals, double* x,
-                       double* r, double* p, double* q, void* ctl, double* part, double* hist, void* stream);
+                       double* r, double* p, double* p2, double* q, void* ctl, double* part, double* hist, void* stream);
 int b200sp_cg_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals, float* x,
-                       float* r, float* p, float* q, void* ctl, double* part, double* hist, void* stream);
+                       float* r, float* p, float* p2, float* q, void* ctl, double* part, double* hist, void* stream);
 int64_t b200sp_krylov_ctl_bytes(void);
 int64_t b200sp_krylov_part_elems(void);
 int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,

@@ -63,7 +63,7 @@ _TYPED = {
     "cg_step1": "lpppp",
     "cg_step1_put": "lpppippppipp",
     "cg_sigma": "lppppp",
-    "cg_coop": "lppppppppppp",
+    "cg_coop": "lpppppppppppp",
     "csr_spmv_dot": "lppppppiippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
     "fcg_step2": "lplppppp" + "lpppp" + "pppp",

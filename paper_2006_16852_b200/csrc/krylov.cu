@@ -301,6 +301,9 @@ __device__ __forceinline__ void coop_totals(const double* part, double (&tot)[NV
     __syncthreads();
 }
 
+__device__ __forceinline__ double fma_t(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fma_t(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
 // grid-wide barrier; a one-block grid (tiny systems) only needs the block
 // barrier (cooperative grid.sync costs microseconds even then)
 __device__ __forceinline__ void coop_sync(cooperative_groups::grid_group& grid) {
@@ -308,10 +311,15 @@ __device__ __forceinline__ void coop_sync(cooperative_groups::grid_group& grid) 
     else grid.sync();
 }
 
+// Two grid barriers per iteration: p = r + beta p is not a phase of its own
+// but recomputed inside the SpMV for every column it gathers (r and the
+// previous p of the neighbours are final since the last barrier) and written
+// for the thread's own rows into the other of two p buffers -- the same
+// fused multiply-add as CgStep1 (steps.py:93-119), so the same values.
 template <typename T>
 __global__ void __launch_bounds__(KRY_BLOCK)
 cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
-               T* __restrict__ x, T* __restrict__ r, T* __restrict__ p, T* __restrict__ q, KrylovCtl* c,
+               T* __restrict__ x, T* __restrict__ r, T* p_a, T* p_b, T* __restrict__ q, KrylovCtl* c,
                double* part, double* hist) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -323,22 +331,28 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
     double rho = c->rho, beta = c->beta;
     int it = c->it;
     bool done = c->done;
+    T* pin = p_a;   // p of the previous iteration
+    T* pout = p_b;  // p of this one
     while (!done) {
         const T tb = (T)beta;
-        for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + tb * p[i];
-        coop_sync(grid);
         double sg = 0;
         for (int64_t i = gt; i < n; i += gs) {
             T s = 0;
-            for (int k = rp[i]; k < rp[i + 1]; ++k) s += av[k] * p[ci[k]];
+            for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                const int j = ci[k];
+                s += av[k] * fma_t(tb, pin[j], r[j]);
+            }
             q[i] = s;
-            sg += (double)p[i] * (double)s;
+            const T pi = fma_t(tb, pin[i], r[i]);
+            pout[i] = pi;
+            sg += (double)pi * (double)s;
         }
         double v1[1] = {sg}, t1[1];
         coop_block_partials<1>(v1, part, sh, sh_tot);
         coop_sync(grid);
         coop_totals<1>(part, t1, sh_tot);
         const double sigma = t1[0];
+        T* const p = pout;
         if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
             if (gt == 0) {
                 c->sigma = sigma;
@@ -393,6 +407,8 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
         // phase, and a partial slot is rewritten only after the next barrier,
         // by which time every block has finished reading it
         done = stop;
+        pout = pin;
+        pin = p;
     }
 }
 
@@ -1227,7 +1243,7 @@ int64_t b200sp_gmres_workspace_elems(int32_t k) { return (int64_t)(k + 1) * k + 
 }  // extern "C"
 
 template <typename T>
-static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, T* p, T* q, void* ctl,
+static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, T* p, T* p2, T* q, void* ctl,
                    double* part, double* hist, void* stream) {
     int dev = 0, sms = 0, per_sm = 0;
     B200SP_CHECK_CUDA(cudaGetDevice(&dev));
@@ -1241,7 +1257,7 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
     if (cap > 0 && grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
-    void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &q, &c, &part, &hist};
+    void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &p2, &q, &c, &part, &hist};
     B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cg_coop_kernel<T>, dim3((unsigned)grid), dim3(KRY_BLOCK),
                                                   args, 0, as_stream(stream)));
     count_launch();
@@ -1250,12 +1266,12 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
 
 extern "C" {
 int b200sp_cg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
-                       double* p, double* q, void* ctl, double* part, double* hist, void* stream) {
-    return cg_coop<double>(n, rp, ci, v, x, r, p, q, ctl, part, hist, stream);
+                       double* p, double* p2, double* q, void* ctl, double* part, double* hist, void* stream) {
+    return cg_coop<double>(n, rp, ci, v, x, r, p, p2, q, ctl, part, hist, stream);
 }
 int b200sp_cg_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, float* x, float* r,
-                       float* p, float* q, void* ctl, double* part, double* hist, void* stream) {
-    return cg_coop<float>(n, rp, ci, v, x, r, p, q, ctl, part, hist, stream);
+                       float* p, float* p2, float* q, void* ctl, double* part, double* hist, void* stream) {
+    return cg_coop<float>(n, rp, ci, v, x, r, p, p2, q, ctl, part, hist, stream);
 }
 
 int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, const double* p,

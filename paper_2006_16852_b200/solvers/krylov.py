@@ -111,8 +111,8 @@ class CgSolver(IterativeSolver):
         if self._coop_ok(J, S):
             # small system: the whole solve is one persistent cooperative launch
             a = self._coop_csr()
-            _lib.call("cg_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(p), ptr(q),
-                      S.c, S.p, S.h, exc.stream)
+            _lib.call("cg_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(p),
+                      ptr(S.vec("p2")), ptr(q), S.c, S.p, S.h, exc.stream)
             return finish_from_device(self, S, S.status(), x)
 
         fa = fused_csr(self)
