@@ -52,12 +52,16 @@ def bench_solver(args, world, rank, local, kind):
         a = problems.stencil(exc, "5pt", 256)
         fac = b2.Cg(exc, criteria=[b2.Iteration(10000), b2.ResidualNormReduction(1e-8)])
         wl = "C1: CG, 2-D 5-point Poisson 256^2 (65,536 rows), rhs ones, x0 = 0, RNR 1e-8, fp64"
-        vec_passes = 9
+        vec_passes = 8  # the cooperative kernel folds p = r + beta p into the SpMV
     elif kind == "c5":
         a = problems.stencil(exc, "7pt", args.grid or 512)
         fac = b2.Cg(exc, criteria=[b2.Iteration(20000), b2.ResidualNormReduction(1e-8)])
         wl = f"C5: CG, 3-D 7-point Poisson {args.grid or 512}^3, rhs ones, x0 = 0, RNR 1e-8, fp64, 1 GPU"
-        vec_passes = 9
+        # SpMV + p update (3n) + x, r update with r.r (6n); with the p update
+        # folded into the SpMV (config.CG_FOLD_P) the SpMV reads z as well and
+        # writes p: SpMV + 2n + 6n
+        from paper_2006_16852_b200 import config as _cfg
+        vec_passes = 8 if _cfg.CG_FOLD_P else 9
     else:
         g = args.grid or 256
         a = problems.stencil(exc, "convdiff", g)
@@ -152,7 +156,7 @@ def bench_solver(args, world, rank, local, kind):
         by = bytes_csr(n, a.nnz, 8) + vec_passes * n * 8
         out["roofline"] = {"bound": "hbm", "achieved": round(by / (t / its) / 1e9, 1), "peak": peak,
                            "unit": "GB/s", "frac": round(by / (t / its) / 1e9 / peak, 4), "traffic": None,
-                           "peak_source": peak_src, "kernel": "whole CG iteration",
+                           "peak_source": peak_src, "kernel": f"whole CG iteration (Csr SpMV + {vec_passes}n values)",
                            "bytes_per_launch": by}
     return out
 

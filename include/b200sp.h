@@ -390,6 +390,17 @@ int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* row_ptrs, const int32_t* c
 int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
                             const float* p, float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl,
                             double* part, void* stream);
+/* CG's p update folded into the fused SpMV: q = A p_new and sigma = p_new.q
+ * with p_new = z + beta p_old (beta from the control block, the CgStep1
+ * multiply-add, steps.py:93-119) recomputed for every gathered column and
+ * stored for the own rows into p_new (p_old != p_new: alternate two
+ * buffers). Replaces b200sp_cg_step1_* + b200sp_csr_spmv_dot_* phase 1. */
+int b200sp_csr_spmv_dot_p_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
+                              const double* p_old, const double* z, double* p_new, double* q, int32_t subwarp,
+                              void* ctl, double* part, void* stream);
+int b200sp_csr_spmv_dot_p_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
+                              const float* p_old, const float* z, float* p_new, float* q, int32_t subwarp,
+                              void* ctl, double* part, void* stream);
 
 /* ---- device assembly of coordinate triples (reference MatrixData.canonicalize,
  * src/formats.py:40-53, bit for bit) ------------------------------------------

@@ -65,6 +65,7 @@ _TYPED = {
     "cg_sigma": "lppppp",
     "cg_coop": "lpppppppppppp",
     "csr_spmv_dot": "lppppppiippp",
+    "csr_spmv_dot_p": "lpppppppippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
     "fcg_step2": "lplppppp" + "lpppp" + "pppp",
     "cgs_step1": "lppppp" + "lpppp" + "pp",
