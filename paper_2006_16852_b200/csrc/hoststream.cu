@@ -48,12 +48,11 @@ template <typename T, int SW, int U>
 __global__ void __launch_bounds__(HS_BLOCK)
 csr_host_stream_kernel(int64_t n, int64_t ncols, const int* __restrict__ rp, const int* __restrict__ ci,
                        const T* __restrict__ v, const T* bh, T* bd, T* xh, const int* __restrict__ tile_need,
-                       int tile_rows, int* flags, int epoch, int nprod, int vec, int dbg) {
+                       int tile_rows, int* flags, int epoch, int nprod, int vec) {
     extern __shared__ __align__(16) unsigned char hs_smem[];
     constexpr int64_t CHUNK = HS_CHUNK_BYTES / sizeof(T);
     const int64_t nchunks = (ncols + CHUNK - 1) / CHUNK;
     if ((int)blockIdx.x < nprod) {
-        if (dbg == 3) return;  // (probe only: no H2D, consumers do not wait)
         // ---- producer: host b -> device staging, chunk by chunk ----
         constexpr int NV = HS_CHUNK_BYTES / 16 / HS_BLOCK;
         for (int64_t c = blockIdx.x; c < nchunks; c += nprod) {
@@ -86,7 +85,7 @@ csr_host_stream_kernel(int64_t n, int64_t ncols, const int* __restrict__ rp, con
     int ready = 0;  // thread 0: chunks [0, ready) have landed
     for (int64_t t = (int)blockIdx.x - nprod; t < ntiles; t += ncons) {
         const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
-        if (threadIdx.x == 0 && dbg != 1 && dbg != 3) {
+        if (threadIdx.x == 0) {
             const int need = tile_need[t];
             while (ready <= need) {
                 if (ld_acquire_gpu(flags + ready) == epoch)
@@ -134,7 +133,7 @@ csr_host_stream_kernel(int64_t n, int64_t ncols, const int* __restrict__ rp, con
         }
         __syncthreads();
         const int cnt = (int)(r1 - r0);
-        T* dst = (dbg == 2 ? bd + ncols : xh) + r0;  // (probe only: x to device scratch)
+        T* dst = xh + r0;
         constexpr int PER = 16 / sizeof(T);
         if (vec && cnt % PER == 0) {
             const int4* s4 = reinterpret_cast<const int4*>(xs);
@@ -182,12 +181,9 @@ static int launch_host_stream(int64_t n, int64_t ncols, const int* rp, const int
     int nprod = tuning("hs_producers", 4);  // fewer readers measured faster: 4 -> 537 us, 32 -> 661 us on C2
     nprod = std::max(1, std::min(nprod, grid / 2));
     const int vec = aligned16(bh) && aligned16(bd) && aligned16(xh);
-    // probe-only modes (tools/e2e_probe.py; results invalid): 1 consumers do not
-    // wait, 2 x goes to device scratch (b_dev must hold ncols + n), 3 no H2D
-    int dbg = tuning("hs_debug", 0);
     void* args[] = {(void*)&n, (void*)&ncols, (void*)&rp, (void*)&ci, (void*)&v, (void*)&bh, (void*)&bd,
                     (void*)&xh, (void*)&need, (void*)&tile_rows, (void*)&flags, (void*)&epoch, (void*)&nprod,
-                    (void*)&vec, (void*)&dbg};
+                    (void*)&vec};
     B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(HS_BLOCK), args,
                                                   smem, st));
     return B200SP_OK;
