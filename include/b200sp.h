@@ -327,6 +327,17 @@ int b200sp_cg_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_id
                        double* r, double* p, double* p2, double* q, void* ctl, double* part, double* hist, void* stream);
 int b200sp_cg_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals, float* x,
                        float* r, float* p, float* p2, float* q, void* ctl, double* part, double* hist, void* stream);
+/* Persistent cooperative BiCGSTAB for small unpreconditioned Csr systems
+ * (one launch per solve; after b200sp_bicgstab_init_*, y = p and z = s;
+ * contiguous x): BicgstabStep1/2/3, the gamma and (t.s, t.t) reductions,
+ * the mid check with finalize and the top check (src/solvers/krylov.py:
+ * 190-271, steps.py:348-480), five grid barriers per cycle. */
+int b200sp_bicgstab_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
+                             double* x, double* r, const double* rt, double* p, double* v, double* s, double* t,
+                             void* ctl, double* part, double* hist, void* stream);
+int b200sp_bicgstab_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
+                             float* x, float* r, const float* rt, float* p, float* v, float* s, float* t,
+                             void* ctl, double* part, double* hist, void* stream);
 int64_t b200sp_krylov_ctl_bytes(void);
 int64_t b200sp_krylov_part_elems(void);
 int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,

@@ -64,6 +64,7 @@ _TYPED = {
     "cg_step1_put": "lpppippppipp",
     "cg_sigma": "lppppp",
     "cg_coop": "lpppppppppppp",
+    "bicgstab_coop": "lpppppppppppppp",
     "csr_spmv_dot": "lppppppiippp",
     "csr_spmv_dot_p": "lpppppppippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",

@@ -616,6 +616,140 @@ bicg_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, c
     bicg_cycle_start(c, tot[1], tot[0]);
 }
 
+// Persistent cooperative BiCGSTAB for small unpreconditioned Csr systems:
+// the whole solve in one launch (y = p, z = s). Every block keeps a copy of
+// the control block in shared memory and runs the same control functions on
+// the same all-reduced totals (bicg_gamma_ctl, bicg_tst_ctl, the mid and top
+// checks, bicg_cycle_start), so every block takes the same decisions; block
+// 0 writes the state back. Vector updates are the step kernels' expressions
+// (steps.py:348-480); the reductions alternate between two partial-sum
+// regions so a region is rewritten only after every block has read it.
+template <typename T>
+__device__ __forceinline__ void coop_row_dot(int64_t i, const int* __restrict__ rp, const int* __restrict__ ci,
+                                             const T* __restrict__ av, const T* u, T& out) {
+    T acc = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) acc += av[k] * u[ci[k]];
+    out = acc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                 T* __restrict__ x, T* r, const T* __restrict__ rt, T* p, T* v, T* s, T* t, KrylovCtl* c,
+                 double* part, double* hist) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ KrylovCtl sc;
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh_tot[2];
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    double* const hb = blockIdx.x == 0 ? hist : nullptr;
+    double* const part0 = part;
+    double* const part1 = part + 2 * KRY_MAX_GRID;
+    if (threadIdx.x == 0) sc = *c;
+    __syncthreads();
+    while (!sc.done) {
+        {   // p = r + beta (p - omega v)   (BicgstabStep1)
+            const T beta = (T)sc.beta, omega = (T)sc.omega;
+            for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+        }
+        coop_sync(grid);
+        {   // v = A p; gamma = rt.v
+            double g = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                T vi;
+                coop_row_dot(i, rp, ci, av, p, vi);
+                v[i] = vi;
+                g += (double)rt[i] * (double)vi;
+            }
+            double vv[1] = {g}, tot[1];
+            coop_block_partials<1>(vv, part0, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<1>(part0, tot, sh_tot);
+            if (threadIdx.x == 0) bicg_gamma_ctl(&sc, tot);
+            __syncthreads();
+            if (sc.done) break;
+        }
+        {   // s = r - alpha v; it++; mid check on ||s||   (BicgstabStep2)
+            const T alpha = (T)sc.alpha;
+            double ss = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                const T sv = r[i] - alpha * v[i];
+                s[i] = sv;
+                ss += (double)sv * (double)sv;
+            }
+            double vv[1] = {ss}, tot[1];
+            coop_block_partials<1>(vv, part1, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<1>(part1, tot, sh_tot);
+            if (threadIdx.x == 0) {
+                sc.it += 1;
+                sc.snorm = sqrt(tot[0]);
+                hist_put(&sc, hb, sc.it, sc.snorm);
+                crit_check(&sc, sc.it, sc.snorm);
+                if (sc.stopped) {
+                    sc.mid_final = sc.needs_residual;
+                    sc.done = 1;
+                }
+            }
+            __syncthreads();
+            if (sc.done) {  // converged on ||s||: x += alpha y   (BicgstabFinalize)
+                if (sc.mid_final)
+                    for (int64_t i = gt; i < n; i += gs) x[i] = x[i] + alpha * p[i];
+                __syncthreads();
+                if (threadIdx.x == 0) sc.mid_final = 0;
+                break;
+            }
+        }
+        {   // t = A s; ts = t.s, tt = t.t
+            double a = 0, bb = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                T ti;
+                coop_row_dot(i, rp, ci, av, s, ti);
+                t[i] = ti;
+                const double tv = ti;
+                a += tv * (double)s[i];
+                bb += tv * tv;
+            }
+            double vv[2] = {a, bb}, tot[2];
+            coop_block_partials<2>(vv, part0, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<2>(part0, tot, sh_tot);
+            if (threadIdx.x == 0) bicg_tst_ctl(&sc, tot);
+            __syncthreads();
+            if (sc.done) break;
+        }
+        {   // x += alpha y + omega z; r = s - omega t; it++; check; next rho   (BicgstabStep3)
+            const T alpha = (T)sc.alpha, omega = (T)sc.omega;
+            double rr = 0, rtr = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                const T upd = alpha * p[i] + omega * s[i];
+                x[i] = x[i] + upd;
+                const T rv = s[i] - omega * t[i];
+                r[i] = rv;
+                rr += (double)rv * (double)rv;
+                rtr += (double)rt[i] * (double)rv;
+            }
+            double vv[2] = {rr, rtr}, tot[2];
+            coop_block_partials<2>(vv, part1, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<2>(part1, tot, sh_tot);
+            if (threadIdx.x == 0) {
+                sc.rho_prev = sc.rho;
+                sc.it += 1;
+                sc.rnorm = sqrt(tot[0]);
+                hist_put(&sc, hb, sc.it, sc.rnorm);
+                crit_check(&sc, sc.it, sc.rnorm);
+                sc.done = sc.stopped;
+                bicg_cycle_start(&sc, tot[1], tot[0]);
+            }
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *c = sc;
+}
+
 // ===========================================================================
 // CGS (src/solvers/krylov.py:128-187; steps.py:246-345). Initialisation is
 // BiCGSTAB's (rt = b, workspace zeroed, rho = rt.r, beta = rho / 1); the
@@ -1279,6 +1413,28 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
     return B200SP_OK;
 }
 
+template <typename T>
+static int bicg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, const T* rt, T* p,
+                     T* vv, T* s, T* t, void* ctl, double* part, double* hist, void* stream) {
+    int dev = 0, sms = 0, per_sm = 0;
+    B200SP_CHECK_CUDA(cudaGetDevice(&dev));
+    B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bicg_coop_kernel<T>, KRY_BLOCK, 0));
+    int64_t grid = (int64_t)sms * per_sm;
+    if (grid > KRY_MAX_GRID) grid = KRY_MAX_GRID;
+    const int64_t need = ceil_div(n, KRY_BLOCK);
+    if (grid > need) grid = need;
+    const int cap = tuning("coop_blocks", 0);
+    if (cap > 0 && grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    KrylovCtl* c = (KrylovCtl*)ctl;
+    void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, (void*)&rt, &p, &vv, &s, &t, &c, &part, &hist};
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)bicg_coop_kernel<T>, dim3((unsigned)grid),
+                                                  dim3(KRY_BLOCK), args, 0, as_stream(stream)));
+    count_launch();
+    return B200SP_OK;
+}
+
 extern "C" {
 int b200sp_cg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
                        double* p, double* p2, double* q, void* ctl, double* part, double* hist, void* stream) {
@@ -1298,6 +1454,17 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* rp, const int32_t* ci, con
                             float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
                             void* stream) {
     return csr_spmv_dot<float>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
+}
+
+int b200sp_bicgstab_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x,
+                             double* r, const double* rt, double* p, double* vv, double* s, double* t, void* ctl,
+                             double* part, double* hist, void* stream) {
+    return bicg_coop<double>(n, rp, ci, v, x, r, rt, p, vv, s, t, ctl, part, hist, stream);
+}
+int b200sp_bicgstab_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, float* x, float* r,
+                             const float* rt, float* p, float* vv, float* s, float* t, void* ctl, double* part,
+                             double* hist, void* stream) {
+    return bicg_coop<float>(n, rp, ci, v, x, r, rt, p, vv, s, t, ctl, part, hist, stream);
 }
 
 int b200sp_csr_spmv_dot_p_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, const double* p_old,

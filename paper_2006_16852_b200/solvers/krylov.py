@@ -169,6 +169,13 @@ class BicgstabSolver(IterativeSolver):
         _lib.call("bicgstab_init_" + suf, n, ptr(S.b), 1, ptr(r), ptr(rt), ptr(p), ptr(v), ptr(s), ptr(t),
                   ptr(y), ptr(z), S.c, S.p, S.h, exc.stream)
 
+        if config.BICGSTAB_COOP and CgSolver._coop_ok(self, J, S):
+            # small system: the whole solve is one persistent cooperative launch
+            a = CgSolver._coop_csr(self)
+            _lib.call("bicgstab_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(rt),
+                      ptr(p), ptr(v), ptr(s), ptr(t), S.c, S.p, S.h, exc.stream)
+            return finish_from_device(self, S, S.status(), x)
+
         fa = fused_csr(self)
 
         def body():
