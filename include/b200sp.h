@@ -338,6 +338,15 @@ int b200sp_bicgstab_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* 
 int b200sp_bicgstab_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
                              float* x, float* r, const float* rt, float* p, float* v, float* s, float* t,
                              void* ctl, double* part, double* hist, void* stream);
+/* Persistent cooperative FCG for small unpreconditioned Csr systems (one
+ * launch per solve, after b200sp_cg_init_* + b200sp_fcg_init_ctl; z = r):
+ * CgStep1, SpMV + sigma, FcgStep2 (src/solvers/krylov.py:80-125). */
+int b200sp_fcg_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals, double* x,
+                        double* r, double* p, double* q, double* t, void* ctl, double* part, double* hist,
+                        void* stream);
+int b200sp_fcg_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals, float* x,
+                        float* r, float* p, float* q, float* t, void* ctl, double* part, double* hist,
+                        void* stream);
 int64_t b200sp_krylov_ctl_bytes(void);
 int64_t b200sp_krylov_part_elems(void);
 int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,

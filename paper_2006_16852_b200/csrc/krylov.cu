@@ -616,6 +616,15 @@ bicg_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, c
     bicg_cycle_start(c, tot[1], tot[0]);
 }
 
+// Persistent cooperative FCG for small unpreconditioned Csr systems (z = r):
+// CgStep1, SpMV + sigma (cg_sigma_ctl), FcgStep2 (t = r_new - r_old, rho =
+// r.z, rho_t = t.z, ||r||, check, beta = rho_t / rho_prev) in one launch,
+// with the block-local control copies of the cooperative BiCGSTAB below.
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                T* __restrict__ x, T* r, T* p, T* q, T* t, KrylovCtl* c, double* part, double* hist);
+
 // Persistent cooperative BiCGSTAB for small unpreconditioned Csr systems:
 // the whole solve in one launch (y = p, z = s). Every block keeps a copy of
 // the control block in shared memory and runs the same control functions on
@@ -743,6 +752,79 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
                 crit_check(&sc, sc.it, sc.rnorm);
                 sc.done = sc.stopped;
                 bicg_cycle_start(&sc, tot[1], tot[0]);
+            }
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *c = sc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                T* __restrict__ x, T* r, T* p, T* q, T* t, KrylovCtl* c, double* part, double* hist) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ KrylovCtl sc;
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh_tot[4];
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    double* const hb = blockIdx.x == 0 ? hist : nullptr;
+    double* const part_s = part;                 // sigma: 1 value per block
+    double* const part_2 = part + KRY_MAX_GRID;  // step 2: 3 values per block
+    if (threadIdx.x == 0) sc = *c;
+    __syncthreads();
+    while (!sc.done) {
+        {   // p = z + beta p   (CgStep1, z = r)
+            const T beta = (T)sc.beta;
+            for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + beta * p[i];
+        }
+        coop_sync(grid);
+        {   // q = A p; sigma = p.q
+            double sg = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                T qi;
+                coop_row_dot(i, rp, ci, av, p, qi);
+                q[i] = qi;
+                sg += (double)p[i] * (double)qi;
+            }
+            double vv[1] = {sg}, tot[1];
+            coop_block_partials<1>(vv, part_s, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<1>(part_s, tot, sh_tot);
+            if (threadIdx.x == 0) cg_sigma_ctl(&sc, tot);
+            __syncthreads();
+            if (sc.done) break;
+        }
+        {   // FcgStep2
+            const T alpha = (T)sc.alpha;
+            double rz = 0, tz = 0, rr = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                x[i] = x[i] + mul_rn(alpha, p[i]);
+                const T ro = r[i];
+                const T rv = ro - mul_rn(alpha, q[i]);
+                const T tv = rv - ro;
+                t[i] = tv;
+                r[i] = rv;
+                rz += (double)rv * (double)rv;
+                tz += (double)tv * (double)rv;
+                rr += (double)rv * (double)rv;
+            }
+            double vv[3] = {rz, tz, rr}, tot[3];
+            coop_block_partials<3>(vv, part_2, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<3>(part_2, tot, sh_tot);
+            if (threadIdx.x == 0) {
+                sc.rho_prev = sc.rho;
+                sc.rho = tot[0];
+                sc.rho_t = tot[1];
+                sc.it += 1;
+                sc.rnorm = sqrt(tot[2]);
+                hist_put(&sc, hb, sc.it, sc.rnorm);
+                crit_check(&sc, sc.it, sc.rnorm);
+                sc.done = sc.stopped;
+                sc.beta = safe_div(sc.rho_t, sc.rho_prev);
             }
             __syncthreads();
         }
@@ -1435,6 +1517,28 @@ static int bicg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v
     return B200SP_OK;
 }
 
+template <typename T>
+static int fcg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, T* p, T* q, T* t,
+                    void* ctl, double* part, double* hist, void* stream) {
+    int dev = 0, sms = 0, per_sm = 0;
+    B200SP_CHECK_CUDA(cudaGetDevice(&dev));
+    B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fcg_coop_kernel<T>, KRY_BLOCK, 0));
+    int64_t grid = (int64_t)sms * per_sm;
+    if (grid > KRY_MAX_GRID) grid = KRY_MAX_GRID;
+    const int64_t need = ceil_div(n, KRY_BLOCK);
+    if (grid > need) grid = need;
+    const int cap = tuning("coop_blocks", 0);
+    if (cap > 0 && grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    KrylovCtl* c = (KrylovCtl*)ctl;
+    void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &q, &t, &c, &part, &hist};
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)fcg_coop_kernel<T>, dim3((unsigned)grid),
+                                                  dim3(KRY_BLOCK), args, 0, as_stream(stream)));
+    count_launch();
+    return B200SP_OK;
+}
+
 extern "C" {
 int b200sp_cg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
                        double* p, double* p2, double* q, void* ctl, double* part, double* hist, void* stream) {
@@ -1454,6 +1558,15 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* rp, const int32_t* ci, con
                             float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
                             void* stream) {
     return csr_spmv_dot<float>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
+}
+
+int b200sp_fcg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
+                        double* p, double* q, double* t, void* ctl, double* part, double* hist, void* stream) {
+    return fcg_coop<double>(n, rp, ci, v, x, r, p, q, t, ctl, part, hist, stream);
+}
+int b200sp_fcg_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, float* x, float* r,
+                        float* p, float* q, float* t, void* ctl, double* part, double* hist, void* stream) {
+    return fcg_coop<float>(n, rp, ci, v, x, r, p, q, t, ctl, part, hist, stream);
 }
 
 int b200sp_bicgstab_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x,

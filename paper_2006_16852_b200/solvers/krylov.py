@@ -220,6 +220,11 @@ class FcgSolver(IterativeSolver):
         td.fill(0.0)
         _lib.call("cg_init_" + suf, n, ptr(r), ptr(z), ptr(p), *J, S.c, S.p, S.h, exc.stream)
         _lib.call("fcg_init_ctl", S.c, exc.stream)
+        if config.BICGSTAB_COOP and CgSolver._coop_ok(self, J, S):
+            a = CgSolver._coop_csr(self)  # small system: one persistent cooperative launch
+            _lib.call("fcg_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(p), ptr(q),
+                      ptr(t), S.c, S.p, S.h, exc.stream)
+            return finish_from_device(self, S, S.status(), x)
         fa = fused_csr(self)
 
         def body():
