@@ -347,6 +347,15 @@ int b200sp_fcg_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_i
 int b200sp_fcg_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals, float* x,
                         float* r, float* p, float* q, float* t, void* ctl, double* part, double* hist,
                         void* stream);
+/* Persistent cooperative CGS for small unpreconditioned Csr systems (one
+ * launch per solve, after b200sp_bicgstab_init_*; ph = p, uh = w):
+ * CgsStep1/2/3, gamma, the mid check (src/solvers/krylov.py:128-187). */
+int b200sp_cgs_coop_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals, double* x,
+                        double* r, const double* rt, double* p, double* q, double* u, double* vh, double* w,
+                        double* t, void* ctl, double* part, double* hist, void* stream);
+int b200sp_cgs_coop_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals, float* x,
+                        float* r, const float* rt, float* p, float* q, float* u, float* vh, float* w, float* t,
+                        void* ctl, double* part, double* hist, void* stream);
 int64_t b200sp_krylov_ctl_bytes(void);
 int64_t b200sp_krylov_part_elems(void);
 int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,

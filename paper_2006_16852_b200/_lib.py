@@ -66,6 +66,7 @@ _TYPED = {
     "cg_coop": "lpppppppppppp",
     "bicgstab_coop": "lpppppppppppppp",
     "fcg_coop": "lpppppppppppp",
+    "cgs_coop": "l" + "p" * 16,
     "csr_spmv_dot": "lppppppiippp",
     "csr_spmv_dot_p": "lpppppppippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",

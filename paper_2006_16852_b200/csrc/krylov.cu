@@ -944,6 +944,102 @@ cgs_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, co
     cgs_cycle_start(c, tot[1], tot[0]);
 }
 
+// Persistent cooperative CGS for small unpreconditioned Csr systems (ph = p,
+// uh = w): CgsStep1, SpMV + gamma, CgsStep2, the mid check, SpMV,
+// CgsStep3 and the next rho in one launch (block-local control copies as
+// in the cooperative BiCGSTAB); four grid barriers per cycle.
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                T* __restrict__ x, T* r, const T* __restrict__ rt, T* p, T* q, T* u, T* vh, T* w, T* t, KrylovCtl* c,
+                double* part, double* hist) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ KrylovCtl sc;
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh_tot[2];
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    double* const hb = blockIdx.x == 0 ? hist : nullptr;
+    double* const part0 = part;
+    double* const part1 = part + 2 * KRY_MAX_GRID;
+    if (threadIdx.x == 0) sc = *c;
+    __syncthreads();
+    while (!sc.done) {
+        {   // u = r + beta q; p = u + beta (q + beta p)   (CgsStep1)
+            const T beta = (T)sc.beta;
+            for (int64_t i = gt; i < n; i += gs) {
+                const T qv = q[i];
+                const T uv = r[i] + mul_rn(beta, qv);
+                u[i] = uv;
+                p[i] = uv + mul_rn(beta, qv + mul_rn(beta, p[i]));
+            }
+        }
+        coop_sync(grid);
+        {   // v_hat = A p; gamma = rt.v_hat
+            double g = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                T vi;
+                coop_row_dot(i, rp, ci, av, p, vi);
+                vh[i] = vi;
+                g += (double)rt[i] * (double)vi;
+            }
+            double vv[1] = {g}, tot[1];
+            coop_block_partials<1>(vv, part0, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<1>(part0, tot, sh_tot);
+            if (threadIdx.x == 0) bicg_gamma_ctl(&sc, tot);
+            __syncthreads();
+            if (sc.done) break;
+        }
+        const T alpha = (T)sc.alpha;
+        // q = u - alpha v_hat; w = u + q   (CgsStep2)
+        for (int64_t i = gt; i < n; i += gs) {
+            const T uv = u[i];
+            const T qv = uv - mul_rn(alpha, vh[i]);
+            q[i] = qv;
+            w[i] = uv + qv;
+        }
+        if (threadIdx.x == 0) {  // mid check on the unchanged ||r|| (krylov.py:171-176)
+            sc.it += 1;
+            hist_put(&sc, hb, sc.it, sc.rnorm);
+            crit_check(&sc, sc.it, sc.rnorm);
+            sc.done = sc.stopped;
+        }
+        __syncthreads();
+        if (sc.done) break;
+        coop_sync(grid);
+        {   // t = A w; r -= alpha t; x += alpha w; it++; check; next rho   (CgsStep3)
+            double rr = 0, rtr = 0;
+            for (int64_t i = gt; i < n; i += gs) {
+                T ti;
+                coop_row_dot(i, rp, ci, av, w, ti);
+                t[i] = ti;
+                const T rv = r[i] - mul_rn(alpha, ti);
+                r[i] = rv;
+                x[i] = x[i] + mul_rn(alpha, w[i]);
+                rr += (double)rv * (double)rv;
+                rtr += (double)rt[i] * (double)rv;
+            }
+            double vv[2] = {rr, rtr}, tot[2];
+            coop_block_partials<2>(vv, part1, sh, sh_tot);
+            coop_sync(grid);
+            coop_totals<2>(part1, tot, sh_tot);
+            if (threadIdx.x == 0) {
+                sc.rho_prev = sc.rho;
+                sc.it += 1;
+                sc.rnorm = sqrt(tot[0]);
+                hist_put(&sc, hb, sc.it, sc.rnorm);
+                crit_check(&sc, sc.it, sc.rnorm);
+                sc.done = sc.stopped;
+                cgs_cycle_start(&sc, tot[1], tot[0]);
+            }
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *c = sc;
+}
+
 // ===========================================================================
 // GMRES(k), right preconditioned, m = 1.
 // gm layout: H[(k+1) x k] row-major | cs[k] | sn[k] | gamma[k+1] | y[k]
@@ -1539,6 +1635,28 @@ static int fcg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v,
     return B200SP_OK;
 }
 
+template <typename T>
+static int cgs_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, const T* rt, T* p, T* q,
+                    T* u, T* vh, T* w, T* t, void* ctl, double* part, double* hist, void* stream) {
+    int dev = 0, sms = 0, per_sm = 0;
+    B200SP_CHECK_CUDA(cudaGetDevice(&dev));
+    B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs_coop_kernel<T>, KRY_BLOCK, 0));
+    int64_t grid = (int64_t)sms * per_sm;
+    if (grid > KRY_MAX_GRID) grid = KRY_MAX_GRID;
+    const int64_t need = ceil_div(n, KRY_BLOCK);
+    if (grid > need) grid = need;
+    const int cap = tuning("coop_blocks", 0);
+    if (cap > 0 && grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    KrylovCtl* c = (KrylovCtl*)ctl;
+    void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, (void*)&rt, &p, &q, &u, &vh, &w, &t, &c, &part, &hist};
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cgs_coop_kernel<T>, dim3((unsigned)grid),
+                                                  dim3(KRY_BLOCK), args, 0, as_stream(stream)));
+    count_launch();
+    return B200SP_OK;
+}
+
 extern "C" {
 int b200sp_cg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
                        double* p, double* p2, double* q, void* ctl, double* part, double* hist, void* stream) {
@@ -1558,6 +1676,17 @@ int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* rp, const int32_t* ci, con
                             float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl, double* part,
                             void* stream) {
     return csr_spmv_dot<float>(n, rp, ci, v, p, q, u, phase, subwarp, ctl, part, stream);
+}
+
+int b200sp_cgs_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,
+                        const double* rt, double* p, double* q, double* u, double* vh, double* w, double* t, void* ctl,
+                        double* part, double* hist, void* stream) {
+    return cgs_coop<double>(n, rp, ci, v, x, r, rt, p, q, u, vh, w, t, ctl, part, hist, stream);
+}
+int b200sp_cgs_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, float* x, float* r,
+                        const float* rt, float* p, float* q, float* u, float* vh, float* w, float* t, void* ctl,
+                        double* part, double* hist, void* stream) {
+    return cgs_coop<float>(n, rp, ci, v, x, r, rt, p, q, u, vh, w, t, ctl, part, hist, stream);
 }
 
 int b200sp_fcg_coop_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, double* x, double* r,

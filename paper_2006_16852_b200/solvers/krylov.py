@@ -266,6 +266,11 @@ class CgsSolver(IterativeSolver):
         # rt = b, p q u uh vh t = 0, baseline / check(0), rho = rt.r, beta
         _lib.call("bicgstab_init_" + suf, n, ptr(S.b), 1, ptr(r), ptr(rt), ptr(p), ptr(q), ptr(u), ptr(t),
                   ptr(uh), ptr(vh), S.c, S.p, S.h, exc.stream)
+        if config.BICGSTAB_COOP and CgSolver._coop_ok(self, J, S):
+            a = CgSolver._coop_csr(self)  # small system: one persistent cooperative launch
+            _lib.call("cgs_coop_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(r), ptr(rt), ptr(p),
+                      ptr(q), ptr(u), ptr(vh), ptr(w), ptr(t), S.c, S.p, S.h, exc.stream)
+            return finish_from_device(self, S, S.status(), x)
         fa = fused_csr(self)
 
         def body():
