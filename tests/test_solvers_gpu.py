@@ -508,3 +508,27 @@ def test_cg_fold_p_matches_separate_step(cuda, monkeypatch):
         out[fold] = (s.last_status.iterations, np.asarray(x.data).copy())
     assert out[True][0] == out[False][0]
     np.testing.assert_array_equal(out[True][1], out[False][1])
+
+
+@pytest.mark.parametrize("name", ["Bicgstab", "Cgs", "Fcg"])
+def test_cooperative_small_system_path(cuda, monkeypatch, name):
+    """Small unpreconditioned systems run BiCGSTAB / CGS / FCG as one
+    persistent cooperative launch; it must agree with the batched kernels
+    (same iteration count +-1, same solution to 1e-10)."""
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib, config, problems
+
+    kind = "7pt" if name == "Fcg" else "convdiff"
+    a = problems.stencil(cuda, kind, 16)
+    n = a.size.rows
+    res = {}
+    for coop in (True, False):
+        monkeypatch.setattr(config, "BICGSTAB_COOP", coop)
+        s = getattr(b2, name)(cuda, criteria=[b2.Iteration(2000), b2.ResidualNormReduction(1e-10)]).generate(a)
+        x = b2.Dense.zeros(cuda, n, 1)
+        l0 = _lib.launch_count()
+        s.apply(b2.Dense(cuda, np.ones((n, 1))), x)
+        res[coop] = (s.last_status.iterations, np.asarray(x.data).copy(), _lib.launch_count() - l0)
+    assert res[True][0] > 0 and abs(res[True][0] - res[False][0]) <= 1
+    assert res[True][2] < res[False][2]  # one solve launch vs batches of step kernels
+    np.testing.assert_allclose(res[True][1], res[False][1], rtol=0, atol=1e-10 * np.abs(res[False][1]).max())
