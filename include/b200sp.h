@@ -404,6 +404,15 @@ int b200sp_gmres_after_commit(void* ctl, void* stream);
                                    const double* gm, void* stream);
 B200SP_KRYLOV_DECL(double, f64)
 B200SP_KRYLOV_DECL(float, f32)
+/* Arnoldi step j of GMRES for small systems (n <= b200sp_gmres_small_rows()):
+ * dot0, every MGS step, the Givens update + check and the normalisation of
+ * v_j in one single-block launch (replaces gmres_dot0 + j x gmres_mgs +
+ * gmres_normalize; gmres.py:88-129). */
+int32_t b200sp_gmres_small_rows(void);
+int b200sp_gmres_arnoldi_small_f64(int64_t n, int32_t j, double* V, double* w, void* ctl, double* gm, double* hist,
+                                   void* stream);
+int b200sp_gmres_arnoldi_small_f32(int64_t n, int32_t j, float* V, float* w, void* ctl, double* gm, double* hist,
+                                   void* stream);
 
 /* Csr SpMV q = A p fused with the solver reduction that follows it (sub-warp
  * per row, classical layout): phase 1 = CG sigma = p.q (replaces

@@ -85,6 +85,7 @@ _TYPED = {
     "gmres_dot0": "lipppppp",
     "gmres_mgs": "lii" + "ppppppp",
     "gmres_normalize": "lipppp",
+    "gmres_arnoldi_small": "lipppppp",
     "gmres_combine": "lppl" + "lpppp" + "ppp",
     # distributed
     "split_fill": "lpppippppppp",
@@ -115,6 +116,7 @@ _UNTYPED = {
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_seg_plan": ("llppp", ctypes.c_int),
     "peer_max": ("", ctypes.c_int32),
+    "gmres_small_rows": ("", ctypes.c_int32),
     "peer_wait": ("pipip", ctypes.c_int),
     "peer_allreduce": ("piiippip", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),

@@ -22,6 +22,8 @@ SOLVER_BATCH = int(os.environ.get("B200SP_SOLVER_BATCH", "16"))
 #: unpreconditioned Csr CG up to this many rows runs as one persistent
 #: cooperative kernel (0 disables)
 CG_COOP_MAX_ROWS = int(os.environ.get("B200SP_CG_COOP_MAX_ROWS", str(1 << 20)))
+# GMRES: one single-block launch per Arnoldi step for systems of <= 4096 rows
+GMRES_SMALL = os.environ.get("B200SP_GMRES_SMALL", "1") != "0"
 # BiCGSTAB and FCG on the same cooperative single-launch path as CG (same row limit)
 BICGSTAB_COOP = os.environ.get("B200SP_BICGSTAB_COOP", "1") != "0"
 

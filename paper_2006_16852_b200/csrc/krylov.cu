@@ -1120,32 +1120,11 @@ gmres_dot0_kernel(int64_t n, int j, const T* __restrict__ V, const T* __restrict
     G.H[0 * G.k + (j - 1)] = tot[0];
 }
 
-// MGS step i of Arnoldi step j: w -= h_i v_i, then h_{i+1} = v_{i+1}.w, or,
-// for i = j-1, ||w||, the Givens update and the next check (gmres.py:88-129)
-template <typename T>
-__global__ void __launch_bounds__(KRY_BLOCK)
-gmres_mgs_kernel(int64_t n, int j, int i, const T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* part,
-                 double* gm, double* hist) {
-    if (c->stopped || c->done) return;
-    GmresView G(gm, c->kdim);
-    const T h = (T)G.H[i * G.k + (j - 1)];
-    const T* vi = V + (int64_t)i * n;
-    const bool last = (i == j - 1);
-    const T* vn = last ? w : V + (int64_t)(i + 1) * n;
-    double s = 0;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-        const T wv = w[r] - h * vi[r];
-        w[r] = wv;
-        s += (double)(last ? wv : vn[r]) * (double)wv;
-    }
-    double vv[1] = {s}, tot[1];
-    if (!grid_reduce<1>(vv, part, &c->ticket[2], tot)) return;
-    if (!last) {
-        G.H[(i + 1) * G.k + (j - 1)] = tot[0];
-        return;
-    }
+// end of Arnoldi step j: h_{j+1,j} = ||w|| (ww = w.w), the Givens update of
+// column j-1, the new residual estimate and the check (gmres.py:88-129)
+__device__ inline void gmres_givens_ctl(KrylovCtl* c, GmresView& G, int j, double ww, double* hist) {
     const int col = j - 1;
-    const double hj = sqrt(tot[0]);
+    const double hj = sqrt(ww);
     c->hnorm = hj;
     G.H[j * G.k + col] = hj;
     for (int q = 0; q < j - 1; ++q) {
@@ -1176,6 +1155,118 @@ gmres_mgs_kernel(int64_t n, int j, int i, const T* __restrict__ V, T* __restrict
     if (j < G.k) {  // at j == k the restart recomputes the residual before the check
         hist_put(c, hist, c->it, c->rnorm);
         crit_check(c, c->it, c->rnorm);
+    }
+}
+
+// MGS step i of Arnoldi step j: w -= h_i v_i, then h_{i+1} = v_{i+1}.w, or,
+// for i = j-1, ||w||, the Givens update and the next check (gmres.py:88-129)
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_mgs_kernel(int64_t n, int j, int i, const T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* part,
+                 double* gm, double* hist) {
+    if (c->stopped || c->done) return;
+    GmresView G(gm, c->kdim);
+    const T h = (T)G.H[i * G.k + (j - 1)];
+    const T* vi = V + (int64_t)i * n;
+    const bool last = (i == j - 1);
+    const T* vn = last ? w : V + (int64_t)(i + 1) * n;
+    double s = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const T wv = w[r] - h * vi[r];
+        w[r] = wv;
+        s += (double)(last ? wv : vn[r]) * (double)wv;
+    }
+    double vv[1] = {s}, tot[1];
+    if (!grid_reduce<1>(vv, part, &c->ticket[2], tot)) return;
+    if (!last) {
+        G.H[(i + 1) * G.k + (j - 1)] = tot[0];
+        return;
+    }
+    gmres_givens_ctl(c, G, j, tot[0], hist);
+}
+
+// Small systems (one block covers every row): the whole MGS of Arnoldi step
+// j -- h_0 = v_0.w, then for every i: w -= h_i v_i and the next product, the
+// Givens update and check, and v_j = w / h -- in ONE single-block launch
+// with block barriers instead of j + 2 grid-wide launches (the reference's
+// MGS order, gmres.py:88-129, is kept: every h_i uses the updated w).
+constexpr int GMRES_SMALL_RPT = 8;  // rows per thread
+constexpr int GMRES_SMALL_ROWS = KRY_BLOCK * GMRES_SMALL_RPT;
+
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_arnoldi_small_kernel(int64_t n, int j, T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm,
+                           double* hist) {
+    constexpr int R = GMRES_SMALL_RPT;
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double bc;
+    if (c->stopped || c->done) return;
+    GmresView G(gm, c->kdim);
+    auto reduce = [&](double v) {  // block sum broadcast to every thread
+        const double t = block_sum(v, sh);
+        if (threadIdx.x == 0) bc = t;
+        __syncthreads();
+        const double r = bc;
+        __syncthreads();
+        return r;
+    };
+    auto load = [&](const T* src, T (&dst)[R]) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int64_t r = threadIdx.x + (int64_t)q * KRY_BLOCK;
+            dst[q] = r < n ? src[r] : T(0);
+        }
+    };
+    // w and the basis rows live in registers; the next basis row is loaded
+    // one pass ahead so its latency overlaps the current pass's reduction
+    T wr[R], vi[R], vn[R];
+    load(w, wr);
+    load(V, vi);
+    if (j > 1) load(V + n, vn);
+    double s = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) s += (double)vi[q] * (double)wr[q];
+    double h = reduce(s);
+    if (threadIdx.x == 0) G.H[0 * G.k + (j - 1)] = h;
+    for (int i = 0; i < j; ++i) {
+        const T th = (T)h;
+        const bool last = (i == j - 1);
+        T vnn[R];
+        if (i + 2 < j) load(V + (int64_t)(i + 2) * n, vnn);
+        s = 0;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const T wv = wr[q] - th * vi[q];
+            wr[q] = wv;
+            s += (double)(last ? wv : vn[q]) * (double)wv;
+        }
+        h = reduce(s);
+        if (!last) {
+            if (threadIdx.x == 0) G.H[(i + 1) * G.k + (j - 1)] = h;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                vi[q] = vn[q];
+                vn[q] = vnn[q];
+            }
+        } else if (threadIdx.x == 0) {
+            gmres_givens_ctl(c, G, j, h, hist);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int64_t r = threadIdx.x + (int64_t)q * KRY_BLOCK;
+        if (r < n) w[r] = wr[q];
+    }
+    __syncthreads();
+    // v_j = w / h_{j,j-1}   (gmres_normalize)
+    if (((volatile KrylovCtl*)c)->done) return;
+    if (((volatile KrylovCtl*)c)->stopped && ((volatile KrylovCtl*)c)->jpos != j) return;
+    const double hj = ((volatile KrylovCtl*)c)->hnorm;
+    T* vj = V + (int64_t)j * n;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int64_t r = threadIdx.x + (int64_t)q * KRY_BLOCK;
+        if (r < n) vj[r] = hj == 0.0 ? T(0) : (T)((double)wr[q] / hj);
     }
 }
 
@@ -1544,6 +1635,14 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
                                double* gm, double* hist, void* stream) {                                          \
         KRY_LAUNCH(gmres_mgs_kernel<T>, n, KRY_BLOCK, n, j, i, V, w, (KrylovCtl*)ctl, part, gm, hist);            \
     }                                                                                                             \
+    int b200sp_gmres_arnoldi_small_##SUF(int64_t n, int32_t j, T* V, T* w, void* ctl, double* gm, double* hist, \
+                                         void* stream) {                                                          \
+        B200SP_REQUIRE(n <= GMRES_SMALL_ROWS, B200SP_EINVAL, "gmres_arnoldi_small: n must be <= %d",             \
+                       GMRES_SMALL_ROWS);                                                                         \
+        gmres_arnoldi_small_kernel<T><<<1, KRY_BLOCK, 0, as_stream(stream)>>>(n, j, V, w, (KrylovCtl*)ctl, gm, hist); \
+        count_launch();                                                                                           \
+        return check_launch("gmres_arnoldi_small");                                                               \
+    }                                                                                                             \
     int b200sp_gmres_normalize_##SUF(int64_t n, int32_t j, T* V, const T* w, const void* ctl, void* stream) {     \
         KRY_LAUNCH(gmres_normalize_kernel<T>, n, KRY_BLOCK, n, j, V, w, (const KrylovCtl*)ctl);                   \
     }                                                                                                             \
@@ -1554,6 +1653,8 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
 
 KRYLOV_T(double, f64)
 KRYLOV_T(float, f32)
+
+int32_t b200sp_gmres_small_rows(void) { return GMRES_SMALL_ROWS; }
 
 int b200sp_gmres_backsolve(void* ctl, double* gm, void* stream) {
     gmres_backsolve_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl, gm);

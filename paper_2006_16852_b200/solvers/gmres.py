@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import torch
 
-from .. import _lib
+from .. import _lib, config
 from ..errors import ParameterError
 from ..executor import ptr
 from . import generic
@@ -54,6 +54,8 @@ class GmresSolver(IterativeSolver):
         _lib.call("gmres_scale_v0_" + suf, n, ptr(r), ptr(V), S.c, exc.stream)
         stopped_guard, done_guard = S.guard(1), S.guard(0)
 
+        small = config.GMRES_SMALL and n <= int(_lib.query("gmres_small_rows"))
+
         def cycle():
             _lib.query("set_guard", stopped_guard)
             for j in range(1, k + 1):
@@ -62,6 +64,9 @@ class GmresSolver(IterativeSolver):
                     self.precond.apply(src, zd)
                     src = zd
                 self.a.apply(src, wd)
+                if small:  # the whole MGS + Givens + normalisation in one single-block launch
+                    _lib.call("gmres_arnoldi_small_" + suf, n, j, ptr(V), ptr(w), S.c, ptr(gm), S.h, exc.stream)
+                    continue
                 _lib.call("gmres_dot0_" + suf, n, j, ptr(V), ptr(w), S.c, S.p, ptr(gm), exc.stream)
                 for i in range(j):
                     _lib.call("gmres_mgs_" + suf, n, j, i, ptr(V), ptr(w), S.c, S.p, ptr(gm), S.h, exc.stream)
