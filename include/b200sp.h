@@ -413,6 +413,13 @@ int b200sp_gmres_arnoldi_small_f64(int64_t n, int32_t j, double* V, double* w, v
                                    void* stream);
 int b200sp_gmres_arnoldi_small_f32(int64_t n, int32_t j, float* V, float* w, void* ctl, double* gm, double* hist,
                                    void* stream);
+/* A whole Arnoldi cycle (j = 1..k until a check stops it) of an
+ * unpreconditioned Csr system of n <= b200sp_gmres_small_rows() rows in one
+ * single-block launch: w = A v_{j-1} and the Arnoldi step above. */
+int b200sp_gmres_cycle_small_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
+                                 double* V, double* w, void* ctl, double* gm, double* hist, void* stream);
+int b200sp_gmres_cycle_small_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
+                                 float* V, float* w, void* ctl, double* gm, double* hist, void* stream);
 
 /* Csr SpMV q = A p fused with the solver reduction that follows it (sub-warp
  * per row, classical layout): phase 1 = CG sigma = p.q (replaces

@@ -86,6 +86,7 @@ _TYPED = {
     "gmres_mgs": "lii" + "ppppppp",
     "gmres_normalize": "lipppp",
     "gmres_arnoldi_small": "lipppppp",
+    "gmres_cycle_small": "l" + "p" * 9,
     "gmres_combine": "lppl" + "lpppp" + "ppp",
     # distributed
     "split_fill": "lpppippppppp",

@@ -1158,6 +1158,45 @@ __device__ inline void gmres_givens_ctl(KrylovCtl* c, GmresView& G, int j, doubl
     }
 }
 
+// gmres_givens_ctl on a staged copy: L.H / L.cs / L.sn point at shared memory
+// (the new column of H with stride 1, the previous rotations); the new
+// rotation and the g updates go straight to the workspace G
+__device__ inline void gmres_givens_ctl_col(KrylovCtl* c, GmresView& L, GmresView& G, int j, double ww, double* hist) {
+    const int col = j - 1;
+    const double hj = sqrt(ww);
+    c->hnorm = hj;
+    L.H[j * L.k + col] = hj;
+    for (int q = 0; q < j - 1; ++q) {
+        const double h1 = L.H[q * L.k + col], h2 = L.H[(q + 1) * L.k + col];
+        L.H[q * L.k + col] = L.cs[q] * h1 + L.sn[q] * h2;
+        L.H[(q + 1) * L.k + col] = -L.sn[q] * h1 + L.cs[q] * h2;
+    }
+    const double h1 = L.H[col * L.k + col], h2 = L.H[j * L.k + col];
+    const double den = hypot(h1, h2);
+    const double cc = den != 0.0 ? h1 / den : 1.0, sn = den != 0.0 ? h2 / den : 0.0;
+    G.cs[col] = cc;
+    G.sn[col] = sn;
+    L.H[col * L.k + col] = den;
+    L.H[j * L.k + col] = 0.0;
+    const double gv = G.g[col];
+    G.g[col] = cc * gv;
+    G.g[j] = -sn * gv;
+    c->rnorm = fabs(G.g[j]);
+    c->jpos = j;
+    c->it += 1;
+    if (hj == 0.0) {  // happy breakdown: declared exact (gmres.py:245-248, :262-268)
+        c->stopped = 1;
+        c->stopping_id = EXACT_CONVERGENCE_ID;
+        c->finalized = 1;
+        c->rnorm = 0.0;
+        return;
+    }
+    if (j < G.k) {
+        hist_put(c, hist, c->it, c->rnorm);
+        crit_check(c, c->it, c->rnorm);
+    }
+}
+
 // MGS step i of Arnoldi step j: w -= h_i v_i, then h_{i+1} = v_{i+1}.w, or,
 // for i = j-1, ||w||, the Givens update and the next check (gmres.py:88-129)
 template <typename T>
@@ -1192,15 +1231,15 @@ gmres_mgs_kernel(int64_t n, int j, int i, const T* __restrict__ V, T* __restrict
 // MGS order, gmres.py:88-129, is kept: every h_i uses the updated w).
 constexpr int GMRES_SMALL_RPT = 8;  // rows per thread
 constexpr int GMRES_SMALL_ROWS = KRY_BLOCK * GMRES_SMALL_RPT;
+constexpr int GMRES_SMALL_MAXK = 256;  // Givens column staged in shared memory up to this restart length
 
 template <typename T>
-__global__ void __launch_bounds__(KRY_BLOCK)
-gmres_arnoldi_small_kernel(int64_t n, int j, T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm,
-                           double* hist) {
+__device__ void gmres_arnoldi_small_body(int64_t n, int j, T* __restrict__ V, T* __restrict__ w, KrylovCtl* c,
+                                         double* gm, double* hist) {
     constexpr int R = GMRES_SMALL_RPT;
     __shared__ double sh[KRY_BLOCK / 32];
     __shared__ double bc;
-    if (c->stopped || c->done) return;
+    if (((volatile KrylovCtl*)c)->stopped || ((volatile KrylovCtl*)c)->done) return;
     GmresView G(gm, c->kdim);
     auto reduce = [&](double v) {  // block sum broadcast to every thread
         const double t = block_sum(v, sh);
@@ -1248,6 +1287,30 @@ gmres_arnoldi_small_kernel(int64_t n, int j, T* __restrict__ V, T* __restrict__ 
                 vi[q] = vn[q];
                 vn[q] = vnn[q];
             }
+        } else if (j <= GMRES_SMALL_MAXK) {
+            // the Givens sweep over the new column runs out of shared memory:
+            // stage the column and the rotations (parallel loads), rotate in
+            // one thread, write back (a global-memory sweep is a chain of
+            // dependent L2 round trips, ~0.5 us per rotation)
+            __shared__ double colb[GMRES_SMALL_MAXK + 1], csb[GMRES_SMALL_MAXK], snb[GMRES_SMALL_MAXK];
+            const int col = j - 1;
+            __syncthreads();
+            for (int q = threadIdx.x; q < j; q += KRY_BLOCK) colb[q] = G.H[q * G.k + col];
+            for (int q = threadIdx.x; q < j - 1; q += KRY_BLOCK) {
+                csb[q] = G.cs[q];
+                snb[q] = G.sn[q];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                GmresView L = G;
+                L.H = colb - col;  // column view: L.H[q * L.k + col] = colb[q] with L.k = 1
+                L.k = 1;
+                L.cs = csb;
+                L.sn = snb;
+                gmres_givens_ctl_col(c, L, G, j, h, hist);
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q <= j; q += KRY_BLOCK) G.H[q * G.k + col] = colb[q];
         } else if (threadIdx.x == 0) {
             gmres_givens_ctl(c, G, j, h, hist);
         }
@@ -1270,6 +1333,21 @@ gmres_arnoldi_small_kernel(int64_t n, int j, T* __restrict__ V, T* __restrict__ 
     }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_arnoldi_small_kernel(int64_t n, int j, T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm,
+                           double* hist) {
+    gmres_arnoldi_small_body<T>(n, j, V, w, c, gm, hist);
+}
+
+// A whole Arnoldi cycle of an unpreconditioned small system in one
+// single-block launch: for j = 1..k (until a check stops it) w = A v_{j-1}
+// (rows summed left to right), then the single-block Arnoldi step above.
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_cycle_small_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                         T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm, double* hist);
+
 // v_j = w / h_{j,j-1} (0 on happy breakdown)
 template <typename T>
 __global__ void gmres_normalize_kernel(int64_t n, int j, T* __restrict__ V, const T* __restrict__ w, const KrylovCtl* c) {
@@ -1279,6 +1357,25 @@ __global__ void gmres_normalize_kernel(int64_t n, int j, T* __restrict__ V, cons
     T* vj = V + (int64_t)j * n;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
         vj[r] = hj == 0.0 ? T(0) : (T)((double)w[r] / hj);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KRY_BLOCK)
+gmres_cycle_small_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                         T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm, double* hist) {
+    const int k = c->kdim;
+    for (int j = 1; j <= k; ++j) {
+        if (((volatile KrylovCtl*)c)->stopped || ((volatile KrylovCtl*)c)->done) return;
+        const T* src = V + (int64_t)(j - 1) * n;
+        for (int64_t r = threadIdx.x; r < n; r += KRY_BLOCK) {
+            T acc = 0;
+            for (int q = rp[r]; q < rp[r + 1]; ++q) acc += av[q] * src[ci[q]];
+            w[r] = acc;
+        }
+        __syncthreads();
+        gmres_arnoldi_small_body<T>(n, j, V, w, c, gm, hist);
+        __syncthreads();
+    }
 }
 
 // back-solve of the rotated triangular system at jc = jpos (gmres.py:157-167)
@@ -1642,6 +1739,15 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
         gmres_arnoldi_small_kernel<T><<<1, KRY_BLOCK, 0, as_stream(stream)>>>(n, j, V, w, (KrylovCtl*)ctl, gm, hist); \
         count_launch();                                                                                           \
         return check_launch("gmres_arnoldi_small");                                                               \
+    }                                                                                                             \
+    int b200sp_gmres_cycle_small_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* V, T* w,  \
+                                       void* ctl, double* gm, double* hist, void* stream) {                      \
+        B200SP_REQUIRE(n <= GMRES_SMALL_ROWS, B200SP_EINVAL, "gmres_cycle_small: n must be <= %d",               \
+                       GMRES_SMALL_ROWS);                                                                         \
+        gmres_cycle_small_kernel<T><<<1, KRY_BLOCK, 0, as_stream(stream)>>>(n, rp, ci, v, V, w, (KrylovCtl*)ctl, gm, \
+                                                                             hist);                               \
+        count_launch();                                                                                           \
+        return check_launch("gmres_cycle_small");                                                                 \
     }                                                                                                             \
     int b200sp_gmres_normalize_##SUF(int64_t n, int32_t j, T* V, const T* w, const void* ctl, void* stream) {     \
         KRY_LAUNCH(gmres_normalize_kernel<T>, n, KRY_BLOCK, n, j, V, w, (const KrylovCtl*)ctl);                   \

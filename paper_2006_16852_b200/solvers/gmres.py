@@ -26,6 +26,12 @@ DEFAULT_KRYLOV_DIM = 100
 EXACT_CONVERGENCE_ID = 254
 
 
+def _sparse(a):
+    from ..formats import _Sparse
+
+    return isinstance(a, _Sparse)
+
+
 class GmresSolver(IterativeSolver):
     def _apply_impl(self, b, x):
         k = int(self.params.get("krylov_dim") or DEFAULT_KRYLOV_DIM)
@@ -55,10 +61,18 @@ class GmresSolver(IterativeSolver):
         stopped_guard, done_guard = S.guard(1), S.guard(0)
 
         small = config.GMRES_SMALL and n <= int(_lib.query("gmres_small_rows"))
+        whole = small and z is None and _sparse(self.a)
+        if whole:
+            from .krylov import CgSolver
+
+            a = CgSolver._coop_csr(self)
 
         def cycle():
             _lib.query("set_guard", stopped_guard)
-            for j in range(1, k + 1):
+            if whole:  # the whole Arnoldi cycle in one single-block launch
+                _lib.call("gmres_cycle_small_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(V), ptr(w), S.c,
+                          ptr(gm), S.h, exc.stream)
+            for j in range(1, k + 1) if not whole else ():
                 src = vdense[j - 1]
                 if z is not None:
                     self.precond.apply(src, zd)
