@@ -1231,17 +1231,19 @@ gmres_mgs_kernel(int64_t n, int j, int i, const T* __restrict__ V, T* __restrict
 // MGS order, gmres.py:88-129, is kept: every h_i uses the updated w).
 constexpr int GMRES_SMALL_RPT = 8;  // rows per thread
 constexpr int GMRES_SMALL_ROWS = KRY_BLOCK * GMRES_SMALL_RPT;
-constexpr int GMRES_SMALL_MAXK = 256;  // Givens column staged in shared memory up to this restart length
+constexpr int GMRES_SMALL_MAXK = 256;
+constexpr int GMRES_SMEM_BYTES = 32 * 1024;  // on-chip basis for tiny systems  // Givens column staged in shared memory up to this restart length
 
-template <typename T>
+template <typename T, int NT>
 __device__ void gmres_arnoldi_small_body(int64_t n, int j, T* __restrict__ V, T* __restrict__ w, KrylovCtl* c,
                                          double* gm, double* hist) {
     constexpr int R = GMRES_SMALL_RPT;
-    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh[NT / 32 > 0 ? NT / 32 : 1];
     __shared__ double bc;
     if (((volatile KrylovCtl*)c)->stopped || ((volatile KrylovCtl*)c)->done) return;
     GmresView G(gm, c->kdim);
     auto reduce = [&](double v) {  // block sum broadcast to every thread
+        if (NT == 32) return warp_sum(v);  // one warp: no barriers at all
         const double t = block_sum(v, sh);
         if (threadIdx.x == 0) bc = t;
         __syncthreads();
@@ -1252,7 +1254,7 @@ __device__ void gmres_arnoldi_small_body(int64_t n, int j, T* __restrict__ V, T*
     auto load = [&](const T* src, T (&dst)[R]) {
 #pragma unroll
         for (int q = 0; q < R; ++q) {
-            const int64_t r = threadIdx.x + (int64_t)q * KRY_BLOCK;
+            const int64_t r = threadIdx.x + (int64_t)q * NT;
             dst[q] = r < n ? src[r] : T(0);
         }
     };
@@ -1295,8 +1297,8 @@ __device__ void gmres_arnoldi_small_body(int64_t n, int j, T* __restrict__ V, T*
             __shared__ double colb[GMRES_SMALL_MAXK + 1], csb[GMRES_SMALL_MAXK], snb[GMRES_SMALL_MAXK];
             const int col = j - 1;
             __syncthreads();
-            for (int q = threadIdx.x; q < j; q += KRY_BLOCK) colb[q] = G.H[q * G.k + col];
-            for (int q = threadIdx.x; q < j - 1; q += KRY_BLOCK) {
+            for (int q = threadIdx.x; q < j; q += NT) colb[q] = G.H[q * G.k + col];
+            for (int q = threadIdx.x; q < j - 1; q += NT) {
                 csb[q] = G.cs[q];
                 snb[q] = G.sn[q];
             }
@@ -1310,14 +1312,14 @@ __device__ void gmres_arnoldi_small_body(int64_t n, int j, T* __restrict__ V, T*
                 gmres_givens_ctl_col(c, L, G, j, h, hist);
             }
             __syncthreads();
-            for (int q = threadIdx.x; q <= j; q += KRY_BLOCK) G.H[q * G.k + col] = colb[q];
+            for (int q = threadIdx.x; q <= j; q += NT) G.H[q * G.k + col] = colb[q];
         } else if (threadIdx.x == 0) {
             gmres_givens_ctl(c, G, j, h, hist);
         }
     }
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-        const int64_t r = threadIdx.x + (int64_t)q * KRY_BLOCK;
+        const int64_t r = threadIdx.x + (int64_t)q * NT;
         if (r < n) w[r] = wr[q];
     }
     __syncthreads();
@@ -1328,7 +1330,7 @@ __device__ void gmres_arnoldi_small_body(int64_t n, int j, T* __restrict__ V, T*
     T* vj = V + (int64_t)j * n;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-        const int64_t r = threadIdx.x + (int64_t)q * KRY_BLOCK;
+        const int64_t r = threadIdx.x + (int64_t)q * NT;
         if (r < n) vj[r] = hj == 0.0 ? T(0) : (T)((double)wr[q] / hj);
     }
 }
@@ -1337,14 +1339,14 @@ template <typename T>
 __global__ void __launch_bounds__(KRY_BLOCK)
 gmres_arnoldi_small_kernel(int64_t n, int j, T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm,
                            double* hist) {
-    gmres_arnoldi_small_body<T>(n, j, V, w, c, gm, hist);
+    gmres_arnoldi_small_body<T, KRY_BLOCK>(n, j, V, w, c, gm, hist);
 }
 
 // A whole Arnoldi cycle of an unpreconditioned small system in one
 // single-block launch: for j = 1..k (until a check stops it) w = A v_{j-1}
 // (rows summed left to right), then the single-block Arnoldi step above.
-template <typename T>
-__global__ void __launch_bounds__(KRY_BLOCK)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT)
 gmres_cycle_small_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                          T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm, double* hist);
 
@@ -1359,22 +1361,38 @@ __global__ void gmres_normalize_kernel(int64_t n, int j, T* __restrict__ V, cons
         vj[r] = hj == 0.0 ? T(0) : (T)((double)w[r] / hj);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(KRY_BLOCK)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT)
 gmres_cycle_small_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
-                         T* __restrict__ V, T* __restrict__ w, KrylovCtl* c, double* gm, double* hist) {
+                         T* __restrict__ Vg, T* __restrict__ wg, KrylovCtl* c, double* gm, double* hist) {
+    // tiny systems (the basis fits in shared memory, `dynamic` bytes): the
+    // cycle runs on an on-chip copy of V and w, written back at the end
+    extern __shared__ __align__(16) unsigned char gsm[];
     const int k = c->kdim;
+    const bool onchip = (size_t)(k + 2) * n * sizeof(T) <= GMRES_SMEM_BYTES;
+    T* V = onchip ? reinterpret_cast<T*>(gsm) : Vg;
+    T* w = onchip ? V + (size_t)(k + 1) * n : wg;
+    if (onchip) {
+        for (int64_t r = threadIdx.x; r < n; r += NT) V[r] = Vg[r];  // v_0 from gmres_scale_v0
+        __syncthreads();
+    }
+    int jdone = 0;
     for (int j = 1; j <= k; ++j) {
-        if (((volatile KrylovCtl*)c)->stopped || ((volatile KrylovCtl*)c)->done) return;
+        if (((volatile KrylovCtl*)c)->stopped || ((volatile KrylovCtl*)c)->done) break;
         const T* src = V + (int64_t)(j - 1) * n;
-        for (int64_t r = threadIdx.x; r < n; r += KRY_BLOCK) {
+        for (int64_t r = threadIdx.x; r < n; r += NT) {
             T acc = 0;
             for (int q = rp[r]; q < rp[r + 1]; ++q) acc += av[q] * src[ci[q]];
             w[r] = acc;
         }
         __syncthreads();
-        gmres_arnoldi_small_body<T>(n, j, V, w, c, gm, hist);
+        gmres_arnoldi_small_body<T, NT>(n, j, V, w, c, gm, hist);
         __syncthreads();
+        jdone = j;
+    }
+    if (onchip) {  // the basis rows written this cycle (gmres_combine reads them)
+        for (int64_t e = n + threadIdx.x; e < (int64_t)(jdone + 1) * n; e += NT) Vg[e] = V[e];
+        for (int64_t r = threadIdx.x; r < n; r += NT) wg[r] = w[r];
     }
 }
 
@@ -1744,8 +1762,12 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
                                        void* ctl, double* gm, double* hist, void* stream) {                      \
         B200SP_REQUIRE(n <= GMRES_SMALL_ROWS, B200SP_EINVAL, "gmres_cycle_small: n must be <= %d",               \
                        GMRES_SMALL_ROWS);                                                                         \
-        gmres_cycle_small_kernel<T><<<1, KRY_BLOCK, 0, as_stream(stream)>>>(n, rp, ci, v, V, w, (KrylovCtl*)ctl, gm, \
-                                                                             hist);                               \
+        if (n <= 32 * GMRES_SMALL_RPT) /* one warp: reductions without block barriers */                        \
+            gmres_cycle_small_kernel<T, 32><<<1, 32, GMRES_SMEM_BYTES, as_stream(stream)>>>(n, rp, ci, v, V, w,  \
+                                                                                           (KrylovCtl*)ctl, gm, hist); \
+        else                                                                                                      \
+            gmres_cycle_small_kernel<T, KRY_BLOCK><<<1, KRY_BLOCK, GMRES_SMEM_BYTES, as_stream(stream)>>>(         \
+                n, rp, ci, v, V, w, (KrylovCtl*)ctl, gm, hist);                                                   \
         count_launch();                                                                                           \
         return check_launch("gmres_cycle_small");                                                                 \
     }                                                                                                             \
