@@ -1397,8 +1397,12 @@ gmres_cycle_small_kernel(int64_t n, const int* __restrict__ rp, const int* __res
 }
 
 // back-solve of the rotated triangular system at jc = jpos (gmres.py:157-167)
+// One warp: row i's dot with y[i+1:jc] (the reference's h[i, i+1:jc] @ y)
+// is spread over the lanes and shuffle-summed -- a single thread's serial
+// sweep is jc^2/2 dependent global loads (~340 us per GMRES(100) cycle).
 __global__ void gmres_backsolve_kernel(KrylovCtl* c, double* gm) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
     if (c->done || c->committed) return;
     GmresView G(gm, c->kdim);
     const int jc = c->jpos;
@@ -1407,16 +1411,20 @@ __global__ void gmres_backsolve_kernel(KrylovCtl* c, double* gm) {
     for (int i = jc - 1; i >= 0; --i) {
         const double d = G.H[i * G.k + i];
         if (d == 0.0) {
-            c->breakdown = BD_HESSENBERG;
-            c->breakdown_it = c->it;
-            c->done = 1;
+            if (lane == 0) {
+                c->breakdown = BD_HESSENBERG;
+                c->breakdown_it = c->it;
+                c->done = 1;
+            }
             return;
         }
         double acc = 0.0;
-        for (int q = i + 1; q < jc; ++q) acc += G.H[i * G.k + q] * G.y[q];
-        G.y[i] = (G.g[i] - acc) / d;
+        for (int q = i + 1 + lane; q < jc; q += 32) acc += G.H[i * G.k + q] * ((volatile double*)G.y)[q];
+        acc = warp_sum(acc);
+        if (lane == 0) G.y[i] = (G.g[i] - acc) / d;
+        __syncwarp();
     }
-    c->committed = 1;  // combine pending
+    if (lane == 0) c->committed = 1;  // combine pending
 }
 
 // x += M (V y): u = sum_i y_i v_i row-wise, then the block-Jacobi of u
