@@ -870,9 +870,22 @@ csr_lb2_kernel(int64_t n, int64_t ntiles, const int* __restrict__ rp, const int*
                 x[(int64_t)row * xs] = out;
             }
         }
-        // carry-out: the entries of row r1 inside this tile
+        // carry-out: the entries of row r1 inside this tile (a short segment
+        // -- up to 128 entries -- is summed by warp 0 alone, no CTA barrier)
         T carry = 0;
-        if (r1 < n) carry = lb2_block_dot(max(__ldg(rp + r1), k0), k1, ci, v, b, bs, s_red);
+        if (r1 < n) {
+            const int cs = max(__ldg(rp + r1), k0);
+            if (k1 - cs <= 128) {
+                if (threadIdx.x < 32) {
+                    T a0 = 0;
+                    for (int k = cs + (int)threadIdx.x; k < k1; k += 32)
+                        a0 += __ldg(v + k) * ld_gather(b + (int64_t)__ldg(ci + k) * bs);
+                    carry = warp_sum(a0);
+                }
+            } else {
+                carry = lb2_block_dot(cs, k1, ci, v, b, bs, s_red);
+            }
+        }
         if (threadIdx.x == 0) {
             carry_row[tile] = r1;
             carry_val[tile] = carry;
