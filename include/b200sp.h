@@ -304,6 +304,26 @@ int b200sp_jacobi_apply_f64(int64_t nblocks, const int32_t* starts, const int64_
 int b200sp_jacobi_apply_f32(int64_t nblocks, const int32_t* starts, const int64_t* offs, const uint8_t* prec,
                             const void* storage, int32_t m, const float* r, int64_t rs, float* z, int64_t zs,
                             void* stream);
+/* Blocks of more than 32 rows (any block_size / block_boundaries, reference
+ * src/precond.py:155-197): same arithmetic contract as the warp kernels, one
+ * CTA per block with [B | I] in a caller-provided fp64 scratch of
+ * slots x max_bs x 2 max_bs (slots = CTAs in flight), max_bs <=
+ * b200sp_jacobi_large_max_block(). The apply takes any block sizes. */
+int64_t b200sp_jacobi_large_max_block(void);
+int b200sp_jacobi_invert_large_f64(int64_t nblocks, const int32_t* starts, const int32_t* rp, const int32_t* ci,
+                                   const double* vals, const int64_t* off64, double* inv64, double* cond,
+                                   uint8_t* prec, int32_t* nbytes, int32_t adaptive, double threshold,
+                                   int64_t* singular, int32_t max_bs, double* scratch, int32_t slots, void* stream);
+int b200sp_jacobi_invert_large_f32(int64_t nblocks, const int32_t* starts, const int32_t* rp, const int32_t* ci,
+                                   const float* vals, const int64_t* off64, double* inv64, double* cond,
+                                   uint8_t* prec, int32_t* nbytes, int32_t adaptive, double threshold,
+                                   int64_t* singular, int32_t max_bs, double* scratch, int32_t slots, void* stream);
+int b200sp_jacobi_apply_large_f64(int64_t nblocks, const int32_t* starts, const int64_t* offs, const uint8_t* prec,
+                                  const void* storage, int32_t m, const double* r, int64_t rs, double* z, int64_t zs,
+                                  void* stream);
+int b200sp_jacobi_apply_large_f32(int64_t nblocks, const int32_t* starts, const int64_t* offs, const uint8_t* prec,
+                                  const void* storage, int32_t m, const float* r, int64_t rs, float* z, int64_t zs,
+                                  void* stream);
 
 /* ---- device-resident Krylov iterations (m = 1) ---------------------------
  * Control block (b200sp_krylov_ctl_bytes) holds iteration count, status

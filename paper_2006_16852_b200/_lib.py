@@ -58,6 +58,8 @@ _TYPED = {
     # block-Jacobi
     "jacobi_invert": "lpppppppppidpp",
     "jacobi_apply": "lppppiplplp",
+    "jacobi_invert_large": "lpppppppppidppipip",
+    "jacobi_apply_large": "lppppiplplp",
     # Krylov (JAC = l p p p p)
     "cg_init": "lppp" + "lpppp" + "pppp",
     "cg_step1": "lpppp",
@@ -148,6 +150,7 @@ _UNTYPED = {
     "mm_parse": ("plpippplpp", ctypes.c_int),
     "jacobi_block_sizes_sq": ("lppp", ctypes.c_int),
     "jacobi_pack": ("lppppppp", ctypes.c_int),
+    "jacobi_large_max_block": ("", ctypes.c_int64),
     "krylov_ctl_bytes": ("", ctypes.c_int64),
     "krylov_part_elems": ("", ctypes.c_int64),
     "krylov_ctl_init": ("pippiiip", ctypes.c_int),

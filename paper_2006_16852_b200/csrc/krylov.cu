@@ -383,8 +383,7 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
         bool stop = false;
         int sid = 0;
         for (int i = 0; i < c->n_crit && !stop; ++i) {
-            if (c->crit_type[i] == CRIT_ITERATION && it >= (int)c->crit_param[i]) stop = true, sid = i + 1;
-            else if (c->crit_type[i] == CRIT_RNR && nrm <= c->crit_param[i] * c->baseline) stop = true, sid = i + 1;
+            if (crit_fires(c, i, it, nrm)) stop = true, sid = i + 1;
         }
         beta = safe_div(rho, rho_prev);
         if (gt == 0) {
@@ -1631,6 +1630,8 @@ static int csr_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, co
 #define RB(n) make_rb((n), jnb, jstarts, joffs, jprec, jstore)
 #define RB_UNITS(n) (jnb ? jnb * 32 : ((n) + 31) / 32 * 32)
 
+__global__ void krylov_start_clock_kernel(KrylovCtl* c) { c->t_start = global_ns(); }
+
 extern "C" {
 
 int64_t b200sp_krylov_ctl_bytes(void) { return (int64_t)sizeof(KrylovCtl); }
@@ -1650,8 +1651,10 @@ int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, 
     h.hist_cap = hist_cap;
     h.kdim = kdim;
     B200SP_CHECK_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, as_stream(stream)));
+    krylov_start_clock_kernel<<<1, 1, 0, as_stream(stream)>>>((KrylovCtl*)ctl);  // TimeLimit origin
+    count_launch();
     B200SP_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));  // &h is a stack buffer
-    return B200SP_OK;
+    return check_launch("krylov_ctl_init");
 }
 
 // status: ints [it, stopped, stopping_id, finalized, done, breakdown, breakdown_it, jpos]

@@ -20,7 +20,7 @@ constexpr int KRY_MAX_GRID = kNumSMs * 8;
 constexpr int KRY_MAX_CRIT = 8;
 constexpr int KRY_NRED = 4;  // partial-sum slots per reduction
 
-enum CritType : int { CRIT_ITERATION = 1, CRIT_RNR = 2 };
+enum CritType : int { CRIT_ITERATION = 1, CRIT_RNR = 2, CRIT_TIME = 3 };
 enum Breakdown : int { BD_NONE = 0, BD_CG_SIGMA = 1, BD_RHO = 2, BD_GAMMA = 3, BD_TT = 4, BD_HESSENBERG = 5 };
 constexpr int EXACT_CONVERGENCE_ID = 254;  // src/solvers/gmres.py:31
 
@@ -50,7 +50,26 @@ struct KrylovCtl {
     int pad2;
     double red[4];     // local reduction results, all-reduced across ranks in place
     double rho_t;      // FCG: t.z with t = r_new - r_old (src/solvers/krylov.py:80-125)
+    unsigned long long t_start;  // %globaltimer (ns) when the solve's control block was initialised
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One child of Combined: Iteration `it >= max` (src/stop.py:95-106), RNR
+// `||r|| <= factor ||r0||` (src/stop.py:187-196), TimeLimit `elapsed >= limit`
+// (src/stop.py:134-147) -- all evaluated at EVERY check, on the device: the
+// wall clock is the GPU's global nanosecond timer, started by ctl_init.
+__device__ __forceinline__ bool crit_fires(const KrylovCtl* c, int i, int it, double nrm) {
+    const int t = c->crit_type[i];
+    if (t == CRIT_ITERATION) return it >= (int)c->crit_param[i];
+    if (t == CRIT_RNR) return nrm <= c->crit_param[i] * c->baseline;
+    if (t == CRIT_TIME) return (double)(global_ns() - c->t_start) >= c->crit_param[i] * 1e9;
+    return false;
+}
 
 // ---------------------------------------------------------------------------
 // criteria: Combined ORs the children in order; child i stamps id i+1
@@ -60,10 +79,7 @@ struct KrylovCtl {
 __device__ inline void crit_check(KrylovCtl* c, int it, double nrm) {
     if (c->stopped) return;
     for (int i = 0; i < c->n_crit; ++i) {
-        bool fire = false;
-        if (c->crit_type[i] == CRIT_ITERATION) fire = it >= (int)c->crit_param[i];
-        else if (c->crit_type[i] == CRIT_RNR) fire = nrm <= c->crit_param[i] * c->baseline;
-        if (fire) {
+        if (crit_fires(c, i, it, nrm)) {
             c->stopped = 1;
             c->stopping_id = i + 1;
             c->finalized = 1;  // solvers pass set_finalized=True

@@ -410,7 +410,7 @@ class DistCg:
         self.exec = a.exec
         self.factory = Combined(criteria if isinstance(criteria, (list, tuple)) else [criteria])
         spec = self.factory.device_spec()
-        if spec is None or spec[1] is not None:
+        if spec is None or spec[1]:
             raise NotImplementedError("DistCg supports Iteration / ResidualNormReduction criteria")
         self.spec = spec[0]
         self.batch = int(batch or config.SOLVER_BATCH)

@@ -372,10 +372,16 @@ class _Sparse(LinOp):
                 setattr(obj, name, val.clone().to(target.device))
             elif isinstance(val, _Sparse):
                 setattr(obj, name, val.clone_to(target))
-        for cache in ("_plan", "_ws"):
+        # per-instance caches hold device buffers, streams and CUDA graphs
+        # captured against the SOURCE's pointers: the clone rebuilds its own
+        for cache in _INSTANCE_CACHES:
             if hasattr(obj, cache):
                 setattr(obj, cache, None)
         return obj
+
+
+#: lazily built per-instance state that must never be shared by clones
+_INSTANCE_CACHES = ("_plan", "_ws", "_pplan", "_hsplan")
 
 
 # ---------------------------------------------------------------------------
@@ -711,13 +717,17 @@ class Csr(_Sparse):
     def _pipeline_ok(self, b, x):
         from .executor import HostExecutor
 
-        return (self.HOST_PIPELINE_CHUNKS > 0 and isinstance(getattr(b, "exec", None), HostExecutor)
-                and isinstance(getattr(x, "exec", None), HostExecutor) and b.exec.pinned
+        if not (self.HOST_PIPELINE_CHUNKS > 0 and isinstance(getattr(b, "exec", None), HostExecutor)
+                and isinstance(getattr(x, "exec", None), HostExecutor) and b.exec.pinned and x.exec.pinned
                 and getattr(b, "is_dense", False) and getattr(x, "is_dense", False)
                 and b.size.cols == 1 and x.size.cols == 1 and self.size.rows >= (1 << 16)
                 and self._resolved_strategy() == "classical"
                 and np.asarray(b.values).flags.c_contiguous and np.asarray(x.values).flags.c_contiguous
-                and np.dtype(b.dtype) == self.value_dtype and np.dtype(x.dtype) == self.value_dtype)
+                and np.dtype(b.dtype) == self.value_dtype and np.dtype(x.dtype) == self.value_dtype):
+            return False
+        # the graph issues non_blocking copies: both buffers must really be
+        # page-locked (a Dense.wrap of a user ndarray on a pinned executor is not)
+        return all(torch.from_numpy(np.asarray(v.values).reshape(-1)).is_pinned() for v in (b, x))
 
     #: "copies": the copy-engine pipeline (chunked H2D / SpMV / D2H in a graph);
     #: "kernel": one cooperative kernel streams b in, reduces row tiles as their

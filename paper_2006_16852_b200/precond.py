@@ -6,8 +6,11 @@ reference's exact arithmetic order (bit-identical inverses), kappa_inf is
 computed with NumPy's pairwise row sums, and with ``adaptive_precision`` a
 block whose kappa is below ``condition_threshold`` is stored in fp32. The
 apply is a batched warp-per-block mat-vec; the solvers fuse it into their
-update kernels. Blocks are limited to 32 rows (one warp); larger explicit
-blocks raise Unsupported.
+update kernels. Blocks of up to 32 rows take the warp-per-block kernels
+(fused into the solver steps); larger blocks (any block_size or explicit
+boundaries up to 4096 rows, src/precond.py:155-197) take a CTA-per-block
+generation with the same Gauss-Jordan arithmetic and a CTA-per-block apply,
+and the solvers then apply the preconditioner as its own launch.
 """
 
 from __future__ import annotations
@@ -21,14 +24,16 @@ from .errors import DimensionMismatch, Singular, Unsupported
 from .executor import ptr
 from .formats import Csr, _require_cuda, convert
 
-MAX_BLOCK = 32
+WARP_BLOCK = 32     # largest block the fused warp-per-block kernels take
+MAX_BLOCK = 4096    # b200sp_jacobi_large_max_block()
+LARGE_SCRATCH_BYTES = 1 << 30  # Gauss-Jordan [B | I] scratch of the large-block path
 
 
 def gauss_jordan_inverse(block, exc=None):
     """Explicit inverse of a dense block by Gauss-Jordan elimination with
     partial pivoting (src/precond.py:28-46), computed by the device
     generation kernel -- bit-identical to the reference -- or None when a
-    pivot vanishes. Blocks are limited to 32 rows on this backend."""
+    pivot vanishes. Blocks are limited to 4096 rows on this backend."""
     from .executor import CudaExecutor
     from .formats import MatrixData
 
@@ -65,10 +70,20 @@ def _scan64(exc, counts):
 class JacobiOperator(LinOp):
     """Block-diagonal preconditioner holding the inverted diagonal blocks."""
 
-    def __init__(self, exc, size, starts, offs, prec, storage, cond):
+    def __init__(self, exc, size, starts, offs, prec, storage, cond, max_block=None):
         super().__init__(exc, size)
         self._starts, self._offs, self._prec = starts, offs, prec
         self._storage, self._cond = storage, cond
+        if max_block is None:
+            st = starts.cpu().numpy()
+            max_block = int(np.diff(st).max()) if st.size > 1 else 0
+        self.max_block = int(max_block)
+
+    @property
+    def fusable(self):
+        """True when the solvers can fuse the apply into their step kernels
+        (warp-per-block: every block at most 32 rows)."""
+        return self.max_block <= WARP_BLOCK
 
     @property
     def num_blocks(self):
@@ -100,7 +115,8 @@ class JacobiOperator(LinOp):
     def _apply_impl(self, b, x):
         bt, xt = b.values, x.values
         suf = _lib.suffix(xt.dtype)
-        _lib.call("jacobi_apply_" + suf, *self.jac_args(), xt.shape[1], ptr(bt), bt.stride(0), ptr(xt),
+        kern = "jacobi_apply_" if self.fusable else "jacobi_apply_large_"
+        _lib.call(kern + suf, *self.jac_args(), xt.shape[1], ptr(bt), bt.stride(0), ptr(xt),
                   xt.stride(0), self.exec.stream)
 
     def clone_to(self, target):
@@ -108,7 +124,7 @@ class JacobiOperator(LinOp):
         dev = target.device
         return JacobiOperator(target, self.size, self._starts.clone().to(dev), self._offs.clone().to(dev),
                               self._prec.clone().to(dev), self._storage.clone().to(dev),
-                              self._cond.clone().to(dev))
+                              self._cond.clone().to(dev), self.max_block)
 
 
 class Jacobi(LinOpFactory):
@@ -160,9 +176,17 @@ class Jacobi(LinOpFactory):
         nbytes = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
         singular = torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device=dev)
         suf = _lib.suffix(csr._v.dtype)
-        _lib.call("jacobi_invert_" + suf, nb, ptr(starts), ptr(csr._rp), ptr(csr._ci), ptr(csr._v), ptr(off64),
-                  ptr(inv64), ptr(cond), ptr(prec), ptr(nbytes), int(bool(self.adaptive_precision)),
-                  float(self.condition_threshold), ptr(singular), exc.stream)
+        max_bs = int(np.diff(host_starts).max()) if nb else 0
+        args = (nb, ptr(starts), ptr(csr._rp), ptr(csr._ci), ptr(csr._v), ptr(off64), ptr(inv64), ptr(cond),
+                ptr(prec), ptr(nbytes), int(bool(self.adaptive_precision)), float(self.condition_threshold),
+                ptr(singular))
+        if max_bs <= WARP_BLOCK:
+            _lib.call("jacobi_invert_" + suf, *args, exc.stream)
+        else:
+            slot = 2 * max_bs * max_bs
+            slots = max(1, min(nb, 2 * 148, LARGE_SCRATCH_BYTES // (8 * slot)))
+            scratch = torch.empty(slots * slot, dtype=torch.float64, device=dev)
+            _lib.call("jacobi_invert_large_" + suf, *args, max_bs, ptr(scratch), slots, exc.stream)
         bad = int(singular.item())
         if bad != np.iinfo(np.int64).max:
             raise Singular(f"diagonal block {bad} is singular")
@@ -175,7 +199,7 @@ class Jacobi(LinOpFactory):
         else:
             offs = (off64[:nb] * 8).contiguous()
             storage = inv64.view(torch.uint8)
-        return JacobiOperator(exc, a.size, starts, offs, prec[:nb], storage, cond[:nb])
+        return JacobiOperator(exc, a.size, starts, offs, prec[:nb], storage, cond[:nb], max_bs)
 
 
 # ---------------------------------------------------------------------------

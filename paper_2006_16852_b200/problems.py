@@ -89,6 +89,20 @@ def random_sparse(n, density=0.1, seed=0, diag_dominant=True):
     return MatrixData.from_dense_array(dense)
 
 
+def random_spd(n, density=0.2, seed=0):
+    """Seeded random sparse SPD matrix: symmetric pattern, diagonal made
+    strictly dominant (src/problems.py:61-69)."""
+    from .formats import MatrixData
+
+    rng = np.random.default_rng(seed)
+    mask = np.triu(rng.random((n, n)) < density / 2)
+    dense = np.where(mask, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+    dense = dense + dense.T
+    off = np.abs(dense).sum(axis=1) - np.abs(np.diag(dense))
+    np.fill_diagonal(dense, off + 1.0)
+    return MatrixData.from_dense_array(dense)
+
+
 def power_law(exc, n, seed=0, max_len=50000, c=5.5154, value_dtype="float64", strategy="automatic"):
     """Synthetic power-law matrix (mean row length ~16 for c=5.5154, longest
     rows capped at max_len), generated on the device."""

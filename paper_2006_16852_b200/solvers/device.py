@@ -23,7 +23,7 @@ from .. import _lib, config
 from ..executor import ptr
 from ..formats import Dense
 from ..loggers import EventKind
-from ..stop import CRIT_ITERATION, CRIT_RNR, CriterionArgs, ResidualNormReduction
+from ..stop import CRIT_ITERATION, CRIT_RNR, ResidualNormReduction
 
 HIST_CAP = 1 << 16
 
@@ -76,7 +76,7 @@ class DeviceSolve:
     def begin(self, b, x):
         solver = self.solver
         fac = solver.criterion_factory
-        self.spec, self.time_child = fac.device_spec()
+        self.spec, self.timed = fac.device_spec()
         self.logging = bool(solver._log_channels)
         iters = [int(p) for t, p in self.spec if t == CRIT_ITERATION]
         cap = (min(min(iters) + 2, HIST_CAP) if iters else HIST_CAP) if self.logging else 0
@@ -85,9 +85,6 @@ class DeviceSolve:
         needs_res = int(any(isinstance(f, ResidualNormReduction) for f in fac.factories))
         _lib.call("krylov_ctl_init", self.c, len(self.spec), ctypes.addressof(types),
                   ctypes.addressof(params), needs_res, cap, int(self.kdim), self.exc.stream)
-        self.time_crit = None
-        if self.time_child is not None:
-            self.time_crit = fac.factories[self.time_child].generate(CriterionArgs(solver.a, b, x))
         self.xd.copy_from(x)
         self.bd.copy_from(b)
 
@@ -106,7 +103,7 @@ class DeviceSolve:
         return out
 
     # -- batches -----------------------------------------------------------------------
-    def run(self, body, iters, guard_which=0, gmres=False):
+    def run(self, body, iters, guard_which=0):
         """Replay the captured ``iters`` x ``body`` graph until done."""
         st = self.status()
         if st["done"]:
@@ -139,15 +136,6 @@ class DeviceSolve:
             st = self.status()
             if st["done"]:
                 return st
-            if self._time_expired(gmres):
-                self.graph.replay()  # GMRES commits its partial segment
-                return self.status()
-
-    def _time_expired(self, gmres):
-        if self.time_crit is None or not self.time_crit.expired():
-            return False
-        _lib.call("krylov_force_stop", self.c, self.time_child + 1, int(gmres), self.exc.stream)
-        return True
 
     # -- logger replay --------------------------------------------------------------------
     def replay_events(self, st):

@@ -93,7 +93,7 @@ class GmresSolver(IterativeSolver):
             _lib.call("gmres_reset_" + suf, n, ptr(r), S.c, S.p, ptr(gm), S.h, 0, exc.stream)
             _lib.call("gmres_scale_v0_" + suf, n, ptr(r), ptr(V), S.c, exc.stream)
 
-        st = S.run(cycle, 1, guard_which=1, gmres=True)
+        st = S.run(cycle, 1, guard_which=1)
         finish_from_device(self, S, st, x)
 
 

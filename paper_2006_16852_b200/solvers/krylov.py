@@ -30,6 +30,8 @@ def device_path_ok(solver, b):
         return False
     if not isinstance(solver.precond, (Identity, JacobiOperator)):
         return False
+    if isinstance(solver.precond, JacobiOperator) and not solver.precond.fusable:
+        return False  # blocks over 32 rows: host-sequenced loop, apply as its own launch
     return str(b.values.dtype) in ("torch.float64", "torch.float32")
 
 
@@ -79,7 +81,7 @@ class CgSolver(IterativeSolver):
         from ..formats import _Sparse
 
         return (config.CG_COOP_MAX_ROWS > 0 and self.size.rows <= config.CG_COOP_MAX_ROWS and J[0] == 0
-                and isinstance(self.a, _Sparse) and S.time_child is None)
+                and isinstance(self.a, _Sparse) and not S.timed)
 
     def _coop_csr(self):
         """The system as Csr for the cooperative kernel (other sparse formats

@@ -333,6 +333,47 @@ def jacobi_cases():
     return out
 
 
+def jacobi_large_cases():
+    """Blocks of more than 32 rows (uniform block_size and explicit
+    boundaries, incl. a block over 128 rows for NumPy's recursive pairwise
+    row sums), adaptive precision, the apply, and a preconditioned solve."""
+    out = {}
+    n, r, c, v = P.stencil3d(8, "convdiff")
+    data = md(n, r, c, v)
+    a = Csr.from_data(REF, data)
+    d = data.canonicalize()
+    rr = np.random.default_rng(8).standard_normal((n, 2))
+    for name, kw in (("bs64", {"block_size": 64}), ("bs100", {"block_size": 100}),
+                     ("bounds", {"block_boundaries": [0, 5, 37, 40, 240, 300, 301, 420]}),
+                     ("bs64_adapt", {"block_size": 64, "adaptive_precision": True, "condition_threshold": 1e2})):
+        jac = Jacobi(REF, **kw).generate(a)
+        z = Dense.zeros(REF, n, 2)
+        jac.apply(Dense(REF, rr), z)
+        out[f"convdiff_g8_{name}"] = {
+            "rows": d.rows, "cols": d.cols, "vals": d.vals, "n": n,
+            "starts": np.array([b.start for b in jac.blocks]),
+            "inv_flat": np.concatenate([b.inv.astype(np.float64).reshape(-1) for b in jac.blocks]),
+            "reduced": np.array([b.inv.dtype == np.float32 for b in jac.blocks]),
+            "cond": np.array(jac.block_conditions), "r": rr, "z": z.data.copy(),
+        }
+    # pivoting-heavy dense-ish random matrix, one 150-row block + a 50-row block
+    dr = random_sparse(200, density=0.3, seed=23, diag_dominant=False).canonicalize()
+    jac = Jacobi(REF, block_boundaries=[0, 150]).generate(Csr.from_data(REF, dr))
+    out["rand200_b150"] = {
+        "rows": dr.rows, "cols": dr.cols, "vals": dr.vals, "n": 200,
+        "inv_flat": np.concatenate([b.inv.reshape(-1) for b in jac.blocks]),
+        "cond": np.array(jac.block_conditions),
+    }
+    n, r, c, v = P.stencil3d(12, "convdiff")
+    dd = md(n, r, c, v)
+    out["bicgstab_bj64_cd_g12"] = solve_case("bicgstab_bj64_cd_g12", dd, "bicgstab", 64, np.ones(n), 10000, 1e-8)
+    out["gmres30_bj144_cd_g12"] = solve_case("gmres30_bj144_cd_g12", dd, "gmres", 144, np.ones(n), 10000, 1e-8,
+                                             krylov_dim=30)
+    out["cg_bj64_7pt_g12"] = solve_case("cg_bj64_7pt_g12", md(*P.stencil3d(12, "7pt")), "cg", 64, np.ones(1728),
+                                        10000, 1e-8)
+    return out
+
+
 def misc_cases():
     out = {}
     n, r, c, v = triples(convection_diffusion(20))
@@ -362,6 +403,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["ilu"]:
         save("ilu.npz", ilu_cases())
+        sys.exit(0)
+    if sys.argv[1:] == ["jacobi_large"]:
+        save("jacobi_large.npz", jacobi_large_cases())
         sys.exit(0)
     if sys.argv[1:] == ["assemble"]:
         save("assemble.npz", assemble_cases())
