@@ -58,7 +58,7 @@ _TYPED = {
     # block-Jacobi
     "jacobi_invert": "lpppppppppidpp",
     "jacobi_apply": "lppppiplplp",
-    "jacobi_invert_large": "lpppppppppidppipip",
+    "jacobi_invert_large": "lpppppppppidpipip",
     "jacobi_apply_large": "lppppiplplp",
     # Krylov (JAC = l p p p p)
     "cg_init": "lppp" + "lpppp" + "pppp",
@@ -92,7 +92,7 @@ _TYPED = {
     "gmres_combine": "lppl" + "lpppp" + "ppp",
     # distributed
     "split_fill": "lpppippppppp",
-    "assemble_coo": "lpppllppppp",
+    "assemble_coo": "lpppllpppppp",
     "diag": "lpppppp",
     "ilu_fill": "lppppppppppppp",
     "parilu_sweep": "lllppppppppppppp",

@@ -58,3 +58,39 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(KernelNotImplemented):
         _lib._load()
+
+
+def _prototype_arg_counts():
+    """{symbol: number of parameters} for every prototype spelled out in the
+    header (macro-generated ones are expanded for f64 / f32)."""
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    text = re.sub(r"//[^\n]*", "", text)
+    text = text.replace("B200SP_JAC_DECL", "a, b, c, d, e")  # the 5 block-Jacobi parameters
+    out = {}
+    for m in re.finditer(r"\b(b200sp_[a-z0-9_#A-Z]+)\s*\(([^)]*)\)\s*;", text):
+        name, params = m.group(1), m.group(2).strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        if "##SUF" in name:
+            for suf in ("f64", "f32"):
+                out[name.replace("##SUF", suf)] = n
+        else:
+            out[name] = n
+    return out
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libb200sp.so not built")
+def test_binding_signatures_match_header_arity():
+    """Every ctypes signature in _lib has as many parameters as the header's
+    prototype (a mismatch would only surface as a TypeError on the GPU)."""
+    from paper_2006_16852_b200 import _lib
+
+    _lib._load()
+    protos = _prototype_arg_counts()
+    bad = []
+    for key, fn in _lib._funcs.items():
+        sym = "b200sp_" + key
+        if sym in protos and len(fn.argtypes) != protos[sym]:
+            bad.append((sym, len(fn.argtypes), protos[sym]))
+    assert not bad, bad
+    assert len([k for k in _lib._funcs if "b200sp_" + k in protos]) > 50
