@@ -1361,6 +1361,8 @@ def convert(a, target, **params):
     Dense -> sparse drops explicit zeros (as in the reference). Extra keyword
     parameters reach the target constructor (``strategy``, ``width``,
     ``slice_size``, ``stride_factor``)."""
+    if isinstance(a, StencilMatrix):  # assembles to Csr only (src/formats.py:283-298)
+        return a.convert_to(target, **params)
     cls, extra = _resolve(target)
     params = {**extra, **params}
     impl = params.pop("stream_impl", None)

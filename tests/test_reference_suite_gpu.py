@@ -475,7 +475,10 @@ def test_two_rhs_column_convergence_order(ref):
 def test_time_limit_stops_device_solve_per_iteration(ref, name):
     from paper_2006_16852_b200 import problems
 
-    a = problems.stencil(ref, "7pt" if name in ("cg", "fcg") else "convdiff", 48)
+    # 128^3: ~0.1 ms per iteration, so the limit lands after a few hundred
+    # iterations -- long before the recurrence residual underflows toward the
+    # 1e-300 reduction (it keeps shrinking past machine precision)
+    a = problems.stencil(ref, "7pt" if name in ("cg", "fcg") else "convdiff", 128)
     n = a.size.rows
     limit = 0.05
     crit = [Iteration(1_000_000), ResidualNormReduction(1e-300), TimeLimit(limit)]
@@ -882,7 +885,9 @@ def test_gmres_rotation_residual_matches_true_residual(ref):
         _factory("gmres", ref, [Iteration(j), ProbeFactory()], krylov_dim=50).generate(a).apply(b, x)
         true_r = np.linalg.norm(b.data[:, 0] - dense @ x.data[:, 0])
         if true_r > 1e-10 * np.linalg.norm(b.data):
-            assert abs(estimates[j] - true_r) <= 1e-8 * true_r
+            # + 1e-14 ||b||: near 1e-8 ||b|| the test's own evaluation of b - A x
+            # carries ~eps ||A|| ||x|| of rounding (j = 20 differs by 4.6e-16)
+            assert abs(estimates[j] - true_r) <= 1e-8 * true_r + 1e-14 * np.linalg.norm(b.data)
 
 
 def test_lower_trs_hand_example(ref):
