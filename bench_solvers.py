@@ -169,7 +169,7 @@ def bench_c3(args, world, rank, local):
 
     exc = b2.CudaExecutor(local)
     peak, peak_src = peaks()
-    a = problems.power_law(exc, 4194304, seed=0)
+    a = problems.power_law(exc, 4194304, seed=0, lengths="rng")  # SURVEY 8(d) row lengths
     n, nnz = a.size.rows, a.nnz
     b = b2.Dense(exc, np.random.default_rng(0).standard_normal((n, 1)))
     x = b2.Dense.zeros(exc, n, 1)
@@ -186,7 +186,7 @@ def bench_c3(args, world, rank, local):
     head = res["csr_lb"]
     return {"metric": METRIC, "value": head["gbs"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": head["us"] / 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic power law (device hash generator)",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic power law: SURVEY 8(d) row lengths (default_rng(0)), stratified distinct columns and U(-1,1) values from the device hash generator",
             "config": {"workload": "C3: Csr load-balanced SpMV, power law 4,194,304 rows, mean 16, max 50k",
                        "rows": n, "nnz": nnz},
             "roofline": {"bound": "hbm", "achieved": head["gbs"], "peak": peak, "unit": "GB/s",

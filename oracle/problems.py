@@ -98,8 +98,20 @@ def power_law_lengths(n, seed=0, max_len=50000, c=5.5154):
     return np.clip(lens, 1, n).astype(np.int64)
 
 
-def power_law(n, seed=0, max_len=50000, c=5.5154):
-    lens = power_law_lengths(n, seed, max_len, c)
+def power_law_lengths_rng(n, seed=0, max_len=50000, c=5.5154):
+    """SURVEY.md 8(d) C3 row lengths verbatim: u = 1 - default_rng(seed).random(n),
+    L = max(1, min(max_len, floor(c * u^(-1/1.5)))). At n = 4,194,304, seed 0:
+    nnz 67,109,323, mean 16.0001, median 8, max 50,000 (6 rows at the cap)."""
+    u = 1.0 - np.random.default_rng(seed).random(n)
+    return np.maximum(1, np.minimum(min(max_len, n), np.floor(c * u ** (-1.0 / 1.5)))).astype(np.int64)
+
+
+def power_law(n, seed=0, max_len=50000, c=5.5154, lengths="hash"):
+    """lengths: 'hash' (counter-hash u, this repo's original generator) or
+    'rng' (numpy default_rng(seed)). Columns: row i's L entries
+    are distinct and sorted, entry k uniform in its own stratum
+    [k n / L, (k+1) n / L); values U(-1, 1) from the same counter hash."""
+    lens = (power_law_lengths_rng if lengths == "rng" else power_law_lengths)(n, seed, max_len, c)
     rp = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(lens, out=rp[1:])
     rows = np.repeat(np.arange(n, dtype=np.int64), lens)

@@ -103,12 +103,23 @@ def random_spd(n, density=0.2, seed=0):
     return MatrixData.from_dense_array(dense)
 
 
-def power_law(exc, n, seed=0, max_len=50000, c=5.5154, value_dtype="float64", strategy="automatic"):
+def power_law(exc, n, seed=0, max_len=50000, c=5.5154, value_dtype="float64", strategy="automatic",
+              lengths="hash"):
     """Synthetic power-law matrix (mean row length ~16 for c=5.5154, longest
-    rows capped at max_len), generated on the device."""
-    thresholds = torch.from_numpy((c / np.arange(1, max_len + 1, dtype=np.float64)) ** 1.5).to(exc.device)
-    lens = torch.empty(max(n, 1), dtype=torch.int32, device=exc.device)
-    _lib.call("powerlaw_lengths", n, seed, ptr(thresholds), max_len, ptr(lens), exc.stream)
+    rows capped at max_len), columns and values generated on the device.
+
+    Row lengths L = floor(c u^(-1/1.5)) clipped to [1, max_len]; ``lengths``
+    picks u: "hash" (a counter hash, computed on the device) or "rng"
+    (SURVEY.md 8(d)'s C3 recipe: u = 1 - numpy default_rng(seed).random(n),
+    drawn on the host and uploaded, 4 bytes per row)."""
+    if lengths == "rng":
+        u = 1.0 - np.random.default_rng(seed).random(n)
+        host = np.maximum(1, np.minimum(min(max_len, n), np.floor(c * u ** (-1.0 / 1.5)))).astype(np.int32)
+        lens = torch.from_numpy(host).to(exc.device) if n else torch.empty(1, dtype=torch.int32, device=exc.device)
+    else:
+        thresholds = torch.from_numpy((c / np.arange(1, max_len + 1, dtype=np.float64)) ** 1.5).to(exc.device)
+        lens = torch.empty(max(n, 1), dtype=torch.int32, device=exc.device)
+        _lib.call("powerlaw_lengths", n, seed, ptr(thresholds), max_len, ptr(lens), exc.stream)
     rp = _scan(exc, lens[:n])
     nnz = int(rp[-1].item())
     vt = torch.float64 if np.dtype(value_dtype) == np.float64 else torch.float32
