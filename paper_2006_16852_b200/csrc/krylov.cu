@@ -88,8 +88,7 @@ cg_init_kernel(RowBlocks rb, const T* __restrict__ r, T* __restrict__ z, T* __re
     double v[2] = {rz, rr}, tot[2];
     if (!grid_reduce<2>(v, part, &c->ticket[0], tot)) return;
     if (c->dist) {
-        c->red[0] = tot[0];
-        c->red[1] = tot[1];
+        park_check(c, tot[0], tot[1]);
         return;
     }
     cg_init_ctl(c, tot, hist);
@@ -185,8 +184,7 @@ cg_step2_kernel(RowBlocks rb, T* __restrict__ x, int64_t xs, T* __restrict__ r, 
     double v[2] = {rz, rr}, tot[2];
     if (!grid_reduce<2>(v, part, &c->ticket[2], tot)) return;
     if (c->dist) {
-        c->red[0] = tot[0];
-        c->red[1] = tot[1];
+        park_check(c, tot[0], tot[1]);
         return;
     }
     cg_step2_ctl(c, tot, hist);

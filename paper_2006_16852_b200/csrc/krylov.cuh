@@ -63,12 +63,29 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // `||r|| <= factor ||r0||` (src/stop.py:187-196), TimeLimit `elapsed >= limit`
 // (src/stop.py:134-147) -- all evaluated at EVERY check, on the device: the
 // wall clock is the GPU's global nanosecond timer, started by ctl_init.
+// A distributed solve needs every rank to take the same decision: each rank
+// parks its local "limit reached" flag in red[3] next to its partial sums,
+// the all-reduce adds them, and the time child fires on every rank once any
+// rank's clock has passed the limit.
+__device__ __forceinline__ bool time_expired_local(const KrylovCtl* c, int i) {
+    return (double)(global_ns() - c->t_start) >= c->crit_param[i] * 1e9;
+}
 __device__ __forceinline__ bool crit_fires(const KrylovCtl* c, int i, int it, double nrm) {
     const int t = c->crit_type[i];
     if (t == CRIT_ITERATION) return it >= (int)c->crit_param[i];
     if (t == CRIT_RNR) return nrm <= c->crit_param[i] * c->baseline;
-    if (t == CRIT_TIME) return (double)(global_ns() - c->t_start) >= c->crit_param[i] * 1e9;
+    if (t == CRIT_TIME) return c->dist ? c->red[3] > 0.0 : time_expired_local(c, i);
     return false;
+}
+// local partial sums of a check phase, parked for the cross-rank all-reduce
+__device__ __forceinline__ void park_check(KrylovCtl* c, double s0, double s1) {
+    double flag = 0.0;
+    for (int i = 0; i < c->n_crit; ++i)
+        if (c->crit_type[i] == CRIT_TIME && time_expired_local(c, i)) flag = 1.0;
+    c->red[0] = s0;
+    c->red[1] = s1;
+    c->red[2] = 0.0;
+    c->red[3] = flag;
 }
 
 // ---------------------------------------------------------------------------

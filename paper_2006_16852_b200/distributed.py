@@ -36,7 +36,7 @@ from .executor import ptr
 from .formats import Csr, Dense, _scan
 from .problems import STENCILS
 from .solvers.common import BreakdownInfo, SolveStatus
-from .stop import CRIT_ITERATION, Combined
+from .stop import Combined
 
 
 # ---------------------------------------------------------------------------
@@ -171,6 +171,10 @@ class DistCsr(LinOp):
     @property
     def n_local(self):
         return self.plan.n_local
+
+    def _operand_rows(self):
+        """apply(b, x) takes this rank's rows: (n_local, m) slices."""
+        return self.n_local, self.n_local
 
     @property
     def n_ext(self):
@@ -400,26 +404,50 @@ class PeerReduce:
 # ---------------------------------------------------------------------------
 # distributed CG
 # ---------------------------------------------------------------------------
-class DistCg:
-    """Row-partitioned CG on DistCsr (unpreconditioned), criteria
-    Iteration / ResidualNormReduction evaluated on the device from
-    all-reduced norms. ``solve`` takes this rank's slices of b and x."""
+def is_distributed(a):
+    return isinstance(a, DistCsr)
 
-    def __init__(self, a, criteria, batch=None):
+
+class DistCg:
+    """Row-partitioned CG engine on DistCsr: the device-resident CG kernels
+    with every reduction split as local sum -> all-reduce (NCCL, or peer
+    memory) -> control step (b200sp_cg_finish), two all-reduces per
+    iteration. Criteria: every device-evaluable child of Combined --
+    Iteration and ResidualNormReduction from the all-reduced norms, and
+    TimeLimit through a per-rank "limit reached" flag summed by the same
+    all-reduce, so every rank stops at the same iteration. Preconditioner:
+    none or block-Jacobi on this rank's rows (blocks fused into the steps).
+
+    Reached through the reference API -- ``Cg(exc, criteria,
+    preconditioner=Jacobi(...)).generate(dist_csr).apply(b_local, x_local)``
+    (solvers/krylov.py routes a DistCsr system here) -- or standalone via
+    ``solve(b, x)`` on this rank's (n_local,) tensors."""
+
+    def __init__(self, a, criteria, batch=None, precond=None):
+        from .errors import Unsupported
+
         self.a = a
         self.exec = a.exec
-        self.factory = Combined(criteria if isinstance(criteria, (list, tuple)) else [criteria])
+        if isinstance(criteria, Combined):
+            self.factory = criteria
+        else:
+            self.factory = Combined(criteria if isinstance(criteria, (list, tuple)) else [criteria])
         spec = self.factory.device_spec()
-        if spec is None or spec[1]:
-            raise NotImplementedError("DistCg supports Iteration / ResidualNormReduction criteria")
-        self.spec = spec[0]
+        if spec is None:
+            raise Unsupported("the distributed CG evaluates its criteria on the device: use Iteration, "
+                              "ResidualNormReduction and TimeLimit")
+        self.spec, self.timed = spec
+        self.precond = precond
         self.batch = int(batch or config.SOLVER_BATCH)
         self.last_status = None
         dev = self.exec.device
         self.ctl = torch.zeros(int(_lib.query("krylov_ctl_bytes")), dtype=torch.uint8, device=dev)
         self.part = torch.zeros(int(_lib.query("krylov_part_elems")), dtype=torch.float64, device=dev)
-        off = int(_lib.query("krylov_red_offset"))
-        self.red = self.ctl[off:off + 32].view(torch.float64)
+        self._red_off = int(_lib.query("krylov_red_offset"))
+        self.halo = self.reduce = None
+
+    def _jac(self):
+        return self.precond.jac_args() if self.precond is not None else (0, 0, 0, 0, 0)
 
     def _spmv_sigma_peer(self, peer, pext, p, q, c, pp, suf):
         """q = A p, sigma parked; the ghosts arrive by peer stores from the
@@ -465,25 +493,15 @@ class DistCg:
         _lib.call("csr_spmv_dot_" + suf, nl, ptr(gh._rp), ptr(gh._ci), ptr(gh._v), ptr(pext[nl:]), ptr(q), ptr(p),
                   4, gh.subwarp(), c, ptr(pp), exc.stream)
 
-    def _status(self):
+    @staticmethod
+    def _status(c, stream):
         iv, dv = (ctypes.c_int32 * 8)(), (ctypes.c_double * 8)()
-        _lib.call("krylov_status", ptr(self.ctl), ctypes.addressof(iv), ctypes.addressof(dv), self.exec.stream)
+        _lib.call("krylov_status", c, ctypes.addressof(iv), ctypes.addressof(dv), stream)
         return list(iv), list(dv)
 
-    def solve(self, b, x):
-        """b, x: this rank's (n_local,) device tensors; x is the initial guess."""
-        exc, A = self.exec, self.a
-        nl, dt = A.n_local, x.dtype
-        suf = _lib.suffix(dt)
-        comm = A.comm
-        types = (ctypes.c_int32 * len(self.spec))(*[t for t, _ in self.spec])
-        params = (ctypes.c_double * len(self.spec))(*[p for _, p in self.spec])
-        c = ptr(self.ctl)
-        _lib.call("krylov_ctl_init", c, len(self.spec), ctypes.addressof(types), ctypes.addressof(params), 1, 0, 0,
-                  exc.stream)
-        _lib.call("krylov_set_dist", c, 1, exc.stream)
-        r = torch.empty(nl, dtype=dt, device=exc.device)
-        q = torch.empty(nl, dtype=dt, device=exc.device)
+    def _comm_paths(self, dt):
+        """(peer halo or None, extended p vector, peer all-reduce or None)."""
+        A, exc, comm = self.a, self.exec, self.a.comm
         peer = None
         if PeerHalo.usable(A):
             peer = getattr(A, "_peer_halo", {}).get(dt)
@@ -493,52 +511,78 @@ class DistCg:
             pext = peer.pext
         else:
             pext = torch.empty(A.n_ext, dtype=dt, device=exc.device)
-        self.halo = "peer" if peer is not None else "nccl"
         red = None  # the all-reduces ride on peer memory too when the halo does
         if peer is not None and comm.size <= 8:
             red = getattr(A, "_peer_reduce", None)
             if red is None:
                 red = PeerReduce(comm, exc.device)
                 A.__dict__["_peer_reduce"] = red
+        self.halo = "peer" if peer is not None else "nccl"
         self.reduce = "peer" if red is not None else "nccl"
+        return peer, pext, red
+
+    def run(self, ctl, c, pp, hist, b, x):
+        """The iteration loop on an initialised control block ``ctl`` (uint8
+        device tensor, pointer ``c``): b, x are this rank's (n_local,) slices
+        (x = initial guess, overwritten). Returns when the device reports done."""
+        exc, A = self.exec, self.a
+        nl, dt = A.n_local, x.dtype
+        suf = _lib.suffix(dt)
+        comm = A.comm
+        _lib.call("krylov_set_dist", c, 1, exc.stream)
+        red_t = ctl[self._red_off:self._red_off + 32].view(torch.float64)
+        J = self._jac()
+        r = torch.empty(nl, dtype=dt, device=exc.device)
+        q = torch.empty(nl, dtype=dt, device=exc.device)
+        z = r if J[0] == 0 else torch.empty(nl, dtype=dt, device=exc.device)
+        peer, pext, red = self._comm_paths(dt)
+        k_check = 4 if self.timed else 2  # + the summed "time limit reached" flags
 
         def allreduce(k):
             if red is not None:
-                red.allreduce_(self.red[:k], exc.stream)
+                red.allreduce_(red_t[:k], exc.stream)
             else:
-                comm.allreduce_(self.red[:k])
+                comm.allreduce_(red_t[:k])
         p = pext[:nl]
         # r = b - A x  (x staged in the extended vector for its halo)
         pext[:nl].copy_(x)
         A.apply_ext(pext, r, alpha=-1.0, beta=1.0, y_in=b)
-        J = (0, 0, 0, 0, 0)
-        pp = self.part
-        _lib.call("cg_init_" + suf, nl, ptr(r), ptr(r), ptr(p), *J, c, ptr(pp), 0, exc.stream)
-        allreduce(2)
-        _lib.call("cg_finish", c, 0, 0, exc.stream)
+        _lib.call("cg_init_" + suf, nl, ptr(r), ptr(z), ptr(p), *J, c, ptr(pp), hist, exc.stream)
+        allreduce(k_check)
+        _lib.call("cg_finish", c, hist, 0, exc.stream)
         guard = int(_lib.query("krylov_guard", c, 0))
         _lib.query("set_guard", guard)
         try:
             while True:
-                iv, _ = self._status()
+                iv, _ = self._status(c, exc.stream)
                 if iv[4]:
                     break
                 for _ in range(self.batch):
                     if peer is not None:
-                        peer.step1(nl, p, r, c, suf, exc.stream)
+                        peer.step1(nl, p, z, c, suf, exc.stream)
                         self._spmv_sigma_peer(peer, pext, p, q, c, pp, suf)
                     else:
-                        _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(r), c, exc.stream)
+                        _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(z), c, exc.stream)
                         self._spmv_sigma(pext, p, q, c, pp, suf)
                     allreduce(1)
-                    _lib.call("cg_finish", c, 0, 1, exc.stream)
-                    _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(r), *J, c, ptr(pp), 0,
-                              exc.stream)
-                    allreduce(2)
-                    _lib.call("cg_finish", c, 0, 2, exc.stream)
+                    _lib.call("cg_finish", c, hist, 1, exc.stream)
+                    _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(z), *J, c, ptr(pp),
+                              hist, exc.stream)
+                    allreduce(k_check)
+                    _lib.call("cg_finish", c, hist, 2, exc.stream)
         finally:
             _lib.query("set_guard", 0)
-        iv, dv = self._status()
+
+    def solve(self, b, x):
+        """b, x: this rank's (n_local,) device tensors; x is the initial guess."""
+        exc = self.exec
+        types = (ctypes.c_int32 * max(len(self.spec), 1))(*[t for t, _ in self.spec])
+        params = (ctypes.c_double * max(len(self.spec), 1))(*[p for _, p in self.spec])
+        c = ptr(self.ctl)
+        _lib.call("krylov_ctl_init", c, len(self.spec), ctypes.addressof(types), ctypes.addressof(params), 1, 0, 0,
+                  exc.stream)
+        self.run(self.ctl, c, self.part, 0, b, x)
+        iv, dv = self._status(c, exc.stream)
         status = np.zeros(1, dtype=[("stopped", "?"), ("stopping_id", "u1"), ("finalized", "?")])
         status["stopped"][0], status["stopping_id"][0], status["finalized"][0] = bool(iv[1]), iv[2], bool(iv[3])
         bd = BreakdownInfo(iv[6], "non-positive p^T A p") if iv[5] else None
@@ -546,10 +590,35 @@ class DistCg:
         return self.last_status
 
 
+def solve_cg(solver, b, x):
+    """CgSolver._apply_impl for a DistCsr system (the reference factory path,
+    src/solvers/krylov.py:36-77): b and x are this rank's (n_local, 1) slices.
+    Same observable contract as the single-GPU device path: last_status,
+    breakdown as status, logger events replayed from the device history."""
+    from .errors import Unsupported
+    from .precond import JacobiOperator
+    from .solvers.device import get_state
+    from .solvers.krylov import finish_from_device
+
+    A = solver.a
+    if b.size.cols != 1:
+        raise Unsupported("the distributed CG solves one right-hand side at a time")
+    pre = solver.precond
+    if not (isinstance(pre, JacobiOperator) or type(pre).__name__ == "Identity"):
+        raise Unsupported("the distributed CG takes no preconditioner or block-Jacobi")
+    if isinstance(pre, JacobiOperator) and not pre.fusable:
+        raise Unsupported("the distributed CG fuses block-Jacobi blocks of at most 32 rows")
+    eng = solver.__dict__.get("_dist_engine")
+    if eng is None:
+        eng = solver.__dict__["_dist_engine"] = DistCg(
+            A, solver.criterion_factory, precond=pre if isinstance(pre, JacobiOperator) else None)
+    S = get_state(solver, A.n_local, x.values.dtype)
+    S.begin(b, x)
+    eng.run(S.ctl, S.c, S.part, S.h, S.b[:, 0], S.x[:, 0])
+    finish_from_device(solver, S, S.status(), x)
+
+
 def iteration_criteria(max_iters, factor):
     from .stop import Iteration, ResidualNormReduction
 
     return [Iteration(max_iters), ResidualNormReduction(factor)]
-
-
-_ = CRIT_ITERATION

@@ -79,6 +79,13 @@ class JacobiOperator(LinOp):
             max_block = int(np.diff(st).max()) if st.size > 1 else 0
         self.max_block = int(max_block)
 
+    _local_rows = None  # set for the blocks of one rank of a row-partitioned matrix
+
+    def _operand_rows(self):
+        if self._local_rows is not None:
+            return self._local_rows, self._local_rows
+        return super()._operand_rows()
+
     @property
     def fusable(self):
         """True when the solvers can fuse the apply into their step kernels
@@ -157,12 +164,28 @@ class Jacobi(LinOpFactory):
         if sizes.size and sizes.max() > MAX_BLOCK:
             raise Unsupported(f"block-Jacobi blocks are limited to {MAX_BLOCK} rows on this backend")
 
+    def _local_starts(self, a):
+        """Blocks of a row-partitioned matrix (distributed.DistCsr): the
+        global blocks that fall in this rank's rows, which must not straddle
+        a rank boundary; generated from the rank's owned diagonal block."""
+        lo, hi = a.lo, a.hi
+        st = [s for s in self._starts(a.size.rows) if lo <= s < hi]
+        if hi > lo and (not st or st[0] != lo):
+            raise Unsupported("a block-Jacobi block straddles a rank boundary of the row partition "
+                              "(align the partition to the block size)")
+        return [s - lo for s in st], a.a_own
+
     def _generate(self, a):
         exc = a.exec
         _require_cuda(exc)
-        csr = a if isinstance(a, Csr) else convert(a, "csr")
+        local = None
+        if getattr(a, "comm", None) is not None:  # row-partitioned (distributed.DistCsr)
+            starts_l, csr = self._local_starts(a)
+            local = csr.size.rows
+        else:
+            csr = a if isinstance(a, Csr) else convert(a, "csr")
         n = csr.size.rows
-        host_starts = np.asarray(self._starts(n) + [n], dtype=np.int32)
+        host_starts = np.asarray((starts_l if local is not None else self._starts(n)) + [n], dtype=np.int32)
         nb = host_starts.size - 1
         dev = exc.device
         starts = torch.from_numpy(host_starts).to(dev)
@@ -199,7 +222,9 @@ class Jacobi(LinOpFactory):
         else:
             offs = (off64[:nb] * 8).contiguous()
             storage = inv64.view(torch.uint8)
-        return JacobiOperator(exc, a.size, starts, offs, prec[:nb], storage, cond[:nb], max_bs)
+        op = JacobiOperator(exc, a.size, starts, offs, prec[:nb], storage, cond[:nb], max_bs)
+        op._local_rows = local
+        return op
 
 
 # ---------------------------------------------------------------------------

@@ -77,6 +77,8 @@ def finish_from_device(solver, state, st, x):
 class CgSolver(IterativeSolver):
     """Preconditioned conjugate gradients (SPD systems)."""
 
+    supports_distributed = True
+
     def _coop_ok(self, J, S):
         from ..formats import _Sparse
 
@@ -96,6 +98,10 @@ class CgSolver(IterativeSolver):
         return c
 
     def _apply_impl(self, b, x):
+        from .. import distributed
+
+        if distributed.is_distributed(self.a):  # row-partitioned system: one rank's slice
+            return distributed.solve_cg(self, b, x)
         if not device_path_ok(self, b):
             return generic.cg(self, b, x)
         n = self.size.rows

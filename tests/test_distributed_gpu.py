@@ -64,6 +64,34 @@ def _worker(rank, world, port, g, out_dir, halo="0"):
         same = bool(torch.equal(x, x2)) and st2.iterations == st.iterations
         with open(os.path.join(out_dir, f"st{rank}"), "w") as f:
             f.write(f"{lo} {hi} {st.iterations} {int(st.converged)} {err} {solver.halo}/{solver.reduce} {int(same)}")
+        # the reference factory path on the partitioned matrix (row N1):
+        # Cg(exc, criteria, preconditioner=Jacobi(32)).generate(DistCsr)
+        for tag, pre in (("none", None), ("bj32", b2.Jacobi(exc, block_size=32))):
+            crit = [b2.Iteration(1000), b2.ResidualNormReduction(1e-8), b2.TimeLimit(3600.0)]
+            fs = b2.Cg(exc, criteria=crit, preconditioner=pre).generate(A)
+            rec = b2.RecordLogger()
+            fs.attach(rec)
+            xf = b2.Dense.zeros(exc, A.n_local, 1)
+            fs.apply(b2.Dense.wrap(exc, b.view(-1, 1)), xf)
+            stf = fs.last_status
+            np.save(os.path.join(out_dir, f"xf_{tag}{rank}.npy"), np.asarray(xf.data)[:, 0])
+            n_it = len(rec.query(b2.EventKind.ITERATION_COMPLETE))
+            with open(os.path.join(out_dir, f"stf_{tag}{rank}"), "w") as f:
+                f.write(f"{stf.iterations} {int(stf.converged)} {stf.stopping_id} {n_it}")
+        # solvers without a partitioned variant refuse the DistCsr at generate time
+        try:
+            b2.Bicgstab(exc, criteria=[b2.Iteration(5)]).generate(A)
+            refused = 0
+        except b2.Unsupported:
+            refused = 1
+        assert refused == 1
+        # TimeLimit consensus: every rank stops at the same iteration, by the time child
+        ft = b2.Cg(exc, criteria=[b2.Iteration(10**6), b2.ResidualNormReduction(1e-300), b2.TimeLimit(0.005)])
+        ts = ft.generate(A)
+        xt = b2.Dense.zeros(exc, A.n_local, 1)
+        ts.apply(b2.Dense.wrap(exc, b.view(-1, 1)), xt)
+        with open(os.path.join(out_dir, f"stt{rank}"), "w") as f:
+            f.write(f"{ts.last_status.iterations} {ts.last_status.stopping_id}")
     finally:
         dist.destroy_process_group()
 
@@ -98,3 +126,22 @@ def test_multi_rank_cg_matches_single_gpu(tmp_path, cuda, world, halo):
     xd = np.concatenate(parts)
     x1 = np.asarray(x1.data)[:, 0]
     assert np.linalg.norm(xd - x1) <= 1e-7 * np.linalg.norm(x1)
+    # the factory path against the REFERENCE's own runs (tests/golden/solvers.npz:
+    # cg_7pt_g16 / cg_bj32_7pt_g16, made by tests/golden/make_golden.py)
+    from conftest import load_golden
+
+    gold = load_golden("solvers.npz")
+    for tag, key in (("none", "cg_7pt_g16"), ("bj32", "cg_bj32_7pt_g16")):
+        ref = gold[key]
+        stats = [(tmp_path / f"stf_{tag}{rank}").read_text().split() for rank in range(world)]
+        assert len({st_[0] for st_ in stats}) == 1
+        it, conv, sid, n_it = map(int, stats[0])
+        assert conv == 1 and sid == int(ref["stopping_id"]) == 2
+        assert abs(it - int(ref["iterations"])) <= 1, (tag, it, int(ref["iterations"]))
+        assert n_it == it  # ITERATION_COMPLETE events replayed from the device history
+        xf = np.concatenate([np.load(tmp_path / f"xf_{tag}{rank}.npy") for rank in range(world)])
+        xr = ref["x"][:, 0]
+        assert np.linalg.norm(xf - xr) <= 1e-7 * np.linalg.norm(xr), tag
+    stt = [(tmp_path / f"stt{rank}").read_text().split() for rank in range(world)]
+    assert len({st_[0] for st_ in stt}) == 1  # same stop iteration on every rank
+    assert all(int(st_[1]) == 3 for st_ in stt)  # stopped by the TimeLimit child
