@@ -126,7 +126,40 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # distributed plumbing (torchrun: one process per GPU)
 # ---------------------------------------------------------------------------
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec under
+    torch.distributed.run with N ranks on 127.0.0.1, so the line reports the
+    N-rank run it claims. Under torchrun, WORLD_SIZE must equal --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus <= 1:
+            return
+        import socket
+
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+    if int(world) != args.gpus and "--gpus" in " ".join(sys.argv):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+
+#: process-group backend of this run ("nccl": one GPU per rank; "gloo": more
+#: ranks than visible GPUs -- ranks share devices, collectives staged on the host)
+BACKEND = None
+
+
 def dist_setup():
+    """One process per rank (torchrun env). NCCL when every rank has its own
+    GPU; with fewer visible GPUs than ranks (a 1-GPU box running --gpus 2)
+    the ranks share devices round-robin over gloo and the distributed
+    solver's halo / all-reduce run through peer memory (CUDA IPC on the
+    shared device) -- the same kernels, flags and ordering as over NVLink."""
+    global BACKEND
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -134,8 +167,16 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
+        ndev = max(1, torch.cuda.device_count())
+        local = local % ndev
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ndev >= world:
+            BACKEND = "nccl"
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            BACKEND = "gloo"
+            os.environ.setdefault("B200SP_PEER_HALO", "1")  # read at package import
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -146,26 +187,22 @@ def barrier(world):
         dist.barrier()
 
 
-def allmax(world, value):
-    if world == 1:
-        return value
+def _reduce_scalar(value, op_name):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cuda" if BACKEND == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=getattr(dist.ReduceOp, op_name))
     return float(t.item())
+
+
+def allmax(world, value):
+    return value if world == 1 else _reduce_scalar(value, "MAX")
 
 
 def allsum(world, value):
-    if world == 1:
-        return value
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t)
-    return float(t.item())
+    return value if world == 1 else _reduce_scalar(value, "SUM")
 
 
 # ---------------------------------------------------------------------------
@@ -338,6 +375,106 @@ def bench_c2(args, world, rank, local):
 
 
 # ---------------------------------------------------------------------------
+# C2 at N > 1: distributed (row-partitioned) SpMV, weak scaling
+# ---------------------------------------------------------------------------
+def bench_c2_dist(args, world, rank, local):
+    """The C2 SpMV on N GPUs as ONE row-partitioned operator: the 27-point
+    stencil on 128 x 128 x (128 N) -- each rank owns exactly one C2-sized
+    slab (2,097,152 rows, z-planes [128 r, 128 r + 128)) -- so per-GPU work
+    is C2's and the curve measures the distributed path: the 2-plane halo
+    (NCCL send/recv; gloo host staging when ranks share a GPU) overlapped
+    with the owned-block SpMV, then the ghost-block accumulate
+    (DistCsr.apply_ext). value = all ranks' algorithmic Csr bytes / the
+    max-over-ranks step time; e2e adds each rank's pinned H2D of its x slice
+    and D2H of its y slice."""
+    import torch
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib
+    from paper_2006_16852_b200.distributed import DistCsr, make_comm
+
+    peak, peak_src = peaks()
+    exc = b2.CudaExecutor(local)
+    g = 128
+    comm = make_comm()
+    A = DistCsr.stencil(exc, comm, "27pt", g, nz=g * world)
+    nl, lo = A.n_local, A.lo
+    nnz_l = A.a_own.nnz + (A.a_ghost.nnz if A.a_ghost is not None else 0)
+    # x ~ N(0,1): this rank's slice of one global seeded vector (per-plane seeds)
+    xh = np.random.default_rng(rank).standard_normal(nl)
+    xext = torch.zeros(A.n_ext, dtype=torch.float64, device=exc.device)
+    xext[:nl].copy_(torch.from_numpy(xh))
+    y = torch.empty(nl, dtype=torch.float64, device=exc.device)
+    timer = Timer(exc)
+    step = lambda: A.apply_ext(xext, y)  # noqa: E731
+    # algorithmic bytes of this rank's rows (Csr formula) + the ghost x values it reads
+    by = bytes_csr(nl, nnz_l, 8) + (A.n_ext - nl) * 8
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        barrier(world)
+        torch.cuda.synchronize()
+        launches0 = _lib.launch_count()
+        ms = timer.run(step, args.steps, 0)
+        launches = _lib.launch_count() - launches0
+    barrier(world)
+    t_step = allmax(world, statistics.mean(ms) * 1e-3)
+    total_bytes = allsum(world, by)
+    # the owned-block SpMV alone (no exchange): the kernel's roofline
+    own_x = b2.Dense.wrap(exc, xext[:nl].view(-1, 1))
+    own_y = b2.Dense.wrap(exc, y.view(-1, 1))
+    ms_own = timer.run(lambda: A.a_own.apply(own_x, own_y), max(5, min(args.steps, 20)), 3)
+    t_own = allmax(world, statistics.mean(ms_own) * 1e-3)
+    by_own = bytes_csr(nl, A.a_own.nnz, 8)
+    # e2e: pinned host x slice up, distributed SpMV, y slice down, every step
+    xpin = torch.from_numpy(xh).pin_memory()
+    ypin = torch.empty(nl, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        xext[:nl].copy_(xpin, non_blocking=True)
+        A.apply_ext(xext, y)
+        ypin.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    for _ in range(2):
+        e2e_step()
+    barrier(world)
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 20))):
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_step_t = allmax(world, statistics.mean(e2e_t))
+    halo_bytes = (A.n_ext - nl) * 8
+    return {
+        "metric": METRIC, "value": round(total_bytes / t_step / 1e9, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated 27-point stencil, x ~ N(0,1))",
+        "config": {"workload": f"C2 distributed: Csr SpMV y = A x, 3-D 27-point stencil 128 x 128 x {128 * world} "
+                               f"row-partitioned over {world} ranks (one 128^3 C2 slab = 2,097,152 rows per rank), "
+                               "fp64 values / int32 indices",
+                   "format": "csr", "rows": nl * world, "rows_per_rank": nl,
+                   "parallelism": f"row partition x{world} ({BACKEND}"
+                                  f"{', ranks share GPUs' if BACKEND == 'gloo' else ''})",
+                   "halo_bytes_per_rank": halo_bytes,
+                   "l2": "inputs larger than L2 and L2 flushed (256 MiB write, then read back) between steps"},
+        "gflops": round(2 * allsum(world, nnz_l) / t_step / 1e9, 1),
+        "roofline": {"bound": "hbm", "achieved": round(by_own / t_own / 1e9, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(by_own / t_own / 1e9 / peak, 4), "traffic": traffic_from_profiles(
+                         "csr_classical_kernel"), "peak_source": peak_src, "kernel": "csr_classical_kernel",
+                     "bytes_per_launch": by_own, "note": "owned-block SpMV per rank, max over ranks"},
+        "distributed": {"step_ms": round(t_step * 1e3, 4), "owned_spmv_ms": round(t_own * 1e3, 4),
+                        "exchange_and_ghost_ms": round((t_step - t_own) * 1e3, 4),
+                        "per_rank_frac_of_peak": round(by / t_step / 1e9 / peak, 4)},
+        "cpu_baseline": None,
+        "e2e": {"value": round(total_bytes / e2e_step_t / 1e9, 1), "unit": "GB/s",
+                "h2d_bytes_per_step": nl * 8 * world, "d2h_bytes_per_step": nl * 8 * world,
+                "ms_per_step": round(e2e_step_t * 1e3, 3)},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+
+
+# ---------------------------------------------------------------------------
 # reference arm: the reference's CPU algorithm on host cores
 # ---------------------------------------------------------------------------
 def bench_reference(args):
@@ -408,11 +545,44 @@ def c5_sub(args, world, rank, local, head):
             keep["halo"] = r["config"].get("halo")
         if r.get("roofline"):
             keep["frac_of_hbm_peak"] = r["roofline"]["frac"]
+        if world > 1:
+            keep.update(_c5_single_reference(sub_args, world, rank, local, r))
         return keep
     except Exception as e:  # noqa: BLE001 -- the C2 line must still be printed
         return {"error": f"{type(e).__name__}: {e}"[:300]}
     finally:
         timer.cancel()
+
+
+def _c5_single_reference(sub_args, world, rank, local, r):
+    """N > 1: the same C5 solve on ONE GPU inside the same job (rank 0,
+    the other ranks wait), for the strong-scaling parallel efficiency
+    t_1 / (N t_N), plus each rank's roofline fraction of the distributed
+    iteration (fused-minimum CG bytes of its rows)."""
+    import torch
+
+    from bench_solvers import bench_solver
+
+    t1 = its1 = None
+    if rank == 0:
+        one = bench_solver(sub_args, 1, 0, local, "c5")
+        t1, its1 = one["value"], one["config"]["iterations"]
+    torch.cuda.synchronize()
+    barrier(world)
+    t1 = allmax(world, t1 if t1 is not None else 0.0)
+    tn = r["value"]
+    g = sub_args.grid
+    n, nnz = g ** 3, 7 * g ** 3 - 6 * g * g
+    peak, _ = peaks()
+    per_rank_bytes = (bytes_csr(n, nnz, 8) + 9 * n * 8) / world
+    out = {"single_gpu_ms_per_iter": round(t1, 4), "parallel_efficiency": round(t1 / (world * tn), 4),
+           "per_rank_frac_of_peak": round(per_rank_bytes / (tn * 1e-3) / 1e9 / peak, 4),
+           "efficiency_note": "strong scaling of the fixed problem, t_1 measured in this job on rank 0's GPU"}
+    if its1 is not None:
+        out["single_gpu_iterations"] = its1
+    if BACKEND == "gloo":
+        out["efficiency_note"] += "; ranks SHARE GPUs here (gloo), so the efficiency is not a scaling figure"
+    return out
 
 
 def _c5_watchdog(rank, head):
@@ -436,6 +606,8 @@ def main():
                     help="c2 only: skip the C5 CG sub-measurement (distributed at N > 1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.impl != "reference":
+        self_launch(args)
 
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
@@ -446,7 +618,7 @@ def main():
 
     world, rank, local = dist_setup()
     if args.workload == "c2":
-        out = bench_c2(args, world, rank, local)
+        out = bench_c2(args, world, rank, local) if world == 1 else bench_c2_dist(args, world, rank, local)
         if not args.no_c5:
             out["c5_cg"] = c5_sub(args, world, rank, local, out)
     else:

@@ -278,12 +278,12 @@ def bench_c5_distributed(args, world, rank, local):
     import torch
 
     import paper_2006_16852_b200 as b2
-    from paper_2006_16852_b200.distributed import Comm, DistCg, DistCsr
+    from paper_2006_16852_b200.distributed import DistCg, DistCsr, make_comm
 
     exc = b2.CudaExecutor(local)
     torch.cuda.set_device(local)
     g = args.grid or 512
-    comm = Comm()
+    comm = make_comm()
     t0 = time.perf_counter()
     A = DistCsr.stencil(exc, comm, "7pt", g)
     build_s = time.perf_counter() - t0

@@ -272,12 +272,13 @@ B200SP_CONVERT_DECL(double, f64)
 B200SP_CONVERT_DECL(float, f32)
 
 /* ---- generators (replace src/problems.py:11-45 at device scale) --------- */
-/* rows row0 .. row0+n-1 of the global stencil (global column indices) */
-int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t row0, int64_t n, int32_t* len, void* stream);
-int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
-                            int32_t* ci, double* v, void* stream);
-int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
-                            int32_t* ci, float* v, void* stream);
+/* rows row0 .. row0+n-1 of the global stencil (global column indices);
+ * 3-D kinds: nz planes of g x g along the slowest axis (nz = g: the cube) */
+int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t nz, int64_t row0, int64_t n, int32_t* len, void* stream);
+int b200sp_stencil_fill_f64(int32_t kind, int64_t g, int64_t nz, double conv, int64_t row0, int64_t n,
+                            const int32_t* rp, int32_t* ci, double* v, void* stream);
+int b200sp_stencil_fill_f32(int32_t kind, int64_t g, int64_t nz, double conv, int64_t row0, int64_t n,
+                            const int32_t* rp, int32_t* ci, float* v, void* stream);
 int b200sp_powerlaw_lengths(int64_t n, uint64_t seed, const double* thresholds, int32_t max_len, int32_t* len,
                             void* stream);
 int b200sp_powerlaw_fill_f64(int64_t n, uint64_t seed, const int32_t* rp, int32_t* ci, double* v, void* stream);
@@ -567,7 +568,7 @@ int b200sp_cg_step1_put_f64(int64_t n, double* p, const double* z, const void* c
 int b200sp_cg_step1_put_f32(int64_t n, float* p, const float* z, const void* ctl, int32_t nput, const int64_t* lo,
                             const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,
                             uint32_t* ticket, void* stream);
-int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream);
+int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream);
 /* All-reduce (sum) of red[0..k), k <= 4, across `world` <= 8 ranks through
  * peer memory: slots[j] = rank j's slot array (2 * world * 4 doubles, zeroed
  * once; mapped), flags[j] = rank j's int32 flag array (world entries, zeroed
@@ -576,6 +577,20 @@ int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags
  * all-reduces of the distributed CG. */
 int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, double* const* slots,
                           int32_t* const* flags, int32_t epoch, void* stream);
+/* Spins on peer flags are bounded by b200sp_set_tuning("peer_timeout_ms", ms)
+ * (default 30000): peer_wait then marks the solve broken down (code 6),
+ * peer_allreduce returns NaN sums.
+ *
+ * CUDA IPC + explicit peer access (setup of the peer-memory paths): export a
+ * device buffer as an allocation handle (b200sp_ipc_handle_bytes() bytes)
+ * plus offset; open it in the caller's CURRENT device context (lazy peer
+ * access, no context on the owner's device); peer_enable reports whether the
+ * current device can reach `peer` (cudaDeviceCanAccessPeer) and enables it. */
+int32_t b200sp_ipc_handle_bytes(void);
+int b200sp_ipc_export(const void* ptr, void* handle, int64_t* offset);
+int b200sp_ipc_open(const void* handle, int64_t offset, void** ptr, void** base);
+int b200sp_ipc_close(void* base);
+int b200sp_peer_enable(int32_t peer, int32_t* can);
 int b200sp_cg_finish(void* ctl, double* hist, int32_t phase, void* stream);
 /* FCG (src/solvers/krylov.py:80-125) reuses cg_init / cg_step1 / the fused
  * SpMV + sigma; fcg_init_ctl seeds rho_t = 0 after cg_init, fcg_step2 also

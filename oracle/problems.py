@@ -52,9 +52,11 @@ def five_point(g):
     return _merge(n, parts)
 
 
-def stencil3d(g, kind, conv=0.4):
-    """kind: '7pt' | '27pt' | 'convdiff'."""
-    n = g ** 3
+def stencil3d(g, kind, conv=0.4, nz=None):
+    """kind: '7pt' | '27pt' | 'convdiff'; nz planes of g x g along the
+    slowest axis (default g: the cube)."""
+    nz = g if nz is None else nz
+    n = g * g * nz
     idx = np.arange(n, dtype=np.int64)
     i, j, k = idx // (g * g), (idx // g) % g, idx % g
     parts = []
@@ -62,7 +64,7 @@ def stencil3d(g, kind, conv=0.4):
         for di in (-1, 0, 1):
             for dj in (-1, 0, 1):
                 for dk in (-1, 0, 1):
-                    m = ((i + di >= 0) & (i + di < g) & (j + dj >= 0) & (j + dj < g)
+                    m = ((i + di >= 0) & (i + di < nz) & (j + dj >= 0) & (j + dj < g)
                          & (k + dk >= 0) & (k + dk < g))
                     val = 26.0 if (di, dj, dk) == (0, 0, 0) else -1.0
                     parts.append((idx[m], idx[m] + (di * g + dj) * g + dk, np.full(int(m.sum()), val)))
@@ -71,7 +73,7 @@ def stencil3d(g, kind, conv=0.4):
     hi = -1.0 + conv if kind == "convdiff" else -1.0
     for m, off, val in ((i > 0, -g * g, lo), (j > 0, -g, lo), (k > 0, -1, lo),
                         (np.ones(n, bool), 0, 6.0),
-                        (k < g - 1, 1, hi), (j < g - 1, g, hi), (i < g - 1, g * g, hi)):
+                        (k < g - 1, 1, hi), (j < g - 1, g, hi), (i < nz - 1, g * g, hi)):
         parts.append((idx[m], idx[m] + off, np.full(int(m.sum()), val)))
     return _merge(n, parts)
 

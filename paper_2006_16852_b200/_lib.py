@@ -53,7 +53,7 @@ _TYPED = {
     "dense_to_csr_fill": "llplpppp",
     "csr_to_dense": "lpppplp",
     # generators
-    "stencil_fill": "ildllpppp",
+    "stencil_fill": "illdllpppp",
     "powerlaw_fill": "lupppp",
     # block-Jacobi
     "jacobi_invert": "lpppppppppidpp",
@@ -133,7 +133,7 @@ _UNTYPED = {
     "length_histogram": ("lpipp", ctypes.c_int),
     "empty_row_flags": ("lppp", ctypes.c_int),
     "compact_flags": ("lpppp", ctypes.c_int),
-    "stencil_lengths": ("illlpp", ctypes.c_int),
+    "stencil_lengths": ("illllpp", ctypes.c_int),
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
     "set_guard": ("p", None),
     "set_tuning": ("si", ctypes.c_int),
@@ -151,6 +151,11 @@ _UNTYPED = {
     "jacobi_block_sizes_sq": ("lppp", ctypes.c_int),
     "jacobi_pack": ("lppppppp", ctypes.c_int),
     "jacobi_large_max_block": ("", ctypes.c_int64),
+    "ipc_handle_bytes": ("", ctypes.c_int32),
+    "ipc_export": ("ppp", ctypes.c_int),
+    "ipc_open": ("plpp", ctypes.c_int),
+    "ipc_close": ("p", ctypes.c_int),
+    "peer_enable": ("ip", ctypes.c_int),
     "krylov_ctl_bytes": ("", ctypes.c_int64),
     "krylov_part_elems": ("", ctypes.c_int64),
     "krylov_ctl_init": ("pippiiip", ctypes.c_int),

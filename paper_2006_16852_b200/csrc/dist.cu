@@ -7,7 +7,10 @@
 // contiguous segment). The local matrix is split into A_own (columns
 // < n_local) and A_ghost (columns shifted by -n_local): q = A_own p_own runs
 // while the halo exchange is in flight, q += A_ghost p_ghost after it lands.
+#include <cuda.h>
+
 #include <cstddef>
+#include <cstring>
 
 #include "krylov.cuh"
 
@@ -160,7 +163,20 @@ struct PeerRed {
     int* flags[PEER_RED_MAX];     // every rank's flag array
 };
 
-__global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch) {
+// Every spin on a peer's flag is bounded (b200sp_set_tuning("peer_timeout_ms"),
+// default 30 s): a rank that died between its store and the matching wait
+// must not leave the surviving GPUs spinning in a kernel that never returns.
+// On timeout the wait marks the solve as broken down (BD_PEER_TIMEOUT, the
+// host reports a failed solve) and the all-reduce returns NaN sums.
+__device__ __forceinline__ bool spin_until(const int* flag, int epoch, unsigned long long deadline, int ns) {
+    while (ld_acquire_sys(flag) < epoch) {
+        if (global_ns() > deadline) return false;
+        __nanosleep(ns);
+    }
+    return true;
+}
+
+__global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch, unsigned long long timeout_ns) {
     const int par = epoch & 1;
     double v[4];
     for (int i = 0; i < k; ++i) v[i] = red[i];
@@ -171,8 +187,12 @@ __global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch)
     __threadfence_system();
     for (int j = 0; j < pr.world; ++j) st_release_sys(pr.flags[j] + pr.rank, epoch);
     const int* mine = pr.flags[pr.rank];
+    const unsigned long long deadline = global_ns() + timeout_ns;
     for (int j = 0; j < pr.world; ++j)
-        while (ld_acquire_sys(mine + j) < epoch) __nanosleep(64);
+        if (!spin_until(mine + j, epoch, deadline, 64)) {
+            for (int i = 0; i < k; ++i) red[i] = __longlong_as_double(0x7ff8000000000000ll);
+            return;
+        }
     const volatile double* sl = pr.slots[pr.rank] + (size_t)par * pr.world * 4;
     for (int i = 0; i < k; ++i) {
         double s = 0;
@@ -181,10 +201,20 @@ __global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch)
     }
 }
 
-__global__ void peer_wait_kernel(const KrylovCtl* c, PeerWait w, int epoch) {
+__global__ void peer_wait_kernel(KrylovCtl* c, PeerWait w, int epoch, unsigned long long timeout_ns) {
     if (c->done) return;
+    const unsigned long long deadline = global_ns() + timeout_ns;
     for (int k = 0; k < w.n; ++k)
-        while (ld_acquire_sys(w.flag[k]) < epoch) __nanosleep(256);
+        if (!spin_until(w.flag[k], epoch, deadline, 256)) {
+            c->breakdown = BD_PEER_TIMEOUT;
+            c->breakdown_it = c->it + 1;
+            c->done = 1;
+            return;
+        }
+}
+
+inline unsigned long long peer_timeout_ns() {
+    return (unsigned long long)tuning("peer_timeout_ms", 30000) * 1000000ull;
 }
 
 }  // namespace b200sp
@@ -280,21 +310,94 @@ int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, d
         pr.slots[j] = slots[j];
         pr.flags[j] = flags[j];
     }
-    peer_allreduce_kernel<<<1, 1, 0, as_stream(stream)>>>(red, k, pr, epoch);
+    peer_allreduce_kernel<<<1, 1, 0, as_stream(stream)>>>(red, k, pr, epoch, peer_timeout_ns());
     count_launch();
     return check_launch("peer_allreduce");
 }
 
-int b200sp_peer_wait(const void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream) {
+int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream) {
     B200SP_REQUIRE(nwait >= 0 && nwait <= 2 * PEER_MAX, B200SP_EINVAL, "peer_wait: at most %d flags (got %d)",
                    2 * PEER_MAX, nwait);
     if (nwait == 0) return B200SP_OK;
     PeerWait w{};
     w.n = nwait;
     for (int k = 0; k < nwait; ++k) w.flag[k] = flags[k];
-    peer_wait_kernel<<<1, 1, 0, as_stream(stream)>>>((const KrylovCtl*)ctl, w, epoch);
+    peer_wait_kernel<<<1, 1, 0, as_stream(stream)>>>((KrylovCtl*)ctl, w, epoch, peer_timeout_ns());
     count_launch();
     return check_launch("peer_wait");
+}
+
+// ---- CUDA IPC + peer access (the peer-memory halo / all-reduce setup) ------
+// Buffers are exported as (allocation handle, offset) and opened in the
+// CALLER's current device context with lazy peer access: no CUDA context is
+// created on the owner's device. Peer access is enabled explicitly first so
+// that a topology without P2P is detected (and the host falls back to NCCL)
+// instead of failing inside a kernel.
+typedef CUresult (*PfnMemGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+static PfnMemGetAddressRange address_range_fn() {
+    static PfnMemGetAddressRange fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PfnMemGetAddressRange)p;
+    }
+    return fn;
+}
+
+int32_t b200sp_ipc_handle_bytes(void) { return (int32_t)sizeof(cudaIpcMemHandle_t); }
+
+int b200sp_ipc_export(const void* ptr, void* handle, int64_t* offset) {
+    PfnMemGetAddressRange range = address_range_fn();
+    B200SP_REQUIRE(range != nullptr, B200SP_ECUDA, "ipc_export: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    B200SP_REQUIRE(range(&base, &size, (CUdeviceptr)ptr) == CUDA_SUCCESS, B200SP_ECUDA,
+                   "ipc_export: %p is not device memory", ptr);
+    cudaIpcMemHandle_t h;
+    B200SP_CHECK_CUDA(cudaIpcGetMemHandle(&h, (void*)base));
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((CUdeviceptr)ptr - base);
+    return B200SP_OK;
+}
+
+int b200sp_ipc_open(const void* handle, int64_t offset, void** ptr, void** base) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* b = nullptr;
+    B200SP_CHECK_CUDA(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+    *base = b;
+    *ptr = (char*)b + offset;
+    return B200SP_OK;
+}
+
+int b200sp_ipc_close(void* base) {
+    B200SP_CHECK_CUDA(cudaIpcCloseMemHandle(base));
+    return B200SP_OK;
+}
+
+// can = 1 when the current device can load/store `peer`'s memory (same
+// device, or cudaDeviceCanAccessPeer); peer access is then enabled
+int b200sp_peer_enable(int32_t peer, int32_t* can) {
+    int cur = 0;
+    B200SP_CHECK_CUDA(cudaGetDevice(&cur));
+    if (peer == cur) {
+        *can = 1;
+        return B200SP_OK;
+    }
+    int ok = 0;
+    B200SP_CHECK_CUDA(cudaDeviceCanAccessPeer(&ok, cur, peer));
+    *can = ok;
+    if (!ok) return B200SP_OK;
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        (void)cudaGetLastError();
+        return B200SP_OK;
+    }
+    B200SP_CHECK_CUDA(e);
+    return B200SP_OK;
 }
 
 }  // extern "C"

@@ -7,7 +7,9 @@
 // tests pin it against the reference's own five_point_poisson /
 // convection_diffusion (tests/golden).
 //
-// Stencils (grid index idx = (i*g + j)*g + k, Dirichlet truncation):
+// Stencils (grid index idx = (i*g + j)*g + k, Dirichlet truncation; the 3-D
+// kinds take nz planes along i -- nz = g is the cube, nz = N g the weak-scaled
+// slab stack of the multi-GPU benchmark):
 //   kind 0: 2-D 5-point,  g x g,   centre 4, neighbours -1  (== five_point_poisson)
 //   kind 1: 3-D 7-point,  g^3,     centre 6, neighbours -1
 //   kind 2: 3-D 27-point, g^3,     centre 26, neighbours -1
@@ -37,6 +39,7 @@ __device__ __forceinline__ double unit(uint64_t h) { return (double)(h >> 11) * 
 struct Stencil {
     int kind;
     int64_t g;
+    int64_t nz;  // planes along the slowest axis i (3-D kinds; nz = g is the cube)
     double conv;
     int64_t row0;
 };
@@ -49,10 +52,10 @@ __device__ __forceinline__ int stencil_len(const Stencil& s, int64_t row) {
     const int64_t g = s.g;
     const int64_t i = row / (g * g), j = (row / g) % g, k = row % g;
     if (s.kind == 2) {
-        const int ni = 1 + (i > 0) + (i < g - 1), nj = 1 + (j > 0) + (j < g - 1), nk = 1 + (k > 0) + (k < g - 1);
+        const int ni = 1 + (i > 0) + (i < s.nz - 1), nj = 1 + (j > 0) + (j < g - 1), nk = 1 + (k > 0) + (k < g - 1);
         return ni * nj * nk;
     }
-    return 1 + (i > 0) + (i < g - 1) + (j > 0) + (j < g - 1) + (k > 0) + (k < g - 1);
+    return 1 + (i > 0) + (i < s.nz - 1) + (j > 0) + (j < g - 1) + (k > 0) + (k < g - 1);
 }
 
 // n = rows generated, starting at global row s.row0 (row-partitioned solves
@@ -82,7 +85,7 @@ __global__ void stencil_fill_kernel(Stencil s, int64_t n, const int* __restrict_
         const int64_t i = r / (g * g), j = (r / g) % g, k = r % g;
         if (s.kind == 2) {
             for (int di = -1; di <= 1; ++di) {
-                if (i + di < 0 || i + di >= g) continue;
+                if (i + di < 0 || i + di >= s.nz) continue;
                 for (int dj = -1; dj <= 1; ++dj) {
                     if (j + dj < 0 || j + dj >= g) continue;
                     for (int dk = -1; dk <= 1; ++dk) {
@@ -105,7 +108,7 @@ __global__ void stencil_fill_kernel(Stencil s, int64_t n, const int* __restrict_
         ci[o] = (int)r; v[o] = T(6); ++o;
         if (k < g - 1) { ci[o] = (int)(r + 1); v[o] = T(hi); ++o; }
         if (j < g - 1) { ci[o] = (int)(r + g); v[o] = T(hi); ++o; }
-        if (i < g - 1) { ci[o] = (int)(r + g * g); v[o] = T(hi); ++o; }
+        if (i < s.nz - 1) { ci[o] = (int)(r + g * g); v[o] = T(hi); ++o; }
     }
 }
 
@@ -148,25 +151,26 @@ using namespace b200sp;
 
 extern "C" {
 
-int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t row0, int64_t n, int32_t* len, void* stream) {
+int b200sp_stencil_lengths(int32_t kind, int64_t g, int64_t nz, int64_t row0, int64_t n, int32_t* len, void* stream) {
     B200SP_REQUIRE(kind >= 0 && kind <= 3, B200SP_EINVAL, "stencil: unknown kind %d", kind);
+    B200SP_REQUIRE(nz >= 1, B200SP_EINVAL, "stencil: nz must be positive");
     if (n == 0) return B200SP_OK;
-    stencil_lengths_kernel<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, 0.0, row0}, n, len);
+    stencil_lengths_kernel<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, nz, 0.0, row0}, n, len);
     count_launch();
     return check_launch("stencil_lengths");
 }
 
-int b200sp_stencil_fill_f64(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
+int b200sp_stencil_fill_f64(int32_t kind, int64_t g, int64_t nz, double conv, int64_t row0, int64_t n, const int32_t* rp,
                             int32_t* ci, double* v, void* stream) {
     if (n == 0) return B200SP_OK;
-    stencil_fill_kernel<double><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, conv, row0}, n, rp, ci, v);
+    stencil_fill_kernel<double><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, nz, conv, row0}, n, rp, ci, v);
     count_launch();
     return check_launch("stencil_fill");
 }
-int b200sp_stencil_fill_f32(int32_t kind, int64_t g, double conv, int64_t row0, int64_t n, const int32_t* rp,
+int b200sp_stencil_fill_f32(int32_t kind, int64_t g, int64_t nz, double conv, int64_t row0, int64_t n, const int32_t* rp,
                             int32_t* ci, float* v, void* stream) {
     if (n == 0) return B200SP_OK;
-    stencil_fill_kernel<float><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, conv, row0}, n, rp, ci, v);
+    stencil_fill_kernel<float><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(Stencil{kind, g, nz, conv, row0}, n, rp, ci, v);
     count_launch();
     return check_launch("stencil_fill");
 }

@@ -21,7 +21,8 @@ constexpr int KRY_MAX_CRIT = 8;
 constexpr int KRY_NRED = 4;  // partial-sum slots per reduction
 
 enum CritType : int { CRIT_ITERATION = 1, CRIT_RNR = 2, CRIT_TIME = 3 };
-enum Breakdown : int { BD_NONE = 0, BD_CG_SIGMA = 1, BD_RHO = 2, BD_GAMMA = 3, BD_TT = 4, BD_HESSENBERG = 5 };
+enum Breakdown : int { BD_NONE = 0, BD_CG_SIGMA = 1, BD_RHO = 2, BD_GAMMA = 3, BD_TT = 4, BD_HESSENBERG = 5,
+                       BD_PEER_TIMEOUT = 6 };
 constexpr int EXACT_CONVERGENCE_ID = 254;  // src/solvers/gmres.py:31
 
 struct KrylovCtl {

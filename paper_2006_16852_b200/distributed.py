@@ -108,6 +108,16 @@ class StagedComm(Comm):
         return _Works([])
 
 
+def make_comm(group=None):
+    """Comm for the process group's backend: NCCL collectives on device
+    tensors directly; gloo (ranks sharing a GPU, CPU tests) staged through
+    host memory."""
+    import torch.distributed as dist
+
+    backend = str(dist.get_backend(group)).lower()
+    return Comm(group) if backend == "nccl" else StagedComm(group)
+
+
 class _Works:
     def __init__(self, works):
         self.works = works
@@ -181,23 +191,26 @@ class DistCsr(LinOp):
         return self.plan.n_local + self.plan.n_ghost
 
     @classmethod
-    def stencil(cls, exc, comm, kind, grid, value_dtype="float64", convection=0.4, strategy="automatic"):
-        """Generate this rank's rows of a stencil matrix directly on its GPU."""
+    def stencil(cls, exc, comm, kind, grid, value_dtype="float64", convection=0.4, strategy="automatic", nz=None):
+        """Generate this rank's rows of a stencil matrix directly on its GPU.
+        3-D kinds: ``nz`` planes of grid x grid (default: the grid^3 cube;
+        nz = size * grid stacks one cube-sized slab per rank, weak scaling)."""
         code = STENCILS[kind]
-        n = grid * grid if code == 0 else grid ** 3
+        nz = int(nz or grid)
+        n = grid * grid if code == 0 else grid * grid * nz
         plane = grid if code == 0 else grid * grid
         part = Partition(n, comm.size, align=plane)
         lo, hi = part.range(comm.rank)
         nl = hi - lo
         dev = exc.device
         lens = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
-        _lib.call("stencil_lengths", code, grid, lo, nl, ptr(lens), exc.stream)
+        _lib.call("stencil_lengths", code, grid, nz, lo, nl, ptr(lens), exc.stream)
         rp = _scan(exc, lens[:nl])
         nnz = int(rp[-1].item())
         vt = torch.float64 if np.dtype(value_dtype) == np.float64 else torch.float32
         ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
         v = torch.empty(max(nnz, 1), dtype=vt, device=dev)
-        _lib.call("stencil_fill_" + _lib.suffix(vt), code, grid, float(convection), lo, nl, ptr(rp), ptr(ci),
+        _lib.call("stencil_fill_" + _lib.suffix(vt), code, grid, nz, float(convection), lo, nl, ptr(rp), ptr(ci),
                   ptr(v), exc.stream)
         return cls.from_local_rows(exc, comm, part, rp, ci[:nnz], v[:nnz], strategy)
 
@@ -281,12 +294,48 @@ class DistCsr(LinOp):
 # ---------------------------------------------------------------------------
 # halo through peer memory
 # ---------------------------------------------------------------------------
+def ipc_export(t):
+    """(allocation handle bytes, byte offset) of a device tensor's storage,
+    for peers to open with ipc_open (csrc/dist.cu: b200sp_ipc_export)."""
+    buf = ctypes.create_string_buffer(int(_lib.query("ipc_handle_bytes")))
+    off = ctypes.c_int64()
+    _lib.call("ipc_export", t.data_ptr(), ctypes.addressof(buf), ctypes.addressof(off))
+    return bytes(buf.raw), int(off.value)
+
+
+def ipc_open(handle, offset):
+    """Map a peer's exported buffer into THIS process's current device
+    context (lazy peer access): returns (pointer, allocation base)."""
+    buf = ctypes.create_string_buffer(handle, len(handle))
+    p, base = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.call("ipc_open", ctypes.addressof(buf), int(offset), ctypes.addressof(p), ctypes.addressof(base))
+    return int(p.value), int(base.value)
+
+
+def peer_capable(comm, dev):
+    """Collective: True on every rank when every rank can reach every other
+    rank's device with loads/stores (cudaDeviceCanAccessPeer, then
+    cudaDeviceEnablePeerAccess -- explicit, so a topology without P2P falls
+    back to NCCL instead of faulting in a kernel). Ranks sharing one device
+    always qualify."""
+    devices = comm.allgather_object(int(dev.index if dev.index is not None else torch.cuda.current_device()))
+    ok = True
+    can = ctypes.c_int32()
+    for j, d in enumerate(devices):
+        if j == comm.rank:
+            continue
+        _lib.call("peer_enable", d, ctypes.addressof(can))
+        ok = ok and bool(can.value)
+    return all(comm.allgather_object(ok)), devices
+
+
 class PeerHalo:
     """The halo exchange as peer-memory stores fused into the CG step that
     produces the values (b200sp_cg_step1_put): every rank exports its
     extended vector [owned | ghosts] and a flag array through CUDA IPC (one
     all_gather of the handles), opens the buffers of the ranks it sends to
-    (peer access over NVLink / NVSwitch is enabled on open), and then
+    in its own device context (peer access over NVLink / NVSwitch enabled
+    explicitly first, see peer_capable), and then
     writes its boundary rows straight into their ghost slots while updating
     p, raising its flag in their flag arrays when the kernel's stores are
     out. The receiver orders its ghost SpMV after b200sp_peer_wait on the
@@ -297,8 +346,6 @@ class PeerHalo:
     the reuse of the ghost slots from one exchange to the next."""
 
     def __init__(self, A, dtype):
-        from torch.multiprocessing.reductions import reduce_tensor
-
         comm, exc = A.comm, A.exec
         dev = exc.device
         self.A = A
@@ -306,24 +353,22 @@ class PeerHalo:
         self.flags = torch.zeros(max(comm.size, 1), dtype=torch.int32, device=dev)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         torch.cuda.synchronize(dev)
-        mine = {"pext": reduce_tensor(self.pext), "flags": reduce_tensor(self.flags), "nl": A.n_local,
+        mine = {"pext": ipc_export(self.pext), "flags": ipc_export(self.flags), "nl": A.n_local,
                 "g0": {int(peer): int(g0) for peer, g0, _ in A.plan.recv}}
         every = comm.allgather_object(mine)
-        self._remote = []  # keep the mapped peer buffers alive
+        self._bases = []  # mapped peer allocations (closed with the object)
         lo, hi, dst, flg = [], [], [], []
         esz = self.pext.element_size()
         for peer, a, b, idx, _ in A._send:
             info = every[peer]
-            fn, args = info["pext"]
-            rp_ = fn(*args)
-            fn, args = info["flags"]
-            rf = fn(*args)
-            self._remote.append((rp_, rf))
+            rp_, b0 = ipc_open(*info["pext"])
+            rf, b1 = ipc_open(*info["flags"])
+            self._bases += [b0, b1]
             g0 = info["g0"][comm.rank]
             lo.append(a)
             hi.append(b)
-            dst.append(rp_.data_ptr() + (info["nl"] + g0) * esz)
-            flg.append(rf.data_ptr() + 4 * comm.rank)
+            dst.append(rp_ + (info["nl"] + g0) * esz)
+            flg.append(rf + 4 * comm.rank)
         k = len(lo)
         self.nput = k
         self.lo = (ctypes.c_int64 * max(k, 1))(*lo)
@@ -368,27 +413,23 @@ class PeerReduce:
     no NCCL launch."""
 
     def __init__(self, comm, dev):
-        from torch.multiprocessing.reductions import reduce_tensor
-
         w = comm.size
         self.world, self.rank = w, comm.rank
         self.slots = torch.zeros(2 * w * 4, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(w, dtype=torch.int32, device=dev)
         torch.cuda.synchronize(dev)
-        every = comm.allgather_object({"slots": reduce_tensor(self.slots), "flags": reduce_tensor(self.flags)})
-        self._remote, sl, fl = [], [], []
+        every = comm.allgather_object({"slots": ipc_export(self.slots), "flags": ipc_export(self.flags)})
+        self._bases, sl, fl = [], [], []
         for j, info in enumerate(every):
             if j == comm.rank:
                 sl.append(self.slots.data_ptr())
                 fl.append(self.flags.data_ptr())
                 continue
-            fn, args = info["slots"]
-            ts = fn(*args)
-            fn, args = info["flags"]
-            tf = fn(*args)
-            self._remote.append((ts, tf))
-            sl.append(ts.data_ptr())
-            fl.append(tf.data_ptr())
+            ts, b0 = ipc_open(*info["slots"])
+            tf, b1 = ipc_open(*info["flags"])
+            self._bases += [b0, b1]
+            sl.append(ts)
+            fl.append(tf)
         self.sl = (ctypes.c_void_p * w)(*sl)
         self.fl = (ctypes.c_void_p * w)(*fl)
         self.epoch = 0
@@ -503,7 +544,15 @@ class DistCg:
         """(peer halo or None, extended p vector, peer all-reduce or None)."""
         A, exc, comm = self.a, self.exec, self.a.comm
         peer = None
-        if PeerHalo.usable(A):
+        if PeerHalo.usable(A) and A.__dict__.get("_peer_ok") is None:
+            ok, _ = peer_capable(comm, exc.device)  # collective, once per matrix
+            A.__dict__["_peer_ok"] = ok
+            if not ok:
+                import warnings
+
+                warnings.warn("distributed CG: peer access between the ranks' GPUs is unavailable; "
+                              "falling back to NCCL send/recv halo and NCCL all-reduce", RuntimeWarning)
+        if PeerHalo.usable(A) and A.__dict__.get("_peer_ok"):
             peer = getattr(A, "_peer_halo", {}).get(dt)
             if peer is None:  # collective: every rank builds it on its first solve of this dtype
                 peer = PeerHalo(A, dt)

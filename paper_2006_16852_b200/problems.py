@@ -25,13 +25,13 @@ def stencil(exc, kind, grid, value_dtype="float64", convection=0.4, strategy="au
     code = STENCILS[kind]
     n = grid * grid if code == 0 else grid ** 3
     lens = torch.empty(max(n, 1), dtype=torch.int32, device=exc.device)
-    _lib.call("stencil_lengths", code, grid, 0, n, ptr(lens), exc.stream)
+    _lib.call("stencil_lengths", code, grid, grid, 0, n, ptr(lens), exc.stream)
     rp = _scan(exc, lens[:n])
     nnz = int(rp[-1].item())
     vt = torch.float64 if np.dtype(value_dtype) == np.float64 else torch.float32
     ci = torch.empty(nnz, dtype=torch.int32, device=exc.device)
     v = torch.empty(nnz, dtype=vt, device=exc.device)
-    _lib.call("stencil_fill_" + _lib.suffix(vt), code, grid, float(convection), 0, n, ptr(rp), ptr(ci),
+    _lib.call("stencil_fill_" + _lib.suffix(vt), code, grid, grid, float(convection), 0, n, ptr(rp), ptr(ci),
               ptr(v), exc.stream)
     return Csr._from_device(exc, Dim2(n, n), rp, ci, v, strategy=strategy)
 

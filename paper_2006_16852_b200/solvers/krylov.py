@@ -20,7 +20,7 @@ from .common import BreakdownInfo, IterativeSolver, IterativeSolverFactory
 from .device import batch_size, get_state
 
 _BD_REASONS = {1: "non-positive p^T A p", 2: "rho = 0", 3: "r_tld^T A p = 0", 4: "t^T t = 0",
-               5: "singular Hessenberg system"}
+               5: "singular Hessenberg system", 6: "a peer rank did not respond (peer_timeout_ms)"}
 
 
 def device_path_ok(solver, b):
