@@ -306,7 +306,7 @@ def bench_c5_distributed(args, world, rank, local):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated 7-point Poisson, b = ones, x0 = 0)",
             "config": {"workload": f"C5: row-partitioned CG, 3-D 7-point Poisson {g}^3, RNR 1e-8, "
-                                   f"{'peer-memory' if solver.halo == 'peer' else 'NCCL'} halo + NCCL all-reduce",
+                                   f"{'peer-memory' if solver.halo == 'peer' else 'NCCL'} halo + {'peer-memory' if solver.reduce == 'peer' else 'NCCL'} all-reduce",
                        "halo": solver.halo, "iterations": its,
                        "converged": bool(st.converged), "parallelism": f"row partition x{world}",
                        "rows_per_rank": A.n_local, "build_s": round(build_s, 3), "breakdown": brk},

@@ -48,7 +48,7 @@ for fmt in fmts:
     attrs = {}
     if ":" in fmt:  # e.g. coo:chunk=128
         fmt, kv = fmt.split(":")
-        attrs = {k: int(v) for k, v in (p.split("=") for p in kv.split(";"))}
+        attrs = {k: (int(v) if v.lstrip("-").isdigit() else v) for k, v in (p.split("=") for p in kv.split(";"))}
     m = b2.convert(a, fmt.split("/")[0])
     for k, v in attrs.items():
         setattr(m, k, v)
