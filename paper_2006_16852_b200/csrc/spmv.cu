@@ -1281,7 +1281,7 @@ coo_fixup_kernel(int64_t nchunks, Rows R, const T* __restrict__ carry_head, cons
 // skewed row lengths (the C3 power law): every warp gets the same number
 // of nonzeros and all of a lane's gathers are independent.
 // ===========================================================================
-constexpr int SEG_E = 8;  // entries per lane: 4 -> 464 us, 8 -> 433 us, 16 -> 679 us (123 registers) on C3
+constexpr int SEG_E = 8;  // entries per lane (round 1: 4 -> 464 us, 8 -> 433 us, 16 -> 679 us on C3)
 constexpr int SEG_CHUNK = 32 * SEG_E;
 
 // srow[c] = row of chunk c's first entry; srow[nchunks] = n
@@ -1303,8 +1303,8 @@ __global__ void csr_seg_plan_kernel(int64_t n, int64_t nnz, const int* __restric
     srow[t] = (int)lo;
 }
 
-template <typename T, bool XIN, bool VEC>
-__global__ void __launch_bounds__(COO_BLOCK)
+template <typename T, bool XIN, bool VEC, int MINB>
+__global__ void __launch_bounds__(COO_BLOCK, MINB)
 csr_seg_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __restrict__ ci,
                const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
                Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins, const int* __restrict__ srow,
@@ -1350,7 +1350,57 @@ csr_seg_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __
     const int head_row = srow[c];
     int r[E];
     int cur = head_row;
-    if (cnt > 0) {
+    // Fast path: the chunk's row starts as a 256-bit mask. Row starts inside
+    // (e0, e1) are rp[head_row + 1 .. srow[c + 1]] -- loaded once per chunk,
+    // coalesced, one per lane -- and bit q marks a row starting at entry
+    // e0 + q; an entry's row is head_row + the set bits at or before it. No
+    // per-lane search, no load chain. Taken when the chunk holds no empty row
+    // (set bits == starts) and at most 256 row starts; else the search below.
+    __shared__ unsigned s_mask[COO_BLOCK / 32][SEG_CHUNK / 32];
+    unsigned* mask = s_mask[threadIdx.x >> 5];
+    const int nstart = min(srow[c + 1], (int)n) - head_row;
+    const int clen = (int)(e1 - e0);
+    bool fast = nstart <= SEG_CHUNK;
+    int mine_starts = 0;
+    if (fast) {
+#pragma unroll
+        for (int w = lane; w < SEG_CHUNK / 32; w += 32) mask[w] = 0u;
+        __syncwarp();
+        int& mine = mine_starts;
+        for (int j = lane; j < nstart; j += 32) {
+            const int q = __ldg(rp + head_row + 1 + j) - (int)e0;
+            if (q > 0 && q < clen) {
+                atomicOr(&mask[q >> 5], 1u << (q & 31));
+                ++mine;
+            }
+        }
+        __syncwarp();
+    }
+    // lane w < 8 holds mask word w and the count of set bits in words < w
+    const unsigned mw = fast && lane < SEG_CHUNK / 32 ? mask[lane] : 0u;
+    int incl = __popc(mw);
+#pragma unroll
+    for (int o = 1; o < SEG_CHUNK / 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (fast) fast = __all_sync(0xffffffffu, warp_sum(mine_starts) == __shfl_sync(0xffffffffu, incl, SEG_CHUNK / 32 - 1));
+    if (fast) {
+        // rows started at or before the lane's first entry (positions <= E lane)
+        const int p0 = lane * E;
+        const int wl = p0 >> 5;  // E | 32: the lane's bits stay in one word
+        const unsigned myw = __shfl_sync(0xffffffffu, mw, wl);
+        int d = __shfl_sync(0xffffffffu, incl - __popc(mw), wl) + __popc(myw & (0xffffffffu >> (31 - (p0 & 31))));
+        const unsigned word = myw >> (p0 & 31);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            if (i > 0) d += (word >> i) & 1u;
+            r[i] = i < cnt ? head_row + d : INT_MAX;
+            if (i < cnt) cur = head_row + d;
+        }
+        if (lane == 0 && __ldg(rp + head_row) == e0)  // empty rows ending right before the chunk
+            for (int q = head_row - 1; q >= 0 && __ldg(rp + q) == e0; --q) write_empty(q);
+    } else if (cnt > 0) {
         int lo = head_row, hi = min(srow[c + 1], (int)n - 1);
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -1401,6 +1451,7 @@ csr_seg_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int* __
 #pragma unroll
         for (int i = 0; i < E; ++i) r[i] = INT_MAX;
     }
+    if (fast && cnt == 0) cur = head_row;
     const int last_lane = (int)((e1 - 1 - e0) / E);
     const int tail_row = __shfl_sync(0xffffffffu, cur, last_lane);
     const bool head_shared = e0 > 0 && __ldg(rp + head_row) < e0;
@@ -1432,9 +1483,23 @@ static int csr_seg(int64_t n, int64_t nnz, const int* rp, const int* ci, const T
     const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
     const bool vec = aligned16(ci) && aligned16(v);
     const CsrChunkRows R{srow, ctail};
+    // 5 CTAs per SM (48 registers): C3 404.5 us vs 447.7 unbounded (70 registers, 3 CTAs), 420.9 at 4, 451.7 at 6 (spills)
+    const int minb = tuning("seg_minb", 5);
 #define SEG_LAUNCH(XI, VE)                                                                                   \
-    csr_seg_kernel<T, XI, VE><<<grid, COO_BLOCK, 0, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be, xin, xins, \
-                                                          srow, ctail, carry_head, carry_tail)
+    do {                                                                                                     \
+        if (minb >= 6)                                                                                       \
+            csr_seg_kernel<T, XI, VE, 6><<<grid, COO_BLOCK, 0, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be,  \
+                                                                     xin, xins, srow, ctail, carry_head, carry_tail); \
+        else if (minb == 4)                                                                                  \
+            csr_seg_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be,  \
+                                                                     xin, xins, srow, ctail, carry_head, carry_tail); \
+        else if (minb == 5)                                                                                  \
+            csr_seg_kernel<T, XI, VE, 5><<<grid, COO_BLOCK, 0, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be,  \
+                                                                     xin, xins, srow, ctail, carry_head, carry_tail); \
+        else                                                                                                 \
+            csr_seg_kernel<T, XI, VE, 1><<<grid, COO_BLOCK, 0, st>>>(n, nnz, rp, ci, v, b, bs, x, xs, al, be,  \
+                                                                     xin, xins, srow, ctail, carry_head, carry_tail); \
+    } while (0)
     if (xin) {
         if (vec) SEG_LAUNCH(true, true); else SEG_LAUNCH(true, false);
         coo_fixup_kernel<T, true><<<fgrid, 256, 0, st>>>(nchunks, R, carry_head, carry_tail, x, xs, al, be, xin, xins);
