@@ -321,7 +321,7 @@ def bench_c2(args, world, rank, local):
                           "strategy": m.strategy}
     kern = {"classical": "csr_classical_kernel",
             "stream": "csr_pipe_kernel" if m.stream_impl() == "tma" else "csr_stream_kernel",
-            "load_balance": {1: "csr_lb_kernel", 2: "csr_lb2_kernel", 3: "csr_seg_kernel"}[m.lb_mode()]}[m.strategy]
+            "load_balance": {2: "csr_lb2_kernel", 3: "csr_seg_kernel"}[m.lb_mode()]}[m.strategy]
     roofline = {"bound": "hbm", "achieved": round(by / t_step / 1e9, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(by / t_step / 1e9 / peak, 4), "traffic": traffic_from_profiles(kern),
                 "peak_source": peak_src, "kernel": kern, "bytes_per_launch": by}

@@ -57,11 +57,8 @@ def bench_solver(args, world, rank, local, kind):
         a = problems.stencil(exc, "7pt", args.grid or 512)
         fac = b2.Cg(exc, criteria=[b2.Iteration(20000), b2.ResidualNormReduction(1e-8)])
         wl = f"C5: CG, 3-D 7-point Poisson {args.grid or 512}^3, rhs ones, x0 = 0, RNR 1e-8, fp64, 1 GPU"
-        # SpMV + p update (3n) + x, r update with r.r (6n); with the p update
-        # folded into the SpMV (config.CG_FOLD_P) the SpMV reads z as well and
-        # writes p: SpMV + 2n + 6n
-        from paper_2006_16852_b200 import config as _cfg
-        vec_passes = 8 if _cfg.CG_FOLD_P else 9
+        # SpMV + p update (3n) + x, r update with r.r (6n)
+        vec_passes = 9
     else:
         g = args.grid or 256
         a = problems.stencil(exc, "convdiff", g)

@@ -111,28 +111,6 @@ int b200sp_csr_spmv_stream_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, 
                                const float* x_in, int64_t x_in_stride, int32_t chunk_cap, int32_t tpr,
                                int32_t rpt, int32_t gather_in_reduce, void* stream);
 int32_t b200sp_csr_stream_capacity(int32_t value_bytes);
-/* Csr apply with b and x in pinned (mapped) host memory, as one cooperative
- * kernel: producer CTAs stream b over PCIe into `b_dev` in chunks of
- * b200sp_csr_host_chunk_elems() entries and publish each with
- * flags[chunk] = epoch (release); consumer CTAs reduce row tiles of
- * `tile_rows` rows (classical sub-warp scheme, identical results to
- * b200sp_csr_spmv_classical_*) as soon as the chunks up to tile_need[tile]
- * have landed, and store x straight into host memory. flags: int32
- * [ceil(ncols / chunk_elems)], zero-initialised once; epoch > 0 and
- * different from the previous call's. tile_need from b200sp_csr_tile_chunks.
- * Replaces LinOp.apply on host operands (src/base.py:60-70, migration
- * src/base.py:99-127) for CsrSpmvKernel (src/kernels.py:278-316). */
-int32_t b200sp_csr_host_chunk_elems(int32_t value_bytes);
-int b200sp_csr_tile_chunks(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, int32_t tile_rows,
-                           int64_t chunk_elems, int32_t* tile_need, void* stream);
-int b200sp_csr_spmv_host_f64(int64_t n, int64_t ncols, const int32_t* row_ptrs, const int32_t* col_idxs,
-                             const double* vals, const double* b_host, double* b_dev, double* x_host,
-                             const int32_t* tile_need, int32_t tile_rows, int32_t* flags, int32_t epoch,
-                             int32_t subwarp, void* stream);
-int b200sp_csr_spmv_host_f32(int64_t n, int64_t ncols, const int32_t* row_ptrs, const int32_t* col_idxs,
-                             const float* vals, const float* b_host, float* b_dev, float* x_host,
-                             const int32_t* tile_need, int32_t tile_rows, int32_t* flags, int32_t epoch,
-                             int32_t subwarp, void* stream);
 /* Csr, stream strategy as a persistent TMA pipeline ("pipe"): one or two CTAs per SM
  * of `consumers` (256/512) consumer threads + 1 producer warp; tiles of
  * consumers/tpr*rpt rows, each row reduced by `tpr` (1/2/4) threads; each
@@ -155,8 +133,7 @@ int b200sp_csr_spmv_tma_f32(int64_t n, int64_t nnz, const int32_t* row_ptrs, con
                             int32_t consumers, int32_t tpr, void* stream);
 int64_t b200sp_csr_tma_stage_bytes(int32_t value_bytes, int32_t rows_per_tile, int32_t cap);
 /* Csr, load-balanced strategy: merge-path tiles of `tile` merge items (rows +
- * nonzeros) with a deterministic carry fix-up. mode 1: items merged
- * thread-by-thread from shared memory (skewed rows); mode 2: the tile's rows
+ * nonzeros) with a deterministic carry fix-up. mode 2: the tile's rows
  * reduced sub-warp-per-row from global memory, long rows and the carried-out
  * row by the whole CTA. Plan once per matrix: tile = b200sp_csr_lb_tile(vb,
  * mode), coords = 2*(num_tiles+1) int32; workspace carry_row / carry_val
@@ -456,17 +433,6 @@ int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* row_ptrs, const int32_t* c
 int b200sp_csr_spmv_dot_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
                             const float* p, float* q, const float* u, int32_t phase, int32_t subwarp, void* ctl,
                             double* part, void* stream);
-/* CG's p update folded into the fused SpMV: q = A p_new and sigma = p_new.q
- * with p_new = z + beta p_old (beta from the control block, the CgStep1
- * multiply-add, steps.py:93-119) recomputed for every gathered column and
- * stored for the own rows into p_new (p_old != p_new: alternate two
- * buffers). Replaces b200sp_cg_step1_* + b200sp_csr_spmv_dot_* phase 1. */
-int b200sp_csr_spmv_dot_p_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
-                              const double* p_old, const double* z, double* p_new, double* q, int32_t subwarp,
-                              void* ctl, double* part, void* stream);
-int b200sp_csr_spmv_dot_p_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
-                              const float* p_old, const float* z, float* p_new, float* q, int32_t subwarp,
-                              void* ctl, double* part, void* stream);
 
 /* ---- device assembly of coordinate triples (reference MatrixData.canonicalize,
  * src/formats.py:40-53, bit for bit) ------------------------------------------

@@ -35,7 +35,6 @@ _TYPED = {
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppiip",
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
     "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iiiiip",
-    "csr_spmv_host": "llpppppppipiip",
     "coo_spmv": "lipppplpl" + _SPMV_TAIL + "pppp",
     "rows_scale": "lpplVpplp",
     "ell_spmv": "lllppplpl" + _SPMV_TAIL + "p",
@@ -70,7 +69,6 @@ _TYPED = {
     "fcg_coop": "lpppppppppppp",
     "cgs_coop": "l" + "p" * 16,
     "csr_spmv_dot": "lppppppiippp",
-    "csr_spmv_dot_p": "lpppppppippp",
     "cg_step2": "lplpppp" + "lpppp" + "pppp",
     "fcg_step2": "lplppppp" + "lpppp" + "pppp",
     "cgs_step1": "lppppp" + "lpppp" + "pp",
@@ -113,8 +111,6 @@ _UNTYPED = {
     "csr_lb_tile": ("ii", ctypes.c_int32),
     "csr_lb_num_tiles": ("lli", ctypes.c_int64),
     "csr_stream_capacity": ("i", ctypes.c_int32),
-    "csr_host_chunk_elems": ("i", ctypes.c_int32),
-    "csr_tile_chunks": ("lppilpp", ctypes.c_int),
     "csr_tma_stage_bytes": ("iii", ctypes.c_int64),
     "csr_lb_plan": ("llpipp", ctypes.c_int),
     "csr_seg_plan": ("llppp", ctypes.c_int),

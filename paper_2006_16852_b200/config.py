@@ -30,10 +30,6 @@ BICGSTAB_COOP = os.environ.get("B200SP_BICGSTAB_COOP", "1") != "0"
 #: CG / BiCGSTAB on a classical-strategy Csr fuse the reduction after each
 #: SpMV into its epilogue (csr_spmv_dot); False runs SpMV + dot kernels
 FUSED_SPMV_DOT = os.environ.get("B200SP_FUSED_SPMV_DOT", "1") != "0"
-# CG: fold p = z + beta p into the fused SpMV (two alternating p buffers).
-# Off by default: one n-pass fewer, but gathering z and p_old per nonzero
-# measured slower at C5 (4.49 vs 4.36 ms/iteration, 512^3 7-point)
-CG_FOLD_P = os.environ.get("B200SP_CG_FOLD_P", "0") == "1"
 # distributed CG halo: "auto" = peer memory (CUDA IPC) under NCCL when every
 # send is a row range, "1" = force it (also over gloo: ranks sharing one GPU),
 # "0" = NCCL send/recv

@@ -997,6 +997,9 @@ cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
             q[i] = qv;
             w[i] = uv + qv;
         }
+        // every thread has read sc (done, alpha) before thread 0 updates it:
+        // compute-sanitizer racecheck flagged the unguarded update (round 2)
+        __syncthreads();
         if (threadIdx.x == 0) {  // mid check on the unchanged ||r|| (krylov.py:171-176)
             sc.it += 1;
             hist_put(&sc, hb, sc.it, sc.rnorm);
@@ -1485,11 +1488,10 @@ namespace b200sp {
 // ===========================================================================
 // PH_SIGMA_ACC (distributed CG, ghost block): q += A_ghost p_ghost and
 // sigma = u.q with u = the owned p (the SpMV input is the ghost vector)
-// PH_SIGMA_P (CG, p update folded in): the gathered p values are
-// recomputed as z + beta p_old (the same fused multiply-add as CgStep1), the
-// own rows' new p is written to p_new, and sigma = p_new.q: one pass over p
-// fewer per iteration and one launch less (cg_step1 is skipped).
-enum FusedPhase : int { PH_SIGMA = 1, PH_GAMMA = 2, PH_TST = 3, PH_SIGMA_ACC = 4, PH_SIGMA_P = 5 };
+// (Round 1's phase 5 -- CgStep1 folded into the SpMV, p recomputed for every
+// gathered column -- measured no faster than the separate step and was
+// removed; the cooperative small-system CG keeps that idea on chip.)
+enum FusedPhase : int { PH_SIGMA = 1, PH_GAMMA = 2, PH_TST = 3, PH_SIGMA_ACC = 4 };
 
 // 8 CTAs per SM (<= 32 registers): the unbounded build took 40 registers at
 // sub-warp 1 (6 CTAs per SM) and ran slower than SpMV + separate dot
@@ -1497,10 +1499,9 @@ template <typename T, int SW, int PH>
 __global__ void __launch_bounds__(KRY_BLOCK, SW <= 4 ? 8 : 4)
 csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                     const T* __restrict__ p, T* __restrict__ q, const T* __restrict__ u, KrylovCtl* c,
-                    double* part, T* __restrict__ pout) {
+                    double* part) {
     if (c->done) return;
     constexpr int U = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1);
-    const T beta = PH == PH_SIGMA_P ? (T)c->beta : T(0);
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & (SW - 1);
     const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
@@ -1531,10 +1532,7 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
             }
 #pragma unroll
             for (int k = 0; k < U; ++k)
-                if (cc[k] >= 0) {
-                    if (PH == PH_SIGMA_P) acc[k] += vv[k] * fma_t(beta, __ldg(p + cc[k]), __ldg(u + cc[k]));
-                    else acc[k] += vv[k] * __ldg(p + cc[k]);
-                }
+                if (cc[k] >= 0) acc[k] += vv[k] * __ldg(p + cc[k]);
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) acc[k] = subwarp_sum<SW>(acc[k]);
@@ -1549,11 +1547,6 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
                 }
                 q[row] = mine;
                 if (PH == PH_SIGMA) d0 += (double)__ldg(p + row) * (double)mine;
-                if (PH == PH_SIGMA_P) {
-                    const T pn = fma_t(beta, __ldg(p + row), __ldg(u + row));
-                    pout[row] = pn;
-                    d0 += (double)pn * (double)mine;
-                }
                 if (PH == PH_GAMMA) d0 += (double)__ldg(u + row) * (double)mine;
                 if (PH == PH_TST) {
                     d0 += (double)mine * (double)__ldg(u + row);
@@ -1569,7 +1562,7 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
     } else {
         double v[1] = {d0}, tot[1];
         if (!grid_reduce<1>(v, part, &c->ticket[1], tot)) return;
-        if (PH == PH_SIGMA || PH == PH_SIGMA_ACC || PH == PH_SIGMA_P) {
+        if (PH == PH_SIGMA || PH == PH_SIGMA_ACC) {
             if (c->dist) {
                 c->red[0] = tot[0];
                 return;
@@ -1583,32 +1576,30 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
 
 template <typename T, int SW>
 static void launch_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
-                            int phase, KrylovCtl* c, double* part, cudaStream_t st, T* pout = nullptr) {
+                            int phase, KrylovCtl* c, double* part, cudaStream_t st) {
     constexpr int U = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1);
     const int grid = kry_grid(ceil_div(n, U) * SW, KRY_BLOCK);
-    if (phase == PH_SIGMA) csr_spmv_dot_kernel<T, SW, PH_SIGMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part, pout);
-    else if (phase == PH_GAMMA) csr_spmv_dot_kernel<T, SW, PH_GAMMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part, pout);
-    else if (phase == PH_SIGMA_ACC) csr_spmv_dot_kernel<T, SW, PH_SIGMA_ACC><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part, pout);
-    else if (phase == PH_SIGMA_P) csr_spmv_dot_kernel<T, SW, PH_SIGMA_P><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part, pout);
-    else csr_spmv_dot_kernel<T, SW, PH_TST><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part, pout);
+    if (phase == PH_SIGMA) csr_spmv_dot_kernel<T, SW, PH_SIGMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else if (phase == PH_GAMMA) csr_spmv_dot_kernel<T, SW, PH_GAMMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else if (phase == PH_SIGMA_ACC) csr_spmv_dot_kernel<T, SW, PH_SIGMA_ACC><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else csr_spmv_dot_kernel<T, SW, PH_TST><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
 }
 
 template <typename T>
 static int csr_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
-                        int phase, int subwarp, void* ctl, double* part, void* stream, T* pout = nullptr) {
-    B200SP_REQUIRE(phase >= PH_SIGMA && phase <= PH_SIGMA_P, B200SP_EINVAL, "csr_spmv_dot: phase must be 1..5");
-    B200SP_REQUIRE(phase != PH_SIGMA_P || pout, B200SP_EINVAL, "csr_spmv_dot: phase 5 needs p_new");
+                        int phase, int subwarp, void* ctl, double* part, void* stream) {
+    B200SP_REQUIRE(phase >= PH_SIGMA && phase <= PH_SIGMA_ACC, B200SP_EINVAL, "csr_spmv_dot: phase must be 1..4");
     B200SP_REQUIRE(phase == PH_SIGMA || u, B200SP_EINVAL, "csr_spmv_dot: phase %d needs the second vector", phase);
     if (n == 0) return B200SP_OK;
     cudaStream_t st = as_stream(stream);
     KrylovCtl* c = (KrylovCtl*)ctl;
     switch (subwarp) {
-        case 1: launch_spmv_dot<T, 1>(n, rp, ci, av, p, q, u, phase, c, part, st, pout); break;
-        case 2: launch_spmv_dot<T, 2>(n, rp, ci, av, p, q, u, phase, c, part, st, pout); break;
-        case 4: launch_spmv_dot<T, 4>(n, rp, ci, av, p, q, u, phase, c, part, st, pout); break;
-        case 8: launch_spmv_dot<T, 8>(n, rp, ci, av, p, q, u, phase, c, part, st, pout); break;
-        case 16: launch_spmv_dot<T, 16>(n, rp, ci, av, p, q, u, phase, c, part, st, pout); break;
-        case 32: launch_spmv_dot<T, 32>(n, rp, ci, av, p, q, u, phase, c, part, st, pout); break;
+        case 1: launch_spmv_dot<T, 1>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 2: launch_spmv_dot<T, 2>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 4: launch_spmv_dot<T, 4>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 8: launch_spmv_dot<T, 8>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 16: launch_spmv_dot<T, 16>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 32: launch_spmv_dot<T, 32>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
         default: set_error("csr_spmv_dot: subwarp must be a power of two <= 32 (got %d)", subwarp); return B200SP_EINVAL;
     }
     count_launch();
@@ -1945,17 +1936,6 @@ int b200sp_bicgstab_coop_f32(int64_t n, const int32_t* rp, const int32_t* ci, co
                              const float* rt, float* p, float* vv, float* s, float* t, void* ctl, double* part,
                              double* hist, void* stream) {
     return bicg_coop<float>(n, rp, ci, v, x, r, rt, p, vv, s, t, ctl, part, hist, stream);
-}
-
-int b200sp_csr_spmv_dot_p_f64(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, const double* p_old,
-                              const double* z, double* p_new, double* q, int32_t subwarp, void* ctl, double* part,
-                              void* stream) {
-    return csr_spmv_dot<double>(n, rp, ci, v, p_old, q, z, PH_SIGMA_P, subwarp, ctl, part, stream, p_new);
-}
-int b200sp_csr_spmv_dot_p_f32(int64_t n, const int32_t* rp, const int32_t* ci, const float* v, const float* p_old,
-                              const float* z, float* p_new, float* q, int32_t subwarp, void* ctl, double* part,
-                              void* stream) {
-    return csr_spmv_dot<float>(n, rp, ci, v, p_old, q, z, PH_SIGMA_P, subwarp, ctl, part, stream, p_new);
 }
 
 int b200sp_cgs_mid(void* ctl, double* hist, void* stream) {

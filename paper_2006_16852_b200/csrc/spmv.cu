@@ -585,27 +585,18 @@ static int csr_pipe(int64_t n, const int* rp, const int* ci, const T* v, const T
 // ===========================================================================
 // Csr, load-balanced strategy: merge-path decomposition (Merrill & Garland).
 // The merge of the row-end offsets rp[1..n] with the nonzero indices 0..nnz-1
-// is cut into equal tiles of LB_TILE items; each CTA stages its tile's row
-// ends and products in shared memory, every thread consumes LB_IPT items,
-// partial rows are combined with a block-wide segmented scan, and the partial
-// row straddling each tile end is carried out and added by a deterministic
-// fix-up pass. Work per CTA is bounded regardless of row-length skew.
+// is cut into equal tiles of merge items; a CTA reduces its tile's rows
+// (mode 2, below), and the partial row straddling each tile end is carried
+// out and added by a deterministic fix-up pass. Work per CTA is bounded
+// regardless of row-length skew. (Round 1's item-level merge through shared
+// memory, "mode 1", measured slower on every matrix -- C2 0.43, C3 497 us --
+// and was removed: profiles/r02_lb_coo_sweep.txt.)
 // ===========================================================================
 constexpr int LB_BLOCK = 256;
-#ifndef LB_IPT_F64
-#define LB_IPT_F64 7
-#endif
-#ifndef LB_IPT_F32
-#define LB_IPT_F32 9
-#endif
-template <typename T> struct LbIpt { static constexpr int v = LB_IPT_F64; };
-template <> struct LbIpt<float> { static constexpr int v = LB_IPT_F32; };
 
-// merge items (rows + nonzeros) per tile: mode 1 (item merge) is fixed by
-// its shared-memory staging arrays; mode 2 (row-parallel) takes 16384
-// (measured best of 2K/8K/16K on the stencils; knob "lb_tile")
-template <typename T>
-inline int lb_tile(int mode) { return mode == 2 ? tuning("lb_tile", 16384) : LB_BLOCK * LbIpt<T>::v; }
+// merge items (rows + nonzeros) per tile of mode 2: 16384 (measured best of
+// 2K/8K/16K on the stencils; knob "lb_tile")
+inline int lb_tile() { return tuning("lb_tile", 16384); }
 
 // merge-path search: returns number of row-end items (rows) consumed at `diag`
 __device__ __forceinline__ int64_t merge_search_global(int64_t diag, const int* rp, int64_t n,
@@ -630,112 +621,6 @@ __global__ void csr_lb_plan_kernel(int64_t n, int64_t nnz, const int* __restrict
     int64_t r = merge_search_global(diag, rp, n, nnz);
     coords[2 * t] = (int)r;
     coords[2 * t + 1] = (int)(diag - r);
-}
-
-template <typename T, bool XIN>
-__global__ void __launch_bounds__(LB_BLOCK)
-csr_lb_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
-              const T* __restrict__ v, const T* __restrict__ b, int64_t bs, T* __restrict__ x,
-              int64_t xs, Coef<T> alpha, Coef<T> beta, const T* __restrict__ xin, int64_t xins,
-              const int* __restrict__ coords, int* __restrict__ carry_row,
-              T* __restrict__ carry_val) {
-    if (alpha.skip()) return;
-    constexpr int IPT = LbIpt<T>::v;
-    constexpr int TILE = LB_BLOCK * IPT;
-    __shared__ int s_rowend[TILE];
-    __shared__ T s_prod[TILE];
-    __shared__ T s_wval[LB_BLOCK / 32];
-    __shared__ int s_wflag[LB_BLOCK / 32];
-
-    const int tile = blockIdx.x;
-    const int r0 = coords[2 * tile], k0 = coords[2 * tile + 1];
-    const int r1 = coords[2 * tile + 2], k1 = coords[2 * tile + 3];
-    const int nrows = r1 - r0, nnzt = k1 - k0;
-    const int tid = threadIdx.x;
-
-    // stage row ends and products (coalesced streams, gathered x)
-    for (int i = tid; i < nrows; i += LB_BLOCK) s_rowend[i] = ld_stream(rp + r0 + 1 + i);
-#pragma unroll 4
-    for (int i = tid; i < nnzt; i += LB_BLOCK) {
-        const int k = k0 + i;
-        s_prod[i] = ld_stream(v + k) * ld_gather(b + (int64_t)ld_stream(ci + k) * bs);
-    }
-    __syncthreads();
-
-    // per-thread merge-path search inside the tile
-    const int items = nrows + nnzt;
-    int diag = tid * IPT;
-    if (diag > items) diag = items;
-    int lo = diag > nnzt ? diag - nnzt : 0, hi = diag < nrows ? diag : nrows;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (s_rowend[mid] <= k0 + diag - mid - 1) lo = mid + 1;
-        else hi = mid;
-    }
-    int tr = lo, tk = diag - lo;
-    const int dend = min(diag + IPT, items);
-
-    const T a = alpha.get();
-    const T bt = XIN ? beta.get() : T(0);
-    T acc = 0, first_val = 0;
-    int first_row = -1;
-    for (int d = diag; d < dend; ++d) {
-        if (tk < nnzt && (tr >= nrows || k0 + tk < s_rowend[tr])) {
-            acc += s_prod[tk];
-            ++tk;
-        } else {
-            if (first_row < 0) {
-                first_row = r0 + tr;
-                first_val = acc;
-            } else {
-                const int64_t row = r0 + tr;
-                T out = a * acc;
-                if (XIN) out += bt * xin[row * xins];
-                x[row * xs] = out;
-            }
-            acc = 0;
-            ++tr;
-        }
-    }
-
-    // block-wide segmented inclusive scan of carry-outs; heads = threads with a close
-    const int lane = tid & 31, wid = tid >> 5;
-    T sv = acc;
-    int sf = first_row >= 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        T vn = __shfl_up_sync(0xffffffffu, sv, o);
-        int fn = __shfl_up_sync(0xffffffffu, sf, o);
-        if (lane >= o) {
-            if (!sf) sv += vn;
-            sf |= fn;
-        }
-    }
-    if (lane == 31) {
-        s_wval[wid] = sv;
-        s_wflag[wid] = sf;
-    }
-    __syncthreads();
-    // exclusive prefix over previous warps
-    T wpre = 0;
-    for (int w = 0; w < wid; ++w) {
-        if (s_wflag[w]) wpre = s_wval[w];
-        else wpre += s_wval[w];
-    }
-    T incl = sf ? sv : sv + wpre;  // inclusive value for this thread
-    T excl = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) excl = wpre;
-    if (tid == 0) excl = 0;
-    if (first_row >= 0) {
-        const int64_t row = first_row;
-        T out = a * (first_val + excl);
-        if (XIN) out += bt * xin[row * xins];
-        x[row * xs] = out;
-    }
-    if (tid == LB_BLOCK - 1) {
-        carry_row[tile] = r1;
-        carry_val[tile] = incl;
-    }
 }
 
 // deterministic fix-up: the first tile of each run of equal carry rows adds the
@@ -899,23 +784,19 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
                   const T* beta_dev, const T* xin, int64_t xins, const int* coords,
                   int* carry_row, T* carry_val, int tile, int mode, void* stream) {
     if (n == 0) return B200SP_OK;
-    B200SP_REQUIRE(mode == 1 || mode == 2, B200SP_EINVAL, "csr lb: mode must be 1 (merge) or 2 (rows), got %d", mode);
-    B200SP_REQUIRE(tile > 0 && (mode == 2 || tile == lb_tile<T>(1)), B200SP_EINVAL,
-                   "csr lb: tile %d does not match mode %d (plan with b200sp_csr_lb_tile)", tile, mode);
+    B200SP_REQUIRE(mode == 2, B200SP_EINVAL, "csr lb: mode must be 2 (row tiles) or 3 (nnz split), got %d", mode);
+    B200SP_REQUIRE(tile > 0, B200SP_EINVAL, "csr lb: tile must be positive (plan with b200sp_csr_lb_tile)");
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int64_t ntiles = ceil_div(n + nnz, tile);
-    if (mode == 2) {
+    {
         // fp64: one entry per step (27-pt 0.686 vs 0.653, 7-pt 0.848 vs 0.804); fp32: 4 (0.620 vs 0.571)
         auto k2 = tuning("lb2_unroll", sizeof(T) == 8 ? 1 : 4) == 4 ? (xin ? csr_lb2_kernel<T, true, true> : csr_lb2_kernel<T, false, true>)
                                                 : (xin ? csr_lb2_kernel<T, true, false> : csr_lb2_kernel<T, false, false>);
         const unsigned g2 = (unsigned)std::min<int64_t>(ntiles, (int64_t)kNumSMs * tuning("lb2_per_sm", 1 << 20));  // one CTA per tile measured best (0.66 vs 0.51 persistent)
         k2<<<g2, LB_BLOCK, 0, st>>>(n, ntiles, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row,
                                     carry_val);
-    } else if (xin)
-        csr_lb_kernel<T, true><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
-    else
-        csr_lb_kernel<T, false><<<(unsigned)ntiles, LB_BLOCK, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row, carry_val);
+    }
     csr_lb_fixup_kernel<T><<<(unsigned)ceil_div(ntiles, 256), 256, 0, st>>>(n, ntiles, carry_row, carry_val, x, xs, al);
     count_launch(2);
     return check_launch("csr_lb");
@@ -1087,98 +968,6 @@ __global__ void __launch_bounds__(COO_BLOCK, 6) coo_kernel_b6(COO_ARGS) {
 #undef COO_ARGS
 #undef COO_PASS
 
-// Entry-interleaved variant ("seg"): lane l of step s takes entry
-// e0 + 32 s + l of the warp's 256-entry chunk, so every load and every x
-// gather of a warp instruction covers 32 consecutive entries (~1 stencil
-// row: a few sectors instead of the ~32 the lane-contiguous layout touches
-// -- ncu: L1TEX 79% busy there). Rows are joined by a shuffle segmented
-// scan per step (keys sorted, so "same row as lane - o" delimits segments)
-// and a warp-uniform carry between steps. Chunking, carries and the fix-up
-// pass are exactly those of the lane-contiguous kernel.
-template <typename T, bool XIN>
-__global__ void __launch_bounds__(COO_BLOCK)
-coo_kernel_seg(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols, const T* __restrict__ vals,
-               const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
-               const T* __restrict__ xin, int64_t xins, T* __restrict__ carry_head, T* __restrict__ carry_tail,
-               int2* __restrict__ chunk_rows) {
-    if (alpha.skip()) return;
-    constexpr int STEPS = 8;
-    constexpr int CHUNK = 32 * STEPS;
-    const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t e0 = c * CHUNK;
-    if (e0 >= nnz) return;
-    const int64_t e1 = min(e0 + (int64_t)CHUNK, nnz);
-    const int head_row = __ldg(rows + e0), tail_row = __ldg(rows + e1 - 1);
-    const bool head_shared = e0 > 0 && __ldg(rows + e0 - 1) == head_row;
-    const bool tail_shared = e1 < nnz && __ldg(rows + e1) == tail_row;
-    const bool single = head_row == tail_row;
-    if (chunk_rows && lane == 0) chunk_rows[c] = make_int2(head_row, tail_row);
-    const T a = alpha.get();
-    const T bt = XIN ? beta.get() : T(0);
-    int rr[STEPS], cc[STEPS];
-    T vv[STEPS];
-#pragma unroll
-    for (int s = 0; s < STEPS; ++s) {
-        const int64_t e = e0 + s * 32 + lane;
-        const bool ok = e < e1;
-        rr[s] = ok ? __ldg(rows + e) : INT_MAX;
-        cc[s] = ok ? __ldg(cols + e) : 0;
-        vv[s] = ok ? __ldg(vals + e) : T(0);
-    }
-#pragma unroll
-    for (int s = 0; s < STEPS; ++s) vv[s] = rr[s] != INT_MAX ? vv[s] * ld_gather(b + (int64_t)cc[s] * bs) : T(0);
-    auto emit = [&](int row, T val) {  // a row completed inside this chunk (not the tail)
-        if (row == head_row && head_shared) {
-            carry_head[c] = val;
-        } else {
-            T out = a * val;
-            if (XIN) out += bt * xin[(int64_t)row * xins];
-            x[(int64_t)row * xs] = out;
-        }
-    };
-    int carry_r = INT_MIN;
-    T carry_v = 0;
-#pragma unroll
-    for (int s = 0; s < STEPS; ++s) {
-        const int r = rr[s];
-        T val = vv[s];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const T vn = __shfl_up_sync(0xffffffffu, val, o);
-            const int rn = __shfl_up_sync(0xffffffffu, r, o);
-            if (lane >= o && rn == r) val += vn;
-        }
-        const int r0 = __shfl_sync(0xffffffffu, r, 0);
-        if (r0 == INT_MAX) break;  // step past the chunk end (warp-uniform)
-        if (carry_r != INT_MIN) {
-            if (r0 == carry_r) {
-                if (r == carry_r) val += carry_v;
-            } else if (lane == 0) {
-                emit(carry_r, carry_v);
-            }
-        }
-        const int rnext = __shfl_down_sync(0xffffffffu, r, 1);
-        const unsigned valid = __ballot_sync(0xffffffffu, r != INT_MAX);
-        const int last = 31 - __clz(valid);
-        const bool end = r != INT_MAX && (lane == last || rnext != r);
-        // the segment ending at the last valid lane continues as the carry
-        carry_r = __shfl_sync(0xffffffffu, r, last);
-        carry_v = __shfl_sync(0xffffffffu, val, last);
-        if (end && lane != last) emit(r, val);
-    }
-    if (lane == 0) {  // the tail row
-        if (!(tail_shared || (single && head_shared))) {
-            T out = a * carry_v;
-            if (XIN) out += bt * xin[(int64_t)tail_row * xins];
-            x[(int64_t)tail_row * xs] = out;
-        } else if (single) {
-            carry_head[c] = carry_v;
-        } else {
-            carry_tail[c] = carry_v;
-        }
-    }
-}
 
 // Carry fix-up: the owner of a row shared by several chunks (the chunk holding
 // the row's first entries) adds the head partials of the chunks that follow
@@ -1527,16 +1316,12 @@ static int coo_spmv(int64_t nnz, int chunk, const int* rows, const int* cols, co
     const unsigned fgrid = (unsigned)ceil_div(nchunks, 256);
     const bool vec = aligned16(rows) && aligned16(cols) && aligned16(vals);
     const int minb = tuning("coo_minb", sizeof(T) == 4 ? 6 : 1);
-    const int seg = tuning("coo_seg", 0) && chunk == 256;
     int2* crows = reinterpret_cast<int2*>(chunk_rows_ws);
     B200SP_REQUIRE(!crows || (reinterpret_cast<uintptr_t>(crows) & 7) == 0, B200SP_EINVAL,
                    "coo: chunk_rows must be 8-byte aligned");
 #define COO_LAUNCH(XI, VE)                                                                                  \
     do {                                                                                                    \
-        if (seg)                                                                                            \
-            coo_kernel_seg<T, XI><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al, be,   \
-                                                              xin, xins, carry_head, carry_tail, crows);    \
-        else if (chunk == 128)                                                                              \
+        if (chunk == 128)                                                                                   \
             coo_kernel<T, XI, VE, 4><<<grid, COO_BLOCK, 0, st>>>(nnz, rows, cols, vals, b, bs, x, xs, al,  \
                                                                     be, xin, xins, carry_head, carry_tail, crows); \
         else if (minb == 6)                                                                                 \
@@ -1838,8 +1623,8 @@ int32_t b200sp_csr_stream_capacity(int32_t value_bytes) {
 }
 
 int32_t b200sp_csr_lb_tile(int32_t value_bytes, int32_t mode) {
-    if (mode == 3) return SEG_CHUNK;
-    return value_bytes == 4 ? lb_tile<float>(mode) : lb_tile<double>(mode);
+    (void)value_bytes;
+    return mode == 3 ? SEG_CHUNK : lb_tile();
 }
 
 int b200sp_csr_seg_plan(int64_t n, int64_t nnz, const int32_t* rp, int32_t* chunk_rows, void* stream) {

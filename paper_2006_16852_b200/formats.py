@@ -381,7 +381,7 @@ class _Sparse(LinOp):
 
 
 #: lazily built per-instance state that must never be shared by clones
-_INSTANCE_CACHES = ("_plan", "_ws", "_pplan", "_hsplan")
+_INSTANCE_CACHES = ("_plan", "_ws", "_pplan")
 
 
 # ---------------------------------------------------------------------------
@@ -514,8 +514,8 @@ class Csr(_Sparse):
         self._stream_stages = int(stream_stages) if stream_stages else None
         self._stream_consumers = int(stream_consumers) if stream_consumers else None
         if lb_mode is not None:
-            if lb_mode not in (1, 2, 3):
-                raise Unsupported("lb_mode must be 1 (item merge), 2 (row-parallel) or 3 (nnz split)")
+            if lb_mode not in (2, 3):
+                raise Unsupported("lb_mode must be 2 (row-parallel tiles) or 3 (nnz split)")
             self._lb_mode = int(lb_mode)
         if stream_impl is not None:
             self._stream_impl = stream_impl
@@ -639,10 +639,10 @@ class Csr(_Sparse):
         return min(cap, need), tpr, rpt, gr
 
     def lb_mode(self):
-        """1 = item-level merge, 2 = row-parallel tiles (stencils: C2 fp64 0.68
-        vs 0.43, 7-point 0.85 vs 0.44; profiles/r02_lb_sweep.txt), 3 = nnz
-        split with Coo-style warp chunks (skewed rows: C3 power law 433 us vs
-        497 us merge, 617 us row-parallel; profiles/r02_c3_lb3.txt)."""
+        """2 = row-parallel merge-path tiles (stencils: C2 fp64 0.70, 7-point
+        0.85), 3 = nnz split with Coo-style warp chunks (skewed rows: C3 power
+        law 404 us vs 617 us row-parallel; profiles/r03_c3_seg.txt). Chosen
+        automatically from the longest row."""
         mode = getattr(self, "_lb_mode", None)
         if mode is None:
             n = self.size.rows
@@ -708,10 +708,7 @@ class Csr(_Sparse):
         self._check_conformal(b, x)
         self._log(EventKind.LINOP_APPLY_STARTED, {"op": type(self).__name__, "uid": self.uid})
         with _PIPELINE_LOCK:  # the plan's device buffers / graphs are shared
-            if self.HOST_STREAM == "kernel":
-                self._host_stream_apply(b, x)
-            else:
-                self._pipelined_apply(b, x)
+            self._pipelined_apply(b, x)
         self._log(EventKind.LINOP_APPLY_COMPLETED, {"op": type(self).__name__, "uid": self.uid})
 
     def _pipeline_ok(self, b, x):
@@ -729,48 +726,10 @@ class Csr(_Sparse):
         # page-locked (a Dense.wrap of a user ndarray on a pinned executor is not)
         return all(torch.from_numpy(np.asarray(v.values).reshape(-1)).is_pinned() for v in (b, x))
 
-    #: "copies": the copy-engine pipeline (chunked H2D / SpMV / D2H in a graph);
-    #: "kernel": one cooperative kernel streams b in, reduces row tiles as their
-    #: columns land and stores x straight to host memory (csrc/hoststream.cu).
-    #: Over PCIe Gen5 the copy engines win (C2: 0.50 vs 0.54 ms; SM loads / stores
-    #: to host memory reach ~40 GB/s per direction vs the engines' 55,
-    #: profiles/r02_e2e_probe.txt); the kernel is the design for hosts whose
-    #: memory the SMs reach over a coherent link
-    HOST_STREAM = "copies"
-    HOST_TILE_BYTES = 8192  # x bytes per consumer tile (1024 fp64 rows)
-
-    def _host_stream_plan(self):
-        plan = getattr(self, "_hsplan", None)
-        if plan is None:
-            n = self.size.rows
-            vb = self._v.element_size()
-            tile = self.HOST_TILE_BYTES // vb
-            chunk = int(_lib.query("csr_host_chunk_elems", vb))
-            dev = self.exec.device
-            ntiles = (n + tile - 1) // tile
-            need = torch.empty(ntiles, dtype=torch.int32, device=dev)
-            _lib.call("csr_tile_chunks", n, ptr(self._rp), ptr(self._ci), tile, chunk, ptr(need),
-                              self.exec.stream)
-            m = self.size.cols
-            plan = {"tile": tile, "need": need, "epoch": 0,
-                    "flags": torch.zeros((m + chunk - 1) // chunk, dtype=torch.int32, device=dev),
-                    "b": torch.empty(max(1, m), dtype=self._v.dtype, device=dev)}
-            self._hsplan = plan
-        return plan
-
-    def _host_stream_apply(self, b, x):
-        P = self._host_stream_plan()
-        P["epoch"] += 1
-        if P["epoch"] >= 2**31 - 1:
-            P["flags"].zero_()
-            P["epoch"] = 1
-        bh = np.asarray(b.values)
-        xh = np.asarray(x.values)
-        suf = _lib.suffix(self._v.dtype)
-        _lib.call("csr_spmv_host_" + suf, self.size.rows, self.size.cols, ptr(self._rp), ptr(self._ci),
-                  ptr(self._v), bh.ctypes.data, ptr(P["b"]), xh.ctypes.data, ptr(P["need"]), P["tile"],
-                  ptr(P["flags"]), P["epoch"], self.subwarp(), self.exec.stream)
-        torch.cuda.current_stream(self.exec.device).synchronize()
+    # (a cooperative kernel streaming b from / x to host memory over PCIe --
+    # SM loads / stores to host memory -- measured slower than the copy
+    # engines: C2 0.54 vs 0.50 ms, profiles/r02_e2e_probe.txt; archived as
+    # tools/hoststream_probe.cu)
 
     def _pipeline_plan(self):
         plan = getattr(self, "_pplan", None)

@@ -124,25 +124,6 @@ class CgSolver(IterativeSolver):
             return finish_from_device(self, S, S.status(), x)
 
         fa = fused_csr(self)
-        if fa is not None and config.CG_FOLD_P:
-            # p = z + beta p folded into the SpMV (no cg_step1 pass): p
-            # alternates between two buffers, so a graph body is two iterations
-            p2 = S.vec("p2")
-
-            def half(pin, pout):
-                _lib.call("csr_spmv_dot_p_" + suf, n, ptr(fa._rp), ptr(fa._ci), ptr(fa._v), ptr(pin), ptr(z),
-                          ptr(pout), ptr(q), fa.subwarp(), S.c, S.p, exc.stream)
-                _lib.call("cg_step2_" + suf, n, ptr(S.x), 1, ptr(r), ptr(pout), ptr(q), ptr(z), *J, S.c, S.p, S.h,
-                          exc.stream)
-
-            def pair():
-                half(p, p2)
-                half(p2, p)
-
-            st = S.run(pair, max(1, batch_size() // 2))
-            finish_from_device(self, S, st, x)
-            return
-
         def body():
             _lib.call("cg_step1_" + suf, n, ptr(p), ptr(z), S.c, exc.stream)
             if fa is not None:  # q = A p and sigma = p.q in one pass

@@ -489,27 +489,6 @@ def test_gmres_rotation_residual_matches_true_residual(cuda):
             assert abs(est[j] - true_r) <= 1e-8 * true_r + 1e-14 * np.linalg.norm(bv), j
 
 
-def test_cg_fold_p_matches_separate_step(cuda, monkeypatch):
-    """The opt-in CG variant that folds p = z + beta p into the fused SpMV
-    (two alternating p buffers, config.CG_FOLD_P) takes the same iterations
-    and produces the same x bit for bit: the folded multiply-add is CgStep1's."""
-    import paper_2006_16852_b200 as b2
-    from paper_2006_16852_b200 import config, problems
-
-    g = 112  # 1.4M rows: above the cooperative-kernel limit, so the batched path runs
-    a = problems.stencil(cuda, "7pt", g)
-    n = g ** 3
-    out = {}
-    for fold in (False, True):
-        monkeypatch.setattr(config, "CG_FOLD_P", fold)
-        s = b2.Cg(cuda, criteria=[b2.Iteration(2000), b2.ResidualNormReduction(1e-8)]).generate(a)
-        x = b2.Dense.zeros(cuda, n, 1)
-        s.apply(b2.Dense(cuda, np.ones((n, 1))), x)
-        out[fold] = (s.last_status.iterations, np.asarray(x.data).copy())
-    assert out[True][0] == out[False][0]
-    np.testing.assert_array_equal(out[True][1], out[False][1])
-
-
 @pytest.mark.parametrize("name", ["Bicgstab", "Cgs", "Fcg"])
 def test_cooperative_small_system_path(cuda, monkeypatch, name):
     """Small unpreconditioned systems run BiCGSTAB / CGS / FCG as one

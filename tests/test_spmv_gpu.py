@@ -20,7 +20,6 @@ TOL = {"float64": 1e-14, "float32": 1e-6}
 FORMATS = [
     ("csr", {"strategy": "classical"}),
     ("csr", {"strategy": "load_balance"}),
-    ("csr", {"strategy": "load_balance", "impl": "lb1"}),
     ("csr", {"strategy": "load_balance", "impl": "lb2"}),
     ("csr", {"strategy": "load_balance", "impl": "lb3"}),
     ("csr", {"strategy": "stream"}),
@@ -37,14 +36,14 @@ FORMATS = [
     ("hybrid", {"strategy": "imbalance"}),
     ("hybrid", {"strategy": "col1"}),
 ]
-IDS = ["csr_classical", "csr_lb", "csr_lb_merge", "csr_lb_rows", "csr_lb_nnz", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
+IDS = ["csr_classical", "csr_lb", "csr_lb_rows", "csr_lb_nnz", "csr_stream", "csr_pipe", "csr_pipe_small", "csr_stream_ld", "csr_pipe_tpr4", "csr_pipe_tpr2", "coo", "ell", "sellp64", "sellp4", "hybrid_auto", "hybrid_imb",
        "hybrid_col1"]
 
 
 def make(b2, exc, data, fmt, kw, dtype="float64"):
     kw = dict(kw)
     impl = kw.pop("impl", None)
-    if impl in ("lb1", "lb2", "lb3"):
+    if impl in ("lb2", "lb3"):
         a = b2.matrix_from_data(exc, data, fmt, value_dtype=dtype, **kw)
         a.set_strategy("load_balance", lb_mode=int(impl[-1]))
         return a
@@ -341,14 +340,14 @@ def test_dense_blas(cuda):
     np.testing.assert_array_equal(np.asarray(y.data), ref * [2.0, -1.0])
 
 
-@pytest.mark.parametrize("knob,val", [("coo_seg", 1), ("coo_minb", 6)])
+@pytest.mark.parametrize("knob,val", [("coo_minb", 6)])
 def test_coo_kernel_variants(cuda, golden_spmv, knob, val):
     """Every Coo kernel variant (b200sp_set_tuning) reproduces the reference,
     including rows spanning many chunks and empty rows."""
     import paper_2006_16852_b200 as b2
     from paper_2006_16852_b200 import _lib
 
-    default = {"coo_seg": 0, "coo_minb": 1}[knob]
+    default = {"coo_minb": 1}[knob]
     _lib.set_tuning(knob, val)
     try:
         for name, g in golden_spmv.items():
@@ -370,16 +369,14 @@ def test_coo_kernel_variants(cuda, golden_spmv, knob, val):
         _lib.set_tuning(knob, default)
 
 
-@pytest.mark.parametrize("mode", ["kernel", "copies"])
 @pytest.mark.parametrize("kind", ["27pt", "random", "odd"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_pipelined_host_apply_bitwise(cuda, host, kind, mode, dtype):
-    """Host operands on a large Csr take the streaming path (the cooperative
-    host-stream kernel, or the chunked copy-engine pipeline); results are
-    bitwise those of the device-resident apply."""
+def test_pipelined_host_apply_bitwise(cuda, host, kind, dtype):
+    """Host operands on a large Csr take the streaming path (the chunked
+    copy-engine pipeline); results are bitwise those of the device-resident
+    apply."""
     import paper_2006_16852_b200 as b2
     from paper_2006_16852_b200 import problems
-    from paper_2006_16852_b200.formats import Csr
 
     if kind == "27pt":
         a = problems.stencil(cuda, "27pt", 64, value_dtype=dtype)
@@ -392,38 +389,58 @@ def test_pipelined_host_apply_bitwise(cuda, host, kind, mode, dtype):
         a = b2.matrix_from_data(cuda, data, "csr", value_dtype=dtype)
     a = b2.convert(a, "csr_classical")  # (fp32 long rows default to the stream strategy)
     n = a.size.rows
-    old = Csr.HOST_STREAM
-    Csr.HOST_STREAM = mode
-    try:
-        assert a._pipeline_ok(b2.Dense(host, np.zeros((n, 1)), value_dtype=dtype),
-                              b2.Dense(host, np.zeros((n, 1)), value_dtype=dtype))
-        bv = np.random.default_rng(1).standard_normal((n, 1))
-        xh = b2.Dense(host, np.full((n, 1), 3.0), value_dtype=dtype)
-        a.apply(b2.Dense(host, bv, value_dtype=dtype), xh)
-        xd = b2.Dense.zeros(cuda, n, 1, value_dtype=dtype)
-        a.apply(b2.Dense(cuda, bv, value_dtype=dtype), xd)
-        np.testing.assert_array_equal(np.asarray(xh.data), np.asarray(xd.data))
-        for f in (2.0, 0.5, 4.0):  # plan, flags (epochs) and buffers reused; exact scalings
-            a.apply(b2.Dense(host, f * bv, value_dtype=dtype), xh)
-            np.testing.assert_array_equal(np.asarray(xh.data), f * np.asarray(xd.data))
-    finally:
-        Csr.HOST_STREAM = old
+    assert a._pipeline_ok(b2.Dense(host, np.zeros((n, 1)), value_dtype=dtype),
+                          b2.Dense(host, np.zeros((n, 1)), value_dtype=dtype))
+    bv = np.random.default_rng(1).standard_normal((n, 1))
+    xh = b2.Dense(host, np.full((n, 1), 3.0), value_dtype=dtype)
+    a.apply(b2.Dense(host, bv, value_dtype=dtype), xh)
+    xd = b2.Dense.zeros(cuda, n, 1, value_dtype=dtype)
+    a.apply(b2.Dense(cuda, bv, value_dtype=dtype), xd)
+    np.testing.assert_array_equal(np.asarray(xh.data), np.asarray(xd.data))
+    for f in (2.0, 0.5, 4.0):  # plan, flags (epochs) and buffers reused; exact scalings
+        a.apply(b2.Dense(host, f * bv, value_dtype=dtype), xh)
+        np.testing.assert_array_equal(np.asarray(xh.data), f * np.asarray(xd.data))
 
 
-def test_host_stream_rejects_pageable(cuda):
-    """The host-stream kernel needs page-locked operands: plain NumPy memory
-    is refused with ParameterError (the Python layer never sends it there)."""
-    from paper_2006_16852_b200 import _lib, problems
-    from paper_2006_16852_b200.errors import ParameterError
-    import torch
+def test_pipeline_refuses_pageable_memory(cuda, host):
+    """The pipelined host apply issues asynchronous copies: it is taken only
+    when both host operands are really page-locked (a Dense.wrap of a plain
+    NumPy array on a pinned host executor is not); otherwise the plain
+    migrate-apply-copy path runs -- same result."""
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import problems
 
-    a = problems.stencil(cuda, "27pt", 16)
+    a = problems.stencil(cuda, "27pt", 64)
     n = a.size.rows
-    P = a._host_stream_plan()
-    b = np.ones(n)
-    x = np.zeros(n)
-    with pytest.raises(ParameterError, match="pinned"):
-        _lib.call("csr_spmv_host_f64", n, n, a._rp.data_ptr(), a._ci.data_ptr(), a._v.data_ptr(), b.ctypes.data,
-                  P["b"].data_ptr(), x.ctypes.data, P["need"].data_ptr(), P["tile"], P["flags"].data_ptr(), 1,
-                  a.subwarp(), a.exec.stream)
-    torch.cuda.synchronize()
+    bv = np.random.default_rng(2).standard_normal((n, 1))
+    pageable = b2.Dense.wrap(host, bv.copy())
+    xh = b2.Dense(host, np.zeros((n, 1)))
+    assert not a._pipeline_ok(pageable, xh)
+    a.apply(pageable, xh)
+    xd = b2.Dense.zeros(cuda, n, 1)
+    a.apply(b2.Dense(cuda, bv), xd)
+    np.testing.assert_array_equal(np.asarray(xh.data), np.asarray(xd.data))
+
+
+def test_clone_gets_its_own_pipeline_plan(cuda, host):
+    """clone_to must not share the source's host-pipeline plan (device
+    staging buffers, streams, CUDA graphs captured against the source's
+    arrays): applying the clone after the source is freed stays correct."""
+    import gc
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import problems
+
+    a = problems.stencil(cuda, "27pt", 48)
+    n = a.size.rows
+    bv = np.random.default_rng(3).standard_normal((n, 1))
+    bh, xh = b2.Dense(host, bv), b2.Dense(host, np.zeros((n, 1)))
+    a.apply(bh, xh)  # builds and caches the source's plan + graph
+    ref = np.asarray(xh.data).copy()
+    c = a.clone_to(cuda)
+    assert getattr(c, "_pplan", None) is None
+    del a
+    gc.collect()
+    xh2 = b2.Dense(host, np.zeros((n, 1)))
+    c.apply(bh, xh2)
+    np.testing.assert_array_equal(np.asarray(xh2.data), ref)
