@@ -418,6 +418,17 @@ int b200sp_gmres_cycle_small_f64(int64_t n, const int32_t* row_ptrs, const int32
                                  double* V, double* w, void* ctl, double* gm, double* hist, void* stream);
 int b200sp_gmres_cycle_small_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
                                  float* V, float* w, void* ctl, double* gm, double* hist, void* stream);
+/* The WHOLE restarted GMRES(k) solve of an unpreconditioned system of n <= 4
+ * rows in one launch (the paper's 1x1 overhead benchmark): cycles, the
+ * back-solve, x += V y, the true residual and the restart, all on chip
+ * (k <= 128), after gmres_reset(first) and gmres_scale_v0 of the initial
+ * residual; x is updated in place. */
+int b200sp_gmres_solve_tiny_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
+                                double* x, const double* b, double* V, double* w, void* ctl, double* gm,
+                                double* hist, int32_t k, void* stream);
+int b200sp_gmres_solve_tiny_f32(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const float* vals,
+                                float* x, const float* b, float* V, float* w, void* ctl, double* gm, double* hist,
+                                int32_t k, void* stream);
 
 /* Csr SpMV q = A p fused with the solver reduction that follows it (sub-warp
  * per row, classical layout): phase 1 = CG sigma = p.q (replaces

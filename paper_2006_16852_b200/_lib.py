@@ -87,6 +87,7 @@ _TYPED = {
     "gmres_normalize": "lipppp",
     "gmres_arnoldi_small": "lipppppp",
     "gmres_cycle_small": "l" + "p" * 9,
+    "gmres_solve_tiny": "l" + "p" * 10 + "ip",
     "gmres_combine": "lppl" + "lpppp" + "ppp",
     # distributed
     "split_fill": "lpppippppppp",

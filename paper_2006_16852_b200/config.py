@@ -24,6 +24,8 @@ SOLVER_BATCH = int(os.environ.get("B200SP_SOLVER_BATCH", "16"))
 CG_COOP_MAX_ROWS = int(os.environ.get("B200SP_CG_COOP_MAX_ROWS", str(1 << 20)))
 # GMRES: one single-block launch per Arnoldi step for systems of <= 4096 rows
 GMRES_SMALL = os.environ.get("B200SP_GMRES_SMALL", "1") != "0"
+# GMRES: systems of <= 4 rows run a whole Arnoldi cycle in one thread, on chip
+GMRES_TINY = os.environ.get("B200SP_GMRES_TINY", "1") != "0"
 # BiCGSTAB and FCG on the same cooperative single-launch path as CG (same row limit)
 BICGSTAB_COOP = os.environ.get("B200SP_BICGSTAB_COOP", "1") != "0"
 

@@ -1396,11 +1396,244 @@ gmres_cycle_small_kernel(int64_t n, const int* __restrict__ rp, const int* __res
     }
 }
 
+// Tiny systems (n <= GMRES_TINY_ROWS, the paper's 1x1 overhead benchmark):
+// a whole Arnoldi cycle AND its back-solve in one launch. Thread 0 runs the
+// cycle -- no cross-lane reduction is worth its shuffles when a dot has at
+// most four terms (the row count is a template constant: every row loop
+// unrolls) -- with the basis, the rotations, gamma and the Hessenberg matrix
+// in shared memory and the control block in a local copy; then the warp
+// back-solves the rotated triangle column by column from shared memory (row
+// i's y_i by its owner lane, broadcast, the other rows' partial sums updated
+// in parallel) instead of a separate kernel paying an L2 round trip per row.
+// Same arithmetic as the single-block kernel (dots accumulated in fp64 in row
+// order; MGS, Givens and the checks of gmres_givens_ctl in the reference's
+// order, gmres.py:88-129); the back-solve sums h[i, i+1:jc] @ y in
+// descending column order (the reference's NumPy dot order is unspecified).
+constexpr int GMRES_TINY_ROWS = 4;
+constexpr int GMRES_TINY_MAXK = 128;
+
+__host__ __device__ inline size_t gmres_tiny_smem(int k, int64_t n, size_t tb) {
+    return ((size_t)(k + 1) * n * tb + 15) / 16 * 16 + ((size_t)(k + 1) * k + 4 * k + 3) * sizeof(double);
+}  // V | cs, sn (k) | g, y (k + 1) | H ((k + 1) x k)
+
+template <typename T, int N>
+__global__ void __launch_bounds__(32)
+gmres_solve_tiny_kernel(const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                        T* __restrict__ xg, const T* __restrict__ bg, T* __restrict__ Vg, T* __restrict__ wg,
+                        KrylovCtl* c, double* gm, double* hist) {
+    extern __shared__ __align__(16) unsigned char gsm[];
+    __shared__ int sh_jc, sh_solve, sh_bd;
+    constexpr int64_t n = N;  // rows, a compile-time constant: every row loop unrolls
+    const int k = c->kdim;
+    const int lane = threadIdx.x;
+    GmresView G(gm, k);
+    T* V = reinterpret_cast<T*>(gsm);
+    double* cs = reinterpret_cast<double*>(gsm + ((size_t)(k + 1) * n * sizeof(T) + 15) / 16 * 16);
+    double* sn = cs + k;
+    double* g = sn + k;
+    double* ys = g + k + 1;
+    double* H = ys + k + 1;  // (k + 1) x k, row-major like the workspace
+    KrylovCtl s;
+    T w[N], x[N], bv[N];
+    if (lane == 0) {
+        s = *c;
+#pragma unroll
+        for (int64_t r = 0; r < n; ++r) {
+            V[r] = Vg[r];  // v_0 from gmres_scale_v0
+            x[r] = xg[r];
+            bv[r] = bg[r];
+        }
+        for (int i = 0; i <= k; ++i) g[i] = G.g[i];
+    }
+    while (true) {
+        // ---- one Arnoldi cycle (thread 0) ----
+        if (lane == 0) {
+            int jdone = 0;
+            for (int j = 1; j <= k; ++j) {
+                if (s.stopped || s.done) break;
+                const T* src = V + (int64_t)(j - 1) * n;
+#pragma unroll
+                for (int64_t r = 0; r < n; ++r) {
+                    T acc = 0;
+                    for (int q = rp[r]; q < rp[r + 1]; ++q) acc += av[q] * src[ci[q]];
+                    w[r] = acc;
+                }
+                // modified Gram-Schmidt: h_i from the current w, then w -= h_i v_i
+                double* __restrict__ hcol = ys;  // scratch for the new column (ys is free during the cycle)
+                // the basis row of step i + 1 is loaded while step i runs (the
+                // loads are off the MGS dependency chain)
+                T vnext[N];
+#pragma unroll
+                for (int64_t r = 0; r < n; ++r) vnext[r] = V[r];
+                for (int i = 0; i < j; ++i) {
+                    T vi[N];
+#pragma unroll
+                    for (int64_t r = 0; r < n; ++r) vi[r] = vnext[r];
+                    if (i + 1 < j) {
+#pragma unroll
+                        for (int64_t r = 0; r < n; ++r) vnext[r] = V[(int64_t)(i + 1) * n + r];
+                    }
+                    double h = 0;
+#pragma unroll
+                    for (int64_t r = 0; r < n; ++r) h += (double)vi[r] * (double)w[r];
+                    hcol[i] = h;
+                    const T th = (T)h;
+#pragma unroll
+                    for (int64_t r = 0; r < n; ++r) w[r] = w[r] - th * vi[r];
+                }
+                double ww = 0;
+#pragma unroll
+                for (int64_t r = 0; r < n; ++r) ww += (double)w[r] * (double)w[r];
+                // Givens update of column j-1 (gmres_givens_ctl): the running
+                // entry stays in a register, each finished entry goes to H
+                const int cl = j - 1;
+                const double hj = sqrt(ww);
+                s.hnorm = hj;
+                double run = hcol[0];
+                double h2n = j > 1 ? hcol[1] : 0.0, csn = cs[0], snn = sn[0];  // prefetched one rotation ahead
+                for (int q = 0; q < j - 1; ++q) {
+                    const double h2 = h2n, cq = csn, sq = snn;
+                    if (q + 2 < j) {
+                        h2n = hcol[q + 2];
+                        csn = cs[q + 1];
+                        snn = sn[q + 1];
+                    }
+                    H[q * k + cl] = cq * run + sq * h2;
+                    run = -sq * run + cq * h2;
+                }
+                const double h1 = run, h2 = hj;
+                const double den = hypot(h1, h2);
+                const double cc = den != 0.0 ? h1 / den : 1.0, sv = den != 0.0 ? h2 / den : 0.0;
+                cs[cl] = cc;
+                sn[cl] = sv;
+                H[cl * k + cl] = den;
+                H[j * k + cl] = 0.0;
+                const double gv = g[cl];
+                g[cl] = cc * gv;
+                g[j] = -sv * gv;
+                s.rnorm = fabs(g[j]);
+                s.jpos = j;
+                s.it += 1;
+                jdone = j;
+                if (hj == 0.0) {  // happy breakdown: declared exact (gmres.py:245-248, :262-268)
+                    s.stopped = 1;
+                    s.stopping_id = EXACT_CONVERGENCE_ID;
+                    s.finalized = 1;
+                    s.rnorm = 0.0;
+                } else if (j < k) {
+                    hist_put(&s, hist, s.it, s.rnorm);
+                    crit_check(&s, s.it, s.rnorm);
+                }
+                if (!s.stopped || s.jpos == j) {  // v_j = w / h_{j,j-1}
+                    T* vj = V + (int64_t)j * n;
+#pragma unroll
+                    for (int64_t r = 0; r < n; ++r) vj[r] = hj == 0.0 ? T(0) : (T)((double)w[r] / hj);
+                }
+            }
+            (void)jdone;
+            // the cycle ends in a commit when stopped or at j == k (gmres_backsolve_kernel's rule)
+            const int jc = s.jpos;
+            const bool solve = !s.done && (s.stopped || jc == k);
+            sh_jc = jc;
+            sh_solve = solve;
+            sh_bd = 0;
+        }
+        __syncwarp();
+        // ---- back-solve of the rotated triangle, column by column (warp) ----
+        if (sh_solve) {
+            const int jc = sh_jc;
+            double acc[GMRES_TINY_MAXK / 32];
+#pragma unroll
+            for (int m = 0; m < GMRES_TINY_MAXK / 32; ++m) acc[m] = 0.0;
+            for (int i = jc - 1; i >= 0; --i) {
+                const double d = H[i * k + i];
+                if (d == 0.0) {  // singular rotated triangle (gmres.py:157-167)
+                    if (lane == 0) sh_bd = 1;
+                    break;
+                }
+                double mine = 0.0;
+#pragma unroll
+                for (int m = 0; m < GMRES_TINY_MAXK / 32; ++m)
+                    if (m == (i >> 5)) mine = acc[m];
+                const double yi = __shfl_sync(0xffffffffu, (g[i] - mine) / d, i & 31);
+                if (lane == (i & 31)) ys[i] = yi;
+#pragma unroll
+                for (int m = 0; m < GMRES_TINY_MAXK / 32; ++m) {
+                    const int r = lane + 32 * m;
+                    if (r < i) acc[m] += H[r * k + i] * yi;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- commit, restart (thread 0): gmres_combine, gmres_after_commit,
+        //      the true residual, gmres_reset and gmres_scale_v0 ----
+        int fin = 0;
+        if (lane == 0) {
+            if (sh_bd) {
+                s.breakdown = BD_HESSENBERG;
+                s.breakdown_it = s.it;
+                s.done = 1;
+            } else if (sh_solve) {
+                const int jc = sh_jc;
+#pragma unroll
+                for (int64_t r = 0; r < n; ++r) {  // x += V y
+                    T u = T(0);
+                    for (int q = 0; q < jc; ++q) u += (T)ys[q] * V[(int64_t)q * n + r];
+                    x[r] += u;
+                }
+                if (s.stopped) s.done = 1;
+            } else if (s.stopped) {
+                s.done = 1;
+            }
+            if (!s.done) {
+#pragma unroll
+                for (int64_t r = 0; r < n; ++r) {  // r = b - A x (the fused residual: -acc + b)
+                    T acc = 0;
+                    for (int q = rp[r]; q < rp[r + 1]; ++q) acc += av[q] * x[ci[q]];
+                    w[r] = -acc + bv[r];
+                }
+                double rr = 0;
+#pragma unroll
+                for (int64_t r = 0; r < n; ++r) rr += (double)w[r] * (double)w[r];
+                const double beta = sqrt(rr);
+                for (int i = 0; i <= k; ++i) g[i] = 0.0;
+                for (int i = 0; i < k; ++i) cs[i] = sn[i] = 0.0;
+                g[0] = beta;
+                s.rnorm = beta;
+                s.jpos = 0;
+                s.committed = 0;
+                hist_put(&s, hist, s.it, s.rnorm);
+                crit_check(&s, s.it, s.rnorm);
+                if (!s.stopped) {
+#pragma unroll
+                    for (int64_t r = 0; r < n; ++r) V[r] = beta == 0.0 ? T(0) : (T)((double)w[r] / beta);
+                }
+            }
+            fin = s.done;
+        }
+        fin = __shfl_sync(0xffffffffu, fin, 0);
+        if (fin) break;
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int64_t r = 0; r < n; ++r) xg[r] = x[r];
+        for (int i = 0; i <= k; ++i) G.g[i] = g[i];
+        s.committed = 0;
+        *c = s;
+    }
+}
+
 // back-solve of the rotated triangular system at jc = jpos (gmres.py:157-167)
 // One warp: row i's dot with y[i+1:jc] (the reference's h[i, i+1:jc] @ y)
 // is spread over the lanes and shuffle-summed -- a single thread's serial
 // sweep is jc^2/2 dependent global loads (~340 us per GMRES(100) cycle).
+// The triangle is first staged in shared memory with coalesced loads when it
+// fits (jc <= GMRES_BS_STAGE): the sweep's dependent steps then read shared
+// memory instead of paying an L2 round trip each (GMRES(100): 64 -> ~10 us).
+constexpr int GMRES_BS_STAGE = 128;
+
 __global__ void gmres_backsolve_kernel(KrylovCtl* c, double* gm) {
+    extern __shared__ double bs_h[];  // GMRES_BS_STAGE^2 (+ GMRES_BS_STAGE for y) doubles
     if (blockIdx.x != 0 || threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     if (c->done || c->committed) return;
@@ -1408,7 +1641,35 @@ __global__ void gmres_backsolve_kernel(KrylovCtl* c, double* gm) {
     const int jc = c->jpos;
     const bool restart = !c->stopped && jc == G.k;
     if (!(c->stopped || restart)) return;
+    const bool staged = jc <= GMRES_BS_STAGE;
+    double* ys = bs_h + GMRES_BS_STAGE * GMRES_BS_STAGE;  // y on chip while solving
+    if (staged) {
+        for (int i = 0; i < jc; ++i)
+            for (int q = i + lane; q < jc; q += 32) bs_h[i * GMRES_BS_STAGE + q] = G.H[i * G.k + q];
+        __syncwarp();
+    }
     for (int i = jc - 1; i >= 0; --i) {
+        if (staged) {
+            const double d = bs_h[i * GMRES_BS_STAGE + i];
+            if (d == 0.0) {
+                if (lane == 0) {
+                    c->breakdown = BD_HESSENBERG;
+                    c->breakdown_it = c->it;
+                    c->done = 1;
+                }
+                return;
+            }
+            double acc = 0.0;
+            for (int q = i + 1 + lane; q < jc; q += 32) acc += bs_h[i * GMRES_BS_STAGE + q] * ys[q];
+            acc = warp_sum(acc);
+            if (lane == 0) {
+                const double yi = (G.g[i] - acc) / d;
+                ys[i] = yi;
+                G.y[i] = yi;
+            }
+            __syncwarp();
+            continue;
+        }
         const double d = G.H[i * G.k + i];
         if (d == 0.0) {
             if (lane == 0) {
@@ -1771,6 +2032,19 @@ const int32_t* b200sp_krylov_guard(const void* ctl, int32_t which) {
         count_launch();                                                                                           \
         return check_launch("gmres_cycle_small");                                                                 \
     }                                                                                                             \
+    int b200sp_gmres_solve_tiny_##SUF(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x,        \
+                                      const T* b, T* V, T* w, void* ctl, double* gm, double* hist, int32_t k,    \
+                                      void* stream) {                                                             \
+        B200SP_REQUIRE(n >= 1 && n <= GMRES_TINY_ROWS && k >= 1 && k <= GMRES_TINY_MAXK, B200SP_EINVAL,          \
+                       "gmres_solve_tiny: n must be 1..%d and k 1..%d", GMRES_TINY_ROWS, GMRES_TINY_MAXK);       \
+        const size_t sm = gmres_tiny_smem(k, n, sizeof(T));                                                      \
+        auto kern = n == 1 ? gmres_solve_tiny_kernel<T, 1> : n == 2 ? gmres_solve_tiny_kernel<T, 2>               \
+                  : n == 3 ? gmres_solve_tiny_kernel<T, 3> : gmres_solve_tiny_kernel<T, 4>;                        \
+        B200SP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));      \
+        kern<<<1, 32, sm, as_stream(stream)>>>(rp, ci, v, x, b, V, w, (KrylovCtl*)ctl, gm, hist);                \
+        count_launch();                                                                                           \
+        return check_launch("gmres_solve_tiny");                                                                  \
+    }                                                                                                             \
     int b200sp_gmres_normalize_##SUF(int64_t n, int32_t j, T* V, const T* w, const void* ctl, void* stream) {     \
         KRY_LAUNCH(gmres_normalize_kernel<T>, n, KRY_BLOCK, n, j, V, w, (const KrylovCtl*)ctl);                   \
     }                                                                                                             \
@@ -1785,7 +2059,13 @@ KRYLOV_T(float, f32)
 int32_t b200sp_gmres_small_rows(void) { return GMRES_SMALL_ROWS; }
 
 int b200sp_gmres_backsolve(void* ctl, double* gm, void* stream) {
-    gmres_backsolve_kernel<<<1, 32, 0, as_stream(stream)>>>((KrylovCtl*)ctl, gm);
+    constexpr int smem = (GMRES_BS_STAGE * GMRES_BS_STAGE + GMRES_BS_STAGE) * (int)sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        B200SP_CHECK_CUDA(cudaFuncSetAttribute(gmres_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    gmres_backsolve_kernel<<<1, 32, smem, as_stream(stream)>>>((KrylovCtl*)ctl, gm);
     count_launch();
     return check_launch("gmres_backsolve");
 }

@@ -67,6 +67,13 @@ class GmresSolver(IterativeSolver):
 
             a = CgSolver._coop_csr(self)
 
+        if whole and config.GMRES_TINY and n <= 4 and k <= 128:
+            # tiny system: the whole restarted solve is one launch (cycles,
+            # back-solve, commit, true residual, restart -- all on chip)
+            _lib.call("gmres_solve_tiny_" + suf, n, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(S.x), ptr(S.b), ptr(V),
+                      ptr(w), S.c, ptr(gm), S.h, k, exc.stream)
+            return finish_from_device(self, S, S.status(), x)
+
         def cycle():
             _lib.query("set_guard", stopped_guard)
             if whole:  # the whole Arnoldi cycle in one single-block launch

@@ -76,7 +76,21 @@ def solvers(b2, exc):
                 res = np.linalg.norm(bv[:, 0] - dense @ np.asarray(x.data)[:, 0]) / np.linalg.norm(bv)
                 assert s.last_status.converged and res < 1e-7, (name, pre, s.last_status, res)
                 print(f"solver {name} {kind} pre={pre} it={s.last_status.iterations} ok", flush=True)
-    # GMRES above the single-block limit (batched Arnoldi kernels) and CG above the cooperative limit
+    # GMRES at <= 2048 rows: the single-block Arnoldi step (with block-Jacobi)
+    # and the whole-cycle single-block kernel (unpreconditioned, basis on chip)
+    a = problems.stencil(exc, "convdiff", 10)
+    for pre in (None, 32):
+        s = b2.Gmres(exc, criteria=crit, krylov_dim=25,
+                     preconditioner=b2.Jacobi(exc, block_size=pre) if pre else None).generate(a)
+        x = b2.Dense.zeros(exc, a.size.rows, 1)
+        s.apply(b2.Dense(exc, np.ones((a.size.rows, 1))), x)
+        assert s.last_status.converged, s.last_status
+    a = problems.stencil(exc, "convdiff", 4)  # 64 rows: the one-warp on-chip cycle
+    s = b2.Gmres(exc, criteria=crit, krylov_dim=10).generate(a)
+    x = b2.Dense.zeros(exc, 64, 1)
+    s.apply(b2.Dense(exc, np.ones((64, 1))), x)
+    assert s.last_status.converged
+        # GMRES above the single-block limit (batched Arnoldi kernels) and CG above the cooperative limit
     a = problems.stencil(exc, "convdiff", 24)
     s = b2.Gmres(exc, criteria=crit, krylov_dim=20).generate(a)
     x = b2.Dense.zeros(exc, a.size.rows, 1)
