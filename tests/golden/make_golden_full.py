@@ -86,15 +86,53 @@ class _HistoryFactory(CriterionFactory):
         return _History(self.rows, self.t0)
 
 
+def csr_7pt(g):
+    """The 7-point Poisson CSR (canonical order, int32 indices) built plane by
+    plane -- the same matrix as oracle/problems.stencil3d(g, "7pt") without the
+    22.5 GB of int64 triples MatrixData would hold at 512^3."""
+    n = g ** 3
+    p2 = g * g
+    jj, kk = np.divmod(np.arange(p2, dtype=np.int64), g)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    for i in range(g):
+        lens = (1 + (i > 0) + (i < g - 1) + (jj > 0) + (jj < g - 1) + (kk > 0) + (kk < g - 1)).astype(np.int64)
+        np.cumsum(lens, out=rp[i * p2 + 1:(i + 1) * p2 + 1])
+        rp[i * p2 + 1:(i + 1) * p2 + 1] += rp[i * p2]
+    nnz = int(rp[-1])
+    ci = np.empty(nnz, dtype=np.int32)
+    vals = np.empty(nnz, dtype=np.float64)
+    offs = np.array([-p2, -g, -1, 0, 1, g, p2], dtype=np.int64)
+    cvals = np.array([-1.0, -1.0, -1.0, 6.0, -1.0, -1.0, -1.0])
+    for i in range(g):
+        rows = i * p2 + np.arange(p2, dtype=np.int64)
+        keep = np.stack([np.full(p2, i > 0), jj > 0, kk > 0, np.ones(p2, bool), kk < g - 1, jj < g - 1,
+                         np.full(p2, i < g - 1)], axis=1)
+        cols = rows[:, None] + offs[None, :]
+        lo, hi = rp[i * p2], rp[(i + 1) * p2]
+        ci[lo:hi] = cols[keep]
+        vals[lo:hi] = np.broadcast_to(cvals, (p2, 7))[keep]
+    return rp.astype(np.int32), ci, vals
+
+
 def run(name):
     g, kind, solver, bs, kw = CASES[name]
     t0 = time.time()
     exc = opalg.ParallelExecutor(int(os.environ.get("GOLDEN_WORKERS", os.cpu_count())))
-    n, r, c, v = P.stencil3d(g, kind)
-    data = MatrixData(Dim2(n, n), r, c, v)
-    del r, c, v
-    a = Csr.from_data(exc, data)
-    del data
+    if kind == "7pt" and g >= 512:  # lean build (the reference's own Csr constructor)
+        rp8, ci8, v8 = csr_7pt(8)
+        n8, r8, c8, vv8 = P.stencil3d(8, "7pt")
+        rpo, cio, vo = P.to_csr(n8, r8, c8, vv8)
+        assert np.array_equal(rp8, rpo) and np.array_equal(ci8, cio) and np.array_equal(v8, vo)
+        rp, ci, vals = csr_7pt(g)
+        n = g ** 3
+        a = Csr(exc, Dim2(n, n), rp, ci, vals)
+        del rp, ci, vals
+    else:
+        n, r, c, v = P.stencil3d(g, kind)
+        data = MatrixData(Dim2(n, n), r, c, v)
+        del r, c, v
+        a = Csr.from_data(exc, data)
+        del data
     print(f"{name}: n={n} nnz={a.col_idxs.size} matrix ready ({time.time() - t0:.0f} s)", flush=True)
     hist = _HistoryFactory(t0)
     crits = [Iteration(10000), ResidualNormReduction(1e-8), hist]
