@@ -539,13 +539,18 @@ int64_t b200sp_krylov_red_offset(void);
  * epoch (acquire) -- order the ghost SpMV after it. Both skip when the
  * solve is done. At most b200sp_peer_max() puts, twice that many waits. */
 int32_t b200sp_peer_max(void);
+/* epoch_dev (nullable): a device int32 holding the last epoch -- the kernels
+ * then take epoch = *epoch_dev + 1 (put, all-reduce) / *epoch_dev (wait) and
+ * advance it themselves, so the sequence can be captured in a CUDA graph and
+ * replayed; `epoch` is ignored then. */
 int b200sp_cg_step1_put_f64(int64_t n, double* p, const double* z, const void* ctl, int32_t nput, const int64_t* lo,
                             const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,
-                            uint32_t* ticket, void* stream);
+                            uint32_t* ticket, int32_t* epoch_dev, void* stream);
 int b200sp_cg_step1_put_f32(int64_t n, float* p, const float* z, const void* ctl, int32_t nput, const int64_t* lo,
                             const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,
-                            uint32_t* ticket, void* stream);
-int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream);
+                            uint32_t* ticket, int32_t* epoch_dev, void* stream);
+int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, const int32_t* epoch_dev,
+                     void* stream);
 /* All-reduce (sum) of red[0..k), k <= 4, across `world` <= 8 ranks through
  * peer memory: slots[j] = rank j's slot array (2 * world * 4 doubles, zeroed
  * once; mapped), flags[j] = rank j's int32 flag array (world entries, zeroed
@@ -553,7 +558,7 @@ int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int3
  * identical on every rank. One thread; replaces the 8-32 byte NCCL
  * all-reduces of the distributed CG. */
 int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, double* const* slots,
-                          int32_t* const* flags, int32_t epoch, void* stream);
+                          int32_t* const* flags, int32_t epoch, int32_t* epoch_dev, void* stream);
 /* Spins on peer flags are bounded by b200sp_set_tuning("peer_timeout_ms", ms)
  * (default 30000): peer_wait then marks the solve broken down (code 6),
  * peer_allreduce returns NaN sums.

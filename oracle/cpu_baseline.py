@@ -17,13 +17,31 @@ from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
-from . import spmv as OS
+
+
+def csr_row_sums(vals, col_idxs, row_ptrs, b, lo, hi):
+    """src/kernels.py:304-316 restated statement by statement (the same NumPy
+    calls on the same dtypes: int32 row pointers and indices)."""
+    e0, e1 = int(row_ptrs[lo]), int(row_ptrs[hi])
+    out = np.zeros((hi - lo, b.shape[1]), dtype=b.dtype)
+    if e0 == e1:
+        return out
+    prod = vals[e0:e1, None] * b[col_idxs[e0:e1]]
+    counts = np.diff(row_ptrs[lo:hi + 1])
+    nonempty = np.flatnonzero(counts > 0)
+    starts = row_ptrs[lo + nonempty] - e0
+    out[nonempty] = np.add.reduceat(prod, starts.astype(np.intp), axis=0)
+    return out
 
 
 class ParallelCsr:
+    """ParallelExecutor.map_blocks (src/executor.py:181-200) around
+    CsrSpmvKernel._run (src/kernels.py:285-293): `x[lo:hi] = csr_row_sums(...)`
+    per contiguous row block on a thread pool of os.cpu_count() workers."""
+
     def __init__(self, rp, ci, vals, workers=None):
-        self.rp = np.asarray(rp, dtype=np.int64)
-        self.ci = np.asarray(ci)
+        self.rp = np.asarray(rp, dtype=np.int32)  # config.DEFAULT_INDEX_DTYPE
+        self.ci = np.asarray(ci, dtype=np.int32)
         self.vals = np.asarray(vals)
         self.n = self.rp.size - 1
         self.workers = workers or os.cpu_count() or 1
@@ -33,8 +51,7 @@ class ParallelCsr:
         self.pool = ThreadPoolExecutor(max_workers=len(self.blocks)) if len(self.blocks) > 1 else None
 
     def _block(self, lo, hi, b, out):
-        e0, e1 = self.rp[lo], self.rp[hi]
-        out[lo:hi] = OS.csr_spmv(self.rp[lo:hi + 1] - e0, self.ci[e0:e1], self.vals[e0:e1], b)
+        out[lo:hi] = csr_row_sums(self.vals, self.ci, self.rp, b, lo, hi)
 
     def apply(self, b, out):
         if self.pool is None:

@@ -62,7 +62,7 @@ _TYPED = {
     # Krylov (JAC = l p p p p)
     "cg_init": "lppp" + "lpppp" + "pppp",
     "cg_step1": "lpppp",
-    "cg_step1_put": "lpppippppipp",
+    "cg_step1_put": "lpppippppippp",
     "cg_sigma": "lppppp",
     "cg_coop": "lpppppppppppp",
     "bicgstab_coop": "lpppppppppppppp",
@@ -117,8 +117,8 @@ _UNTYPED = {
     "csr_seg_plan": ("llppp", ctypes.c_int),
     "peer_max": ("", ctypes.c_int32),
     "gmres_small_rows": ("", ctypes.c_int32),
-    "peer_wait": ("pipip", ctypes.c_int),
-    "peer_allreduce": ("piiippip", ctypes.c_int),
+    "peer_wait": ("pipipp", ctypes.c_int),
+    "peer_allreduce": ("piiippipp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),
     "coo_to_csr_ptrs": ("llppp", ctypes.c_int),

@@ -36,3 +36,6 @@ FUSED_SPMV_DOT = os.environ.get("B200SP_FUSED_SPMV_DOT", "1") != "0"
 # send is a row range, "1" = force it (also over gloo: ranks sharing one GPU),
 # "0" = NCCL send/recv
 PEER_HALO = os.environ.get("B200SP_PEER_HALO", "auto")
+# distributed CG: capture a batch of iterations as a CUDA graph when the halo
+# and the all-reduces both go through peer memory (no host collective inside)
+DIST_GRAPH = os.environ.get("B200SP_DIST_GRAPH", "1") != "0"

@@ -122,8 +122,11 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
 template <typename T>
 __global__ void __launch_bounds__(256)
 cg_step1_put_kernel(int64_t n, T* __restrict__ p, const T* __restrict__ z, const KrylovCtl* c, PeerPut pp,
-                    int epoch, unsigned* ticket) {
+                    int epoch, unsigned* ticket, int* epoch_dev) {
     if (c->done) return;
+    // device-managed epoch (CUDA-graph replays): this launch's = stored + 1,
+    // published by the last CTA once every CTA has read the old value
+    if (epoch_dev) epoch = *(volatile int*)epoch_dev + 1;
     const T beta = (T)c->beta;
     bool wrote = false;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -145,6 +148,7 @@ cg_step1_put_kernel(int64_t n, T* __restrict__ p, const T* __restrict__ z, const
             __threadfence_system();
             *ticket = 0;
             for (int k = 0; k < pp.n; ++k) st_release_sys(pp.flag[k], epoch);
+            if (epoch_dev) *epoch_dev = epoch;
         }
     }
 }
@@ -176,7 +180,9 @@ __device__ __forceinline__ bool spin_until(const int* flag, int epoch, unsigned 
     return true;
 }
 
-__global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch, unsigned long long timeout_ns) {
+__global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch, unsigned long long timeout_ns,
+                                      int* epoch_dev) {
+    if (epoch_dev) epoch = *epoch_dev + 1;
     const int par = epoch & 1;
     double v[4];
     for (int i = 0; i < k; ++i) v[i] = red[i];
@@ -199,10 +205,13 @@ __global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch,
         for (int j = 0; j < pr.world; ++j) s += sl[j * 4 + i];
         red[i] = s;
     }
+    if (epoch_dev) *epoch_dev = epoch;
 }
 
-__global__ void peer_wait_kernel(KrylovCtl* c, PeerWait w, int epoch, unsigned long long timeout_ns) {
+__global__ void peer_wait_kernel(KrylovCtl* c, PeerWait w, int epoch, unsigned long long timeout_ns,
+                                 const int* epoch_dev) {
     if (c->done) return;
+    if (epoch_dev) epoch = *(volatile const int*)epoch_dev;  // this rank's put of the same step published it
     const unsigned long long deadline = global_ns() + timeout_ns;
     for (int k = 0; k < w.n; ++k)
         if (!spin_until(w.flag[k], epoch, deadline, 256)) {
@@ -275,10 +284,10 @@ int32_t b200sp_peer_max(void) { return PEER_MAX; }
 #define PEER_PUT_DEF(SUF, T)                                                                                  \
     int b200sp_cg_step1_put_##SUF(int64_t n, T* p, const T* z, const void* ctl, int32_t nput, const int64_t* lo, \
                                   const int64_t* hi, void* const* dst, int32_t* const* flag, int32_t epoch,     \
-                                  uint32_t* ticket, void* stream) {                                             \
+                                  uint32_t* ticket, int32_t* epoch_dev, void* stream) {                         \
         B200SP_REQUIRE(nput >= 0 && nput <= PEER_MAX, B200SP_EINVAL, "cg_step1_put: at most %d peers (got %d)", \
                        PEER_MAX, nput);                                                                         \
-        B200SP_REQUIRE(epoch > 0, B200SP_EINVAL, "cg_step1_put: epoch must be positive");                       \
+        B200SP_REQUIRE(epoch > 0 || epoch_dev, B200SP_EINVAL, "cg_step1_put: epoch must be positive");         \
         if (n <= 0) return B200SP_OK;                                                                           \
         PeerPut pp{};                                                                                           \
         pp.n = nput;                                                                                            \
@@ -289,7 +298,7 @@ int32_t b200sp_peer_max(void) { return PEER_MAX; }
             pp.flag[k] = flag[k];                                                                               \
         }                                                                                                       \
         cg_step1_put_kernel<T><<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(n, p, z, (const KrylovCtl*)ctl, \
-                                                                                    pp, epoch, ticket);         \
+                                                                                    pp, epoch, ticket, epoch_dev); \
         count_launch();                                                                                         \
         return check_launch("cg_step1_put");                                                                    \
     }
@@ -298,11 +307,11 @@ PEER_PUT_DEF(f32, float)
 #undef PEER_PUT_DEF
 
 int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, double* const* slots,
-                          int32_t* const* flags, int32_t epoch, void* stream) {
+                          int32_t* const* flags, int32_t epoch, int32_t* epoch_dev, void* stream) {
     B200SP_REQUIRE(k >= 1 && k <= 4, B200SP_EINVAL, "peer_allreduce: 1..4 values (got %d)", k);
     B200SP_REQUIRE(world >= 1 && world <= PEER_RED_MAX && rank >= 0 && rank < world, B200SP_EINVAL,
                    "peer_allreduce: world must be 1..%d (got %d, rank %d)", PEER_RED_MAX, world, rank);
-    B200SP_REQUIRE(epoch > 0, B200SP_EINVAL, "peer_allreduce: epoch must be positive");
+    B200SP_REQUIRE(epoch > 0 || epoch_dev, B200SP_EINVAL, "peer_allreduce: epoch must be positive");
     PeerRed pr{};
     pr.world = world;
     pr.rank = rank;
@@ -310,19 +319,20 @@ int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, d
         pr.slots[j] = slots[j];
         pr.flags[j] = flags[j];
     }
-    peer_allreduce_kernel<<<1, 1, 0, as_stream(stream)>>>(red, k, pr, epoch, peer_timeout_ns());
+    peer_allreduce_kernel<<<1, 1, 0, as_stream(stream)>>>(red, k, pr, epoch, peer_timeout_ns(), epoch_dev);
     count_launch();
     return check_launch("peer_allreduce");
 }
 
-int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, void* stream) {
+int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, const int32_t* epoch_dev,
+                     void* stream) {
     B200SP_REQUIRE(nwait >= 0 && nwait <= 2 * PEER_MAX, B200SP_EINVAL, "peer_wait: at most %d flags (got %d)",
                    2 * PEER_MAX, nwait);
     if (nwait == 0) return B200SP_OK;
     PeerWait w{};
     w.n = nwait;
     for (int k = 0; k < nwait; ++k) w.flag[k] = flags[k];
-    peer_wait_kernel<<<1, 1, 0, as_stream(stream)>>>((KrylovCtl*)ctl, w, epoch, peer_timeout_ns());
+    peer_wait_kernel<<<1, 1, 0, as_stream(stream)>>>((KrylovCtl*)ctl, w, epoch, peer_timeout_ns(), epoch_dev);
     count_launch();
     return check_launch("peer_wait");
 }

@@ -378,7 +378,9 @@ class PeerHalo:
         waits = [self.flags.data_ptr() + 4 * int(peer) for peer, _, _ in A.plan.recv]
         self.nwait = len(waits)
         self.waits = (ctypes.c_void_p * max(self.nwait, 1))(*waits)
-        self.epoch = 0
+        # the halo epoch lives on the device: the put kernel advances it, so a
+        # captured CUDA graph of the iteration replays with fresh epochs
+        self.epoch_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         torch.cuda.synchronize(dev)
 
     @staticmethod
@@ -395,13 +397,12 @@ class PeerHalo:
 
     def step1(self, nl, p, z, ctl, suf, stream):
         """p = z + beta p, boundary rows stored into the peers' ghost slots."""
-        self.epoch += 1
         _lib.call("cg_step1_put_" + suf, nl, ptr(p), ptr(z), ctl, self.nput, ctypes.addressof(self.lo),
-                  ctypes.addressof(self.hi), ctypes.addressof(self.dst), ctypes.addressof(self.flag), self.epoch,
-                  ptr(self.ticket), stream)
+                  ctypes.addressof(self.hi), ctypes.addressof(self.dst), ctypes.addressof(self.flag), 0,
+                  ptr(self.ticket), ptr(self.epoch_dev), stream)
 
     def wait(self, ctl, stream):
-        _lib.call("peer_wait", ctl, self.nwait, ctypes.addressof(self.waits), self.epoch, stream)
+        _lib.call("peer_wait", ctl, self.nwait, ctypes.addressof(self.waits), 0, ptr(self.epoch_dev), stream)
 
 
 class PeerReduce:
@@ -432,14 +433,13 @@ class PeerReduce:
             fl.append(tf)
         self.sl = (ctypes.c_void_p * w)(*sl)
         self.fl = (ctypes.c_void_p * w)(*fl)
-        self.epoch = 0
+        self.epoch_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # advanced by the kernel
         torch.cuda.synchronize(dev)
 
     def allreduce_(self, t, stream):
         """Sum a float64 device tensor of 1..4 values across the ranks, in place."""
-        self.epoch += 1
         _lib.call("peer_allreduce", ptr(t), t.numel(), self.world, self.rank, ctypes.addressof(self.sl),
-                  ctypes.addressof(self.fl), self.epoch, stream)
+                  ctypes.addressof(self.fl), 0, ptr(self.epoch_dev), stream)
 
 
 # ---------------------------------------------------------------------------
@@ -486,6 +486,8 @@ class DistCg:
         self.part = torch.zeros(int(_lib.query("krylov_part_elems")), dtype=torch.float64, device=dev)
         self._red_off = int(_lib.query("krylov_red_offset"))
         self.halo = self.reduce = None
+        self._bufs = {}
+        self._graphs = {}
 
     def _jac(self):
         return self.precond.jac_args() if self.precond is not None else (0, 0, 0, 0, 0)
@@ -581,9 +583,13 @@ class DistCg:
         _lib.call("krylov_set_dist", c, 1, exc.stream)
         red_t = ctl[self._red_off:self._red_off + 32].view(torch.float64)
         J = self._jac()
-        r = torch.empty(nl, dtype=dt, device=exc.device)
-        q = torch.empty(nl, dtype=dt, device=exc.device)
-        z = r if J[0] == 0 else torch.empty(nl, dtype=dt, device=exc.device)
+        bufs = self._bufs.get(dt)
+        if bufs is None:  # kept across solves: a captured graph refers to them
+            r = torch.empty(nl, dtype=dt, device=exc.device)
+            q = torch.empty(nl, dtype=dt, device=exc.device)
+            z = r if J[0] == 0 else torch.empty(nl, dtype=dt, device=exc.device)
+            bufs = self._bufs[dt] = (r, q, z)
+        r, q, z = bufs
         peer, pext, red = self._comm_paths(dt)
         k_check = 4 if self.timed else 2  # + the summed "time limit reached" flags
 
@@ -600,25 +606,53 @@ class DistCg:
         allreduce(k_check)
         _lib.call("cg_finish", c, hist, 0, exc.stream)
         guard = int(_lib.query("krylov_guard", c, 0))
+
+        def iteration():
+            if peer is not None:
+                peer.step1(nl, p, z, c, suf, exc.stream)
+                self._spmv_sigma_peer(peer, pext, p, q, c, pp, suf)
+            else:
+                _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(z), c, exc.stream)
+                self._spmv_sigma(pext, p, q, c, pp, suf)
+            allreduce(1)
+            _lib.call("cg_finish", c, hist, 1, exc.stream)
+            _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(z), *J, c, ptr(pp),
+                      hist, exc.stream)
+            allreduce(k_check)
+            _lib.call("cg_finish", c, hist, 2, exc.stream)
+
+        # with the peer halo AND the peer all-reduce an iteration is kernels
+        # only (device-managed epochs): a batch is captured once as a CUDA
+        # graph and replayed -- no per-kernel Python launch cost per iteration
+        graphed = peer is not None and red is not None and config.DIST_GRAPH
         _lib.query("set_guard", guard)
         try:
-            while True:
-                iv, _ = self._status(c, exc.stream)
-                if iv[4]:
-                    break
-                for _ in range(self.batch):
-                    if peer is not None:
-                        peer.step1(nl, p, z, c, suf, exc.stream)
-                        self._spmv_sigma_peer(peer, pext, p, q, c, pp, suf)
-                    else:
-                        _lib.call("cg_step1_" + suf, nl, ptr(p), ptr(z), c, exc.stream)
-                        self._spmv_sigma(pext, p, q, c, pp, suf)
-                    allreduce(1)
-                    _lib.call("cg_finish", c, hist, 1, exc.stream)
-                    _lib.call("cg_step2_" + suf, nl, ptr(x), 1, ptr(r), ptr(p), ptr(q), ptr(z), *J, c, ptr(pp),
-                              hist, exc.stream)
-                    allreduce(k_check)
-                    _lib.call("cg_finish", c, hist, 2, exc.stream)
+            if graphed:
+                key = (dt, c, ptr(x), ptr(pp), hist, ptr(r))
+                g = self._graphs.get(key)
+                while True:
+                    iv, _ = self._status(c, exc.stream)
+                    if iv[4]:
+                        break
+                    if g is None:
+                        iteration()  # eager first (lazily built plans); the graph starts after it
+                        iv, _ = self._status(c, exc.stream)
+                        if iv[4]:
+                            break
+                        g = torch.cuda.CUDAGraph()
+                        torch.cuda.synchronize(exc.device)
+                        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                            for _ in range(self.batch):
+                                iteration()
+                        self._graphs = {key: g}
+                    g.replay()
+            else:
+                while True:
+                    iv, _ = self._status(c, exc.stream)
+                    if iv[4]:
+                        break
+                    for _ in range(self.batch):
+                        iteration()
         finally:
             _lib.query("set_guard", 0)
 
