@@ -145,7 +145,11 @@ __device__ bool grid_reduce(double (&v)[NV], double* part, unsigned* ticket, dou
 
 inline int kry_grid(int64_t units, int per_block) {
     int64_t g = ceil_div(units, per_block);
-    if (g > KRY_MAX_GRID) g = KRY_MAX_GRID;
+    // knob "kry_grid_div": fewer reduction blocks (a different, equally valid
+    // summation partition -- used to measure the solvers' rounding sensitivity)
+    const int div = tuning("kry_grid_div", 1);
+    const int64_t cap = KRY_MAX_GRID / (div > 1 ? div : 1);
+    if (g > cap) g = cap;
     if (g < 1) g = 1;
     return (int)g;
 }
