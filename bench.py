@@ -382,9 +382,10 @@ def bench_c2_dist(args, world, rank, local):
     stencil on 128 x 128 x (128 N) -- each rank owns exactly one C2-sized
     slab (2,097,152 rows, z-planes [128 r, 128 r + 128)) -- so per-GPU work
     is C2's and the curve measures the distributed path: the 2-plane halo
-    (NCCL send/recv; gloo host staging when ranks share a GPU) overlapped
-    with the owned-block SpMV, then the ghost-block accumulate
-    (DistCsr.apply_ext). value = all ranks' algorithmic Csr bytes / the
+    (peer-memory puts gated by the neighbours' acks when every pair of GPUs
+    has P2P access -- the whole step one CUDA graph; NCCL send/recv, or gloo
+    host staging when ranks share a GPU without the peer path, otherwise)
+    overlapped with the owned-block SpMV, then the ghost-block accumulate. value = all ranks' algorithmic Csr bytes / the
     max-over-ranks step time; e2e adds each rank's pinned H2D of its x slice
     and D2H of its y slice."""
     import torch
@@ -402,11 +403,26 @@ def bench_c2_dist(args, world, rank, local):
     nnz_l = A.a_own.nnz + (A.a_ghost.nnz if A.a_ghost is not None else 0)
     # x ~ N(0,1): this rank's slice of one global seeded vector (per-plane seeds)
     xh = np.random.default_rng(rank).standard_normal(nl)
-    xext = torch.zeros(A.n_ext, dtype=torch.float64, device=exc.device)
-    xext[:nl].copy_(torch.from_numpy(xh))
     y = torch.empty(nl, dtype=torch.float64, device=exc.device)
     timer = Timer(exc)
-    step = lambda: A.apply_ext(xext, y)  # noqa: E731
+    peer = A.peer(torch.float64)  # collective: peer-memory halo when every pair of GPUs has P2P access
+    if peer is not None:
+        # put / owned SpMV / wait / ghost SpMV / ack: kernels only, one CUDA graph per step
+        xext = peer.pext
+        xext[:nl].copy_(torch.from_numpy(xh))
+        peer.apply_spmv(y, exc.stream)  # eager once (plans, workspaces)
+        torch.cuda.synchronize()
+        barrier(world)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            peer.apply_spmv(y, exc.stream)
+        step = graph.replay
+        halo = "peer memory (CUDA IPC over NVLink), CUDA graph per step"
+    else:
+        xext = torch.zeros(A.n_ext, dtype=torch.float64, device=exc.device)
+        xext[:nl].copy_(torch.from_numpy(xh))
+        step = lambda: A.apply_ext(xext, y)  # noqa: E731
+        halo = "NCCL send/recv" if BACKEND == "nccl" else "gloo (host-staged)"
     # algorithmic bytes of this rank's rows (Csr formula) + the ghost x values it reads
     by = bytes_csr(nl, nnz_l, 8) + (A.n_ext - nl) * 8
     with ClockSampler(local) as clk:
@@ -456,7 +472,7 @@ def bench_c2_dist(args, world, rank, local):
                    "format": "csr", "rows": nl * world, "rows_per_rank": nl,
                    "parallelism": f"row partition x{world} ({BACKEND}"
                                   f"{', ranks share GPUs' if BACKEND == 'gloo' else ''})",
-                   "halo_bytes_per_rank": halo_bytes,
+                   "halo_bytes_per_rank": halo_bytes, "halo": halo,
                    "l2": "inputs larger than L2 and L2 flushed (256 MiB write, then read back) between steps"},
         "gflops": round(2 * allsum(world, nnz_l) / t_step / 1e9, 1),
         "roofline": {"bound": "hbm", "achieved": round(by_own / t_own / 1e9, 1), "peak": peak, "unit": "GB/s",

@@ -559,6 +559,21 @@ int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int3
  * all-reduces of the distributed CG. */
 int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, double* const* slots,
                           int32_t* const* flags, int32_t epoch, int32_t* epoch_dev, void* stream);
+/* The plain distributed SpMV through peer memory: peer_put copies local rows
+ * [lo[k], hi[k]) of the owned x into dst[k] (a destination's ghost slots)
+ * once every destination has acknowledged the previous epoch (ack_in[k]: the
+ * destination's ack of this rank, in THIS rank's ack array), then raises
+ * flag[k] = epoch (device-managed *epoch_dev + 1); peer_wait_plain waits for
+ * the sources' flags of *epoch_dev; peer_ack (after the ghost SpMV) raises
+ * ack_out[k] = *epoch_dev in every source's ack array. */
+int b200sp_peer_put_f64(const double* x_owned, int32_t nput, const int64_t* lo, const int64_t* hi, void* const* dst,
+                        int32_t* const* flag, int32_t nack, const int32_t* const* ack_in, int32_t* epoch_dev,
+                        uint32_t* ticket, void* stream);
+int b200sp_peer_put_f32(const float* x_owned, int32_t nput, const int64_t* lo, const int64_t* hi, void* const* dst,
+                        int32_t* const* flag, int32_t nack, const int32_t* const* ack_in, int32_t* epoch_dev,
+                        uint32_t* ticket, void* stream);
+int b200sp_peer_ack(int32_t nack, const int32_t* const* ack_out, const int32_t* epoch_dev, void* stream);
+int b200sp_peer_wait_plain(int32_t nwait, const int32_t* const* flags, const int32_t* epoch_dev, void* stream);
 /* Spins on peer flags are bounded by b200sp_set_tuning("peer_timeout_ms", ms)
  * (default 30000): peer_wait then marks the solve broken down (code 6),
  * peer_allreduce returns NaN sums.

@@ -63,6 +63,7 @@ _TYPED = {
     "cg_init": "lppp" + "lpppp" + "pppp",
     "cg_step1": "lpppp",
     "cg_step1_put": "lpppippppippp",
+    "peer_put": "pippppipppp",
     "cg_sigma": "lppppp",
     "cg_coop": "lpppppppppppp",
     "bicgstab_coop": "lpppppppppppppp",
@@ -118,6 +119,8 @@ _UNTYPED = {
     "peer_max": ("", ctypes.c_int32),
     "gmres_small_rows": ("", ctypes.c_int32),
     "peer_wait": ("pipipp", ctypes.c_int),
+    "peer_ack": ("ippp", ctypes.c_int),
+    "peer_wait_plain": ("ippp", ctypes.c_int),
     "peer_allreduce": ("piiippipp", ctypes.c_int),
     "csr_row_lengths": ("lppp", ctypes.c_int),
     "csr_to_coo_rows": ("lppp", ctypes.c_int),

@@ -208,6 +208,82 @@ __global__ void peer_allreduce_kernel(double* red, int k, PeerRed pr, int epoch,
     if (epoch_dev) *epoch_dev = epoch;
 }
 
+// ---------------------------------------------------------------------------
+// Plain distributed SpMV through peer memory (DistCsr.apply_peer): no CG step
+// precedes the SpMV, so a copy kernel puts the boundary rows of x straight
+// into the neighbours' ghost slots. Ghost-slot reuse is ordered by ACK flags
+// (no all-reduce separates two SpMVs): before writing epoch e, every CTA
+// waits until each destination has acknowledged epoch e - 1 (it finished its
+// ghost SpMV); after its ghost SpMV a rank raises its ack in every source's
+// ack array. Epochs live on the device, so the step is graph-capturable.
+// ---------------------------------------------------------------------------
+struct PeerAck {
+    int n;
+    const int* wait[PEER_MAX];  // my slot in each destination's ack array... read side: acks FROM destinations
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+peer_put_kernel(const T* __restrict__ xo, PeerPut pp, PeerAck acks, int* epoch_dev, unsigned* ticket,
+                unsigned long long timeout_ns) {
+    __shared__ int s_epoch, s_ok;
+    if (threadIdx.x == 0) {
+        const int e = *(volatile int*)epoch_dev + 1;
+        s_epoch = e;
+        s_ok = 1;
+        const unsigned long long deadline = global_ns() + timeout_ns;
+        for (int k = 0; k < acks.n; ++k)
+            while (ld_acquire_sys(acks.wait[k]) < e - 1) {
+                if (global_ns() > deadline) {
+                    s_ok = 0;
+                    break;
+                }
+                __nanosleep(64);
+            }
+    }
+    __syncthreads();
+    const int epoch = s_epoch;
+    if (!s_ok) return;  // a destination stopped responding: the flags stay low, the receiver's wait times out
+    bool wrote = false;
+    for (int k = 0; k < pp.n; ++k) {
+        const int64_t cnt = pp.hi[k] - pp.lo[k];
+        T* dst = static_cast<T*>(pp.dst[k]);
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+            dst[i] = xo[pp.lo[k] + i];
+            wrote = true;
+        }
+    }
+    if (wrote) __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        if (t == gridDim.x - 1) {
+            __threadfence_system();
+            *ticket = 0;
+            for (int k = 0; k < pp.n; ++k) st_release_sys(pp.flag[k], epoch);
+            *epoch_dev = epoch;
+        }
+    }
+}
+
+// after the ghost SpMV: acknowledge epoch *epoch_dev to every source
+__global__ void peer_ack_kernel(PeerWait ackout, const int* epoch_dev) {
+    const int e = *(volatile const int*)epoch_dev;
+    for (int k = 0; k < ackout.n; ++k) st_release_sys(const_cast<int*>(ackout.flag[k]), e);
+}
+
+// wait for the sources' flags of the current epoch (no solver control block)
+__global__ void peer_wait_plain_kernel(PeerWait w, const int* epoch_dev, unsigned long long timeout_ns) {
+    const int e = *(volatile const int*)epoch_dev;
+    const unsigned long long deadline = global_ns() + timeout_ns;
+    for (int k = 0; k < w.n; ++k)
+        while (ld_acquire_sys(w.flag[k]) < e) {
+            if (global_ns() > deadline) return;
+            __nanosleep(64);
+        }
+}
+
 __global__ void peer_wait_kernel(KrylovCtl* c, PeerWait w, int epoch, unsigned long long timeout_ns,
                                  const int* epoch_dev) {
     if (c->done) return;
@@ -322,6 +398,58 @@ int b200sp_peer_allreduce(double* red, int32_t k, int32_t world, int32_t rank, d
     peer_allreduce_kernel<<<1, 1, 0, as_stream(stream)>>>(red, k, pr, epoch, peer_timeout_ns(), epoch_dev);
     count_launch();
     return check_launch("peer_allreduce");
+}
+
+#define PEER_PUT_X(SUF, T)                                                                                    \
+    int b200sp_peer_put_##SUF(const T* x_owned, int32_t nput, const int64_t* lo, const int64_t* hi,            \
+                              void* const* dst, int32_t* const* flag, int32_t nack, const int32_t* const* ack_in, \
+                              int32_t* epoch_dev, uint32_t* ticket, void* stream) {                             \
+        B200SP_REQUIRE(nput >= 0 && nput <= PEER_MAX && nack >= 0 && nack <= PEER_MAX, B200SP_EINVAL,           \
+                       "peer_put: at most %d peers", PEER_MAX);                                                 \
+        PeerPut pp{};                                                                                           \
+        pp.n = nput;                                                                                            \
+        int64_t most = 0;                                                                                       \
+        for (int k = 0; k < nput; ++k) {                                                                        \
+            pp.lo[k] = lo[k];                                                                                   \
+            pp.hi[k] = hi[k];                                                                                   \
+            pp.dst[k] = dst[k];                                                                                 \
+            pp.flag[k] = flag[k];                                                                               \
+            most = hi[k] - lo[k] > most ? hi[k] - lo[k] : most;                                                 \
+        }                                                                                                       \
+        PeerAck a{};                                                                                            \
+        a.n = nack;                                                                                             \
+        for (int k = 0; k < nack; ++k) a.wait[k] = ack_in[k];                                                   \
+        const unsigned grid = (unsigned)(most > 0 ? grid_for(most, 256, 4) : 1);                                \
+        peer_put_kernel<T><<<grid, 256, 0, as_stream(stream)>>>(x_owned, pp, a, epoch_dev, ticket,              \
+                                                               peer_timeout_ns());                              \
+        count_launch();                                                                                         \
+        return check_launch("peer_put");                                                                        \
+    }
+PEER_PUT_X(f64, double)
+PEER_PUT_X(f32, float)
+#undef PEER_PUT_X
+
+int b200sp_peer_ack(int32_t nack, const int32_t* const* ack_out, const int32_t* epoch_dev, void* stream) {
+    B200SP_REQUIRE(nack >= 0 && nack <= 2 * PEER_MAX, B200SP_EINVAL, "peer_ack: at most %d sources", 2 * PEER_MAX);
+    if (nack == 0) return B200SP_OK;
+    PeerWait w{};
+    w.n = nack;
+    for (int k = 0; k < nack; ++k) w.flag[k] = ack_out[k];
+    peer_ack_kernel<<<1, 1, 0, as_stream(stream)>>>(w, epoch_dev);
+    count_launch();
+    return check_launch("peer_ack");
+}
+
+int b200sp_peer_wait_plain(int32_t nwait, const int32_t* const* flags, const int32_t* epoch_dev, void* stream) {
+    B200SP_REQUIRE(nwait >= 0 && nwait <= 2 * PEER_MAX, B200SP_EINVAL, "peer_wait_plain: at most %d flags",
+                   2 * PEER_MAX);
+    if (nwait == 0) return B200SP_OK;
+    PeerWait w{};
+    w.n = nwait;
+    for (int k = 0; k < nwait; ++k) w.flag[k] = flags[k];
+    peer_wait_plain_kernel<<<1, 1, 0, as_stream(stream)>>>(w, epoch_dev, peer_timeout_ns());
+    count_launch();
+    return check_launch("peer_wait_plain");
 }
 
 int b200sp_peer_wait(void* ctl, int32_t nwait, const int32_t* const* flags, int32_t epoch, const int32_t* epoch_dev,

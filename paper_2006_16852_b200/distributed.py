@@ -285,7 +285,40 @@ class DistCsr(LinOp):
             gd = Dense.wrap(exc, xext[nl:].view(-1, 1))
             self.a_ghost.apply_advanced(alpha, gd, 1.0, yd)
 
+    def peer(self, dtype):
+        """This matrix's peer-memory halo for ``dtype`` (built collectively on
+        the first call of every rank), or None when the peer path is not
+        usable: non-range sends, too many neighbours, B200SP_PEER_HALO=0, or a
+        pair of devices without P2P access (then every rank falls back to NCCL,
+        with a warning)."""
+        if not PeerHalo.usable(self):
+            return None
+        if self.__dict__.get("_peer_ok") is None:
+            ok, _ = peer_capable(self.comm, self.exec.device)  # collective, once per matrix
+            self.__dict__["_peer_ok"] = ok
+            if not ok:
+                import warnings
+
+                warnings.warn("distributed solve: peer access between the ranks' GPUs is unavailable; "
+                              "falling back to NCCL send/recv halo and NCCL all-reduce", RuntimeWarning)
+        if not self.__dict__["_peer_ok"]:
+            return None
+        cache = self.__dict__.setdefault("_peer_halo", {})
+        if dtype not in cache:
+            cache[dtype] = PeerHalo(self, dtype)
+        return cache[dtype]
+
     def _apply_impl(self, b, x):
+        if b.size.cols == 1:
+            peer = self.peer(b.values.dtype)
+            if peer is not None:  # halo through peer memory (kernels only)
+                peer.pext[:self.n_local].copy_(b.values[:, 0])
+                y = x.values[:, 0]
+                yc = y if y.is_contiguous() else torch.empty_like(y)
+                peer.apply_spmv(yc, self.exec.stream)
+                if yc is not y:
+                    y.copy_(yc)
+                return
         ext = torch.empty(self.n_ext, dtype=b.values.dtype, device=self.exec.device)
         ext[:self.n_local].copy_(b.values[:, 0])
         self.apply_ext(ext, x.values[:, 0])
@@ -350,25 +383,45 @@ class PeerHalo:
         dev = exc.device
         self.A = A
         self.pext = torch.zeros(A.n_ext, dtype=dtype, device=dev)
-        self.flags = torch.zeros(max(comm.size, 1), dtype=torch.int32, device=dev)
+        w = max(comm.size, 1)
+        self.flags = torch.zeros(w, dtype=torch.int32, device=dev)
+        # the plain SpMV's own flags / acks (apply_spmv): [sources' flags | destinations' acks]
+        self.flags_x = torch.zeros(2 * w, dtype=torch.int32, device=dev)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         torch.cuda.synchronize(dev)
-        mine = {"pext": ipc_export(self.pext), "flags": ipc_export(self.flags), "nl": A.n_local,
-                "g0": {int(peer): int(g0) for peer, g0, _ in A.plan.recv}}
+        mine = {"pext": ipc_export(self.pext), "flags": ipc_export(self.flags), "flags_x": ipc_export(self.flags_x),
+                "nl": A.n_local, "g0": {int(peer): int(g0) for peer, g0, _ in A.plan.recv}}
         every = comm.allgather_object(mine)
         self._bases = []  # mapped peer allocations (closed with the object)
-        lo, hi, dst, flg = [], [], [], []
+        lo, hi, dst, flg, flg_x = [], [], [], [], []
         esz = self.pext.element_size()
         for peer, a, b, idx, _ in A._send:
             info = every[peer]
             rp_, b0 = ipc_open(*info["pext"])
             rf, b1 = ipc_open(*info["flags"])
-            self._bases += [b0, b1]
+            rx, b2 = ipc_open(*info["flags_x"])
+            self._bases += [b0, b1, b2]
             g0 = info["g0"][comm.rank]
             lo.append(a)
             hi.append(b)
             dst.append(rp_ + (info["nl"] + g0) * esz)
             flg.append(rf + 4 * comm.rank)
+            flg_x.append(rx + 4 * comm.rank)
+        # plain-SpMV acks: a source's ack array gets this rank's ack at [w + rank];
+        # before a put this rank waits on its own [w + destination] entries
+        ack_out = []
+        for peer, _, _ in A.plan.recv:
+            rx, bx = ipc_open(*every[int(peer)]["flags_x"])
+            self._bases.append(bx)
+            ack_out.append(rx + 4 * (w + comm.rank))
+        ack_in = [self.flags_x.data_ptr() + 4 * (w + int(peer)) for peer, _, _, _, _ in A._send]
+        waits_x = [self.flags_x.data_ptr() + 4 * int(peer) for peer, _, _ in A.plan.recv]
+        self.flag_x = (ctypes.c_void_p * max(len(flg_x), 1))(*flg_x)
+        self.ack_in = (ctypes.c_void_p * max(len(ack_in), 1))(*ack_in)
+        self.ack_out = (ctypes.c_void_p * max(len(ack_out), 1))(*ack_out)
+        self.waits_x = (ctypes.c_void_p * max(len(waits_x), 1))(*waits_x)
+        self.nack_in, self.nack_out = len(ack_in), len(ack_out)
+        self.epoch_x = torch.zeros(1, dtype=torch.int32, device=dev)
         k = len(lo)
         self.nput = k
         self.lo = (ctypes.c_int64 * max(k, 1))(*lo)
@@ -403,6 +456,25 @@ class PeerHalo:
 
     def wait(self, ctl, stream):
         _lib.call("peer_wait", ctl, self.nwait, ctypes.addressof(self.waits), 0, ptr(self.epoch_dev), stream)
+
+    def apply_spmv(self, y, stream):
+        """y = A x with x in self.pext[:n_local]: the boundary rows go into the
+        destinations' ghost slots by a copy kernel (gated by their acks of
+        the previous exchange), the owned-block SpMV runs meanwhile, then the
+        wait on the sources' flags, the ghost-block accumulate and this rank's
+        acks. Kernels only -- capturable in a CUDA graph."""
+        A, exc = self.A, self.A.exec
+        nl = A.n_local
+        suf = _lib.suffix(self.pext.dtype)
+        _lib.call("peer_put_" + suf, ptr(self.pext), self.nput, ctypes.addressof(self.lo), ctypes.addressof(self.hi),
+                  ctypes.addressof(self.dst), ctypes.addressof(self.flag_x), self.nack_in,
+                  ctypes.addressof(self.ack_in), ptr(self.epoch_x), ptr(self.ticket), stream)
+        yd = Dense.wrap(exc, y.view(-1, 1))
+        A.a_own.apply(Dense.wrap(exc, self.pext[:nl].view(-1, 1)), yd)
+        _lib.call("peer_wait_plain", self.nwait, ctypes.addressof(self.waits_x), ptr(self.epoch_x), stream)
+        if A.a_ghost is not None:
+            A.a_ghost.apply_advanced(1.0, Dense.wrap(exc, self.pext[nl:].view(-1, 1)), 1.0, yd)
+        _lib.call("peer_ack", self.nack_out, ctypes.addressof(self.ack_out), ptr(self.epoch_x), stream)
 
 
 class PeerReduce:
@@ -545,20 +617,8 @@ class DistCg:
     def _comm_paths(self, dt):
         """(peer halo or None, extended p vector, peer all-reduce or None)."""
         A, exc, comm = self.a, self.exec, self.a.comm
-        peer = None
-        if PeerHalo.usable(A) and A.__dict__.get("_peer_ok") is None:
-            ok, _ = peer_capable(comm, exc.device)  # collective, once per matrix
-            A.__dict__["_peer_ok"] = ok
-            if not ok:
-                import warnings
-
-                warnings.warn("distributed CG: peer access between the ranks' GPUs is unavailable; "
-                              "falling back to NCCL send/recv halo and NCCL all-reduce", RuntimeWarning)
-        if PeerHalo.usable(A) and A.__dict__.get("_peer_ok"):
-            peer = getattr(A, "_peer_halo", {}).get(dt)
-            if peer is None:  # collective: every rank builds it on its first solve of this dtype
-                peer = PeerHalo(A, dt)
-                A.__dict__.setdefault("_peer_halo", {})[dt] = peer
+        peer = A.peer(dt)  # collective: every rank builds it on its first solve of this dtype
+        if peer is not None:
             pext = peer.pext
         else:
             pext = torch.empty(A.n_ext, dtype=dt, device=exc.device)

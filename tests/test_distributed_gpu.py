@@ -53,6 +53,15 @@ def _worker(rank, world, port, g, out_dir, halo="0"):
         y = torch.zeros(A.n_local, dtype=torch.float64, device=exc.device)
         A.apply_ext(ext, y)
         err = OS.rel_error_inf(y.cpu().numpy(), yg[lo:hi])
+        # the public apply on this rank's slices: the peer-memory halo (put /
+        # wait / ack kernels) when halo == "1"; repeated so the ack-gated reuse
+        # of the ghost slots runs, with a different x each time
+        for rep in range(3):
+            xr = xg * (rep + 1.0)
+            xd = b2.Dense.wrap(exc, torch.from_numpy(xr[lo:hi].copy()).to(exc.device).view(-1, 1))
+            yd = b2.Dense.zeros(exc, A.n_local, 1)
+            A.apply(xd, yd)
+            err = max(err, OS.rel_error_inf(np.asarray(yd.data)[:, 0], (rep + 1.0) * yg[lo:hi]))
         # distributed CG
         b = torch.ones(A.n_local, dtype=torch.float64, device=exc.device)
         x = torch.zeros(A.n_local, dtype=torch.float64, device=exc.device)
