@@ -414,8 +414,10 @@ def bench_c2_dist(args, world, rank, local):
         torch.cuda.synchronize()
         barrier(world)
         graph = torch.cuda.CUDAGraph()
+        l0 = _lib.launch_count()
         with torch.cuda.graph(graph, capture_error_mode="relaxed"):
             peer.apply_spmv(y, exc.stream)
+        per_step_launches = _lib.launch_count() - l0  # kernels in the graph (replays bypass the counter)
         step = graph.replay
         halo = "peer memory (CUDA IPC over NVLink), CUDA graph per step"
     else:
@@ -423,6 +425,7 @@ def bench_c2_dist(args, world, rank, local):
         xext[:nl].copy_(torch.from_numpy(xh))
         step = lambda: A.apply_ext(xext, y)  # noqa: E731
         halo = "NCCL send/recv" if BACKEND == "nccl" else "gloo (host-staged)"
+        per_step_launches = None
     # algorithmic bytes of this rank's rows (Csr formula) + the ghost x values it reads
     by = bytes_csr(nl, nnz_l, 8) + (A.n_ext - nl) * 8
     with ClockSampler(local) as clk:
@@ -433,6 +436,8 @@ def bench_c2_dist(args, world, rank, local):
         launches0 = _lib.launch_count()
         ms = timer.run(step, args.steps, 0)
         launches = _lib.launch_count() - launches0
+        if per_step_launches is not None:
+            launches = per_step_launches * args.steps
     barrier(world)
     t_step = allmax(world, statistics.mean(ms) * 1e-3)
     total_bytes = allsum(world, by)
