@@ -1176,8 +1176,15 @@ class minimal_storage_limit(HybridStrategy):
         return int(np.argmin(cost))
 
 
-class automatic(minimal_storage_limit):
-    pass
+class automatic(imbalance_limit):
+    """Default split: the row length at the 80th percentile (Ginkgo's
+    imbalance-limit rule). On the C3 power law this is width 16 -- 371.9 us
+    -- where the storage-minimising width 6 takes 421.2 us (the Ell pass is
+    the cheaper one per entry even with its padding; widths 0-24 in
+    profiles/r03_hybrid_width.txt); on the stencils every row fits (all Ell)."""
+
+    def __init__(self):
+        super().__init__(0.8)
 
 
 class Hybrid(_Sparse):
