@@ -345,6 +345,16 @@ def ipc_open(handle, offset):
     return int(p.value), int(base.value)
 
 
+def _close_mapped(bases):
+    """Unmap peer allocations opened with ipc_open (weakref finalizer)."""
+    for base in bases:
+        try:
+            _lib.call("ipc_close", base)
+        except Exception:  # noqa: BLE001 -- interpreter / context teardown
+            pass
+    bases.clear()
+
+
 def peer_capable(comm, dev):
     """Collective: True on every rank when every rank can reach every other
     rank's device with loads/stores (cudaDeviceCanAccessPeer, then
@@ -422,6 +432,9 @@ class PeerHalo:
         self.waits_x = (ctypes.c_void_p * max(len(waits_x), 1))(*waits_x)
         self.nack_in, self.nack_out = len(ack_in), len(ack_out)
         self.epoch_x = torch.zeros(1, dtype=torch.int32, device=dev)
+        import weakref
+
+        weakref.finalize(self, _close_mapped, self._bases)
         k = len(lo)
         self.nput = k
         self.lo = (ctypes.c_int64 * max(k, 1))(*lo)
@@ -505,6 +518,9 @@ class PeerReduce:
             fl.append(tf)
         self.sl = (ctypes.c_void_p * w)(*sl)
         self.fl = (ctypes.c_void_p * w)(*fl)
+        import weakref
+
+        weakref.finalize(self, _close_mapped, self._bases)
         self.epoch_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # advanced by the kernel
         torch.cuda.synchronize(dev)
 
