@@ -338,7 +338,7 @@ def bench_c2(args, world, rank, local):
         t0 = time.perf_counter()
         m.apply(bh, xh)  # H2D b, SpMV, D2H x (synchronous on return)
         e2e_t.append(time.perf_counter() - t0)
-    e2e_step = allmax(world, statistics.mean(e2e_t))
+    e2e_step = allmax(world, statistics.median(e2e_t))  # median: robust to host jitter
     e2e = {"value": round(total_bytes / e2e_step / 1e9, 1), "unit": "GB/s",
            "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8,
            "ms_per_step": round(e2e_step * 1e3, 3)}
@@ -464,7 +464,7 @@ def bench_c2_dist(args, world, rank, local):
         t0 = time.perf_counter()
         e2e_step()
         e2e_t.append(time.perf_counter() - t0)
-    e2e_step_t = allmax(world, statistics.mean(e2e_t))
+    e2e_step_t = allmax(world, statistics.median(e2e_t))
     halo_bytes = (A.n_ext - nl) * 8
     return {
         "metric": METRIC, "value": round(total_bytes / t_step / 1e9, 1), "unit": "GB/s", "n_gpus": world,
