@@ -617,6 +617,205 @@ bicg_step3_kernel(int64_t n, T* __restrict__ x, int64_t xs, T* __restrict__ r, c
 // CgStep1, SpMV + sigma (cg_sigma_ctl), FcgStep2 (t = r_new - r_old, rho =
 // r.z, rho_t = t.z, ||r||, check, beta = rho_t / rho_prev) in one launch,
 // with the block-local control copies of the cooperative BiCGSTAB below.
+// ---------------------------------------------------------------------------
+// Tiny systems (n <= 4 rows, the paper's 1x1 overhead benchmark): the whole
+// CG / BiCGSTAB solve in ONE thread with the matrix and every vector in
+// registers (the row count a template constant) and the control block in a
+// local copy -- the cooperative kernels' statements one for one (same
+// products, same fused multiply-adds, dots accumulated in fp64 in row order),
+// without a single memory round trip per iteration. The vectors and the
+// control block are written back at the end.
+// ---------------------------------------------------------------------------
+constexpr int TINY_ROWS = 4;
+
+template <typename T, int N>
+struct TinyCsr {
+    int rp[N + 1];
+    int ci[N * N];
+    T av[N * N];
+    __device__ void load(const int* rpg, const int* cig, const T* avg) {
+#pragma unroll
+        for (int i = 0; i <= N; ++i) rp[i] = rpg[i];
+        for (int k = 0; k < rp[N]; ++k) {
+            ci[k] = cig[k];
+            av[k] = avg[k];
+        }
+    }
+    // out_i = sum_k av[k] * u[ci[k]], left to right (coop_row_dot)
+    __device__ void apply(const T (&u)[N], T (&out)[N]) const {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            T acc = 0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                T uk = u[0];
+#pragma unroll
+                for (int j = 1; j < N; ++j)
+                    if (ci[k] == j) uk = u[j];
+                acc += av[k] * uk;
+            }
+            out[i] = acc;
+        }
+    }
+};
+
+template <typename T, int N>
+__global__ void __launch_bounds__(32)
+cg_tiny_kernel(const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ avg, T* x_g, T* r_g,
+               T* p_g, KrylovCtl* c, double* hist) {
+    if (threadIdx.x != 0) return;
+    TinyCsr<T, N> A;
+    A.load(rp, ci, avg);
+    KrylovCtl s = *c;
+    T x[N], r[N], pin[N], pout[N], q[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x_g[i], r[i] = r_g[i], pin[i] = p_g[i];
+    double rho = s.rho, beta = s.beta;
+    int it = s.it;
+    bool done = s.done;
+    while (!done) {
+        const T tb = (T)beta;
+        T pg[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) pg[j] = fma_t(tb, pin[j], r[j]);  // p recomputed as in the SpMV of cg_coop
+        A.apply(pg, q);
+        double sg = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            pout[i] = pg[i];
+            sg += (double)pg[i] * (double)q[i];
+        }
+        const double sigma = sg;
+        if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
+            s.sigma = sigma;
+            s.breakdown = BD_CG_SIGMA;
+            s.breakdown_it = it + 1;
+            s.done = 1;
+            break;
+        }
+        const double alpha = safe_div(rho, sigma);
+        const T ta = (T)alpha;
+        double rr = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            x[i] = x[i] + ta * pout[i];
+            r[i] = r[i] - ta * q[i];
+            rr += (double)r[i] * (double)r[i];
+        }
+        const double rho_prev = rho;
+        rho = rr;
+        it += 1;
+        const double nrm = sqrt(rho);
+        bool stop = false;
+        int sid = 0;
+        for (int i = 0; i < s.n_crit && !stop; ++i)
+            if (crit_fires(&s, i, it, nrm)) stop = true, sid = i + 1;
+        beta = safe_div(rho, rho_prev);
+        s.it = it;
+        s.rho_prev = rho_prev;
+        s.rho = rho;
+        s.rnorm = nrm;
+        s.sigma = sigma;
+        s.alpha = alpha;
+        s.beta = beta;
+        hist_put(&s, hist, it, nrm);
+        if (stop) {
+            s.stopped = 1;
+            s.stopping_id = sid;
+            s.finalized = 1;
+            s.done = 1;
+        }
+        done = stop;
+#pragma unroll
+        for (int i = 0; i < N; ++i) pin[i] = pout[i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) x_g[i] = x[i], r_g[i] = r[i], p_g[i] = pin[i];
+    *c = s;
+}
+
+template <typename T, int N>
+__global__ void __launch_bounds__(32)
+bicg_tiny_kernel(const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ avg, T* x_g, T* r_g,
+                 const T* __restrict__ rt_g, T* p_g, T* v_g, T* s_g, T* t_g, KrylovCtl* c, double* hist) {
+    if (threadIdx.x != 0) return;
+    TinyCsr<T, N> A;
+    A.load(rp, ci, avg);
+    KrylovCtl sc = *c;
+    T x[N], r[N], rt[N], p[N], v[N], sv[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        x[i] = x_g[i], r[i] = r_g[i], rt[i] = rt_g[i], p[i] = p_g[i], v[i] = v_g[i], sv[i] = s_g[i], t[i] = t_g[i];
+    while (!sc.done) {
+        {   // p = r + beta (p - omega v)   (BicgstabStep1)
+            const T beta = (T)sc.beta, omega = (T)sc.omega;
+#pragma unroll
+            for (int i = 0; i < N; ++i) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+        }
+        A.apply(p, v);  // v = A p; gamma = rt.v
+        double g = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) g += (double)rt[i] * (double)v[i];
+        {
+            const double tot[1] = {g};
+            bicg_gamma_ctl(&sc, tot);
+        }
+        if (sc.done) break;
+        const T alpha = (T)sc.alpha;
+        double ss = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {  // s = r - alpha v   (BicgstabStep2)
+            sv[i] = r[i] - alpha * v[i];
+            ss += (double)sv[i] * (double)sv[i];
+        }
+        sc.it += 1;
+        sc.snorm = sqrt(ss);
+        hist_put(&sc, hist, sc.it, sc.snorm);
+        crit_check(&sc, sc.it, sc.snorm);
+        if (sc.stopped) {  // converged on ||s||: x += alpha y   (BicgstabFinalize)
+            if (sc.needs_residual) {
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = x[i] + alpha * p[i];
+            }
+            sc.done = 1;
+            break;
+        }
+        A.apply(sv, t);  // t = A s; ts = t.s, tt = t.t
+        double a = 0, bb = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const double tv = t[i];
+            a += tv * (double)sv[i];
+            bb += tv * tv;
+        }
+        {
+            const double tot[2] = {a, bb};
+            bicg_tst_ctl(&sc, tot);
+        }
+        if (sc.done) break;
+        const T omega = (T)sc.omega;
+        double rr = 0, rtr = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {  // x += alpha y + omega z; r = s - omega t   (BicgstabStep3)
+            const T upd = alpha * p[i] + omega * sv[i];
+            x[i] = x[i] + upd;
+            r[i] = sv[i] - omega * t[i];
+            rr += (double)r[i] * (double)r[i];
+            rtr += (double)rt[i] * (double)r[i];
+        }
+        sc.rho_prev = sc.rho;
+        sc.it += 1;
+        sc.rnorm = sqrt(rr);
+        hist_put(&sc, hist, sc.it, sc.rnorm);
+        crit_check(&sc, sc.it, sc.rnorm);
+        sc.done = sc.stopped;
+        bicg_cycle_start(&sc, rtr, rr);
+    }
+    sc.mid_final = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) x_g[i] = x[i], r_g[i] = r[i], p_g[i] = p[i], v_g[i] = v[i], s_g[i] = sv[i], t_g[i] = t[i];
+    *c = sc;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(KRY_BLOCK)
 fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
@@ -2078,9 +2277,150 @@ int64_t b200sp_gmres_workspace_elems(int32_t k) { return (int64_t)(k + 1) * k + 
 
 }  // extern "C"
 
+namespace b200sp {
+
+template <typename T, int N>
+__global__ void __launch_bounds__(32)
+fcg_tiny_kernel(const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ avg, T* x_g, T* r_g,
+                T* p_g, T* q_g, T* t_g, KrylovCtl* c, double* hist) {
+    if (threadIdx.x != 0) return;
+    TinyCsr<T, N> A;
+    A.load(rp, ci, avg);
+    KrylovCtl sc = *c;
+    T x[N], r[N], p[N], q[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x_g[i], r[i] = r_g[i], p[i] = p_g[i], q[i] = q_g[i], t[i] = t_g[i];
+    while (!sc.done) {
+        const T beta = (T)sc.beta;
+#pragma unroll
+        for (int i = 0; i < N; ++i) p[i] = r[i] + beta * p[i];  // CgStep1 (z = r)
+        A.apply(p, q);
+        double sg = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) sg += (double)p[i] * (double)q[i];
+        {
+            const double tot[1] = {sg};
+            cg_sigma_ctl(&sc, tot);
+        }
+        if (sc.done) break;
+        const T alpha = (T)sc.alpha;
+        double rz = 0, tz = 0, rr = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {  // FcgStep2
+            x[i] = x[i] + mul_rn(alpha, p[i]);
+            const T ro = r[i];
+            const T rv = ro - mul_rn(alpha, q[i]);
+            const T tv = rv - ro;
+            t[i] = tv;
+            r[i] = rv;
+            rz += (double)rv * (double)rv;
+            tz += (double)tv * (double)rv;
+            rr += (double)rv * (double)rv;
+        }
+        sc.rho_prev = sc.rho;
+        sc.rho = rz;
+        sc.rho_t = tz;
+        sc.it += 1;
+        sc.rnorm = sqrt(rr);
+        hist_put(&sc, hist, sc.it, sc.rnorm);
+        crit_check(&sc, sc.it, sc.rnorm);
+        sc.done = sc.stopped;
+        sc.beta = safe_div(sc.rho_t, sc.rho_prev);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) x_g[i] = x[i], r_g[i] = r[i], p_g[i] = p[i], q_g[i] = q[i], t_g[i] = t[i];
+    *c = sc;
+}
+
+template <typename T, int N>
+__global__ void __launch_bounds__(32)
+cgs_tiny_kernel(const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ avg, T* x_g, T* r_g,
+                const T* __restrict__ rt_g, T* p_g, T* q_g, T* u_g, T* vh_g, T* w_g, T* t_g, KrylovCtl* c,
+                double* hist) {
+    if (threadIdx.x != 0) return;
+    TinyCsr<T, N> A;
+    A.load(rp, ci, avg);
+    KrylovCtl sc = *c;
+    T x[N], r[N], rt[N], p[N], q[N], u[N], vh[N], w[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        x[i] = x_g[i], r[i] = r_g[i], rt[i] = rt_g[i], p[i] = p_g[i], q[i] = q_g[i], u[i] = u_g[i], vh[i] = vh_g[i],
+        w[i] = w_g[i], t[i] = t_g[i];
+    while (!sc.done) {
+        {   // u = r + beta q; p = u + beta (q + beta p)   (CgsStep1)
+            const T beta = (T)sc.beta;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const T qv = q[i];
+                const T uv = r[i] + mul_rn(beta, qv);
+                u[i] = uv;
+                p[i] = uv + mul_rn(beta, qv + mul_rn(beta, p[i]));
+            }
+        }
+        A.apply(p, vh);  // v_hat = A p; gamma = rt.v_hat
+        double g = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) g += (double)rt[i] * (double)vh[i];
+        {
+            const double tot[1] = {g};
+            bicg_gamma_ctl(&sc, tot);
+        }
+        if (sc.done) break;
+        const T alpha = (T)sc.alpha;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {  // q = u - alpha v_hat; w = u + q   (CgsStep2)
+            const T uv = u[i];
+            const T qv = uv - mul_rn(alpha, vh[i]);
+            q[i] = qv;
+            w[i] = uv + qv;
+        }
+        sc.it += 1;  // mid check on the unchanged ||r|| (krylov.py:171-176)
+        hist_put(&sc, hist, sc.it, sc.rnorm);
+        crit_check(&sc, sc.it, sc.rnorm);
+        sc.done = sc.stopped;
+        if (sc.done) break;
+        A.apply(w, t);  // t = A w; r -= alpha t; x += alpha w   (CgsStep3)
+        double rr = 0, rtr = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const T rv = r[i] - mul_rn(alpha, t[i]);
+            r[i] = rv;
+            x[i] = x[i] + mul_rn(alpha, w[i]);
+            rr += (double)rv * (double)rv;
+            rtr += (double)rt[i] * (double)rv;
+        }
+        sc.rho_prev = sc.rho;
+        sc.it += 1;
+        sc.rnorm = sqrt(rr);
+        hist_put(&sc, hist, sc.it, sc.rnorm);
+        crit_check(&sc, sc.it, sc.rnorm);
+        sc.done = sc.stopped;
+        cgs_cycle_start(&sc, rtr, rr);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        x_g[i] = x[i], r_g[i] = r[i], p_g[i] = p[i], q_g[i] = q[i], u_g[i] = u[i], vh_g[i] = vh[i], w_g[i] = w[i],
+        t_g[i] = t[i];
+    *c = sc;
+}
+
+}  // namespace b200sp
+
+// tiny systems (n <= 32 rows): the one-block cooperative solve runs as ONE
+// warp -- its block reductions and barriers then never leave the warp
+static unsigned coop_threads(int64_t n) { return n <= 32 && tuning("coop_tiny_warp", 1) ? 32u : (unsigned)KRY_BLOCK; }
+
 template <typename T>
 static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, T* p, T* p2, T* q, void* ctl,
                    double* part, double* hist, void* stream) {
+    if (n >= 1 && n <= TINY_ROWS && tuning("coop_tiny", 1)) {  // one thread, registers only
+        KrylovCtl* c = (KrylovCtl*)ctl;
+        auto k = n == 1 ? cg_tiny_kernel<T, 1> : n == 2 ? cg_tiny_kernel<T, 2> : n == 3 ? cg_tiny_kernel<T, 3>
+                                                                                      : cg_tiny_kernel<T, 4>;
+        k<<<1, 32, 0, as_stream(stream)>>>(rp, ci, v, x, r, p, c, hist);
+        count_launch();
+        return check_launch("cg_tiny");
+    }
     int dev = 0, sms = 0, per_sm = 0;
     B200SP_CHECK_CUDA(cudaGetDevice(&dev));
     B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2090,11 +2430,12 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
     const int64_t need = ceil_div(n, KRY_BLOCK);
     if (grid > need) grid = need;
     const int cap = tuning("coop_blocks", 0);  // sweep knob: fewer blocks = cheaper grid barriers
+    const unsigned threads = coop_threads(n);
     if (cap > 0 && grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &p2, &q, &c, &part, &hist};
-    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cg_coop_kernel<T>, dim3((unsigned)grid), dim3(KRY_BLOCK),
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cg_coop_kernel<T>, dim3((unsigned)grid), dim3(threads),
                                                   args, 0, as_stream(stream)));
     count_launch();
     return B200SP_OK;
@@ -2103,6 +2444,14 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
 template <typename T>
 static int bicg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, const T* rt, T* p,
                      T* vv, T* s, T* t, void* ctl, double* part, double* hist, void* stream) {
+    if (n >= 1 && n <= TINY_ROWS && tuning("coop_tiny", 1)) {  // one thread, registers only
+        KrylovCtl* c = (KrylovCtl*)ctl;
+        auto k = n == 1 ? bicg_tiny_kernel<T, 1> : n == 2 ? bicg_tiny_kernel<T, 2>
+               : n == 3 ? bicg_tiny_kernel<T, 3> : bicg_tiny_kernel<T, 4>;
+        k<<<1, 32, 0, as_stream(stream)>>>(rp, ci, v, x, r, rt, p, vv, s, t, c, hist);
+        count_launch();
+        return check_launch("bicgstab_tiny");
+    }
     int dev = 0, sms = 0, per_sm = 0;
     B200SP_CHECK_CUDA(cudaGetDevice(&dev));
     B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2112,12 +2461,13 @@ static int bicg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v
     const int64_t need = ceil_div(n, KRY_BLOCK);
     if (grid > need) grid = need;
     const int cap = tuning("coop_blocks", 0);
+    const unsigned threads = coop_threads(n);
     if (cap > 0 && grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, (void*)&rt, &p, &vv, &s, &t, &c, &part, &hist};
     B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)bicg_coop_kernel<T>, dim3((unsigned)grid),
-                                                  dim3(KRY_BLOCK), args, 0, as_stream(stream)));
+                                                  dim3(threads), args, 0, as_stream(stream)));
     count_launch();
     return B200SP_OK;
 }
@@ -2125,6 +2475,14 @@ static int bicg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v
 template <typename T>
 static int fcg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, T* p, T* q, T* t,
                     void* ctl, double* part, double* hist, void* stream) {
+    if (n >= 1 && n <= TINY_ROWS && tuning("coop_tiny", 1)) {  // one thread, registers only
+        KrylovCtl* c = (KrylovCtl*)ctl;
+        auto k = n == 1 ? fcg_tiny_kernel<T, 1> : n == 2 ? fcg_tiny_kernel<T, 2>
+               : n == 3 ? fcg_tiny_kernel<T, 3> : fcg_tiny_kernel<T, 4>;
+        k<<<1, 32, 0, as_stream(stream)>>>(rp, ci, v, x, r, p, q, t, c, hist);
+        count_launch();
+        return check_launch("fcg_tiny");
+    }
     int dev = 0, sms = 0, per_sm = 0;
     B200SP_CHECK_CUDA(cudaGetDevice(&dev));
     B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2134,12 +2492,13 @@ static int fcg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v,
     const int64_t need = ceil_div(n, KRY_BLOCK);
     if (grid > need) grid = need;
     const int cap = tuning("coop_blocks", 0);
+    const unsigned threads = coop_threads(n);
     if (cap > 0 && grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &q, &t, &c, &part, &hist};
     B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)fcg_coop_kernel<T>, dim3((unsigned)grid),
-                                                  dim3(KRY_BLOCK), args, 0, as_stream(stream)));
+                                                  dim3(threads), args, 0, as_stream(stream)));
     count_launch();
     return B200SP_OK;
 }
@@ -2147,6 +2506,14 @@ static int fcg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v,
 template <typename T>
 static int cgs_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, T* x, T* r, const T* rt, T* p, T* q,
                     T* u, T* vh, T* w, T* t, void* ctl, double* part, double* hist, void* stream) {
+    if (n >= 1 && n <= TINY_ROWS && tuning("coop_tiny", 1)) {  // one thread, registers only
+        KrylovCtl* c = (KrylovCtl*)ctl;
+        auto k = n == 1 ? cgs_tiny_kernel<T, 1> : n == 2 ? cgs_tiny_kernel<T, 2>
+               : n == 3 ? cgs_tiny_kernel<T, 3> : cgs_tiny_kernel<T, 4>;
+        k<<<1, 32, 0, as_stream(stream)>>>(rp, ci, v, x, r, rt, p, q, u, vh, w, t, c, hist);
+        count_launch();
+        return check_launch("cgs_tiny");
+    }
     int dev = 0, sms = 0, per_sm = 0;
     B200SP_CHECK_CUDA(cudaGetDevice(&dev));
     B200SP_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2156,12 +2523,13 @@ static int cgs_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v,
     const int64_t need = ceil_div(n, KRY_BLOCK);
     if (grid > need) grid = need;
     const int cap = tuning("coop_blocks", 0);
+    const unsigned threads = coop_threads(n);
     if (cap > 0 && grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, (void*)&rt, &p, &q, &u, &vh, &w, &t, &c, &part, &hist};
     B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cgs_coop_kernel<T>, dim3((unsigned)grid),
-                                                  dim3(KRY_BLOCK), args, 0, as_stream(stream)));
+                                                  dim3(threads), args, 0, as_stream(stream)));
     count_launch();
     return B200SP_OK;
 }
