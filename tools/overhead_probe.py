@@ -1,3 +1,5 @@
+"""The paper's overhead benchmark with the tiny single-thread solvers off / on
+(b200sp_set_tuning("coop_tiny", 0/1)): python tools/overhead_probe.py"""
 import sys, json
 sys.path.insert(0, "/root/repo")
 from paper_2006_16852_b200 import _lib, CudaExecutor
