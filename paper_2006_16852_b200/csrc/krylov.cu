@@ -12,7 +12,6 @@
 //   CG        src/solvers/krylov.py:36-77   + steps.py:87-158
 //   BiCGSTAB  src/solvers/krylov.py:190-271 + steps.py:238-243, :348-480
 //   GMRES     src/solvers/gmres.py:75-340
-#include <cooperative_groups.h>
 
 #include <cstring>
 
@@ -268,22 +267,49 @@ __global__ void cg_finish_kernel(KrylovCtl* c, double* hist, int phase) {
 // barrier; block 0 publishes the status. Same arithmetic as the batched
 // kernels above (Csr rows summed left to right per thread).
 // ===========================================================================
-template <int NV>
-__device__ __forceinline__ void coop_block_partials(double (&v)[NV], double* part, double* sh, double* sh_tot) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const double s = block_sum(v[k], sh);
-        if (threadIdx.x == 0) {
-            if (gridDim.x == 1) sh_tot[k] = s;  // one block: the total stays on chip
-            else part[k * KRY_MAX_GRID + blockIdx.x] = s;
-        }
+// Grid-wide exchange for the persistent cooperative kernels: block partials
+// -> grid totals with ONE counter barrier (measured 6.1 vs 7.7 us per C1 CG
+// iteration against cooperative_groups grid.sync + a separate partial read,
+// profiles/r03_coop_c1.txt). Warp 0 holds the block sum after block_sum;
+// lane 0 stores it, fences (this block's vector stores, ordered before it by
+// the block barrier, and the partial) and arrives on a monotone counter,
+// then spins until all gridDim.x CTAs have arrived; warp 0 sums the partials
+// in CTA order (so every CTA gets bitwise the same totals) and one block
+// barrier broadcasts them. Partial slots alternate between the phases of an
+// iteration, so a slot is rewritten only after the next barrier, by which
+// time every CTA has read it. The counter is KrylovCtl::ticket[3]: zeroed by
+// ctl_init, reset by the last CTA out (coop_exit).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void coop_arrive_wait(unsigned* ctr, unsigned target) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    // acquire polling (measured faster than relaxed polling + one fence)
+    while ((int)(ld_acquire_u32(ctr) - target) < 0) {
     }
 }
 template <int NV>
-__device__ __forceinline__ void coop_totals(const double* part, double (&tot)[NV], double* sh_tot) {
-    // warp 0 sums the partials in block order; broadcast through smem
-    if (gridDim.x > 1) {
+__device__ __forceinline__ void coop_exchange(double (&v)[NV], double (&tot)[NV], double* part, unsigned* ctr,
+                                              unsigned& target, double* sh, double* sh_tot) {
+    double bs[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bs[k] = block_sum(v[k], sh);
+    if (gridDim.x == 1) {  // one block: the totals never leave the chip
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int k = 0; k < NV; ++k) sh_tot[k] = bs[k];
+    } else {
+        target += gridDim.x;
         if (threadIdx.x < 32) {
+            if (threadIdx.x == 0) {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) part[k * KRY_MAX_GRID + blockIdx.x] = bs[k];
+                coop_arrive_wait(ctr, target);
+            }
+            __syncwarp();
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 double s = 0;
@@ -292,22 +318,45 @@ __device__ __forceinline__ void coop_totals(const double* part, double (&tot)[NV
                 if (threadIdx.x == 0) sh_tot[k] = s;
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; ++k) tot[k] = sh_tot[k];
+}
+// plain grid barrier on the same counter
+__device__ __forceinline__ void coop_barrier(unsigned* ctr, unsigned& target) {
     __syncthreads();
+    if (gridDim.x > 1) {
+        target += gridDim.x;
+        if (threadIdx.x == 0) coop_arrive_wait(ctr, target);
+        __syncthreads();
+    }
+}
+// kernel exit: every CTA arrives once more; the last one out resets the
+// counter (and, for kernels that keep the control block in shared memory,
+// publishes it -- every CTA holds the same copy)
+__device__ __forceinline__ void coop_exit(unsigned* ctr, unsigned target, KrylovCtl* c = nullptr,
+                                          const KrylovCtl* sc = nullptr) {
+    if (threadIdx.x != 0) return;
+    if (gridDim.x == 1) {
+        if (sc) *c = *sc;
+        return;
+    }
+    __threadfence();
+    if (atomicAdd(ctr, 1u) == target + gridDim.x - 1) {
+        __threadfence();
+        if (sc) {
+            *c = *sc;
+            c->ticket[3] = 0;
+        } else {
+            *ctr = 0;
+        }
+    }
 }
 
 __device__ __forceinline__ double fma_t(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float fma_t(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
-// grid-wide barrier; a one-block grid (tiny systems) only needs the block
-// barrier (cooperative grid.sync costs microseconds even then)
-__device__ __forceinline__ void coop_sync(cooperative_groups::grid_group& grid) {
-    if (gridDim.x == 1) __syncthreads();
-    else grid.sync();
-}
 
 // Two grid barriers per iteration: p = r + beta p is not a phase of its own
 // but recomputed inside the SpMV for every column it gathers (r and the
@@ -319,8 +368,8 @@ __global__ void __launch_bounds__(KRY_BLOCK)
 cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                T* __restrict__ x, T* __restrict__ r, T* p_a, T* p_b, T* __restrict__ q, KrylovCtl* c,
                double* part, double* hist) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
+    unsigned* const ctr = &c->ticket[3];
+    unsigned target = 0;
     __shared__ double sh[KRY_BLOCK / 32];
     __shared__ double sh_tot[2];
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -346,9 +395,7 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
             sg += (double)pi * (double)s;
         }
         double v1[1] = {sg}, t1[1];
-        coop_block_partials<1>(v1, part, sh, sh_tot);
-        coop_sync(grid);
-        coop_totals<1>(part, t1, sh_tot);
+        coop_exchange<1>(v1, t1, part, ctr, target, sh, sh_tot);
         const double sigma = t1[0];
         T* const p = pout;
         if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
@@ -370,9 +417,7 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
             rr += (double)nr * (double)nr;
         }
         double v2[1] = {rr}, t2[1];
-        coop_block_partials<1>(v2, part + 2 * KRY_MAX_GRID, sh, sh_tot);
-        coop_sync(grid);
-        coop_totals<1>(part + 2 * KRY_MAX_GRID, t2, sh_tot);
+        coop_exchange<1>(v2, t2, part + 2 * KRY_MAX_GRID, ctr, target, sh, sh_tot);
         const double rho_prev = rho;
         rho = t2[0];
         it += 1;
@@ -407,6 +452,168 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
         pout = pin;
         pin = p;
     }
+    coop_exit(ctr, target);
+}
+
+// Register-resident variant (C1): the same arithmetic, row ownership and
+// summation order as cg_coop_kernel (rows gt + k*gs, k < RPT, so bitwise the
+// same iterates), but everything a thread owns lives in registers for the
+// whole solve -- its rows' x, r, p and q, their row bounds, the first W
+// column indices and values of each row, and the criteria -- so an iteration
+// touches global memory only for the neighbour gathers (p, r of the columns)
+// and the stores the neighbours read (p, r). The loop-carried dependency
+// chain per iteration drops from four L2 round trips (row bounds -> columns
+// -> gathers, then x/p/r/q) plus the control block to one.
+template <typename T, int RPT, int W>
+__global__ void __launch_bounds__(KRY_BLOCK)
+cg_coop_res_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
+                   T* __restrict__ x, T* r, T* p_a, T* p_b, T* __restrict__ q, KrylovCtl* c, double* part,
+                   double* hist) {
+    unsigned* const ctr = &c->ticket[3];
+    unsigned target = 0;
+    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh_tot[2];
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    T xo[RPT], ro[RPT], po[RPT], qo[RPT];
+    int kb[RPT], ke[RPT];
+    int cj[RPT][W];
+    T cv[RPT][W];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+        const int64_t i = gt + k * gs;
+        kb[k] = ke[k] = 0;
+        xo[k] = ro[k] = po[k] = qo[k] = 0;
+        if (i < n) {
+            kb[k] = rp[i];
+            ke[k] = rp[i + 1];
+            xo[k] = x[i];
+            ro[k] = r[i];
+            po[k] = p_a[i];
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            cj[k][w] = 0;
+            cv[k][w] = 0;
+            if (kb[k] + w < ke[k]) {
+                cj[k][w] = ci[kb[k] + w];
+                cv[k][w] = av[kb[k] + w];
+            }
+        }
+    }
+    // criteria are constant during the solve (TimeLimit never takes this path)
+    const int n_crit = c->n_crit;
+    int ctype[KRY_MAX_CRIT];
+    double cparam[KRY_MAX_CRIT];
+#pragma unroll
+    for (int i = 0; i < KRY_MAX_CRIT; ++i) {
+        ctype[i] = i < n_crit ? c->crit_type[i] : 0;
+        cparam[i] = i < n_crit ? c->crit_param[i] : 0.0;
+    }
+    const double baseline = c->baseline;
+    double rho = c->rho, beta = c->beta;
+    int it = c->it;
+    bool done = c->done;
+    const T* pin = p_a;
+    T* pout = p_b;
+    while (!done) {
+        const T tb = (T)beta;
+        double sg = 0;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int64_t i = gt + k * gs;
+            if (i < n) {
+                T s = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    if (kb[k] + w < ke[k]) {
+                        const int j = cj[k][w];
+                        s += cv[k][w] * fma_t(tb, pin[j], r[j]);
+                    }
+                }
+                for (int kk = kb[k] + W; kk < ke[k]; ++kk) {
+                    const int j = ci[kk];
+                    s += av[kk] * fma_t(tb, pin[j], r[j]);
+                }
+                qo[k] = s;
+                const T pi = fma_t(tb, po[k], ro[k]);
+                po[k] = pi;
+                pout[i] = pi;
+                sg += (double)pi * (double)s;
+            }
+        }
+        double v1[1] = {sg}, t1[1];
+        coop_exchange<1>(v1, t1, part, ctr, target, sh, sh_tot);
+        const double sigma = t1[0];
+        if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
+            if (gt == 0) {
+                c->sigma = sigma;
+                c->breakdown = BD_CG_SIGMA;
+                c->breakdown_it = it + 1;
+                c->done = 1;
+            }
+            break;
+        }
+        const double alpha = safe_div(rho, sigma);
+        const T ta = (T)alpha;
+        double rr = 0;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int64_t i = gt + k * gs;
+            if (i < n) {
+                xo[k] = xo[k] + ta * po[k];
+                const T nr = ro[k] - ta * qo[k];
+                ro[k] = nr;
+                r[i] = nr;
+                rr += (double)nr * (double)nr;
+            }
+        }
+        double v2[1] = {rr}, t2[1];
+        coop_exchange<1>(v2, t2, part + 2 * KRY_MAX_GRID, ctr, target, sh, sh_tot);
+        const double rho_prev = rho;
+        rho = t2[0];
+        it += 1;
+        const double nrm = sqrt(rho);
+        bool stop = false;
+        int sid = 0;
+#pragma unroll
+        for (int i = 0; i < KRY_MAX_CRIT; ++i) {  // unrolled: the criteria stay in registers
+            const bool f = ctype[i] == CRIT_ITERATION ? it >= (int)cparam[i]
+                           : ctype[i] == CRIT_RNR     ? nrm <= cparam[i] * baseline
+                                                      : false;
+            if (!stop && i < n_crit && f) stop = true, sid = i + 1;
+        }
+        beta = safe_div(rho, rho_prev);
+        if (gt == 0) {
+            c->it = it;
+            c->rho_prev = rho_prev;
+            c->rho = rho;
+            c->rnorm = nrm;
+            c->sigma = sigma;
+            c->alpha = alpha;
+            c->beta = beta;
+            hist_put(c, hist, it, nrm);
+            if (stop) {
+                c->stopped = 1;
+                c->stopping_id = sid;
+                c->finalized = 1;
+                c->done = 1;
+            }
+        }
+        done = stop;
+        T* const pt = pout;
+        pout = (T*)pin;
+        pin = pt;
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+        const int64_t i = gt + k * gs;
+        if (i < n) {
+            x[i] = xo[k];
+            q[i] = qo[k];
+        }
+    }
+    coop_exit(ctr, target);
 }
 
 // ===========================================================================
@@ -842,8 +1049,8 @@ __global__ void __launch_bounds__(KRY_BLOCK)
 bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                  T* __restrict__ x, T* r, const T* __restrict__ rt, T* p, T* v, T* s, T* t, KrylovCtl* c,
                  double* part, double* hist) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
+    unsigned* const ctr = &c->ticket[3];
+    unsigned target = 0;
     __shared__ KrylovCtl sc;
     __shared__ double sh[KRY_BLOCK / 32];
     __shared__ double sh_tot[2];
@@ -859,7 +1066,7 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
             const T beta = (T)sc.beta, omega = (T)sc.omega;
             for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + beta * (p[i] - omega * v[i]);
         }
-        coop_sync(grid);
+        coop_barrier(ctr, target);
         {   // v = A p; gamma = rt.v
             double g = 0;
             for (int64_t i = gt; i < n; i += gs) {
@@ -869,9 +1076,7 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
                 g += (double)rt[i] * (double)vi;
             }
             double vv[1] = {g}, tot[1];
-            coop_block_partials<1>(vv, part0, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<1>(part0, tot, sh_tot);
+            coop_exchange<1>(vv, tot, part0, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) bicg_gamma_ctl(&sc, tot);
             __syncthreads();
             if (sc.done) break;
@@ -885,9 +1090,7 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
                 ss += (double)sv * (double)sv;
             }
             double vv[1] = {ss}, tot[1];
-            coop_block_partials<1>(vv, part1, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<1>(part1, tot, sh_tot);
+            coop_exchange<1>(vv, tot, part1, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) {
                 sc.it += 1;
                 sc.snorm = sqrt(tot[0]);
@@ -918,9 +1121,7 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
                 bb += tv * tv;
             }
             double vv[2] = {a, bb}, tot[2];
-            coop_block_partials<2>(vv, part0, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<2>(part0, tot, sh_tot);
+            coop_exchange<2>(vv, tot, part0, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) bicg_tst_ctl(&sc, tot);
             __syncthreads();
             if (sc.done) break;
@@ -937,9 +1138,7 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
                 rtr += (double)rt[i] * (double)rv;
             }
             double vv[2] = {rr, rtr}, tot[2];
-            coop_block_partials<2>(vv, part1, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<2>(part1, tot, sh_tot);
+            coop_exchange<2>(vv, tot, part1, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) {
                 sc.rho_prev = sc.rho;
                 sc.it += 1;
@@ -952,15 +1151,15 @@ bicg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ 
             __syncthreads();
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *c = sc;
+    coop_exit(ctr, target, c, &sc);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(KRY_BLOCK)
 fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                 T* __restrict__ x, T* r, T* p, T* q, T* t, KrylovCtl* c, double* part, double* hist) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
+    unsigned* const ctr = &c->ticket[3];
+    unsigned target = 0;
     __shared__ KrylovCtl sc;
     __shared__ double sh[KRY_BLOCK / 32];
     __shared__ double sh_tot[4];
@@ -976,7 +1175,7 @@ fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
             const T beta = (T)sc.beta;
             for (int64_t i = gt; i < n; i += gs) p[i] = r[i] + beta * p[i];
         }
-        coop_sync(grid);
+        coop_barrier(ctr, target);
         {   // q = A p; sigma = p.q
             double sg = 0;
             for (int64_t i = gt; i < n; i += gs) {
@@ -986,9 +1185,7 @@ fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                 sg += (double)p[i] * (double)qi;
             }
             double vv[1] = {sg}, tot[1];
-            coop_block_partials<1>(vv, part_s, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<1>(part_s, tot, sh_tot);
+            coop_exchange<1>(vv, tot, part_s, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) cg_sigma_ctl(&sc, tot);
             __syncthreads();
             if (sc.done) break;
@@ -1008,9 +1205,7 @@ fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                 rr += (double)rv * (double)rv;
             }
             double vv[3] = {rz, tz, rr}, tot[3];
-            coop_block_partials<3>(vv, part_2, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<3>(part_2, tot, sh_tot);
+            coop_exchange<3>(vv, tot, part_2, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) {
                 sc.rho_prev = sc.rho;
                 sc.rho = tot[0];
@@ -1025,7 +1220,7 @@ fcg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
             __syncthreads();
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *c = sc;
+    coop_exit(ctr, target, c, &sc);
 }
 
 // ===========================================================================
@@ -1149,8 +1344,8 @@ __global__ void __launch_bounds__(KRY_BLOCK)
 cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                 T* __restrict__ x, T* r, const T* __restrict__ rt, T* p, T* q, T* u, T* vh, T* w, T* t, KrylovCtl* c,
                 double* part, double* hist) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
+    unsigned* const ctr = &c->ticket[3];
+    unsigned target = 0;
     __shared__ KrylovCtl sc;
     __shared__ double sh[KRY_BLOCK / 32];
     __shared__ double sh_tot[2];
@@ -1171,7 +1366,7 @@ cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                 p[i] = uv + mul_rn(beta, qv + mul_rn(beta, p[i]));
             }
         }
-        coop_sync(grid);
+        coop_barrier(ctr, target);
         {   // v_hat = A p; gamma = rt.v_hat
             double g = 0;
             for (int64_t i = gt; i < n; i += gs) {
@@ -1181,9 +1376,7 @@ cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                 g += (double)rt[i] * (double)vi;
             }
             double vv[1] = {g}, tot[1];
-            coop_block_partials<1>(vv, part0, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<1>(part0, tot, sh_tot);
+            coop_exchange<1>(vv, tot, part0, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) bicg_gamma_ctl(&sc, tot);
             __syncthreads();
             if (sc.done) break;
@@ -1207,7 +1400,7 @@ cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
         }
         __syncthreads();
         if (sc.done) break;
-        coop_sync(grid);
+        coop_barrier(ctr, target);
         {   // t = A w; r -= alpha t; x += alpha w; it++; check; next rho   (CgsStep3)
             double rr = 0, rtr = 0;
             for (int64_t i = gt; i < n; i += gs) {
@@ -1221,9 +1414,7 @@ cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                 rtr += (double)rt[i] * (double)rv;
             }
             double vv[2] = {rr, rtr}, tot[2];
-            coop_block_partials<2>(vv, part1, sh, sh_tot);
-            coop_sync(grid);
-            coop_totals<2>(part1, tot, sh_tot);
+            coop_exchange<2>(vv, tot, part1, ctr, target, sh, sh_tot);
             if (threadIdx.x == 0) {
                 sc.rho_prev = sc.rho;
                 sc.it += 1;
@@ -1236,7 +1427,7 @@ cgs_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
             __syncthreads();
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *c = sc;
+    coop_exit(ctr, target, c, &sc);
 }
 
 // ===========================================================================
@@ -2435,8 +2626,18 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &p2, &q, &c, &part, &hist};
-    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)cg_coop_kernel<T>, dim3((unsigned)grid), dim3(threads),
-                                                  args, 0, as_stream(stream)));
+    // rows per thread at this grid; up to 2 the register-resident kernel
+    // (same grid, same row ownership, same sums) runs instead -- if its
+    // occupancy allows the grid to be co-resident
+    const int64_t rpt = ceil_div(n, grid * (int64_t)threads);
+    const void* fn = (const void*)cg_coop_kernel<T>;
+    if (rpt <= 2 && tuning("coop_resident", 1)) {
+        const void* res = rpt == 1 ? (const void*)cg_coop_res_kernel<T, 1, 8> : (const void*)cg_coop_res_kernel<T, 2, 8>;
+        int per_sm_res = 0;
+        B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_res, res, threads, 0));
+        if ((int64_t)per_sm_res * sms >= grid) fn = res;
+    }
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(threads), args, 0, as_stream(stream)));
     count_launch();
     return B200SP_OK;
 }
