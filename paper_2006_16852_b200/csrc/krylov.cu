@@ -332,6 +332,59 @@ __device__ __forceinline__ void coop_barrier(unsigned* ctr, unsigned& target) {
         __syncthreads();
     }
 }
+// Exchange with no memory fence, for a barrier after which no CTA reads
+// another CTA's vector stores (CG's sigma barrier: the next gathers happen
+// only after the rho barrier, whose fence orders them). The partial travels
+// in a flagged 16-byte slot {lo, epoch, hi, epoch} (each aligned 8-byte half
+// is single-copy atomic, so a matching epoch certifies the data word beside
+// it); the counter is only a relaxed hint of when to start reading, and a
+// slot whose epoch does not match yet is re-read. Epochs are 1, 2, ... per
+// launch; coop_slots_clear zeroes the slots before the first use. One slot
+// set suffices when the barriers alternate with fenced ones: a CTA rewrites
+// its slot only after the next barrier, when every CTA has read it.
+__device__ __forceinline__ void coop_slots_clear(uint4* slots, unsigned* ctr, unsigned& target) {
+    if (threadIdx.x == 0) slots[blockIdx.x] = make_uint4(0, 0, 0, 0);
+    coop_barrier(ctr, target);
+}
+__device__ __forceinline__ void coop_exchange_nofence(double v, double& tot, uint4* slots, unsigned epoch, unsigned* ctr,
+                                                      unsigned& target, double* sh, double* sh_tot) {
+    const double bs = block_sum(v, sh);
+    if (gridDim.x == 1) {
+        if (threadIdx.x == 0) sh_tot[0] = bs;
+    } else {
+        target += gridDim.x;
+        if (threadIdx.x < 32) {
+            if (threadIdx.x == 0) {
+                const unsigned long long u = (unsigned long long)__double_as_longlong(bs);
+                asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(slots + blockIdx.x),
+                             "r"((unsigned)u), "r"(epoch), "r"((unsigned)(u >> 32)), "r"(epoch)
+                             : "memory");
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+                unsigned cv;
+                do {
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cv) : "l"(ctr) : "memory");
+                } while ((int)(cv - target) < 0);
+            }
+            __syncwarp();
+            double s = 0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+                unsigned a0, f0, a1, f1;
+                do {
+                    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(a0), "=r"(f0), "=r"(a1), "=r"(f1)
+                                 : "l"(slots + b)
+                                 : "memory");
+                } while (f0 != epoch || f1 != epoch);
+                s += __longlong_as_double((long long)(((unsigned long long)a1 << 32) | a0));
+            }
+            s = warp_sum(s);
+            if (threadIdx.x == 0) sh_tot[0] = s;
+        }
+    }
+    __syncthreads();
+    tot = sh_tot[0];
+}
+
 // kernel exit: every CTA arrives once more; the last one out resets the
 // counter (and, for kernels that keep the control block in shared memory,
 // publishes it -- every CTA holds the same copy)
@@ -464,14 +517,14 @@ cg_coop_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci
 // and the stores the neighbours read (p, r). The loop-carried dependency
 // chain per iteration drops from four L2 round trips (row bounds -> columns
 // -> gathers, then x/p/r/q) plus the control block to one.
-template <typename T, int RPT, int W>
-__global__ void __launch_bounds__(KRY_BLOCK)
+template <typename T, int RPT, int W, int BS>
+__global__ void __launch_bounds__(BS)
 cg_coop_res_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                    T* __restrict__ x, T* r, T* p_a, T* p_b, T* __restrict__ q, KrylovCtl* c, double* part,
-                   double* hist) {
+                   double* hist, int nofence) {
     unsigned* const ctr = &c->ticket[3];
     unsigned target = 0;
-    __shared__ double sh[KRY_BLOCK / 32];
+    __shared__ double sh[BS / 32];
     __shared__ double sh_tot[2];
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gs = (int64_t)gridDim.x * blockDim.x;
@@ -511,11 +564,14 @@ cg_coop_res_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict_
         cparam[i] = i < n_crit ? c->crit_param[i] : 0.0;
     }
     const double baseline = c->baseline;
+    const int hist_cap = c->hist_cap;  // thread 0 must not stall on a control-block load
     double rho = c->rho, beta = c->beta;
     int it = c->it;
     bool done = c->done;
     const T* pin = p_a;
     T* pout = p_b;
+    uint4* const slots = (uint4*)(part + KRY_NRED * KRY_MAX_GRID);
+    if (nofence) coop_slots_clear(slots, ctr, target);
     while (!done) {
         const T tb = (T)beta;
         double sg = 0;
@@ -542,9 +598,14 @@ cg_coop_res_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict_
                 sg += (double)pi * (double)s;
             }
         }
-        double v1[1] = {sg}, t1[1];
-        coop_exchange<1>(v1, t1, part, ctr, target, sh, sh_tot);
-        const double sigma = t1[0];
+        double sigma;
+        if (nofence) {
+            coop_exchange_nofence(sg, sigma, slots, (unsigned)it + 1, ctr, target, sh, sh_tot);
+        } else {
+            double v1[1] = {sg}, t1[1];
+            coop_exchange<1>(v1, t1, part, ctr, target, sh, sh_tot);
+            sigma = t1[0];
+        }
         if (sigma <= 0.0 && rho != 0.0) {  // breakdown (krylov.py:64-70)
             if (gt == 0) {
                 c->sigma = sigma;
@@ -592,7 +653,7 @@ cg_coop_res_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict_
             c->sigma = sigma;
             c->alpha = alpha;
             c->beta = beta;
-            hist_put(c, hist, it, nrm);
+            if (hist && it < hist_cap) hist[it] = nrm;
             if (stop) {
                 c->stopped = 1;
                 c->stopping_id = sid;
@@ -2275,7 +2336,7 @@ __global__ void krylov_start_clock_kernel(KrylovCtl* c) { c->t_start = global_ns
 extern "C" {
 
 int64_t b200sp_krylov_ctl_bytes(void) { return (int64_t)sizeof(KrylovCtl); }
-int64_t b200sp_krylov_part_elems(void) { return (int64_t)KRY_NRED * KRY_MAX_GRID; }
+int64_t b200sp_krylov_part_elems(void) { return (int64_t)(KRY_NRED + 2) * KRY_MAX_GRID; }  // + flagged slots
 
 int b200sp_krylov_ctl_init(void* ctl, int32_t n_crit, const int32_t* crit_type, const double* crit_param,
                            int32_t needs_residual, int32_t hist_cap, int32_t kdim, void* stream) {
@@ -2626,18 +2687,33 @@ static int cg_coop(int64_t n, const int32_t* rp, const int32_t* ci, const T* v, 
     if (grid < 1) grid = 1;
     KrylovCtl* c = (KrylovCtl*)ctl;
     void* args[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &p2, &q, &c, &part, &hist};
-    // rows per thread at this grid; up to 2 the register-resident kernel
-    // (same grid, same row ownership, same sums) runs instead -- if its
-    // occupancy allows the grid to be co-resident
-    const int64_t rpt = ceil_div(n, grid * (int64_t)threads);
+    // the register-resident kernel when a thread owns at most 2 rows of a
+    // co-resident grid of CG_RES_BLOCK-thread CTAs (larger CTAs: fewer
+    // partials to exchange per barrier)
     const void* fn = (const void*)cg_coop_kernel<T>;
-    if (rpt <= 2 && tuning("coop_resident", 1)) {
-        const void* res = rpt == 1 ? (const void*)cg_coop_res_kernel<T, 1, 8> : (const void*)cg_coop_res_kernel<T, 2, 8>;
-        int per_sm_res = 0;
-        B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_res, res, threads, 0));
-        if ((int64_t)per_sm_res * sms >= grid) fn = res;
+    const int res_bs = tuning("coop_res_block", 512);
+    if (n > 32 && tuning("coop_resident", 1) && (res_bs == 256 || res_bs == 512 || res_bs == 1024)) {
+        for (int rpt = 1; rpt <= 2 && fn == (const void*)cg_coop_kernel<T>; ++rpt) {
+            const void* res =
+                res_bs == 256 ? (rpt == 1 ? (const void*)cg_coop_res_kernel<T, 1, 8, 256> : (const void*)cg_coop_res_kernel<T, 2, 8, 256>)
+                : res_bs == 512 ? (rpt == 1 ? (const void*)cg_coop_res_kernel<T, 1, 8, 512> : (const void*)cg_coop_res_kernel<T, 2, 8, 512>)
+                                : (rpt == 1 ? (const void*)cg_coop_res_kernel<T, 1, 8, 1024> : (const void*)cg_coop_res_kernel<T, 2, 8, 1024>);
+            int per_sm_res = 0;
+            B200SP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_res, res, res_bs, 0));
+            int64_t g = ceil_div(n, (int64_t)res_bs * rpt);
+            if (cap > 0 && g > cap) continue;
+            if (g <= (int64_t)per_sm_res * sms && g <= KRY_MAX_GRID) {
+                fn = res;
+                grid = g;
+            }
+        }
     }
-    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(threads), args, 0, as_stream(stream)));
+    const unsigned nthr = fn == (const void*)cg_coop_kernel<T> ? threads : (unsigned)res_bs;
+    int nofence = tuning("coop_nofence", 1);
+    void* args_res[] = {&n, (void*)&rp, (void*)&ci, (void*)&v, &x, &r, &p, &p2, &q, &c, &part, &hist, &nofence};
+    B200SP_CHECK_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(nthr),
+                                                  fn == (const void*)cg_coop_kernel<T> ? args : args_res, 0,
+                                                  as_stream(stream)));
     count_launch();
     return B200SP_OK;
 }
