@@ -53,11 +53,6 @@ void b200sp_set_guard(const int32_t* guard);
  * unset knobs keep the measured-best defaults. Not thread-safe against
  * concurrent set calls; not needed for correct results. */
 int b200sp_set_tuning(const char* key, int32_t value);
-/* stream memory operations (driver cuStreamWriteValue32 / cuStreamWaitValue32,
- * default barrier / GEQ semantics): write `value` to a device word once the
- * stream's prior work is done; make later work wait for (int32)(*addr - value) >= 0 */
-int b200sp_stream_write_u32(void* stream, uint32_t* addr, uint32_t value);
-int b200sp_stream_wait_u32(void* stream, const uint32_t* addr, uint32_t value);
 int64_t b200sp_reduce_workspace_elems(void);
 int64_t b200sp_scan_workspace_elems(int64_t count);
 int b200sp_exclusive_scan_i32(int64_t count, const int32_t* in, int32_t* out, long long* ws, void* stream);
@@ -98,19 +93,6 @@ int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* row_ptrs, const int3
                                   const float* b, int64_t b_stride, float* x, int64_t x_stride, float alpha,
                                   const float* alpha_dev, float beta, const float* beta_dev, const float* x_in,
                                   int64_t x_in_stride, int32_t subwarp, void* stream);
-/* Csr classical, host-operand pipeline (Csr.apply with pinned host b / x):
- * ONE persistent launch walks k row chunks [bounds[j], bounds[j+1]); before
- * chunk j every CTA waits for flags[wait[j]] != 0 (wait[j] < 0: no wait),
- * after it the last CTA sets flags[2k + j] = 1 (flags[k + j] counts CTAs).
- * flags (3k words) must be zero at launch. The H2D / D2H streams drive the
- * flags with b200sp_stream_write_u32 / b200sp_stream_wait_u32. Replaces the
- * same CsrSpmvKernel as above (kernels.py:278-316). */
-int b200sp_csr_spmv_pipe_f64(int32_t k, const int64_t* bounds, const int32_t* wait, const int32_t* row_ptrs,
-                             const int32_t* col_idxs, const double* vals, const double* b, double* x,
-                             uint32_t* flags, int32_t subwarp, void* stream);
-int b200sp_csr_spmv_pipe_f32(int32_t k, const int64_t* bounds, const int32_t* wait, const int32_t* row_ptrs,
-                             const int32_t* col_idxs, const float* vals, const float* b, float* x,
-                             uint32_t* flags, int32_t subwarp, void* stream);
 /* Csr, stream strategy: a CTA of 256 threads owns (256 / tpr) * rpt
  * consecutive rows ((tpr, rpt) in {(1,1), (2,1), (4,1), (1,2), (1,4), (1,8)});
  * their nonzeros are staged through shared memory with 128-bit loads

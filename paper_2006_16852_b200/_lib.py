@@ -32,7 +32,6 @@ _TYPED = {
     "norm2": "liplpppp",
     # SpMV
     "csr_spmv_classical": "lpppplpl" + _SPMV_TAIL + "ip",
-    "csr_spmv_pipe": "ippppppppip",
     "csr_spmv_lb": "llpppplpl" + _SPMV_TAIL + "pppiip",
     "csr_spmv_stream": "llpppplpl" + _SPMV_TAIL + "iiiip",
     "csr_spmv_tma": "llpppplpl" + _SPMV_TAIL + "iiiiip",
@@ -138,8 +137,6 @@ _UNTYPED = {
     "powerlaw_lengths": ("lupipp", ctypes.c_int),
     "set_guard": ("p", None),
     "set_tuning": ("si", ctypes.c_int),
-    "stream_write_u32": ("ppi", ctypes.c_int),
-    "stream_wait_u32": ("ppi", ctypes.c_int),
     "assemble_workspace_bytes": ("l", ctypes.c_int64),
     "ilu_counts": ("lpppppp", ctypes.c_int),
     "csr_rows": ("lppp", ctypes.c_int),

@@ -9,8 +9,6 @@
 #include <cstring>
 #include <atomic>
 
-#include <cuda.h>
-
 #include "common.cuh"
 
 namespace b200sp {
@@ -252,18 +250,6 @@ static int dot_impl(int64_t n, int m, const T* x, int64_t xs, const T* y, int64_
 
 using namespace b200sp;
 
-// ---- stream memory operations (the host-operand pipeline's copy <-> kernel
-// handshakes): driver entry points, resolved once through the runtime ----
-typedef CUresult (*PfnStreamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-static PfnStreamValue32 stream_value_fn(const char* name) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
-        return (PfnStreamValue32)p;
-    return nullptr;
-}
-
 extern "C" {
 
 const char* b200sp_last_error(void) { return g_err; }
@@ -348,23 +334,5 @@ int b200sp_reduce_max_i32(int64_t count, const int32_t* in, int32_t* out, void* 
 
 BLAS1(double, f64)
 BLAS1(float, f32)
-
-// write `value` to device word `addr` once all prior work on `stream` is done
-// (with the default memory barrier: the prior copies are visible first)
-int b200sp_stream_write_u32(void* stream, uint32_t* addr, uint32_t value) {
-    static PfnStreamValue32 fn = stream_value_fn("cuStreamWriteValue32");
-    B200SP_REQUIRE(fn != nullptr, B200SP_ECUDA, "stream_write_u32: cuStreamWriteValue32 unavailable");
-    const CUresult r = fn((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT);
-    B200SP_REQUIRE(r == CUDA_SUCCESS, B200SP_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
-    return B200SP_OK;
-}
-// later work on `stream` waits until (int32_t)(*addr - value) >= 0
-int b200sp_stream_wait_u32(void* stream, const uint32_t* addr, uint32_t value) {
-    static PfnStreamValue32 fn = stream_value_fn("cuStreamWaitValue32");
-    B200SP_REQUIRE(fn != nullptr, B200SP_ECUDA, "stream_wait_u32: cuStreamWaitValue32 unavailable");
-    const CUresult r = fn((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ);
-    B200SP_REQUIRE(r == CUDA_SUCCESS, B200SP_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-    return B200SP_OK;
-}
 
 }  // extern "C"

@@ -34,13 +34,17 @@ namespace b200sp {
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)
 template <typename T, int SW, bool XIN, bool L1, int U>
-__device__ __forceinline__ void classical_rows(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                               const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
-                                               T* __restrict__ x, int64_t xs, T a, T bt, const T* __restrict__ xin,
-                                               int64_t xins) {
+__global__ void __launch_bounds__(256)
+csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
+                     const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
+                     T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
+                     const T* __restrict__ xin, int64_t xins) {
+    if (alpha.skip()) return;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & (SW - 1);
     const int64_t nsw = (int64_t)gridDim.x * blockDim.x / SW;
+    const T a = alpha.get();
+    const T bt = XIN ? beta.get() : T(0);
     // loop while the warp's first sub-warp has rows (uniform trip count: the
     // sub-warp shuffles below use the full mask); later sub-warps are masked
     const int64_t wfirst = (tid / 32) * (32 / SW) * U;
@@ -85,99 +89,6 @@ __device__ __forceinline__ void classical_rows(int64_t n, const int* __restrict_
             }
         }
     }
-}
-
-template <typename T, int SW, bool XIN, bool L1, int U>
-__global__ void __launch_bounds__(256)
-csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
-                     const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
-                     T* __restrict__ x, int64_t xs, Coef<T> alpha, Coef<T> beta,
-                     const T* __restrict__ xin, int64_t xins) {
-    if (alpha.skip()) return;
-    classical_rows<T, SW, XIN, L1, U>(n, rp, ci, v, b, bs, x, xs, alpha.get(), XIN ? beta.get() : T(0), xin, xins);
-}
-
-// ---------------------------------------------------------------------------
-// Host-operand pipeline (Csr.apply with pinned host b and x; the e2e path):
-// ONE persistent launch walks the row chunks in order. Before chunk j each
-// CTA waits for the flag the copy stream writes (cuStreamWriteValue32) after
-// the H2D copy of the last b chunk the rows read; after it, each CTA counts
-// itself done and the last one raises the chunk's output flag, which the D2H
-// stream waits on (cuStreamWaitValue32) before copying the x rows back. No
-// launch or event edge sits between a chunk's arrival and its SpMV, so the
-// SpMV keeps pace with the copy engines.
-// flags: [0, k) input flags, [k, 2k) CTA counters, [2k, 3k) output flags;
-// zeroed (memset) before every pass.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-template <typename T, int SW, int U>
-__global__ void __launch_bounds__(256)
-csr_pipe_kernel(int k, const int64_t* __restrict__ bounds, const int* __restrict__ wait, const int* __restrict__ rp,
-                const int* __restrict__ ci, const T* __restrict__ v, const T* __restrict__ b, T* __restrict__ x,
-                unsigned* flags, int pipe_backoff) {
-    for (int j = 0; j < k; ++j) {
-        if (threadIdx.x == 0 && wait[j] >= 0) {
-            const int backoff = pipe_backoff;
-            if (backoff > 0) {
-                while (*(volatile const unsigned*)(flags + wait[j]) == 0) __nanosleep(backoff);
-                __threadfence_system();
-            } else {
-                while (ld_acquire_sys_u32(flags + wait[j]) == 0) {
-                }
-            }
-        }
-        __syncthreads();
-        const int64_t r0 = bounds[j];
-        classical_rows<T, SW, false, true, U>(bounds[j + 1] - r0, rp + r0, ci, v, b, 1, x + r0, 1, T(1), T(0),
-                                              nullptr, 0);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence_system();
-            if (atomicAdd(flags + k + j, 1u) == gridDim.x - 1) {
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags + 2 * k + j), "r"(1u) : "memory");
-            }
-        }
-    }
-}
-
-template <typename T, int SW>
-static void launch_pipe(int k, const int64_t* bounds, const int* wait, const int* rp, const int* ci, const T* v,
-                        const T* b, T* x, unsigned* flags, cudaStream_t st) {
-    constexpr int U = ClassicalRows<SW>::v;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_pipe_kernel<T, SW, U>, 256, 0);
-    const int cap = tuning("pipe_per_sm", 0);
-    if (cap > 0 && per_sm > cap) per_sm = cap;
-    // every CTA co-resident: a chunk's CTAs start the moment its flag rises
-    csr_pipe_kernel<T, SW, U><<<sms * (per_sm > 0 ? per_sm : 1), 256, 0, st>>>(k, bounds, wait, rp, ci, v, b, x, flags,
-                                                                                 tuning("pipe_backoff", 0));
-}
-
-template <typename T>
-static int csr_pipe(int k, const int64_t* bounds, const int* wait, const int* rp, const int* ci, const T* v, const T* b,
-                    T* x, unsigned* flags, int subwarp, void* stream) {
-    if (k <= 0) return B200SP_OK;
-    cudaStream_t st = as_stream(stream);
-    switch (subwarp) {
-        case 1: launch_pipe<T, 1>(k, bounds, wait, rp, ci, v, b, x, flags, st); break;
-        case 2: launch_pipe<T, 2>(k, bounds, wait, rp, ci, v, b, x, flags, st); break;
-        case 4: launch_pipe<T, 4>(k, bounds, wait, rp, ci, v, b, x, flags, st); break;
-        case 8: launch_pipe<T, 8>(k, bounds, wait, rp, ci, v, b, x, flags, st); break;
-        case 16: launch_pipe<T, 16>(k, bounds, wait, rp, ci, v, b, x, flags, st); break;
-        case 32: launch_pipe<T, 32>(k, bounds, wait, rp, ci, v, b, x, flags, st); break;
-        default: set_error("csr pipe: subwarp must be a power of two <= 32 (got %d)", subwarp);
-                 return B200SP_EINVAL;
-    }
-    count_launch();
-    return check_launch("csr_pipe");
 }
 
 template <typename T, int SW>
@@ -1669,17 +1580,6 @@ int b200sp_csr_spmv_classical_f32(int64_t n, const int32_t* rp, const int32_t* c
                                   const float* alpha_dev, float beta, const float* beta_dev,
                                   const float* xin, int64_t xins, int32_t subwarp, void* stream) {
     return csr_classical<float>(n, rp, ci, v, b, bs, x, xs, alpha, alpha_dev, beta, beta_dev, xin, xins, subwarp, stream);
-}
-
-int b200sp_csr_spmv_pipe_f64(int32_t k, const int64_t* bounds, const int32_t* wait, const int32_t* rp, const int32_t* ci,
-                             const double* v, const double* b, double* x, uint32_t* flags, int32_t subwarp,
-                             void* stream) {
-    return csr_pipe<double>(k, bounds, wait, rp, ci, v, b, x, flags, subwarp, stream);
-}
-int b200sp_csr_spmv_pipe_f32(int32_t k, const int64_t* bounds, const int32_t* wait, const int32_t* rp, const int32_t* ci,
-                             const float* v, const float* b, float* x, uint32_t* flags, int32_t subwarp,
-                             void* stream) {
-    return csr_pipe<float>(k, bounds, wait, rp, ci, v, b, x, flags, subwarp, stream);
 }
 
 int b200sp_csr_spmv_stream_f64(int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v,

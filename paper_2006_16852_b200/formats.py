@@ -693,9 +693,6 @@ class Csr(_Sparse):
     # -- host operands: pipelined transfers -----------------------------------------
     #: row chunks of the pipelined host apply (0 disables it)
     HOST_PIPELINE_CHUNKS = 8  # 4 / 8 / 16 measured 0.626 / 0.568 / 0.649 ms on C2 (link ceiling 0.38)
-    #: "flags": one persistent SpMV launch driven by copy-stream flags
-    #: (b200sp_csr_spmv_pipe); "events": one SpMV launch per chunk behind events
-    HOST_PIPELINE_MODE = "flags"
 
     def apply(self, b, x):
         """x <- A b. With both operands in host (pinned) memory, a single column
@@ -759,9 +756,6 @@ class Csr(_Sparse):
             wait = [next(i for i in range(k) if cb[i + 1] > nd) if nd >= 0 else -1 for nd in need]
             dev = self.exec.device
             plan = {"rows": bounds, "cols": cb, "wait": wait,
-                    "bounds_dev": torch.tensor(bounds, dtype=torch.int64, device=dev),
-                    "wait_dev": torch.tensor(wait, dtype=torch.int32, device=dev),
-                    "flags": torch.zeros(3 * k, dtype=torch.int32, device=dev),
                     "s_in": torch.cuda.Stream(dev), "s_out": torch.cuda.Stream(dev),
                     "b": torch.empty(m, dtype=self._v.dtype, device=dev),
                     "x": torch.empty(n, dtype=self._v.dtype, device=dev)}
@@ -789,8 +783,6 @@ class Csr(_Sparse):
         torch.cuda.current_stream(self.exec.device).synchronize()
 
     def _pipeline_issue(self, P, bh, xh):
-        if self.HOST_PIPELINE_MODE == "flags":
-            return self._pipeline_issue_flags(P, bh, xh)
         exc = self.exec
         k = len(P["wait"])
         bd, xd = P["b"], P["x"]
@@ -819,35 +811,6 @@ class Csr(_Sparse):
             e.record(cur)
             s_out.wait_event(e)
             with torch.cuda.stream(s_out):
-                xh[r0:r1].copy_(xd[r0:r1], non_blocking=True)
-        cur.wait_stream(s_in)
-        cur.wait_stream(s_out)
-
-    def _pipeline_issue_flags(self, P, bh, xh):
-        """H2D chunk j, then flag j (s_in); ONE persistent SpMV launch that
-        starts each row chunk when its last b chunk's flag rises (current
-        stream); wait for row chunk j's output flag, then D2H it (s_out)."""
-        exc = self.exec
-        k = len(P["wait"])
-        bd, xd, fl = P["b"], P["x"], P["flags"]
-        cur = torch.cuda.current_stream(exc.device)
-        fl.zero_()
-        s_in, s_out = P["s_in"], P["s_out"]
-        s_in.wait_stream(cur)
-        s_out.wait_stream(cur)
-        fp = fl.data_ptr()
-        with torch.cuda.stream(s_in):
-            for i in range(k):
-                lo, hi = P["cols"][i], P["cols"][i + 1]
-                bd[lo:hi].copy_(bh[lo:hi], non_blocking=True)
-                _lib.call("stream_write_u32", s_in.cuda_stream, fp + 4 * i, 1)
-        suf = _lib.suffix(self._v.dtype)
-        _lib.call("csr_spmv_pipe_" + suf, k, ptr(P["bounds_dev"]), ptr(P["wait_dev"]), ptr(self._rp), ptr(self._ci),
-                  ptr(self._v), ptr(bd), ptr(xd), fp, self.subwarp(), cur.cuda_stream)
-        with torch.cuda.stream(s_out):
-            for j in range(k):
-                r0, r1 = P["rows"][j], P["rows"][j + 1]
-                _lib.call("stream_wait_u32", s_out.cuda_stream, fp + 4 * (2 * k + j), 1)
                 xh[r0:r1].copy_(xd[r0:r1], non_blocking=True)
         cur.wait_stream(s_in)
         cur.wait_stream(s_out)
