@@ -33,7 +33,13 @@ namespace b200sp {
 
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)
-template <typename T, int SW, bool XIN, bool L1, int U>
+// KM > 0 (U = 1): rows of at most SW * KM entries take a batched path -- the
+// lane's KM column indices and values are loaded first, then its KM gathers,
+// then the KM FMAs in entry order (so the same sums as the loop below): all
+// of a row's loads are in flight together instead of the compiler's pairs
+// of (index load -> gather) round trips (ncu: 41 of 47 stall cycles per
+// issued instruction were long-scoreboard waits in the loop form).
+template <typename T, int SW, bool XIN, bool L1, int U, int KM = 0>
 __global__ void __launch_bounds__(256)
 csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
                      const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
@@ -62,18 +68,36 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
         T acc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = 0;
-        for (int k = lane; k < maxlen; k += SW) {
-            int c[U];
-            T vv[U];
+        if (KM > 0 && U == 1 && maxlen <= SW * KM) {
+            constexpr int K = KM > 0 ? KM : 1;
+            int c[K];
+            T vv[K], g[K];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const bool ok = k < len[u];
-                c[u] = ok ? (L1 ? __ldg(ci + s[u] + k) : ld_stream(ci + s[u] + k)) : -1;
-                vv[u] = ok ? (L1 ? __ldg(v + s[u] + k) : ld_stream(v + s[u] + k)) : T(0);
+            for (int j = 0; j < K; ++j) {
+                const int k = lane + j * SW;
+                const bool ok = k < len[0];
+                c[j] = ok ? (L1 ? __ldg(ci + s[0] + k) : ld_stream(ci + s[0] + k)) : -1;
+                vv[j] = ok ? (L1 ? __ldg(v + s[0] + k) : ld_stream(v + s[0] + k)) : T(0);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
+            for (int j = 0; j < K; ++j) g[j] = c[j] >= 0 ? ld_gather(b + (int64_t)c[j] * bs) : T(0);
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (c[j] >= 0) acc[0] += vv[j] * g[j];
+        } else {
+            for (int k = lane; k < maxlen; k += SW) {
+                int c[U];
+                T vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool ok = k < len[u];
+                    c[u] = ok ? (L1 ? __ldg(ci + s[u] + k) : ld_stream(ci + s[u] + k)) : -1;
+                    vv[u] = ok ? (L1 ? __ldg(v + s[u] + k) : ld_stream(v + s[u] + k)) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = subwarp_sum<SW>(acc[u]);
@@ -108,6 +132,11 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
     const int grid = grid_for(ceil_div(n, two ? U2 : U0) * SW, block, tuning("classical_per_sm", 32));
     auto kern = two ? (xin ? csr_classical_kernel<T, SW, true, true, U2> : csr_classical_kernel<T, SW, false, true, U2>)
                     : (xin ? csr_classical_kernel<T, SW, true, true, U0> : csr_classical_kernel<T, SW, false, true, U0>);
+    if (!two && U0 == 1) {  // batched loads for rows up to SW * km entries (knob "classical_km": 0 / 4 / 8)
+        const int km = tuning("classical_km", 8);
+        if (km == 4) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 4> : csr_classical_kernel<T, SW, false, true, 1, 4>;
+        if (km == 8) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 8> : csr_classical_kernel<T, SW, false, true, 1, 8>;
+    }
     kern<<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
 }
 
@@ -652,24 +681,28 @@ __global__ void csr_lb_fixup_kernel(int64_t n, int64_t ntiles, const int* __rest
 // ---------------------------------------------------------------------------
 constexpr int LB2_LONG = 16;  // x sub-warp width: longer rows take the CTA-wide pass
 
+// rows [r0, r_end) of a tile; row rc (the tile's carried-out last row, or
+// -1) ends at the tile's last entry kc and its partial sum goes to *s_carry
+// for the fix-up instead of x -- it is just one more row of the loop, so no
+// warp-0 epilogue holds the CTA's slot after the other warps are done
 template <typename T, int SW, bool XIN, bool UNR4>
-__device__ __forceinline__ void lb2_rows(int r0, int r1, int k0, const int* __restrict__ rp,
+__device__ __forceinline__ void lb2_rows(int r0, int r_end, int k0, int rc, int kc, const int* __restrict__ rp,
                                          const int* __restrict__ ci, const T* __restrict__ v,
                                          const T* __restrict__ b, int64_t bs, T* __restrict__ x, int64_t xs,
                                          T a, T bt, const T* __restrict__ xin, int64_t xins, int* s_long,
-                                         int* s_nlong) {
+                                         int* s_nlong, T* s_carry) {
     const int lane = threadIdx.x & (SW - 1);
     constexpr int SPW = 32 / SW;  // sub-warps per warp
     // the trip count is uniform across a warp (the sub-warp shuffles use the
-    // full mask); rows past r1 are masked
+    // full mask); rows past r_end are masked
 #pragma unroll 1
-    for (int rb = r0 + (threadIdx.x >> 5) * SPW; rb < r1; rb += LB_BLOCK / SW) {
+    for (int rb = r0 + (threadIdx.x >> 5) * SPW; rb < r_end; rb += LB_BLOCK / SW) {
         const int row = rb + (threadIdx.x & 31) / SW;
-        const bool active = row < r1;
+        const bool active = row < r_end;
         int s = 0, e = 0;
         if (active) {
             s = max(__ldg(rp + row), k0);
-            e = __ldg(rp + row + 1);
+            e = row == rc ? kc : __ldg(rp + row + 1);
         }
         const bool lng = e - s > LB2_LONG * SW;
         if (lng) {  // deferred to the CTA-wide pass
@@ -692,9 +725,13 @@ __device__ __forceinline__ void lb2_rows(int r0, int r1, int k0, const int* __re
         }
         const T sum = subwarp_sum<SW>((a0 + a1) + (a2 + a3));
         if (active && !lng && lane == 0) {
-            T out = a * sum;
-            if (XIN) out += bt * xin[(int64_t)row * xins];
-            x[(int64_t)row * xs] = out;
+            if (row == rc) {
+                *s_carry = sum;
+            } else {
+                T out = a * sum;
+                if (XIN) out += bt * xin[(int64_t)row * xins];
+                x[(int64_t)row * xs] = out;
+            }
         }
     }
 }
@@ -724,57 +761,56 @@ csr_lb2_kernel(int64_t n, int64_t ntiles, const int* __restrict__ rp, const int*
     __shared__ int s_long[LB_BLOCK];
     __shared__ int s_nlong;
     __shared__ T s_red[LB_BLOCK / 32];
+    __shared__ T s_carry;
     const T a = alpha.get();
     const T bt = XIN ? beta.get() : T(0);
-    // persistent CTAs over equal-work tiles (no last-wave tail)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int r0 = coords[2 * tile], k0 = coords[2 * tile + 1];
         const int r1 = coords[2 * tile + 2], k1 = coords[2 * tile + 3];
-        if (threadIdx.x == 0) s_nlong = 0;
+        if (threadIdx.x == 0) {
+            s_nlong = 0;
+            s_carry = T(0);
+        }
         __syncthreads();
-        const int nrows = r1 - r0;
+        // rows r0 .. r1 - 1, plus the carried-out row r1 (its entries before k1)
+        const int rc = r1 < n ? r1 : -1;
+        const int r_end = rc >= 0 ? r1 + 1 : r1;
+        const int nrows = r_end - r0;
         if (nrows > 0) {
             // sub-warp width from the tile's mean row length (classical rule)
             const int mean = (k1 - k0 + nrows - 1) / nrows;
             const int per_lane = (mean + 7) / 8;
-            if (per_lane <= 1) lb2_rows<T, 1, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 2) lb2_rows<T, 2, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 4) lb2_rows<T, 4, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 8) lb2_rows<T, 8, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else if (per_lane <= 16) lb2_rows<T, 16, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
-            else lb2_rows<T, 32, XIN, UNR4>(r0, r1, k0, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, s_long, &s_nlong);
+#define LB2_ROWS(SW) lb2_rows<T, SW, XIN, UNR4>(r0, r_end, k0, rc, k1, rp, ci, v, b, bs, x, xs, a, bt, xin, xins, \
+                                                  s_long, &s_nlong, &s_carry)
+            if (per_lane <= 1) { LB2_ROWS(1); }
+            else if (per_lane <= 2) { LB2_ROWS(2); }
+            else if (per_lane <= 4) { LB2_ROWS(4); }
+            else if (per_lane <= 8) { LB2_ROWS(8); }
+            else if (per_lane <= 16) { LB2_ROWS(16); }
+            else { LB2_ROWS(32); }
+#undef LB2_ROWS
         }
         __syncthreads();
         const int nlong = s_nlong;
         for (int i = 0; i < nlong; ++i) {
             const int row = s_long[i];
-            const T sum = lb2_block_dot(max(__ldg(rp + row), k0), __ldg(rp + row + 1), ci, v, b, bs, s_red);
+            const int e = row == rc ? k1 : __ldg(rp + row + 1);
+            const T sum = lb2_block_dot(max(__ldg(rp + row), k0), e, ci, v, b, bs, s_red);
             if (threadIdx.x == 0) {
-                T out = a * sum;
-                if (XIN) out += bt * xin[(int64_t)row * xins];
-                x[(int64_t)row * xs] = out;
-            }
-        }
-        // carry-out: the entries of row r1 inside this tile (a short segment
-        // -- up to 128 entries -- is summed by warp 0 alone, no CTA barrier)
-        T carry = 0;
-        if (r1 < n) {
-            const int cs = max(__ldg(rp + r1), k0);
-            if (k1 - cs <= 128) {
-                if (threadIdx.x < 32) {
-                    T a0 = 0;
-                    for (int k = cs + (int)threadIdx.x; k < k1; k += 32)
-                        a0 += __ldg(v + k) * ld_gather(b + (int64_t)__ldg(ci + k) * bs);
-                    carry = warp_sum(a0);
+                if (row == rc) {
+                    s_carry = sum;
+                } else {
+                    T out = a * sum;
+                    if (XIN) out += bt * xin[(int64_t)row * xins];
+                    x[(int64_t)row * xs] = out;
                 }
-            } else {
-                carry = lb2_block_dot(cs, k1, ci, v, b, bs, s_red);
             }
         }
         if (threadIdx.x == 0) {
             carry_row[tile] = r1;
-            carry_val[tile] = carry;
+            carry_val[tile] = s_carry;
         }
+        if (gridDim.x < ntiles) __syncthreads();  // persistent: s_carry / s_nlong are reused
     }
 }
 

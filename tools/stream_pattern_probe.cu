@@ -1,0 +1,174 @@
+// Read-bandwidth of HBM streaming patterns (B200): does chunk-per-CTA
+// streaming (load-balanced CSR tiles, Coo warp chunks) lose to grid-stride
+// streaming at the same bytes?
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/spp tools/stream_pattern_probe.cu && /tmp/spp
+//
+// Each kernel sums 1 GiB of doubles with 128-bit loads, 256-thread CTAs:
+//   gridstride  : CTA-sized 4 KiB blocks dealt round-robin over a 2-wave grid
+//   chunk/CTA   : each CTA (one per chunk, many waves) walks its own contiguous
+//                 chunk of `chunk` bytes, the CTA's threads side by side
+//   chunk/warp  : each warp walks its own contiguous chunk
+#include <cstdio>
+#include <cstdint>
+
+__device__ double g_sink;
+__device__ __forceinline__ double sum_of(float v) { return v; }
+__device__ __forceinline__ double sum_of(double v) { return v; }
+__device__ __forceinline__ double sum_of(double2 v) { return v.x + v.y; }
+__device__ __forceinline__ double sum_of(float4 v) { return (double)v.x + v.y + v.z + v.w; }
+
+__global__ void k_gridstride(const double2* __restrict__ a, int64_t n2) {
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 v = __ldcs(a + i);
+        s += v.x + v.y;
+    }
+    if (s == 12345.678) g_sink = s;
+}
+
+__global__ void k_chunk_cta(const double2* __restrict__ a, int64_t n2, int64_t per) {
+    double s = 0;
+    const int64_t base = (int64_t)blockIdx.x * per;
+    for (int64_t i = base + threadIdx.x; i < base + per && i < n2; i += blockDim.x) {
+        double2 v = __ldcs(a + i);
+        s += v.x + v.y;
+    }
+    if (s == 12345.678) g_sink = s;
+}
+
+__global__ void k_chunk_warp(const double2* __restrict__ a, int64_t n2, int64_t per) {
+    double s = 0;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t base = w * per;
+    for (int64_t i = base + lane; i < base + per && i < n2; i += 32) {
+        double2 v = __ldcs(a + i);
+        s += v.x + v.y;
+    }
+    if (s == 12345.678) g_sink = s;
+}
+
+// element width / cache policy: T = float, double, double2; POL 0 = __ldcs
+// (evict-first streaming), 1 = __ldg (L1-allocating), 2 = plain load
+template <typename T, int POL>
+__global__ void k_width(const T* __restrict__ a, int64_t n) {
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T v = POL == 0 ? __ldcs(a + i) : POL == 1 ? __ldg(a + i) : a[i];
+        s += sum_of(v);
+    }
+    if (s == 12345.678) g_sink = s;
+}
+
+// SpMV-like streams: n entries of (int32 column, double value) read as two
+// arrays (1/3 + 2/3 of the bytes) with VEC entries per lane per load
+// (VEC 1: 4-byte + 8-byte loads, VEC 4: int4 + 2x double2), optionally a
+// gather b[col] per entry (b = 2M doubles, L2-resident, 27-point-like columns)
+// and one 8-byte store per 27 entries (the x write)
+template <int VEC, bool GATHER, bool WRITE>
+__global__ void k_spmv_like(const int* __restrict__ ci, const double* __restrict__ v, const double* __restrict__ b,
+                            double* __restrict__ x, int64_t n) {
+    double s = 0;
+    const int64_t nv = n / VEC;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        if (VEC == 1) {
+            const int c = __ldg(ci + i);
+            const double a = __ldg(v + i);
+            s += GATHER ? a * __ldg(b + c) : a + c;
+        } else {
+            const int4 c = __ldg(reinterpret_cast<const int4*>(ci) + i);
+            const double2 a0 = __ldg(reinterpret_cast<const double2*>(v) + 2 * i);
+            const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + 2 * i + 1);
+            if (GATHER)
+                s += a0.x * __ldg(b + c.x) + a0.y * __ldg(b + c.y) + a1.x * __ldg(b + c.z) + a1.y * __ldg(b + c.w);
+            else
+                s += a0.x + a0.y + a1.x + a1.y + c.x + c.y + c.z + c.w;
+        }
+        if (WRITE && (i % (27 / VEC)) == 0) x[(i / (27 / VEC)) % 2097152] = s;
+    }
+    if (s == 12345.678) g_sink = s;
+}
+
+template <typename F>
+static float timeit(F f) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    f();
+    cudaEventRecord(a);
+    for (int r = 0; r < 10; ++r) f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms / 10;
+}
+
+int main() {
+    const int64_t bytes = 1ll << 30, n2 = bytes / 16;
+    double2* a;
+    cudaMalloc(&a, bytes);
+    cudaMemset(a, 0, bytes);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    for (int per_sm : {4, 8}) {
+        const int grid = sms * per_sm;
+        float ms = timeit([&] { k_gridstride<<<grid, 256>>>(a, n2); });
+        printf("gridstride   grid %5d             : %7.1f GB/s\n", grid, bytes / ms / 1e6);
+    }
+    for (int64_t chunk : {16384ll, 65536ll, 196608ll, 786432ll}) {
+        const int64_t per = chunk / 16;
+        const int64_t grid = (n2 + per - 1) / per;
+        float ms = timeit([&] { k_chunk_cta<<<(unsigned)grid, 256>>>(a, n2, per); });
+        printf("chunk/CTA    chunk %7lld B        : %7.1f GB/s\n", (long long)chunk, bytes / ms / 1e6);
+    }
+    for (int64_t chunk : {4096ll, 16384ll, 65536ll}) {
+        const int64_t per = chunk / 16;
+        const int64_t warps = (n2 + per - 1) / per;
+        float ms = timeit([&] { k_chunk_warp<<<(unsigned)((warps + 7) / 8), 256>>>(a, n2, per); });
+        printf("chunk/warp   chunk %7lld B        : %7.1f GB/s\n", (long long)chunk, bytes / ms / 1e6);
+    }
+    const int grid = sms * 8;
+    const char* pol[] = {"ldcs", "ldg", "plain"};
+#define WIDTH(T, P)                                                                                     \
+    {                                                                                                   \
+        float ms = timeit([&] { k_width<T, P><<<grid, 256>>>((const T*)a, bytes / (int64_t)sizeof(T)); }); \
+        printf("gridstride %2d-byte loads, %-5s   : %7.1f GB/s\n", (int)sizeof(T), pol[P], bytes / ms / 1e6); \
+    }
+    WIDTH(float, 0) WIDTH(float, 1) WIDTH(float, 2)
+    WIDTH(double, 0) WIDTH(double, 1) WIDTH(double, 2)
+    WIDTH(double2, 0) WIDTH(double2, 1) WIDTH(double2, 2)
+    {
+        // 56.6M entries (C2), 27-point-like columns over 2.1M rows
+        const int64_t n = 56623104, rows = 2097152;
+        int* ci;
+        double *v, *bb, *x;
+        cudaMalloc(&ci, n * 4);
+        cudaMalloc(&v, n * 8);
+        cudaMalloc(&bb, rows * 8);
+        cudaMalloc(&x, rows * 8);
+        cudaMemset(bb, 0, rows * 8);
+        cudaMemset(v, 0, n * 8);
+        int* h = (int*)malloc(n * 4);
+        const int off[27] = {-16513, -16512, -16511, -16385, -16384, -16383, -16257, -16256, -16255,
+                             -129, -128, -127, -1, 0, 1, 127, 128, 129,
+                             16255, 16256, 16257, 16383, 16384, 16385, 16511, 16512, 16513};
+        for (int64_t k = 0; k < n; ++k) {
+            int64_t c = k / 27 + off[k % 27];
+            h[k] = (int)(c < 0 ? 0 : c >= rows ? rows - 1 : c);
+        }
+        cudaMemcpy(ci, h, n * 4, cudaMemcpyHostToDevice);
+        free(h);
+        const double by = n * 12.0, byw = by + rows * 8.0;
+#define SPL(VEC, G, W)                                                                                    \
+        {                                                                                                 \
+            float ms = timeit([&] { k_spmv_like<VEC, G, W><<<grid, 256>>>(ci, v, bb, x, n); });           \
+            printf("spmv-like vec %d gather %d write %d       : %7.1f GB/s (matrix%s bytes)\n", VEC, G, W, \
+                   (W ? byw : by) / ms / 1e6, W ? " + x" : "");                                           \
+        }
+        SPL(1, false, false) SPL(4, false, false) SPL(1, true, false) SPL(4, true, false)
+        SPL(1, false, true) SPL(4, false, true) SPL(1, true, true) SPL(4, true, true)
+    }
+    return 0;
+}
