@@ -33,13 +33,7 @@ namespace b200sp {
 
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)
-// KM > 0 (U = 1): rows of at most SW * KM entries take a batched path -- the
-// lane's KM column indices and values are loaded first, then its KM gathers,
-// then the KM FMAs in entry order (so the same sums as the loop below): all
-// of a row's loads are in flight together instead of the compiler's pairs
-// of (index load -> gather) round trips (ncu: 41 of 47 stall cycles per
-// issued instruction were long-scoreboard waits in the loop form).
-template <typename T, int SW, bool XIN, bool L1, int U, int KM = 0>
+template <typename T, int SW, bool XIN, bool L1, int U>
 __global__ void __launch_bounds__(256)
 csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
                      const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
@@ -68,36 +62,18 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
         T acc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = 0;
-        if (KM > 0 && U == 1 && maxlen <= SW * KM) {
-            constexpr int K = KM > 0 ? KM : 1;
-            int c[K];
-            T vv[K], g[K];
+        for (int k = lane; k < maxlen; k += SW) {
+            int c[U];
+            T vv[U];
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const int k = lane + j * SW;
-                const bool ok = k < len[0];
-                c[j] = ok ? (L1 ? __ldg(ci + s[0] + k) : ld_stream(ci + s[0] + k)) : -1;
-                vv[j] = ok ? (L1 ? __ldg(v + s[0] + k) : ld_stream(v + s[0] + k)) : T(0);
+            for (int u = 0; u < U; ++u) {
+                const bool ok = k < len[u];
+                c[u] = ok ? (L1 ? __ldg(ci + s[u] + k) : ld_stream(ci + s[u] + k)) : -1;
+                vv[u] = ok ? (L1 ? __ldg(v + s[u] + k) : ld_stream(v + s[u] + k)) : T(0);
             }
 #pragma unroll
-            for (int j = 0; j < K; ++j) g[j] = c[j] >= 0 ? ld_gather(b + (int64_t)c[j] * bs) : T(0);
-#pragma unroll
-            for (int j = 0; j < K; ++j)
-                if (c[j] >= 0) acc[0] += vv[j] * g[j];
-        } else {
-            for (int k = lane; k < maxlen; k += SW) {
-                int c[U];
-                T vv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const bool ok = k < len[u];
-                    c[u] = ok ? (L1 ? __ldg(ci + s[u] + k) : ld_stream(ci + s[u] + k)) : -1;
-                    vv[u] = ok ? (L1 ? __ldg(v + s[u] + k) : ld_stream(v + s[u] + k)) : T(0);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
-            }
+            for (int u = 0; u < U; ++u)
+                if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = subwarp_sum<SW>(acc[u]);
@@ -132,11 +108,6 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
     const int grid = grid_for(ceil_div(n, two ? U2 : U0) * SW, block, tuning("classical_per_sm", 32));
     auto kern = two ? (xin ? csr_classical_kernel<T, SW, true, true, U2> : csr_classical_kernel<T, SW, false, true, U2>)
                     : (xin ? csr_classical_kernel<T, SW, true, true, U0> : csr_classical_kernel<T, SW, false, true, U0>);
-    if (!two && U0 == 1) {  // batched loads for rows up to SW * km entries (knob "classical_km": 0 / 4 / 8)
-        const int km = tuning("classical_km", 8);
-        if (km == 4) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 4> : csr_classical_kernel<T, SW, false, true, 1, 4>;
-        if (km == 8) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 8> : csr_classical_kernel<T, SW, false, true, 1, 8>;
-    }
     kern<<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
 }
 
