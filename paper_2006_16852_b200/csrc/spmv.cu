@@ -33,7 +33,17 @@ namespace b200sp {
 
 // L1: matrix reads allocate in L1 (a sub-warp touches only part of each
 // sector per step; the next steps re-read the rest of it from L1, not L2)
-template <typename T, int SW, bool XIN, bool L1, int U>
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+// KB > 0 (U = 1): the row's entries in predicated blocks of KB per lane --
+// every load of a block is issued before its gathers and no remainder loop
+// adds dependent (index -> gather) round trips after the unrolled body (a
+// 27-entry row at sub-warp 4 is 7 entries per lane: one block of 4 and one
+// of 3 instead of the compiler's pairs plus 2- and 1-entry tails). Same
+// single accumulator and entry order as the loop: the same sums.
+template <typename T, int SW, bool XIN, bool L1, int U, int KB = 0>
 __global__ void __launch_bounds__(256)
 csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci,
                      const T* __restrict__ v, const T* __restrict__ b, int64_t bs,
@@ -62,6 +72,52 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
         T acc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = 0;
+        if (KB < 0 && U == 1) {
+            // entry pairs: lane l reads the 8-byte-aligned pairs (index, value)
+            // starting at (s & ~1) + 2 l; entries outside [s, e) are masked
+            // (a row's first / last pair may straddle its neighbours)
+            constexpr int K = KB < 0 ? -KB : 1;  // pairs per lane per block
+            const int s0 = s[0], e0 = s[0] + len[0];
+            const int a0 = s0 & ~1;
+#pragma unroll 1
+            for (int k0 = a0 + 2 * lane; k0 < e0; k0 += 2 * K * SW) {
+                int2 c[K];
+                typename Vec2<T>::type vv[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int k = k0 + j * 2 * SW;
+                    if (k < e0) {
+                        c[j] = __ldg(reinterpret_cast<const int2*>(ci + k));
+                        vv[j] = __ldg(reinterpret_cast<const typename Vec2<T>::type*>(v + k));
+                    } else {
+                        c[j] = make_int2(-1, -1);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int k = k0 + j * 2 * SW;
+                    if (k >= s0 && c[j].x >= 0) acc[0] += vv[j].x * ld_gather(b + (int64_t)c[j].x * bs);
+                    if (k + 1 < e0 && c[j].y >= 0) acc[0] += vv[j].y * ld_gather(b + (int64_t)c[j].y * bs);
+                }
+            }
+        } else if (KB > 0 && U == 1) {
+            constexpr int K = KB > 0 ? KB : 1;
+#pragma unroll 1
+            for (int k0 = lane; k0 < maxlen; k0 += K * SW) {
+                int c[K];
+                T vv[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int k = k0 + j * SW;
+                    const bool ok = k < len[0];
+                    c[j] = ok ? (L1 ? __ldg(ci + s[0] + k) : ld_stream(ci + s[0] + k)) : -1;
+                    vv[j] = ok ? (L1 ? __ldg(v + s[0] + k) : ld_stream(v + s[0] + k)) : T(0);
+                }
+#pragma unroll
+                for (int j = 0; j < K; ++j)
+                    if (c[j] >= 0) acc[0] += vv[j] * ld_gather(b + (int64_t)c[j] * bs);
+            }
+        } else
         for (int k = lane; k < maxlen; k += SW) {
             int c[U];
             T vv[U];
@@ -108,6 +164,23 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
     const int grid = grid_for(ceil_div(n, two ? U2 : U0) * SW, block, tuning("classical_per_sm", 32));
     auto kern = two ? (xin ? csr_classical_kernel<T, SW, true, true, U2> : csr_classical_kernel<T, SW, false, true, U2>)
                     : (xin ? csr_classical_kernel<T, SW, true, true, U0> : csr_classical_kernel<T, SW, false, true, U0>);
+    const bool pairs_ok = ((reinterpret_cast<uintptr_t>(ci) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    if (!two && U0 == 1) {
+        // predicated entry blocks (knob "classical_kb": 0 = the loop, 2 / 3 / 4
+        // entries per lane per block, -1 / -2 / -4 aligned (index, value) pairs
+        // per lane per block). Measured (profiles/r03_classical_kb.txt): pairs
+        // in blocks of 2 win for fp32 (27-point 0.715 -> 0.808, 7-point 0.767
+        // -> 0.886, 5-point 0.720 -> 0.789) and fp64 thread-per-row (7-point
+        // 0.816 -> 0.876); fp64 sub-warp 4 (27-point) keeps 4-entry blocks
+        // (0.826, pairs 0.735)
+        const int kb = tuning("classical_kb", (sizeof(T) == 4 || SW == 1) ? -2 : 4);
+        if (kb == -1 && pairs_ok) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, -1> : csr_classical_kernel<T, SW, false, true, 1, -1>;
+        if (kb == -2 && pairs_ok) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, -2> : csr_classical_kernel<T, SW, false, true, 1, -2>;
+        if (kb == -4 && pairs_ok) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, -4> : csr_classical_kernel<T, SW, false, true, 1, -4>;
+        if (kb == 2) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 2> : csr_classical_kernel<T, SW, false, true, 1, 2>;
+        if (kb == 3) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 3> : csr_classical_kernel<T, SW, false, true, 1, 3>;
+        if (kb == 4) kern = xin ? csr_classical_kernel<T, SW, true, true, 1, 4> : csr_classical_kernel<T, SW, false, true, 1, 4>;
+    }
     kern<<<grid, block, 0, st>>>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins);
 }
 
@@ -1406,10 +1479,18 @@ __device__ __forceinline__ T strided_dot(const int* __restrict__ ci, const T* __
         for (int u = 0; u < UNR; ++u)
             if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
     }
-#pragma unroll 1
-    for (; k < len; ++k) {
-        const int c = ld_stream(ci + base + (int64_t)k * step);
-        if (c >= 0) acc[0] += ld_stream(v + base + (int64_t)k * step) * ld_gather(b + (int64_t)c * bs);
+    if (k < len) {  // the tail as one more predicated block: its loads in flight together
+        int c[UNR];
+        T vv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const bool ok = k + u < len;
+            c[u] = ok ? ld_stream(ci + base + (int64_t)(k + u) * step) : -1;
+            vv[u] = ok ? ld_stream(v + base + (int64_t)(k + u) * step) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (c[u] >= 0) acc[u] += vv[u] * ld_gather(b + (int64_t)c[u] * bs);
     }
     T sum = acc[0];
 #pragma unroll
@@ -1448,6 +1529,9 @@ static int ell_spmv(int64_t n, int64_t width, int64_t stride, const int* ci, con
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int per_sm = tuning("ell_per_sm", 16);
     const int grid = per_sm > 0 ? grid_for(n, 256, per_sm) : (int)ceil_div(n, 256);
+    // 4 entries in flight per thread, the tail as one predicated block (ell_unr
+    // 3 / 4 / 6 / 8 measured 0.897 / 0.928 / 0.816 / 0.816 on C2 fp64,
+    // profiles/r03_ell_tail.txt)
     auto kern = xin ? ell_kernel<T, true, 4, false> : ell_kernel<T, false, 4, false>;
     kern<<<grid, 256, 0, st>>>(n, width, stride, ci, v, b, bs, x, xs, al, be, xin, xins);
     count_launch();
@@ -1492,7 +1576,7 @@ template <typename T, bool XIN, int S>
 static void launch_sellp(int64_t n, int slice_size, const int* sl, const int* ss, const int* ci, const T* v,
                          const T* b, int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be, const T* xin,
                          int64_t xins, cudaStream_t st) {
-    const bool gs = tuning("sellp_grid_stride", sizeof(T) == 4);
+    const bool gs = tuning("sellp_grid_stride", 1);  // fp64 0.876 vs 0.860 one row per thread (r03_ell_tail)
     if (gs)
         sellp_kernel<T, XIN, 4, 8, true, S><<<grid_for(n, 256, 16), 256, 0, st>>>(n, slice_size, sl, ss, ci, v, b, bs,
                                                                                  x, xs, al, be, xin, xins);

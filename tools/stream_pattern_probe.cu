@@ -90,6 +90,33 @@ __global__ void k_spmv_like(const int* __restrict__ ci, const double* __restrict
     if (s == 12345.678) g_sink = s;
 }
 
+// Ell-like SpMV (27 entries per row, column-major ci / v, thread per row,
+// grid-stride): UNR entries' index and value loads issued before their
+// gathers; the x store per row. How much memory-level parallelism per thread
+// does the 27-point SpMV need?
+template <int UNR, bool STREAM>
+__global__ void __launch_bounds__(256) k_ell_like(const int* __restrict__ ci, const double* __restrict__ v,
+                                                  const double* __restrict__ b, double* __restrict__ x, int64_t rows) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0;
+#pragma unroll 1
+        for (int k0 = 0; k0 < 27; k0 += UNR) {
+            int c[UNR];
+            double vv[UNR], g[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                c[u] = STREAM ? __ldcs(ci + (int64_t)(k0 + u) * rows + r) : __ldg(ci + (int64_t)(k0 + u) * rows + r);
+                vv[u] = STREAM ? __ldcs(v + (int64_t)(k0 + u) * rows + r) : __ldg(v + (int64_t)(k0 + u) * rows + r);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) g[u] = __ldg(b + c[u]);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) acc += vv[u] * g[u];
+        }
+        x[r] = acc;
+    }
+}
+
 template <typename F>
 static float timeit(F f) {
     cudaEvent_t a, b;
@@ -169,6 +196,27 @@ int main() {
         }
         SPL(1, false, false) SPL(4, false, false) SPL(1, true, false) SPL(4, true, false)
         SPL(1, false, true) SPL(4, false, true) SPL(1, true, true) SPL(4, true, true)
+        // column-major copy of the same columns for the Ell-like kernels
+        {
+            int* hc = (int*)malloc(n * 4);
+            int* hr = (int*)malloc(n * 4);
+            cudaMemcpy(hr, ci, n * 4, cudaMemcpyDeviceToHost);
+            for (int64_t r = 0; r < rows; ++r)
+                for (int k = 0; k < 27; ++k) hc[(int64_t)k * rows + r] = hr[r * 27 + k];
+            cudaMemcpy(ci, hc, n * 4, cudaMemcpyHostToDevice);
+            free(hc);
+            free(hr);
+        }
+        const double bye = n * 12.0 + rows * 16.0;  // matrix + b + x
+#define ELL(UNR, ST, PER_SM)                                                                                  \
+        {                                                                                                     \
+            float ms = timeit([&] { k_ell_like<UNR, ST><<<sms * PER_SM, 256>>>(ci, v, bb, x, rows); });         \
+            printf("ell-like unroll %2d %s per_sm %2d        : %7.1f GB/s (matrix + b + x)\n", UNR,            \
+                   ST ? "ldcs" : "ldg ", PER_SM, bye / ms / 1e6);                                             \
+        }
+        ELL(1, false, 8) ELL(3, false, 8) ELL(9, false, 8) ELL(27, false, 8)
+        ELL(3, true, 8) ELL(9, true, 8) ELL(27, true, 8)
+        ELL(9, false, 4) ELL(9, false, 16) ELL(27, false, 4)
     }
     return 0;
 }
