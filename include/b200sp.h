@@ -84,7 +84,11 @@ int b200sp_norm2_f32(int64_t n, int32_t m, const float* x, int64_t xs, float* ou
 
 /* ---- SpMV ---------------------------------------------------------------- */
 /* Csr, classical strategy (sub-warp of `subwarp` lanes per row);
- * replaces CsrSpmvKernel + csr_row_sums (kernels.py:278-316) */
+ * replaces CsrSpmvKernel + csr_row_sums (kernels.py:278-316).
+ * `subwarp` may be OR-ed with B200SP_SUBWARP_EVEN_NNZ when the matrix has an
+ * even number of entries: the kernel may then read entries in aligned pairs
+ * (16-byte aligned col_idxs / vals; a pair never extends past entry nnz - 1). */
+#define B200SP_SUBWARP_EVEN_NNZ 0x100
 int b200sp_csr_spmv_classical_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
                                   const double* b, int64_t b_stride, double* x, int64_t x_stride, double alpha,
                                   const double* alpha_dev, double beta, const double* beta_dev, const double* x_in,
@@ -437,7 +441,8 @@ int b200sp_gmres_solve_tiny_f32(int64_t n, const int32_t* row_ptrs, const int32_
  * bicgstab_tst), 4 = distributed CG ghost block: q += A p (p = the ghost
  * vector) and sigma = u.q with u = the owned p. The control step (or, with a
  * distributed ctl, the parking of the local sum) runs in the last block as in the unfused
- * kernels (src/solvers/krylov.py:56-76, :233-265). */
+ * kernels (src/solvers/krylov.py:56-76, :233-265). `subwarp` takes the
+ * B200SP_SUBWARP_EVEN_NNZ flag as for the classical SpMV. */
 int b200sp_csr_spmv_dot_f64(int64_t n, const int32_t* row_ptrs, const int32_t* col_idxs, const double* vals,
                             const double* p, double* q, const double* u, int32_t phase, int32_t subwarp, void* ctl,
                             double* part, void* stream);

@@ -2207,7 +2207,16 @@ enum FusedPhase : int { PH_SIGMA = 1, PH_GAMMA = 2, PH_TST = 3, PH_SIGMA_ACC = 4
 
 // 8 CTAs per SM (<= 32 registers): the unbounded build took 40 registers at
 // sub-warp 1 (6 CTAs per SM) and ran slower than SpMV + separate dot
-template <typename T, int SW, int PH>
+// MODE (U = 1 only; both keep the loop's entry order, so the same sums):
+// 1 = entries in predicated blocks of 4 per lane (all loads of a block in
+// flight, no dependent remainder loop); 2 = thread per row reading aligned
+// (index, value) pairs in blocks of 2 (needs 16-byte aligned arrays and an
+// even entry count) -- the SpMV kernel's variants (spmv.cu csr_classical)
+template <typename T> struct KVec2;
+template <> struct KVec2<double> { using type = double2; };
+template <> struct KVec2<float> { using type = float2; };
+
+template <typename T, int SW, int PH, int MODE = 0>
 __global__ void __launch_bounds__(KRY_BLOCK, SW <= 4 ? 8 : 4)
 csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ av,
                     const T* __restrict__ p, T* __restrict__ q, const T* __restrict__ u, KrylovCtl* c,
@@ -2233,6 +2242,46 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
         T acc[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) acc[k] = 0;
+        if (MODE == 2 && U == 1 && SW == 1) {
+            const int s0 = st[0], e0 = st[0] + len[0];
+#pragma unroll 1
+            for (int k0 = s0 & ~1; k0 < e0; k0 += 4) {
+                int2 cc[2];
+                typename KVec2<T>::type vv[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int k = k0 + 2 * j;
+                    if (k < e0) {
+                        cc[j] = __ldg(reinterpret_cast<const int2*>(ci + k));
+                        vv[j] = __ldg(reinterpret_cast<const typename KVec2<T>::type*>(av + k));
+                    } else {
+                        cc[j] = make_int2(-1, -1);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int k = k0 + 2 * j;
+                    if (k >= s0 && cc[j].x >= 0) acc[0] += vv[j].x * __ldg(p + cc[j].x);
+                    if (k + 1 < e0 && cc[j].y >= 0) acc[0] += vv[j].y * __ldg(p + cc[j].y);
+                }
+            }
+        } else if (MODE >= 1 && U == 1) {
+#pragma unroll 1
+            for (int e0 = lane; e0 < maxlen; e0 += 4 * SW) {
+                int cc[4];
+                T vv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int e = e0 + j * SW;
+                    const bool ok = e < len[0];
+                    cc[j] = ok ? __ldg(ci + st[0] + e) : -1;
+                    vv[j] = ok ? __ldg(av + st[0] + e) : T(0);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (cc[j] >= 0) acc[0] += vv[j] * __ldg(p + cc[j]);
+            }
+        } else
         for (int e = lane; e < maxlen; e += SW) {
             int cc[U];
             T vv[U];
@@ -2286,15 +2335,27 @@ csr_spmv_dot_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict
     }
 }
 
-template <typename T, int SW>
-static void launch_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
-                            int phase, KrylovCtl* c, double* part, cudaStream_t st) {
+template <typename T, int SW, int MODE>
+static void launch_spmv_dot_m(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
+                              int phase, KrylovCtl* c, double* part, cudaStream_t st) {
     constexpr int U = SW >= 32 ? 4 : (SW >= 8 ? 2 : 1);
     const int grid = kry_grid(ceil_div(n, U) * SW, KRY_BLOCK);
-    if (phase == PH_SIGMA) csr_spmv_dot_kernel<T, SW, PH_SIGMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
-    else if (phase == PH_GAMMA) csr_spmv_dot_kernel<T, SW, PH_GAMMA><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
-    else if (phase == PH_SIGMA_ACC) csr_spmv_dot_kernel<T, SW, PH_SIGMA_ACC><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
-    else csr_spmv_dot_kernel<T, SW, PH_TST><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    if (phase == PH_SIGMA) csr_spmv_dot_kernel<T, SW, PH_SIGMA, MODE><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else if (phase == PH_GAMMA) csr_spmv_dot_kernel<T, SW, PH_GAMMA, MODE><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else if (phase == PH_SIGMA_ACC) csr_spmv_dot_kernel<T, SW, PH_SIGMA_ACC, MODE><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+    else csr_spmv_dot_kernel<T, SW, PH_TST, MODE><<<grid, KRY_BLOCK, 0, st>>>(n, rp, ci, av, p, q, u, c, part);
+}
+template <typename T, int SW>
+static void launch_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, const T* p, T* q, const T* u,
+                            int phase, KrylovCtl* c, double* part, bool even_nnz, cudaStream_t st) {
+    // knob "spmv_dot_mode": 0 = loop, 1 = 4-entry blocks, 2 = pairs (thread per row)
+    const bool pairs = SW == 1 && even_nnz && ((reinterpret_cast<uintptr_t>(ci) | reinterpret_cast<uintptr_t>(av)) & 15) == 0;
+    int mode = tuning("spmv_dot_mode", pairs ? 2 : 1);
+    if (mode == 2 && !pairs) mode = 1;
+    if (SW >= 8) mode = 0;  // U > 1: the loop form
+    if (mode == 2) launch_spmv_dot_m<T, SW, 2>(n, rp, ci, av, p, q, u, phase, c, part, st);
+    else if (mode == 1) launch_spmv_dot_m<T, SW, 1>(n, rp, ci, av, p, q, u, phase, c, part, st);
+    else launch_spmv_dot_m<T, SW, 0>(n, rp, ci, av, p, q, u, phase, c, part, st);
 }
 
 template <typename T>
@@ -2305,13 +2366,15 @@ static int csr_spmv_dot(int64_t n, const int* rp, const int* ci, const T* av, co
     if (n == 0) return B200SP_OK;
     cudaStream_t st = as_stream(stream);
     KrylovCtl* c = (KrylovCtl*)ctl;
+    const bool ev = (subwarp & B200SP_SUBWARP_EVEN_NNZ) != 0;
+    subwarp &= ~B200SP_SUBWARP_EVEN_NNZ;
     switch (subwarp) {
-        case 1: launch_spmv_dot<T, 1>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
-        case 2: launch_spmv_dot<T, 2>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
-        case 4: launch_spmv_dot<T, 4>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
-        case 8: launch_spmv_dot<T, 8>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
-        case 16: launch_spmv_dot<T, 16>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
-        case 32: launch_spmv_dot<T, 32>(n, rp, ci, av, p, q, u, phase, c, part, st); break;
+        case 1: launch_spmv_dot<T, 1>(n, rp, ci, av, p, q, u, phase, c, part, ev, st); break;
+        case 2: launch_spmv_dot<T, 2>(n, rp, ci, av, p, q, u, phase, c, part, ev, st); break;
+        case 4: launch_spmv_dot<T, 4>(n, rp, ci, av, p, q, u, phase, c, part, ev, st); break;
+        case 8: launch_spmv_dot<T, 8>(n, rp, ci, av, p, q, u, phase, c, part, ev, st); break;
+        case 16: launch_spmv_dot<T, 16>(n, rp, ci, av, p, q, u, phase, c, part, ev, st); break;
+        case 32: launch_spmv_dot<T, 32>(n, rp, ci, av, p, q, u, phase, c, part, ev, st); break;
         default: set_error("csr_spmv_dot: subwarp must be a power of two <= 32 (got %d)", subwarp); return B200SP_EINVAL;
     }
     count_launch();

@@ -150,7 +150,7 @@ csr_classical_kernel(int64_t n, const int* __restrict__ rp, const int* __restric
 template <typename T, int SW>
 static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v, const T* b,
                              int64_t bs, T* x, int64_t xs, Coef<T> al, Coef<T> be,
-                             const T* xin, int64_t xins, cudaStream_t st) {
+                             const T* xin, int64_t xins, bool even_nnz, cudaStream_t st) {
     const int block = 256;
     // measured on B200 (profiles/r02_classical_sweep.txt): L1-allocating
     // matrix loads lift C2 fp64 (sub-warp 4) from 0.43 to 0.85 of the HBM
@@ -164,7 +164,9 @@ static void launch_classical(int64_t n, const int* rp, const int* ci, const T* v
     const int grid = grid_for(ceil_div(n, two ? U2 : U0) * SW, block, tuning("classical_per_sm", 32));
     auto kern = two ? (xin ? csr_classical_kernel<T, SW, true, true, U2> : csr_classical_kernel<T, SW, false, true, U2>)
                     : (xin ? csr_classical_kernel<T, SW, true, true, U0> : csr_classical_kernel<T, SW, false, true, U0>);
-    const bool pairs_ok = ((reinterpret_cast<uintptr_t>(ci) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    // pair loads need 16-byte aligned arrays and an even entry count (a pair
+    // starts at an even entry, so it never reaches past entry nnz - 1)
+    const bool pairs_ok = even_nnz && ((reinterpret_cast<uintptr_t>(ci) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
     if (!two && U0 == 1) {
         // predicated entry blocks (knob "classical_kb": 0 = the loop, 2 / 3 / 4
         // entries per lane per block, -1 / -2 / -4 aligned (index, value) pairs
@@ -191,13 +193,15 @@ static int csr_classical(int64_t n, const int* rp, const int* ci, const T* v, co
     if (n == 0) return B200SP_OK;
     cudaStream_t st = as_stream(stream);
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
+    const bool ev = (subwarp & B200SP_SUBWARP_EVEN_NNZ) != 0;  // caller: the matrix has an even entry count
+    subwarp &= ~B200SP_SUBWARP_EVEN_NNZ;
     switch (subwarp) {
-        case 1: launch_classical<T, 1>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
-        case 2: launch_classical<T, 2>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
-        case 4: launch_classical<T, 4>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
-        case 8: launch_classical<T, 8>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
-        case 16: launch_classical<T, 16>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
-        case 32: launch_classical<T, 32>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, st); break;
+        case 1: launch_classical<T, 1>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, ev, st); break;
+        case 2: launch_classical<T, 2>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, ev, st); break;
+        case 4: launch_classical<T, 4>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, ev, st); break;
+        case 8: launch_classical<T, 8>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, ev, st); break;
+        case 16: launch_classical<T, 16>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, ev, st); break;
+        case 32: launch_classical<T, 32>(n, rp, ci, v, b, bs, x, xs, al, be, xin, xins, ev, st); break;
         default: set_error("csr classical: subwarp must be a power of two <= 32 (got %d)", subwarp);
                  return B200SP_EINVAL;
     }

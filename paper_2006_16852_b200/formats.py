@@ -541,8 +541,8 @@ class Csr(_Sparse):
         """automatic: load_balance for skewed row lengths (max > 4 x mean +
         64), else classical -- with L1-allocating matrix loads the sub-warp
         kernel is the fastest Csr SpMV measured on B200 for every stencil
-        (C2 fp64 0.85, fp32 0.74, 7-point 0.85 of the HBM roofline;
-        profiles/r02_classical_sweep.txt) ahead of the staged stream kernels."""
+        (C2 fp64 0.82, fp32 0.79-0.81, 7-point 0.87 of the HBM roofline;
+        profiles/r03_classical_kb.txt) ahead of the staged stream kernels."""
         if self._requested != "automatic":
             return self._requested
         n = self.size.rows
@@ -551,10 +551,9 @@ class Csr(_Sparse):
         mean = self.nnz / n
         if self._row_stats() > 4 * mean + 64:
             return "load_balance"
-        # fp32 with long rows: the TMA pipeline with two CTAs per SM measured
-        # 0.759 vs the classical kernel's 0.72 on C2 (profiles/r02_pipe_sweep.txt)
-        if self._v.element_size() == 4 and mean >= 12 and self._stream_ok() and n >= (1 << 16):
-            return "stream"
+        # (fp32 with long rows took the TMA pipeline, 0.759 vs 0.72, until the
+        # classical kernel's aligned pair loads: 0.79-0.81 vs 0.75 on C2,
+        # profiles/r03_classical_kb.txt)
         return "classical"
 
     def _stream_ok(self):
@@ -800,7 +799,7 @@ class Csr(_Sparse):
                 ev_in.append(e)
         suf = _lib.suffix(self._v.dtype)
         isz = self._v.element_size()
-        sw = self.subwarp()
+        sw = self._subwarp_arg()
         for j in range(k):
             r0, r1 = P["rows"][j], P["rows"][j + 1]
             if P["wait"][j] >= 0:
@@ -833,7 +832,14 @@ class Csr(_Sparse):
                           bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, *self.stream_config(), exc.stream)
         else:
             _lib.call("csr_spmv_classical_" + suf, n, ptr(self._rp), ptr(self._ci), ptr(self._v),
-                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self.subwarp(), exc.stream)
+                      bp, bs, xp, xs, a_h, a_p, b_h, b_p, xin, xins, self._subwarp_arg(), exc.stream)
+
+    def _subwarp_arg(self):
+        """The classical kernel's sub-warp width, flagged B200SP_SUBWARP_EVEN_NNZ
+        when the entry count is even (aligned pair loads stay inside the arrays)."""
+        return self.subwarp() | (self.SUBWARP_EVEN_NNZ if self.nnz % 2 == 0 else 0)
+
+    SUBWARP_EVEN_NNZ = 0x100  # include/b200sp.h
 
     # -- conversions -------------------------------------------------------------------
     def _to_csr(self, **kw):

@@ -58,7 +58,7 @@ def fused_csr(solver):
 
 def spmv_dot(S, a, suf, p, q, u, phase):
     _lib.call("csr_spmv_dot_" + suf, a.size.rows, ptr(a._rp), ptr(a._ci), ptr(a._v), ptr(p), ptr(q),
-              ptr(u) if u is not None else 0, phase, a.subwarp(), S.c, S.p, a.exec.stream)
+              ptr(u) if u is not None else 0, phase, a._subwarp_arg(), S.c, S.p, a.exec.stream)
 
 
 def finish_from_device(solver, state, st, x):
