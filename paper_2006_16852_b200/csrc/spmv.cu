@@ -758,18 +758,28 @@ __device__ __forceinline__ void lb2_rows(int r0, int r_end, int k0, int rc, int 
             e = s;
         }
         T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        int k = s + lane;
-        for (; UNR4 && k + 3 * SW < e; k += 4 * SW) {
-            const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + SW), c2 = __ldg(ci + k + 2 * SW),
-                      c3 = __ldg(ci + k + 3 * SW);
-            a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
-            a1 += __ldg(v + k + SW) * ld_gather(b + (int64_t)c1 * bs);
-            a2 += __ldg(v + k + 2 * SW) * ld_gather(b + (int64_t)c2 * bs);
-            a3 += __ldg(v + k + 3 * SW) * ld_gather(b + (int64_t)c3 * bs);
-        }
-        for (; k < e; k += SW) {
-            int c0 = __ldg(ci + k);
-            a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
+        if (UNR4) {
+            // predicated blocks of 4 entries per lane: every load of a block
+            // in flight together, no dependent remainder loop
+#pragma unroll 1
+            for (int k = s + lane; k < e; k += 4 * SW) {
+                int c[4];
+                T vv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool ok = k + j * SW < e;
+                    c[j] = ok ? __ldg(ci + k + j * SW) : -1;
+                    vv[j] = ok ? __ldg(v + k + j * SW) : T(0);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (c[j] >= 0) a0 += vv[j] * ld_gather(b + (int64_t)c[j] * bs);
+            }
+        } else {
+            for (int k = s + lane; k < e; k += SW) {
+                int c0 = __ldg(ci + k);
+                a0 += __ldg(v + k) * ld_gather(b + (int64_t)c0 * bs);
+            }
         }
         const T sum = subwarp_sum<SW>((a0 + a1) + (a2 + a3));
         if (active && !lng && lane == 0) {
@@ -874,9 +884,12 @@ static int csr_lb(int64_t n, int64_t nnz, const int* rp, const int* ci, const T*
     Coef<T> al = coef(alpha, alpha_dev), be = coef(beta, beta_dev);
     const int64_t ntiles = ceil_div(n + nnz, tile);
     {
-        // fp64: one entry per step (27-pt 0.686 vs 0.653, 7-pt 0.848 vs 0.804); fp32: 4 (0.620 vs 0.571)
-        auto k2 = tuning("lb2_unroll", sizeof(T) == 8 ? 1 : 4) == 4 ? (xin ? csr_lb2_kernel<T, true, true> : csr_lb2_kernel<T, false, true>)
+        // predicated blocks of 4 entries per lane (lb2_unroll 4) vs the plain loop (1):
+        // 27-point fp64 0.711 vs 0.667, fp32 0.629 vs 0.558 (profiles/r03_lb_blocks.txt)
+        auto k2 = tuning("lb2_unroll", 4) == 4 ? (xin ? csr_lb2_kernel<T, true, true> : csr_lb2_kernel<T, false, true>)
                                                 : (xin ? csr_lb2_kernel<T, true, false> : csr_lb2_kernel<T, false, false>);
+        // (aligned pair loads, as the classical kernel's fp32 default, measured
+        // 0.49 / 0.42 vs 0.71 / 0.62 here: profiles/r03_lb_blocks.txt)
         const unsigned g2 = (unsigned)std::min<int64_t>(ntiles, (int64_t)kNumSMs * tuning("lb2_per_sm", 1 << 20));  // one CTA per tile measured best (0.66 vs 0.51 persistent)
         k2<<<g2, LB_BLOCK, 0, st>>>(n, ntiles, rp, ci, v, b, bs, x, xs, al, be, xin, xins, coords, carry_row,
                                     carry_val);
