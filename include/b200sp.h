@@ -52,6 +52,8 @@ void b200sp_set_guard(const int32_t* guard);
 /* Tuning knob for benchmark sweeps (kernel variant / launch shape by name);
  * unset knobs keep the measured-best defaults. Not thread-safe against
  * concurrent set calls; not needed for correct results. */
+/* b200sp_set_tuning(key, B200SP_TUNING_DEFAULT) restores a knob's built-in default */
+#define B200SP_TUNING_DEFAULT (-2147483647 - 1)
 int b200sp_set_tuning(const char* key, int32_t value);
 int64_t b200sp_reduce_workspace_elems(void);
 int64_t b200sp_scan_workspace_elems(int64_t count);

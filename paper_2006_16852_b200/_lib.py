@@ -250,6 +250,14 @@ def set_tuning(key, value):
     call("set_tuning", key.encode(), int(value))
 
 
+TUNING_DEFAULT = -(2 ** 31)  # include/b200sp.h B200SP_TUNING_DEFAULT
+
+
+def reset_tuning(key):
+    """Restore a knob's built-in (measured-best) default."""
+    call("set_tuning", key.encode(), TUNING_DEFAULT)
+
+
 def launch_count():
     _load()
     return int(_funcs["launch_count"]())

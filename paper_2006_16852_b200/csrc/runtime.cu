@@ -47,7 +47,8 @@ static std::atomic<int> g_knobs{0};
 int tuning(const char* key, int dflt) {
     const int k = g_knobs.load(std::memory_order_acquire);
     for (int i = 0; i < k; ++i)
-        if (std::strncmp(g_knob_key[i], key, sizeof(g_knob_key[i])) == 0) return g_knob_val[i];
+        if (std::strncmp(g_knob_key[i], key, sizeof(g_knob_key[i])) == 0)
+            return g_knob_val[i] == B200SP_TUNING_DEFAULT ? dflt : g_knob_val[i];
     return dflt;
 }
 

@@ -444,3 +444,104 @@ def test_clone_gets_its_own_pipeline_plan(cuda, host):
     xh2 = b2.Dense(host, np.zeros((n, 1)))
     c.apply(bh, xh2)
     np.testing.assert_array_equal(np.asarray(xh2.data), ref)
+
+
+# ---------------------------------------------------------------------------
+# row-loop variants of the classical kernel (predicated entry blocks, aligned
+# pair loads) and Ell's predicated tail: every mode on odd / even entry counts
+# and several row-length mixes, against the oracle; pair loads only with the
+# even-count flag (no read past the arrays' end)
+# ---------------------------------------------------------------------------
+def _ragged(n, seed, max_len):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, max_len + 1, n)
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]) if lens.sum() else np.zeros(0, int)
+    vals = rng.standard_normal(rows.size)
+    return rows, cols, vals
+
+
+@pytest.mark.parametrize("kb", [0, 2, 3, 4, -1, -2, -4])
+@pytest.mark.parametrize("sw", [1, 2, 4, 8])
+@pytest.mark.parametrize("case", ["even", "odd", "ragged"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_classical_row_loop_variants(cuda, kb, sw, case, dtype):
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib
+
+    n = 777
+    if case == "ragged":
+        rows, cols, vals = _ragged(n, 5, 40)
+    else:
+        rows, cols, vals = _ragged(n, 6, 9)
+        want_odd = case == "odd"
+        if (rows.size % 2 == 1) != want_odd:  # drop the last entry to flip the parity
+            rows, cols, vals = rows[:-1], cols[:-1], vals[:-1]
+    data = b2.MatrixData((n, n), rows, cols, vals)
+    rp, ci, v = P.to_csr(n, rows, cols, vals)
+    bv = np.random.default_rng(1).standard_normal((n, 1))
+    ref = OS.csr_spmv(rp, ci, v, bv)
+    _lib.set_tuning("classical_kb", kb)
+    try:
+        a = b2.matrix_from_data(cuda, data, "csr", value_dtype=dtype, strategy="classical")
+        a.set_strategy("classical", subwarp=sw)
+        x = b2.Dense.zeros(cuda, n, 1, value_dtype=dtype)
+        a.apply(b2.Dense(cuda, bv, value_dtype=dtype), x)
+        assert OS.rel_error_inf(np.asarray(x.data, dtype=np.float64), ref) <= TOL[dtype]
+        # alpha / beta path through the same kernel
+        x0 = b2.Dense(cuda, np.ones((n, 1)), value_dtype=dtype)
+        a.apply_advanced(0.5, b2.Dense(cuda, bv, value_dtype=dtype), -1.0, x0)
+        assert OS.rel_error_inf(np.asarray(x0.data, dtype=np.float64), 0.5 * ref - 1.0) <= 4 * TOL[dtype]
+    finally:
+        _lib.reset_tuning("classical_kb")
+
+
+@pytest.mark.parametrize("width_max", [1, 3, 4, 5, 8, 9, 27])
+@pytest.mark.parametrize("fmt", ["ell", "sellp", "hybrid"])
+def test_ell_predicated_tail_widths(cuda, width_max, fmt):
+    import paper_2006_16852_b200 as b2
+
+    n = 513
+    rows, cols, vals = _ragged(n, width_max, width_max)
+    data = b2.MatrixData((n, n), rows, cols, vals)
+    rp, ci, v = P.to_csr(n, rows, cols, vals)
+    bv = np.random.default_rng(2).standard_normal((n, 1))
+    a = b2.matrix_from_data(cuda, data, fmt)
+    x = b2.Dense.zeros(cuda, n, 1)
+    a.apply(b2.Dense(cuda, bv), x)
+    assert OS.rel_error_inf(np.asarray(x.data), OS.csr_spmv(rp, ci, v, bv)) <= 1e-14
+
+
+@pytest.mark.parametrize("kind,g", [("7pt", 14), ("27pt", 9)])
+def test_fused_solver_spmv_modes_bitwise(cuda, kind, g):
+    """The fused SpMV + dot kernel's row-loop modes (loop, 4-entry blocks,
+    aligned pairs) keep the loop's entry order: a CG solve gives bitwise the
+    same iterate and iteration count in every mode."""
+    import torch
+
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib, problems
+
+    a = problems.stencil(cuda, kind, g)
+    n = a.size.rows
+    xs = {}
+    try:
+        for mode in (0, 1, 2):
+            _lib.set_tuning("spmv_dot_mode", mode)
+            _lib.set_tuning("coop_resident", 0)
+            from paper_2006_16852_b200 import config
+
+            old = config.CG_COOP_MAX_ROWS
+            config.CG_COOP_MAX_ROWS = 0  # the batched (fused-SpMV) path
+            try:
+                s = b2.Cg(cuda, criteria=[b2.Iteration(500), b2.ResidualNormReduction(1e-10)]).generate(a)
+                x = b2.Dense.wrap(cuda, torch.zeros((n, 1), dtype=torch.float64, device=cuda.device))
+                s.apply(b2.Dense.wrap(cuda, torch.ones((n, 1), dtype=torch.float64, device=cuda.device)), x)
+            finally:
+                config.CG_COOP_MAX_ROWS = old
+            xs[mode] = (s.last_status.iterations, x.values.cpu().numpy().copy())
+    finally:
+        _lib.reset_tuning("spmv_dot_mode")
+        _lib.reset_tuning("coop_resident")
+    assert xs[0][0] == xs[1][0] == xs[2][0]
+    assert np.array_equal(xs[0][1], xs[1][1]) and np.array_equal(xs[0][1], xs[2][1])
