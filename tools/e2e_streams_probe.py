@@ -28,7 +28,7 @@ a.apply(b2.Dense(exc, bv), ref)
 ref = ref.values.cpu().numpy()
 
 
-def run(k, streams, reps=30):
+def run(k, streams, reps=30):  # needs Csr.HOST_PIPELINE_STREAMS (removed after the sweep; see profiles/r03_e2e_streams.txt)
     Csr.HOST_PIPELINE_CHUNKS = k
     Csr.HOST_PIPELINE_STREAMS = streams
     a._pplan = None
