@@ -117,6 +117,28 @@ __global__ void __launch_bounds__(256) k_ell_like(const int* __restrict__ ci, co
     }
 }
 
+// random gathers (C3-like): per entry one coalesced int32 column index, one
+// 8-byte gather from a 33.5 MB vector (L2-resident), VEC entries per lane
+template <int VEC>
+__global__ void __launch_bounds__(256) k_rand_gather(const int* __restrict__ ci, const double* __restrict__ b,
+                                                     int64_t n, double* out) {
+    double s = 0;
+    const int64_t nv = n / VEC;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        int c[VEC];
+        if (VEC == 4) {
+            const int4 q = __ldcs(reinterpret_cast<const int4*>(ci) + i);
+            c[0] = q.x; c[VEC > 1 ? 1 : 0] = q.y; c[VEC > 2 ? 2 : 0] = q.z; c[VEC > 3 ? 3 : 0] = q.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < VEC; ++u) c[u] = __ldcs(ci + i * VEC + u);
+        }
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) s += __ldg(b + c[u]);
+    }
+    if (s == 12345.678) *out = s;
+}
+
 template <typename F>
 static float timeit(F f) {
     cudaEvent_t a, b;
@@ -217,6 +239,30 @@ int main() {
         ELL(1, false, 8) ELL(3, false, 8) ELL(9, false, 8) ELL(27, false, 8)
         ELL(3, true, 8) ELL(9, true, 8) ELL(27, true, 8)
         ELL(9, false, 4) ELL(9, false, 16) ELL(27, false, 4)
+    }
+    {
+        // C3-like: 67.1M random columns over 4,194,304 rows
+        const int64_t n = 67108864, cols = 4194304;
+        int* ci;
+        double *bb, *o;
+        cudaMalloc(&ci, n * 4);
+        cudaMalloc(&bb, cols * 8);
+        cudaMalloc(&o, 8);
+        cudaMemset(bb, 0, cols * 8);
+        int* h = (int*)malloc(n * 4);
+        unsigned long long st = 88172645463325252ull;
+        for (int64_t k = 0; k < n; ++k) {
+            st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+            h[k] = (int)(st % cols);
+        }
+        cudaMemcpy(ci, h, n * 4, cudaMemcpyHostToDevice);
+        free(h);
+        for (int per_sm : {4, 8, 16}) {
+            float ms = timeit([&] { k_rand_gather<1><<<sms * per_sm, 256>>>(ci, bb, n, o); });
+            printf("random gather vec 1 per_sm %2d   : %7.1f us  %6.1f G gathers/s\n", per_sm, ms * 1e3, n / ms / 1e6);
+            ms = timeit([&] { k_rand_gather<4><<<sms * per_sm, 256>>>(ci, bb, n, o); });
+            printf("random gather vec 4 per_sm %2d   : %7.1f us  %6.1f G gathers/s\n", per_sm, ms * 1e3, n / ms / 1e6);
+        }
     }
     return 0;
 }
