@@ -557,9 +557,7 @@ csr_pipe_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                 e[k] = (int)(max((int64_t)rs[k], lo) - lo) + sub;
                 ee[k] = (int)(max(min((int64_t)re[k], hia), lo) - lo);
             }
-            // 8 (then 4) independent smem reads + x gathers in flight per row
-            // step (a predicated fixed-batch variant measured slower on every
-            // stencil: profiles/r02_pipe_sweep.txt)
+            // 8 independent smem reads + x gathers in flight per row step
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
                 int q = e[k];
@@ -577,14 +575,22 @@ csr_pipe_kernel(int64_t n, const int* __restrict__ rp, const int* __restrict__ c
                     s2 += vv[2] + vv[6];
                     s3 += vv[3] + vv[7];
                 }
-                for (; q + 3 * TPR < qe; q += 4 * TPR) {
-                    const int c0 = sci[q], c1 = sci[q + TPR], c2 = sci[q + 2 * TPR], c3 = sci[q + 3 * TPR];
-                    s0 += sv[q] * ld_gather(b + (int64_t)c0 * bs);
-                    s1 += sv[q + TPR] * ld_gather(b + (int64_t)c1 * bs);
-                    s2 += sv[q + 2 * TPR] * ld_gather(b + (int64_t)c2 * bs);
-                    s3 += sv[q + 3 * TPR] * ld_gather(b + (int64_t)c3 * bs);
+                // the rest (< 8 per thread) as one predicated block: all its
+                // gathers in flight together, no dependent remainder loop
+                // (27-point fp64 0.725 -> 0.767, 7-point 0.30 -> 0.46;
+                // profiles/r03_pipe_sweep.txt)
+                if (q < qe) {
+                    T vv[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int qi = q + i * TPR;
+                        vv[i] = qi < qe ? sv[qi] * ld_gather(b + (int64_t)sci[qi] * bs) : T(0);
+                    }
+                    s0 += vv[0] + vv[4];
+                    s1 += vv[1] + vv[5];
+                    s2 += vv[2] + vv[6];
+                    s3 += vv[3] + vv[7];
                 }
-                for (; q < qe; q += TPR) s0 += sv[q] * ld_gather(b + (int64_t)sci[q] * bs);
                 acc[k] += (s0 + s1) + (s2 + s3);
             }
             if (sub == 0) {

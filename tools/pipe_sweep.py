@@ -37,13 +37,17 @@ by = bytes_csr(n, nnz, vt)
 print(f"matrix={args.matrix} g={args.grid} n={n} nnz={nnz} dtype={args.dtype}")
 ref = None
 cases = [("ld", None)]
-for shape, nt in (((2, 1), 256), ((2, 2), 256), ((1, 1), 256), ((2, 2), 512), ((4, 1), 512)):
+for shape, nt in (((2, 1), 256), ((2, 2), 256), ((1, 1), 256), ((2, 1), 512), ((2, 2), 512), ((4, 1), 512),
+                  ((4, 2), 512)):
     for stages in (2, 3):
         cases.append(("tma", (shape, nt, stages)))
+cases.append(("tma-default", None))
 for impl, cfg in cases:
     m = b2.convert(a, "csr")
     if impl == "ld":
         m.set_strategy("stream", stream_impl="ld")
+    elif impl == "tma-default":
+        m.set_strategy("stream", stream_impl="tma")
     else:
         shape, nt, stages = cfg
         m.set_strategy("stream", stream_impl="tma", stream_shape=shape, stream_stages=stages, stream_consumers=nt)
@@ -72,6 +76,6 @@ for impl, cfg in cases:
         e.record()
     torch.cuda.synchronize()
     t = statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3
-    cfg = m.tma_config() if impl == "tma" else m.stream_config()
+    cfg = m.tma_config() if impl.startswith("tma") else m.stream_config()
     print(f"{impl:3s} cfg {str(cfg):24s}: {t * 1e6:8.1f} us {by / t / 1e9:7.1f} GB/s frac {by / t / 1e9 / peak:.3f}"
           f"  err-vs-ld {err:.1e}")
