@@ -342,7 +342,18 @@ csr_stream_kernel(int64_t n, int64_t nnz, const int* __restrict__ rp, const int*
                     s2 += s_v[k + 2 * TPR] * ld_gather(b + (int64_t)c2 * bs);
                     s3 += s_v[k + 3 * TPR] * ld_gather(b + (int64_t)c3 * bs);
                 }
-                for (; k < a1; k += TPR) s0 += s_v[k] * ld_gather(b + (int64_t)s_ci[k] * bs);
+                if (k < a1) {  // the rest (< 4) as one predicated block, gathers in flight together
+                    T t[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int ki = k + i * TPR;
+                        t[i] = ki < a1 ? s_v[ki] * ld_gather(b + (int64_t)s_ci[ki] * bs) : T(0);
+                    }
+                    s0 += t[0];
+                    s1 += t[1];
+                    s2 += t[2];
+                    s3 += t[3];
+                }
                 s0 += s2;
                 s1 += s3;
             } else {
