@@ -511,3 +511,44 @@ def test_cooperative_small_system_path(cuda, monkeypatch, name):
     assert res[True][0] > 0 and abs(res[True][0] - res[False][0]) <= 1
     assert res[True][2] < res[False][2]  # one solve launch vs batches of step kernels
     np.testing.assert_allclose(res[True][1], res[False][1], rtol=0, atol=1e-10 * np.abs(res[False][1]).max())
+
+
+def test_cg_cooperative_variants_and_counter_reuse(cuda):
+    """C1-style CG through the persistent cooperative kernels: the
+    global-memory kernel and the register-resident one give bitwise the same
+    iterate at the same CTA shape; the register-resident one with its fenced
+    or flag-in-data sigma exchange and 256 / 512-thread CTAs stays within the
+    reference's iteration count; and the grid-exchange counter (reset by the
+    last CTA out) survives back-to-back solves of different sizes."""
+    import paper_2006_16852_b200 as b2
+    from paper_2006_16852_b200 import _lib, problems
+
+    def solve(a):
+        n = a.size.rows
+        s = b2.Cg(cuda, criteria=[b2.Iteration(10000), b2.ResidualNormReduction(1e-8)]).generate(a)
+        x = b2.Dense.zeros(cuda, n, 1)
+        s.apply(b2.Dense(cuda, np.ones((n, 1))), x)
+        return s.last_status.iterations, np.asarray(x.data).copy()
+
+    a = problems.stencil(cuda, "5pt", 128)
+    small = problems.stencil(cuda, "5pt", 20)
+    knobs = ("coop_resident", "coop_res_block", "coop_nofence")
+    try:
+        _lib.set_tuning("coop_res_block", 256)
+        _lib.set_tuning("coop_nofence", 0)
+        _lib.set_tuning("coop_resident", 0)
+        it0, x0 = solve(a)
+        _lib.set_tuning("coop_resident", 1)
+        it1, x1 = solve(a)
+        assert it0 == it1 and np.array_equal(x0, x1)
+        for bs in (256, 512):
+            for nofence in (0, 1):
+                _lib.set_tuning("coop_res_block", bs)
+                _lib.set_tuning("coop_nofence", nofence)
+                runs = [solve(a), solve(small), solve(a)]
+                assert runs[0][0] == runs[2][0] and np.array_equal(runs[0][1], runs[2][1])  # counter reset
+                assert abs(runs[0][0] - it0) <= 1
+                np.testing.assert_allclose(runs[0][1], x0, rtol=0, atol=1e-9 * np.abs(x0).max())
+    finally:
+        for k in knobs:
+            _lib.reset_tuning(k)
